@@ -114,7 +114,7 @@ def isotropic(n: int, seed: int = 11102921, kind: str = "pp", kp: float = 4.0,
     shift = np.exp(1j * (KX + KY + KZ) * (h / 2.0) * (2.0 * np.pi / float(BOX_LEN)))
     uh = uh * shift
     # normalise: u' = sqrt(<|u|^2>/3), L = sqrt(2 pi)/kp for the pp spectrum; T = L/u'
-    u = np.stack([np.fft.irfftn(uh[i], s=(n, n, n)) for i in range(3)])
+    u = np.stack([np.fft.irfftn(uh[i], s=(n, n, n), axes=(0, 1, 2)) for i in range(3)])
     up = math.sqrt(float((u ** 2).sum(0).mean()) / 3.0)
     Lint = math.sqrt(2.0 * math.pi) / kp
     scale = (Lint / T) / up if up > 0 else 1.0
@@ -125,7 +125,7 @@ def isotropic(n: int, seed: int = 11102921, kind: str = "pp", kp: float = 4.0,
                    1j * (kz * uh[0] - kx * uh[2]),
                    1j * (kx * uh[1] - ky * uh[0])])
     # irfftn returns [z, y, x] indexed arrays -> ravel gives x fastest
-    om = np.stack([np.fft.irfftn(wh[i], s=(n, n, n)).ravel() for i in range(3)])
+    om = np.stack([np.fft.irfftn(wh[i], s=(n, n, n), axes=(0, 1, 2)).ravel() for i in range(3)])
     pos = lattice(n)
     gam = (om * h ** 3).astype(np.float32)
     return Field(pos, gam, sigma_for(n), float(BOX_LO), float(BOX_LEN), n,

@@ -1,0 +1,414 @@
+"""Pins for the CPU oracle (oracle/) against things other than itself.
+
+Every check here is fixed by PAPER.md's definitions or by mathematics:
+closed forms, printed example values (tests/golden), invariants, special cases,
+finite differences, and an independent 30-digit mpmath brute force.  Chosen so
+that a dropped term, a wrong sign or index, or a transposed operand in
+oracle/oracle.c or oracle/fmm_ref.py fails at least one of them.
+"""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import synthgen
+from oracle import fmm_ref as F
+
+mpmath = pytest.importorskip("mpmath")
+GOLD = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _mp_kernels(r, sigma):
+    """Independent 30-digit zeta, g, f and q = f'(r)/r (q by numerical differentiation)."""
+    mp = mpmath.mp
+    mp.dps = 30
+    r = mp.mpf(r)
+    s = mp.mpf(sigma)
+
+    def g_of(x):
+        rho = x / (mp.sqrt(2) * s)
+        return mp.erf(rho) - mp.sqrt(4 / mp.pi) * rho * mp.exp(-rho * rho)
+
+    def f_of(x):
+        return g_of(x) / (4 * mp.pi * x ** 3)  # gamma x grad(G g), G = 1/(4 pi r) PAPER.md:84
+
+    zeta = (2 * mp.pi * s * s) ** mp.mpf(-1.5) * mp.exp(-r * r / (2 * s * s))
+    return zeta, g_of(r), f_of(r), mp.diff(f_of, r) / r
+
+
+# ---------------------------------------------------------------- scalar kernels
+
+def test_golden_spec_values():
+    gold = json.load(open(os.path.join(GOLD, "kernel_values.json")))
+    z0, _, _, _ = oracle.kernels(0.0, 1.0)
+    assert round(z0, gold["zeta_r0_sigma1"]["digits"] + 1) == pytest.approx(
+        gold["zeta_r0_sigma1"]["value"], abs=10 ** -gold["zeta_r0_sigma1"]["digits"])
+    z, _, _, _ = oracle.kernels(1.0, 0.5)
+    assert z == pytest.approx(gold["zeta_r1_sigma0p5"]["value"], abs=1e-4)
+    _, g, _, _ = oracle.kernels(1.0, 1.0)
+    assert g == pytest.approx(gold["g_r_eq_sigma"]["value"], abs=1e-4)
+    # f at large r reduces to the point vortex 1/(4 pi r^3): G(1)=1/4pi
+    _, _, f, _ = oracle.kernels(1.0, 0.05)
+    assert f == pytest.approx(gold["greens_r1"]["value"], abs=5e-9)
+    assert f == pytest.approx(1.0 / (4 * math.pi), rel=1e-14)
+
+
+@pytest.mark.parametrize("r,sigma", [(0.0, 1.0), (1e-4, 1.0), (0.1, 1.0), (0.3535, 1.0),
+                                     (0.3536, 1.0), (0.5, 1.0), (1.0, 1.0), (2.0, 1.0),
+                                     (3.0, 0.7), (5.0, 1.0), (8.0, 1.0), (11.99, 1.0),
+                                     (12.01, 1.0), (20.0, 1.0), (1.0, 0.5)])
+def test_kernels_vs_mpmath(r, sigma):
+    z, g, f, q = oracle.kernels(r, sigma)
+    if r == 0.0:
+        mp = mpmath.mp
+        mp.dps = 30
+        z0 = (2 * mp.pi * sigma ** 2) ** mp.mpf(-1.5)
+        assert f == pytest.approx(float(z0 / 3), rel=1e-15)        # f(0) = zeta0/3
+        assert q == pytest.approx(float(-z0 / (5 * sigma ** 2)), rel=1e-15)
+        return
+    zm, gm, fm, qm = _mp_kernels(r, sigma)
+    assert z == pytest.approx(float(zm), rel=1e-13, abs=1e-30)  # r >= 12 sigma: zeta := 0
+    assert f == pytest.approx(float(fm), rel=1e-13)
+    assert q == pytest.approx(float(qm), rel=1e-11)
+    assert g == pytest.approx(float(gm), rel=1e-13, abs=1e-16)
+
+
+def test_cutoff_saturation_and_derivative():
+    # g' = 4 pi r^2 zeta (Eq. 6 is the radial integral of Eq. 4)
+    for r in (0.2, 0.9, 1.7, 3.3):
+        h = 1e-6
+        gp = (oracle.kernels(r + h, 1.0)[1] - oracle.kernels(r - h, 1.0)[1]) / (2 * h)
+        assert gp == pytest.approx(4 * math.pi * r * r * oracle.kernels(r, 1.0)[0], rel=1e-7)
+    assert 1.0 - oracle.kernels(8.0, 1.0)[1] < 1e-12
+    assert 1.0 - oracle.kernels(5.0, 1.0)[1] == pytest.approx(1.544e-5, rel=1e-3)
+
+
+# ---------------------------------------------------------------- direct sum
+
+def _direct(pos, gam, sigma, lam, scheme=0, **kw):
+    return oracle.direct(np.asarray(pos, np.float64), np.asarray(gam, np.float64), sigma,
+                         -math.pi, 2 * math.pi, lam, scheme, **kw)
+
+
+def test_right_hand_rule_and_sign():
+    # gamma = z at origin, target (1,0,0): u = (0, +1/4pi, 0) (physical sign, reading R1)
+    pos = np.array([[0.0, 1.0], [0.0, 0.0], [0.0, 0.0]])
+    gam = np.array([[0.0, 0.0], [0.0, 0.0], [1.0, 0.0]])
+    v, s = _direct(pos, gam, 0.05, 0)
+    assert v[:, 1] == pytest.approx([0.0, 1.0 / (4 * math.pi), 0.0], abs=1e-15)
+    assert np.all(v[:, 0] == 0.0)  # the target particle has zero strength
+
+
+def test_single_blob_closed_form_and_curl_of_streamfunction():
+    # u(x) = g(r)/(4 pi r^3) gamma x (x - x0); also u = curl psi, psi = gamma erf(rho)/(4 pi r)
+    rng = np.random.default_rng(5)
+    x0 = np.array([0.1, -0.2, 0.3])
+    g0 = np.array([0.3, -0.5, 0.8])
+    sigma = 0.4
+    probes = x0[:, None] + rng.normal(size=(3, 12)) * 0.5
+    v, _ = _direct(x0[:, None], g0[:, None], sigma, 0, probe_pos=probes,
+                   probe_gamma=np.zeros_like(probes))
+    for t in range(probes.shape[1]):
+        d = probes[:, t] - x0
+        r = np.linalg.norm(d)
+        rho = r / (math.sqrt(2) * sigma)
+        g = math.erf(rho) - 2 / math.sqrt(math.pi) * rho * math.exp(-rho * rho)
+        assert v[:, t] == pytest.approx(g / (4 * math.pi * r ** 3) * np.cross(g0, d), rel=1e-12)
+
+        def psi(x):
+            rr = np.linalg.norm(x - x0)
+            return g0 * math.erf(rr / (math.sqrt(2) * sigma)) / (4 * math.pi * rr)
+
+        h = 1e-5
+        J = np.zeros((3, 3))  # J[c, b] = d psi_c / d x_b
+        for b in range(3):
+            e = np.zeros(3)
+            e[b] = h
+            J[:, b] = (psi(probes[:, t] + e) - psi(probes[:, t] - e)) / (2 * h)
+        curl = np.array([J[2, 1] - J[1, 2], J[0, 2] - J[2, 0], J[1, 0] - J[0, 1]])
+        assert v[:, t] == pytest.approx(curl, rel=1e-6, abs=1e-9)
+
+
+@pytest.mark.parametrize("lam", [0, 1])
+def test_antisymmetry_two_particles(lam):
+    pos = np.array([[0.3, -0.4], [0.1, 0.5], [-0.2, 0.25]])
+    gam = np.array([[0.2, 0.2], [-0.1, -0.1], [0.7, 0.7]])
+    v, _ = _direct(pos, gam, 0.3, lam)
+    assert v[:, 0] == pytest.approx(-v[:, 1], rel=1e-12, abs=1e-15)
+
+
+def test_zero_net_momentum_equal_strengths():
+    rng = np.random.default_rng(7)
+    pos = rng.uniform(-math.pi, math.pi, (3, 40))
+    gam = np.tile(np.array([[0.3], [-0.2], [0.5]]), (1, 40))
+    v, _ = _direct(pos, gam, 0.35, 1)
+    scale = np.abs(v).sum()
+    assert np.abs(v.sum(axis=1)).max() < 1e-13 * scale
+
+
+@pytest.mark.parametrize("lam", [1, 2])
+def test_single_particle_in_periodic_box_is_at_rest(lam):
+    pos = np.array([[0.7], [-1.1], [2.0]])
+    gam = np.array([[0.4], [0.9], [-0.3]])
+    v, s = _direct(pos, gam, 0.3, lam)
+    assert np.abs(v).max() < 1e-14 and np.abs(s).max() < 1e-14
+
+
+def test_divergence_free_and_stretching_by_finite_differences():
+    rng = np.random.default_rng(11)
+    pos = rng.uniform(-math.pi, math.pi, (3, 25))
+    gam = rng.normal(size=(3, 25))
+    sigma = 0.5
+    probes = rng.uniform(-2, 2, (3, 4))
+    pg = rng.normal(size=(3, 4))
+    _, s_cl = _direct(pos, gam, sigma, 1, 0, probe_pos=probes, probe_gamma=pg)
+    _, s_tr = _direct(pos, gam, sigma, 1, 1, probe_pos=probes, probe_gamma=pg)
+    h = 1e-5
+    for t in range(4):
+        J = np.zeros((3, 3))  # J[a, b] = d u_a / d x_b
+        for b in range(3):
+            pp = probes[:, t:t + 1].copy()
+            pm = pp.copy()
+            pp[b] += h
+            pm[b] -= h
+            vp, _ = _direct(pos, gam, sigma, 1, probe_pos=pp, probe_gamma=pg[:, t:t + 1])
+            vm, _ = _direct(pos, gam, sigma, 1, probe_pos=pm, probe_gamma=pg[:, t:t + 1])
+            J[:, b] = (vp[:, 0] - vm[:, 0]) / (2 * h)
+        scale = np.abs(J).max()
+        assert abs(np.trace(J)) < 1e-7 * scale                     # div u = 0
+        assert s_cl[:, t] == pytest.approx(J @ pg[:, t], rel=1e-6, abs=1e-8 * scale)  # (g.grad)u
+        assert s_tr[:, t] == pytest.approx(J.T @ pg[:, t], rel=1e-6, abs=1e-8 * scale)
+
+
+def test_transpose_scheme_sums_to_zero_and_bilinearity():
+    rng = np.random.default_rng(13)
+    pos = rng.uniform(-math.pi, math.pi, (3, 30))
+    gam = rng.normal(size=(3, 30))
+    v, s_tr = _direct(pos, gam, 0.4, 1, 1)
+    assert np.abs(s_tr.sum(axis=1)).max() < 1e-12 * np.abs(s_tr).sum()
+    v2, s2 = _direct(pos, 2.5 * gam, 0.4, 1, 0)
+    _, s1 = _direct(pos, gam, 0.4, 1, 0)
+    assert v2 == pytest.approx(2.5 * v, rel=1e-13)
+    assert s2 == pytest.approx(6.25 * s1, rel=1e-12)
+
+
+def test_taylor_green_closed_form_image_sum():
+    """Lattice TG (c1): u_i = e^{-3 s^2/2} u_TG(x_i), sdot_i = h^3 e^{-3 s^2/2} (w.grad)u_TG,
+    up to lattice aliasing e^{-2 pi^2} ~ 2.7e-9 and float32 input rounding; the cube
+    surface term vanishes by the TG symmetry."""
+    f = synthgen.make("c1")
+    tg = np.array([0, 1234, 4095, 2000])
+    v, s = oracle.direct(f.pos, f.gamma, f.sigma, f.box_lo, f.box_len, 3, 0, targets=tg)
+    x, y, z = (f.pos[i, tg].astype(np.float64) for i in range(3))
+    damp = math.exp(-1.5 * f.sigma ** 2)
+    h = f.box_len / f.n
+    u_tg = np.stack([np.sin(x) * np.cos(y) * np.cos(z), -np.cos(x) * np.sin(y) * np.cos(z),
+                     0 * x]) * damp
+    s_tg = np.stack([-0.25 * np.sin(2 * y) * np.sin(2 * z), 0.25 * np.sin(2 * x) * np.sin(2 * z),
+                     0 * x]) * damp * h ** 3
+    assert np.abs(v - u_tg).max() < 2e-6 * np.abs(u_tg).max()
+    assert np.abs(s - s_tg).max() < 2e-6 * np.abs(s_tg).max()
+
+
+def test_tiny_brute_force_mpmath():
+    """Independent 30-digit brute force (N=3, 27 images): velocity from Eq. (5), stretching
+    as (gamma_i . grad) u by mpmath differentiation of the velocity field (Eq. 8, classical)."""
+    mp = mpmath.mp
+    mp.dps = 30
+    rng = np.random.default_rng(17)
+    pos = rng.uniform(-math.pi, math.pi, (3, 3))
+    gam = rng.normal(size=(3, 3))
+    sigma = 0.9
+    L = 2 * mp.pi
+    v, s = _direct(pos, gam, sigma, 1)
+
+    def vel_at(xt, exclude=None):
+        u = [mp.mpf(0)] * 3
+        for j in range(3):
+            for nx in (-1, 0, 1):
+                for ny in (-1, 0, 1):
+                    for nz in (-1, 0, 1):
+                        d = [xt[0] - mp.mpf(pos[0, j]) - nx * L, xt[1] - mp.mpf(pos[1, j]) - ny * L,
+                             xt[2] - mp.mpf(pos[2, j]) - nz * L]
+                        r = mp.sqrt(d[0] ** 2 + d[1] ** 2 + d[2] ** 2)
+                        if r == 0:
+                            continue
+                        rho = r / (mp.sqrt(2) * sigma)
+                        g = mp.erf(rho) - mp.sqrt(4 / mp.pi) * rho * mp.exp(-rho ** 2)
+                        f = g / (4 * mp.pi * r ** 3)
+                        gj = [mp.mpf(gam[k, j]) for k in range(3)]
+                        c = [gj[1] * d[2] - gj[2] * d[1], gj[2] * d[0] - gj[0] * d[2],
+                             gj[0] * d[1] - gj[1] * d[0]]
+                        u = [u[k] + f * c[k] for k in range(3)]
+        return u
+
+    for i in range(3):
+        xi = [mp.mpf(pos[k, i]) for k in range(3)]
+        gi = [mp.mpf(gam[k, i]) for k in range(3)]
+        u = vel_at(xi)
+        for k in range(3):
+            assert float(u[k]) == pytest.approx(v[k, i], rel=1e-12, abs=1e-15)
+        # directional derivative along gamma_i (the self term is identically zero, smooth)
+        for k in range(3):
+            fk = lambda t: vel_at([xi[a] + t * gi[a] for a in range(3)])[k]
+            sd = mp.diff(fk, 0)
+            assert float(sd) == pytest.approx(s[k, i], rel=1e-9, abs=1e-13)
+
+
+# ---------------------------------------------------------------- Morton tree
+
+def test_morton_hand_example():
+    # depth 1, box [-pi, pi): octant (ix,iy,iz) -> key ix | iy<<1 | iz<<2
+    lo, ln = synthgen.BOX_LO, synthgen.BOX_LEN
+    pos = np.array([[1.0, -1.0, 1.0, -1.0], [1.0, 1.0, -1.0, -1.0], [-1.0, 1.0, 1.0, -1.0]],
+                   np.float32)
+    keys, perm, ls, rc = oracle.morton(pos, 1, lo, ln)
+    assert rc == 0
+    assert list(keys) == [0, 3, 5, 6]
+    assert list(perm) == [3, 0, 2, 1]
+    assert list(ls) == [0, 1, 1, 1, 2, 2, 3, 4, 4]
+
+
+def test_morton_depth2_bits_and_stability():
+    lo, ln = synthgen.BOX_LO, synthgen.BOX_LEN
+    h = float(ln) / 4
+    # cell (ix,iy,iz) = (3,1,2): key bits b0: x0=1,y0=1,z0=0 ; b1: x1=1,y1=0,z1=1
+    c = np.array([3, 1, 2])
+    x = (float(lo) + (c + 0.5) * h).astype(np.float32)
+    pos = np.stack([x, x, x], axis=1).astype(np.float32)  # three identical particles
+    keys, perm, ls, rc = oracle.morton(pos, 2, lo, ln)
+    expect = (1 << 0) | (1 << 1) | (0 << 2) | (1 << 3) | (0 << 4) | (1 << 5)
+    assert list(keys) == [expect] * 3 and list(perm) == [0, 1, 2]  # ties keep input order
+    assert ls[expect] == 0 and ls[expect + 1] == 3 and ls[-1] == 3
+
+
+def test_morton_random_vs_python_sort_and_edges():
+    rng = np.random.default_rng(21)
+    lo, ln = synthgen.BOX_LO, synthgen.BOX_LEN
+    pos = rng.uniform(float(lo), float(lo + ln), (3, 5000)).astype(np.float32)
+    pos[:, :10] = lo  # exact lower faces
+    pos[:, 10:20] = np.nextafter(np.float32(lo + ln), np.float32(0))  # just below upper face
+    depth = 3
+    keys, perm, ls, rc = oracle.morton(pos, depth, lo, ln)
+    assert rc == 0
+    inv = np.float32((1 << depth) / float(ln))
+    q = np.floor((pos - lo) * inv).astype(np.int64).clip(0, (1 << depth) - 1)
+    ref = np.zeros(pos.shape[1], np.int64)
+    for b in range(depth):
+        for a in range(3):
+            ref |= ((q[a] >> b) & 1) << (3 * b + a)
+    order = sorted(range(pos.shape[1]), key=lambda i: (ref[i], i))
+    assert list(perm) == order and list(keys) == [ref[i] for i in order]
+    counts = np.bincount(ref, minlength=8 ** depth)
+    assert np.array_equal(np.diff(ls), counts) and ls[0] == 0 and ls[-1] == pos.shape[1]
+    assert set(perm.tolist()) == set(range(pos.shape[1]))
+
+
+def test_morton_flags_out_of_box():
+    lo, ln = synthgen.BOX_LO, synthgen.BOX_LEN
+    pos = np.zeros((3, 4), np.float32)
+    pos[0, 2] = np.float32(lo + ln)  # upper face is outside the half-open box
+    assert oracle.morton(pos, 2, lo, ln)[3] == -2
+    pos[0, 2] = np.nan
+    assert oracle.morton(pos, 2, lo, ln)[3] == -2
+
+
+def test_lattice_leaves_hold_equal_counts():
+    f = synthgen.make("c1")
+    keys, perm, ls, rc = oracle.morton(f.pos, 2, f.box_lo, f.box_len)
+    assert rc == 0 and np.all(np.diff(ls) == 64)
+
+
+# ---------------------------------------------------------------- FMM oracle (fmm_ref)
+
+def test_expansion_identities():
+    rng = np.random.default_rng(0)
+    x = rng.normal(size=3) * 3
+    y = rng.normal(size=3) * 0.3
+    R = F.solid_R(y[None], 30)[0]
+    I = F.solid_I(x[None], 30)[0]
+    # addition theorem, Eq. (10): 1/|x-y| = sum conj(R_n^m(y)) I_n^m(x)
+    assert np.real((np.conj(R) * I).sum()) == pytest.approx(1 / np.linalg.norm(x - y), rel=1e-14)
+    # R_1: z, -(x+iy)/2
+    r1 = F.solid_R(np.array([[0.3, -0.7, 1.1]]), 1)[0]
+    assert r1[F.kidx(1, 0)] == pytest.approx(1.1)
+    assert r1[F.kidx(1, 1)] == pytest.approx(-(0.3 - 0.7j) / 2)
+    assert r1[F.kidx(1, -1)] == pytest.approx((0.3 + 0.7j) / 2)
+    p = 12
+    src = rng.normal(size=(15, 3)) * 0.25
+    q = rng.normal(size=(15, 3))
+    M = F.p2m(src, q, p)
+    xt = np.array([2.0, 1.0, -1.5])
+    direct = (q / np.linalg.norm(xt - src, axis=1)[:, None]).sum(0)
+    assert np.real(M @ F.solid_I(xt[None], p)[0]) == pytest.approx(direct, rel=1e-7)
+    # M2L then L2L vs direct potential; M2M vs P2M about the other centre
+    D = np.array([3.0, -2.0, 2.5])
+    L = M @ F.m2l_matrix(D, p).T
+    z = np.array([0.1, -0.15, 0.2])
+    direct = (q / np.linalg.norm(D + z - src, axis=1)[:, None]).sum(0)
+    assert np.real(L @ F.solid_R(z[None], p)[0]) == pytest.approx(direct, rel=1e-8)
+    d = np.array([0.05, 0.02, -0.04])
+    L2 = L @ F.l2l_matrix(d, p).T
+    assert np.real(L2 @ F.solid_R((z - d)[None], p)[0]) == pytest.approx(direct, rel=1e-8)
+    dm = np.array([0.3, -0.2, 0.1])
+    assert M @ F.m2m_matrix(dm, p).T == pytest.approx(F.p2m(src + dm, q, p), abs=1e-12)
+    # zero-offset M2M / L2L are the identity
+    assert np.allclose(F.m2m_matrix(np.zeros(3), 4), np.eye(25))
+    assert np.allclose(F.l2l_matrix(np.zeros(3), 4), np.eye(25))
+    # gradient / Hessian stencils vs finite differences of the evaluated local expansion
+    g, h = F.l2p(L, z[None], p)
+    ev = lambda zz: np.real(L @ F.solid_R(zz[None], p)[0])
+    e = 1e-5
+    for a in range(3):
+        dz = np.zeros(3)
+        dz[a] = e
+        assert g[0, :, a] == pytest.approx((ev(z + dz) - ev(z - dz)) / (2 * e), rel=1e-7)
+        gp, _ = F.l2p(L, (z + dz)[None], p)
+        gm, _ = F.l2p(L, (z - dz)[None], p)
+        assert h[0, :, a, :] == pytest.approx((gp - gm)[0] / (2 * e), rel=1e-6, abs=1e-9)
+
+
+def test_periodic_operator_equals_explicit_image_sum():
+    """3x supercell rings == explicit M2L from every image box in the cube minus the near 3^3."""
+    rng = np.random.default_rng(3)
+    p = 6
+    src = rng.uniform(-1, 1, (10, 3)) * 0.5
+    q = rng.normal(size=(10, 3))
+    q -= q.mean(0)
+    M0 = F.p2m(src, q, p)
+    Lr = F.periodic_far(M0, 2 * math.pi, 2, p)
+    Le = np.zeros_like(Lr)
+    for a in range(-4, 5):
+        for b in range(-4, 5):
+            for c in range(-4, 5):
+                if max(abs(a), abs(b), abs(c)) > 1:
+                    Le += M0 @ F.m2l_matrix(-np.array([a, b, c]) * 2 * math.pi, p).T
+    assert Lr == pytest.approx(Le, rel=1e-12, abs=1e-14)
+
+
+def test_fmm_oracle_converges_to_direct_sum():
+    """FMM (fp64) vs direct sum on an isotropic 16^3 field: error decreases with p and is
+    at the paper's accuracy level ('4 significant digits' at p = 10)."""
+    f = synthgen.isotropic(16)
+    tg = synthgen.sample_targets(16 ** 3, 48, n_lattice=16)
+    v, s = oracle.direct(f.pos, f.gamma, f.sigma, f.box_lo, f.box_len, 1, 0, targets=tg)
+    errs = []
+    for p in (2, 4, 6):
+        vf, sf = F.evaluate(f.pos, f.gamma, f.sigma, f.box_lo, f.box_len, 2, p, 1)
+        errs.append((np.linalg.norm(vf[:, tg] - v) / np.linalg.norm(v),
+                     np.linalg.norm(sf[:, tg] - s) / np.linalg.norm(s)))
+    assert errs[0][0] > errs[1][0] > errs[2][0] and errs[0][1] > errs[1][1] > errs[2][1]
+    assert errs[2][0] < 5e-3 and errs[2][1] < 2e-2
+
+
+def test_fmm_oracle_near_only_depth1_equals_direct():
+    """depth 1 in free space (lambda = 0): all 8 octants are mutual neighbours, nothing is
+    well separated, so every interaction is P2P and the FMM equals the direct sum."""
+    f = synthgen.taylor_green(8)
+    vf, sf = F.evaluate(f.pos, f.gamma, f.sigma, f.box_lo, f.box_len, 1, 2, 0)
+    v, s = oracle.direct(f.pos, f.gamma, f.sigma, f.box_lo, f.box_len, 0, 0)
+    assert np.abs(vf - v).max() < 1e-13 * np.abs(v).max()
+    assert np.abs(sf - s).max() < 1e-12 * np.abs(s).max()
