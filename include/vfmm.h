@@ -1,0 +1,160 @@
+/*
+ * vfmm.h -- C ABI of the B200-native periodic vortex FMM (libvfmm.so).
+ *
+ * One call, vfmm_evaluate(), computes for N vortex particles in the triply
+ * periodic box [lo, lo+len)^3 the regularized Biot-Savart velocity and the
+ * vortex-stretching term of Yokota & Barba, arXiv:1110.2921:
+ *
+ *   u_i        = sum_n sum_j gamma_j x grad(G g_sigma)            PAPER.md:81  Eq.(5)
+ *   dgamma_i/dt = sum_n sum_j grad(gamma_j x grad(G g_sigma)) . gamma_i
+ *                                                                  PAPER.md:100 Eq.(8)
+ *   G = 1/(4 pi r), g_sigma the Gaussian cutoff (Eq. 6),
+ *   zeta_sigma the Gaussian core (Eq. 4), n over the periodic image cube
+ *   (PAPER.md:164 "3^3 x 3^3 x 3^3 - 1" images; :361 "27^3 periodic images").
+ *
+ * by the fast multipole method of PAPER.md section 3.1 (Eqs. 10-15):
+ * Morton-sorted uniform octree, P2M / M2M, periodic images via multipole
+ * expansions, M2L, L2L / L2P (far field without cutoff),
+ * and the exact near field P2P ("solving Eq. (5) exactly").
+ * Readings of the paper (sign, stretching scheme, image set, ...) are listed in
+ * DESIGN.md, section "Readings"; the physical sign u = +curl(psi) is used.
+ *
+ * Conventions for every function:
+ *  - All functions return vfmm_status; nothing throws across the ABI.
+ *  - Device buffers are plain CUDA device pointers (cudaMalloc'd or torch-owned);
+ *    "host" buffers are ordinary host memory.  The caller owns every buffer it passes.
+ *  - Arrays are float32 SoA "3 x n": x[0..n), then y[0..n), then z[0..n).
+ *  - A context is bound to one device and is not thread-safe; distinct contexts may
+ *    run concurrently on distinct devices.
+ */
+#ifndef VFMM_H
+#define VFMM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VFMM_ABI_VERSION 1
+#define VFMM_PMAX 16 /* highest supported expansion order p */
+
+typedef struct vfmm_ctx vfmm_ctx; /* opaque: workspace, operator tables, streams */
+
+typedef enum {
+    VFMM_OK = 0,
+    VFMM_EINVAL = -1,  /* bad parameter: n < 1, p < 1 or p > VFMM_PMAX, sigma <= 0 or not
+                          finite, depth out of [1, 10], image_levels out of [0, 6], box_len <= 0,
+                          NULL pointer, aliasing outputs */
+    VFMM_EDOMAIN = -2, /* device-detected (sticky until vfmm_sync_status): a position outside
+                          [lo, lo+len)^3 or a non-finite input; outputs are unspecified then */
+    VFMM_ENOMEM = -3,  /* device allocation failed */
+    VFMM_ECUDA = -4,   /* CUDA runtime error; message in vfmm_last_error_message */
+    VFMM_ENCCL = -5,   /* NCCL error (distributed contexts) */
+    VFMM_ESTATE = -6   /* call not valid in this state (e.g. debug query before evaluate) */
+} vfmm_status;
+
+/* Stretching contraction of Eq. (8) (reading R2 in DESIGN.md). */
+typedef enum {
+    VFMM_STRETCH_CLASSICAL = 0, /* (gamma_i . grad) u   -- Eq. (2)'s omega . grad u, default */
+    VFMM_STRETCH_TRANSPOSE = 1  /* (grad u)^T gamma_i */
+} vfmm_scheme;
+
+/* What vfmm_evaluate computes.  DIRECT / NEAR_ONLY / FAR_ONLY exist for tests. */
+typedef enum {
+    VFMM_MODE_FMM = 0,       /* near (P2P over 27 leaves) + far (expansions)               */
+    VFMM_MODE_DIRECT = 1,    /* all-pairs exact sum over the image cube (O(N^2 27^L), tests) */
+    VFMM_MODE_NEAR_ONLY = 2, /* only the P2P part of MODE_FMM                               */
+    VFMM_MODE_FAR_ONLY = 3   /* only the expansion part of MODE_FMM                          */
+} vfmm_mode;
+
+typedef struct {
+    int32_t p;            /* expansion order: degrees n = 0..p, (p+1)^2 coefficients per
+                             component (PAPER.md:123 Eq. 10; paper default p = 10, :163)       */
+    int32_t depth;        /* uniform octree depth L >= 1: 8^L leaves ("number of
+                             levels"); 0 = auto (about 64 particles per leaf)                  */
+    int32_t image_levels; /* 0 = free space; k >= 1: image cube {-m..m}^3, m = (3^k - 1)/2;
+                             k = 3 gives the paper's 27^3 boxes           */
+    int32_t scheme;       /* vfmm_scheme                                                       */
+    int32_t mode;         /* vfmm_mode                                                         */
+    float sigma;          /* Gaussian core radius sigma > 0, uniform (Eqs. 4-6)                */
+    float box_lo;         /* box is [box_lo, box_lo + box_len)^3, half-open; default -pi       */
+    float box_len;        /* default (float)(2 pi) ([-pi, pi]^3)                 */
+} vfmm_params;
+
+typedef struct {
+    double ms_total, ms_keys, ms_sort, ms_tree, ms_p2m, ms_m2m, ms_m2l, ms_l2l, ms_l2p, ms_p2p;
+    int64_t n_p2p_pairs;  /* ordered near-field pairs evaluated (incl. self pairs)        */
+    int64_t n_m2l;        /* M2L translations (all levels, incl. periodic far images)      */
+    int64_t n_m2m, n_l2l; /* child-parent translations                                     */
+    int32_t depth_used;
+    int32_t n_kernel_launches; /* kernels launched by the last evaluate                  */
+} vfmm_stats;
+
+/* ABI version this library was built with (VFMM_ABI_VERSION). */
+int32_t vfmm_abi_version(void);
+
+/* Fill *prm with defaults: p = 10, depth = 0 (auto), image_levels = 3, classical scheme,
+   FMM mode, sigma = 2 pi / 256, box = [(float)-pi, (float)-pi + (float)(2 pi)). */
+void vfmm_params_default(vfmm_params* prm);
+
+/* Create a context on CUDA device `device`.  Validates *prm (VFMM_EINVAL, synchronous),
+   builds the translation operators once in double precision on the host and uploads them.
+   *ctx is set to NULL on failure. */
+vfmm_status vfmm_create(vfmm_ctx** ctx, const vfmm_params* prm, int device);
+
+/* Evaluate velocity and stretching for n particles.  Asynchronous on `cuda_stream`
+   (a cudaStream_t; NULL = legacy default stream).
+     pos    device, 3 x n float32, read-only: positions, already wrapped into the box
+     gamma  device, 3 x n float32, read-only: vortex strengths gamma_j (Eq. 3)
+     vel    device, 3 x n float32, written:   u_i in input order (Eq. 5)
+     dgamma device, 3 x n float32, written:   dgamma_i/dt in input order (Eq. 8)
+   Outputs are fully overwritten and must not alias inputs or each other.  The workspace
+   grows on the first call with a larger n; steady state performs no allocation.
+   Parameter errors return synchronously; input-domain errors are sticky on the device and
+   reported by vfmm_sync_status(). */
+vfmm_status vfmm_evaluate(vfmm_ctx* ctx, int64_t n, const float* pos, const float* gamma,
+                          float* vel, float* dgamma, void* cuda_stream);
+
+/* Same as vfmm_evaluate but every buffer is HOST memory (pinned or pageable): copies in,
+   evaluates on the context's internal stream, copies out, synchronizes. */
+vfmm_status vfmm_evaluate_host(vfmm_ctx* ctx, int64_t n, const float* pos_h,
+                               const float* gamma_h, float* vel_h, float* dgamma_h);
+
+/* Synchronize the last evaluate's stream; return VFMM_EDOMAIN if the device flagged bad
+   input (and clear the flag), else VFMM_OK or a CUDA error. */
+vfmm_status vfmm_sync_status(vfmm_ctx* ctx);
+
+/* Per-phase timings (CUDA events) and counters of the last evaluate; synchronizes. */
+vfmm_status vfmm_get_stats(vfmm_ctx* ctx, vfmm_stats* out);
+
+/* Change p / depth / image_levels / scheme / mode / sigma / box of an existing context
+   (rebuilds operator tables if p changed).  Synchronous. */
+vfmm_status vfmm_set_params(vfmm_ctx* ctx, const vfmm_params* prm);
+
+/* Tree of the last evaluate, copied to HOST buffers (synchronizes):
+   keys_sorted, perm: n entries (uint32); leaf_start: 8^depth + 1 entries (int32).
+   perm[k] = input index of the k-th particle in Morton order (stable sort);
+   leaf_start[c] = number of keys < c.  Any pointer may be NULL. */
+vfmm_status vfmm_debug_tree(vfmm_ctx* ctx, uint32_t* keys_sorted, uint32_t* perm,
+                            int32_t* leaf_start);
+
+/* Expansion coefficients of the last FMM evaluate at tree level `level` (0..depth),
+   copied to HOST (synchronizes).  kind 0 = multipole, 1 = local.  Layout:
+   [cell (Morton index at that level)][component x,y,z][(p+1)^2] float32, packed real form
+   of DESIGN.md "Expansion convention" (index n^2 for Re(n,0); n^2+2m-1, n^2+2m for
+   Re, Im of (n, m>0)), normalised by the cell width a_l: multipole / a^n, local * a^(n+1).
+   `out` must hold 8^level * 3 * (p+1)^2 floats. */
+vfmm_status vfmm_debug_expansions(vfmm_ctx* ctx, int kind, int level, float* out);
+
+/* Human-readable status name, and the last detailed error message of a context. */
+const char* vfmm_strerror(vfmm_status s);
+const char* vfmm_last_error_message(const vfmm_ctx* ctx);
+
+/* Release the context and everything it owns.  NULL is a no-op. */
+void vfmm_destroy(vfmm_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VFMM_H */

@@ -1,0 +1,235 @@
+"""B200-native periodic vortex FMM (Yokota & Barba, arXiv:1110.2921) -- Python binding.
+
+Thin ctypes marshalling over the C ABI in ``include/vfmm.h`` (``lib/libvfmm.so``, built
+from ``csrc/`` for sm_100a).  Every step of the hot path runs in the CUDA kernels of that
+library; this module only passes device pointers, sizes and the current CUDA stream.
+PyTorch is used for device memory and streams only.  There is no CPU fallback: if the
+library is missing, importing the binding's compute entry points raises.
+
+    ev = Evaluator(p=10, image_levels=3, sigma=h)
+    vel, dgamma = ev.evaluate(pos, gamma)      # (3, N) float32 CUDA tensors, input order
+
+Names follow the paper: positions x, vortex strengths gamma (Eq. 3), core
+radius sigma (Eq. 4), velocity u (Eq. 5), stretching dgamma/dt (Eq. 8), expansion order p
+(Eq. 10), periodic images.
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libvfmm.so")
+HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "vfmm.h")
+
+VFMM_OK, VFMM_EINVAL, VFMM_EDOMAIN, VFMM_ENOMEM, VFMM_ECUDA, VFMM_ENCCL, VFMM_ESTATE = \
+    0, -1, -2, -3, -4, -5, -6
+MODE_FMM, MODE_DIRECT, MODE_NEAR_ONLY, MODE_FAR_ONLY = 0, 1, 2, 3
+STRETCH_CLASSICAL, STRETCH_TRANSPOSE = 0, 1
+
+
+class VfmmError(RuntimeError):
+    def __init__(self, status: int, msg: str = ""):
+        self.status = status
+        super().__init__(f"vfmm status {status}: {msg}")
+
+
+class c_params(ctypes.Structure):
+    _fields_ = [("p", ctypes.c_int32), ("depth", ctypes.c_int32),
+                ("image_levels", ctypes.c_int32), ("scheme", ctypes.c_int32),
+                ("mode", ctypes.c_int32), ("sigma", ctypes.c_float),
+                ("box_lo", ctypes.c_float), ("box_len", ctypes.c_float)]
+
+
+class c_stats(ctypes.Structure):
+    _fields_ = [(k, ctypes.c_double) for k in
+                ("ms_total", "ms_keys", "ms_sort", "ms_tree", "ms_p2m", "ms_m2m", "ms_m2l",
+                 "ms_l2l", "ms_l2p", "ms_p2p")] + \
+               [(k, ctypes.c_int64) for k in ("n_p2p_pairs", "n_m2l", "n_m2m", "n_l2l")] + \
+               [("depth_used", ctypes.c_int32), ("n_kernel_launches", ctypes.c_int32)]
+
+
+_LIB = None
+
+EXPORTS = ["vfmm_abi_version", "vfmm_params_default", "vfmm_create", "vfmm_evaluate",
+           "vfmm_evaluate_host", "vfmm_sync_status", "vfmm_get_stats", "vfmm_set_params",
+           "vfmm_debug_tree", "vfmm_debug_expansions", "vfmm_strerror",
+           "vfmm_last_error_message", "vfmm_destroy"]
+
+
+def load_library(path: str = LIB_PATH):
+    """Load libvfmm.so (raises OSError if it is missing -- there is no fallback)."""
+    global _LIB
+    if _LIB is not None:
+        return _LIB
+    if not os.path.exists(path):
+        raise OSError(f"libvfmm.so not built: {path} (run __graft_entry__.build())")
+    L = ctypes.CDLL(path)
+    vp, i64, i32 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+    L.vfmm_abi_version.restype = ctypes.c_int32
+    L.vfmm_params_default.argtypes = [ctypes.POINTER(c_params)]
+    L.vfmm_create.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(c_params), i32]
+    L.vfmm_evaluate.argtypes = [vp, i64, vp, vp, vp, vp, vp]
+    L.vfmm_evaluate_host.argtypes = [vp, i64, vp, vp, vp, vp]
+    L.vfmm_sync_status.argtypes = [vp]
+    L.vfmm_get_stats.argtypes = [vp, ctypes.POINTER(c_stats)]
+    L.vfmm_set_params.argtypes = [vp, ctypes.POINTER(c_params)]
+    L.vfmm_debug_tree.argtypes = [vp, vp, vp, vp]
+    L.vfmm_debug_expansions.argtypes = [vp, i32, i32, vp]
+    L.vfmm_strerror.argtypes = [i32]
+    L.vfmm_strerror.restype = ctypes.c_char_p
+    L.vfmm_last_error_message.argtypes = [vp]
+    L.vfmm_last_error_message.restype = ctypes.c_char_p
+    L.vfmm_destroy.argtypes = [vp]
+    L.vfmm_destroy.restype = None
+    for f in ("vfmm_create", "vfmm_evaluate", "vfmm_evaluate_host", "vfmm_sync_status",
+              "vfmm_get_stats", "vfmm_set_params", "vfmm_debug_tree", "vfmm_debug_expansions"):
+        getattr(L, f).restype = ctypes.c_int
+    _LIB = L
+    return L
+
+
+@dataclass
+class Params:
+    p: int = 10
+    depth: int = 0
+    image_levels: int = 3
+    scheme: int = STRETCH_CLASSICAL
+    mode: int = MODE_FMM
+    sigma: float = 2.0 * math.pi / 256.0
+    box_lo: float = float(np.float32(-math.pi))
+    box_len: float = float(np.float32(2.0 * math.pi))
+
+    def to_c(self) -> c_params:
+        return c_params(self.p, self.depth, self.image_levels, self.scheme, self.mode,
+                        self.sigma, self.box_lo, self.box_len)
+
+
+def _check(L, ctx, st):
+    if st != VFMM_OK:
+        msg = L.vfmm_strerror(st).decode()
+        if ctx:
+            extra = L.vfmm_last_error_message(ctx)
+            if extra:
+                msg += " -- " + extra.decode()
+        raise VfmmError(st, msg)
+
+
+class Evaluator:
+    """One vfmm context on one CUDA device (not thread-safe)."""
+
+    def __init__(self, device: int | None = None, **kw):
+        import torch
+
+        self._L = load_library()
+        self.params = Params(**kw)
+        self.device = torch.cuda.current_device() if device is None else int(device)
+        self._ctx = ctypes.c_void_p()
+        prm = self.params.to_c()
+        _check(self._L, None, self._L.vfmm_create(ctypes.byref(self._ctx), ctypes.byref(prm),
+                                                   self.device))
+        self._n = 0
+
+    # -- parameters -------------------------------------------------------------------
+    def set_params(self, **kw):
+        for k, v in kw.items():
+            setattr(self.params, k, v)
+        prm = self.params.to_c()
+        _check(self._L, self._ctx, self._L.vfmm_set_params(self._ctx, ctypes.byref(prm)))
+
+    # -- evaluation ---------------------------------------------------------------------
+    def evaluate_into(self, pos, gamma, vel, dgamma, stream=None):
+        """pos, gamma, vel, dgamma: contiguous float32 CUDA tensors of shape (3, N)."""
+        import torch
+
+        for t in (pos, gamma, vel, dgamma):
+            if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()
+                    and t.dim() == 2 and t.shape[0] == 3):
+                raise ValueError("expected contiguous float32 CUDA tensors of shape (3, N)")
+        n = pos.shape[1]
+        if stream is None:
+            stream = torch.cuda.current_stream(pos.device)
+        _check(self._L, self._ctx, self._L.vfmm_evaluate(
+            self._ctx, n, pos.data_ptr(), gamma.data_ptr(), vel.data_ptr(), dgamma.data_ptr(),
+            ctypes.c_void_p(stream.cuda_stream)))
+        self._n = n
+        return vel, dgamma
+
+    def evaluate(self, pos, gamma, stream=None):
+        import torch
+
+        vel = torch.empty_like(pos)
+        dg = torch.empty_like(pos)
+        return self.evaluate_into(pos, gamma, vel, dg, stream)
+
+    def evaluate_host(self, pos, gamma):
+        """Host (numpy) in/out: H2D copy, evaluate, D2H copy inside the library."""
+        pos = np.ascontiguousarray(pos, np.float32)
+        gamma = np.ascontiguousarray(gamma, np.float32)
+        n = pos.shape[1]
+        vel = np.empty_like(pos)
+        dg = np.empty_like(pos)
+        _check(self._L, self._ctx, self._L.vfmm_evaluate_host(
+            self._ctx, n, pos.ctypes.data, gamma.ctypes.data, vel.ctypes.data, dg.ctypes.data))
+        self._n = n
+        return vel, dg
+
+    def evaluate_host_ptr(self, n, pos_ptr, gamma_ptr, vel_ptr, dg_ptr):
+        _check(self._L, self._ctx, self._L.vfmm_evaluate_host(
+            self._ctx, n, pos_ptr, gamma_ptr, vel_ptr, dg_ptr))
+
+    def sync_status(self):
+        _check(self._L, self._ctx, self._L.vfmm_sync_status(self._ctx))
+
+    def stats(self) -> dict:
+        s = c_stats()
+        _check(self._L, self._ctx, self._L.vfmm_get_stats(self._ctx, ctypes.byref(s)))
+        return {k: getattr(s, k) for k, _ in c_stats._fields_}
+
+    # -- debug --------------------------------------------------------------------------
+    def debug_tree(self, depth: int):
+        n = self._n
+        keys = np.zeros(n, np.uint32)
+        perm = np.zeros(n, np.uint32)
+        ls = np.zeros((1 << (3 * depth)) + 1, np.int32)
+        _check(self._L, self._ctx, self._L.vfmm_debug_tree(
+            self._ctx, keys.ctypes.data, perm.ctypes.data, ls.ctypes.data))
+        return keys, perm, ls
+
+    def debug_expansions(self, kind: int, level: int):
+        nc = (self.params.p + 1) ** 2
+        out = np.zeros((1 << (3 * level), 3, nc), np.float32)
+        _check(self._L, self._ctx, self._L.vfmm_debug_expansions(self._ctx, kind, level,
+                                                                  out.ctypes.data))
+        return out
+
+    def close(self):
+        if self._ctx:
+            self._L.vfmm_destroy(self._ctx)
+            self._ctx = ctypes.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def evaluate(pos, gamma, sigma, p=10, depth=0, image_levels=3, scheme=0, mode=MODE_FMM,
+             box_lo=None, box_len=None):
+    """One-shot convenience wrapper around Evaluator."""
+    kw = dict(p=p, depth=depth, image_levels=image_levels, scheme=scheme, mode=mode,
+              sigma=float(sigma))
+    if box_lo is not None:
+        kw["box_lo"] = float(box_lo)
+    if box_len is not None:
+        kw["box_len"] = float(box_len)
+    ev = Evaluator(**kw)
+    try:
+        return ev.evaluate(pos, gamma)
+    finally:
+        ev.close()

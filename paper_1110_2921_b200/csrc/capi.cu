@@ -1,0 +1,513 @@
+// capi.cu -- the C ABI of include/vfmm.h: context, workspace, and the evaluate pipeline
+//   keys -> radix sort -> leaf ranges -> gather -> P2M -> M2M -> periodic -> (L2L, M2L)
+//   per level -> P2P -> L2P + combine + un-permute
+// (section 3.1; the step list is DESIGN.md "Hot path").  Every step is a kernel
+// on the caller's stream; the host only validates parameters and enqueues.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "vfmm_internal.h"
+
+using namespace vfmm;
+
+struct vfmm_ctx {
+    vfmm_params prm{};
+    int device = 0;
+    std::string err;
+    // operators
+    int ops_p = -1, ops_levels = -1;
+    HostOps hops;
+    float *d_m2m = nullptr, *d_l2l = nullptr, *d_m2l = nullptr, *d_per = nullptr;
+    int* d_slots = nullptr;  // [8][189]
+    // workspace
+    int64_t cap_n = 0;
+    int cap_depth = -1, cap_p = -1;
+    uint32_t *keys[2] = {nullptr, nullptr}, *vals[2] = {nullptr, nullptr};
+    void* radix_tmp = nullptr;
+    size_t radix_tmp_bytes = 0;
+    float *sorted6 = nullptr, *near6 = nullptr;
+    int* leaf_start = nullptr;
+    float *Mall = nullptr, *Lall = nullptr;
+    int* d_err = nullptr;
+    // host-API staging
+    int64_t cap_host_n = 0;
+    float* hbuf = nullptr;  // 12 x n
+    cudaStream_t own_stream = nullptr;
+    // last evaluate
+    cudaStream_t last_stream = nullptr;
+    uint32_t *keys_sorted = nullptr, *perm = nullptr;
+    int64_t last_n = 0;
+    int last_depth = 0;
+    bool have_tree = false, have_exp = false;
+    vfmm_stats stats{};
+    cudaEvent_t ev[8] = {};
+};
+
+namespace {
+
+vfmm_status cuda_fail(vfmm_ctx* c, cudaError_t e, const char* where) {
+    if (c) c->err = std::string(where) + ": " + cudaGetErrorString(e);
+    return e == cudaErrorMemoryAllocation ? VFMM_ENOMEM : VFMM_ECUDA;
+}
+
+#define CK(call, where)                                    \
+    do {                                                   \
+        cudaError_t e_ = (call);                           \
+        if (e_ != cudaSuccess) return cuda_fail(c, e_, where); \
+    } while (0)
+
+bool finite_pos(float x) { return std::isfinite(x) && x > 0.f; }
+
+vfmm_status validate(const vfmm_params* p) {
+    if (!p) return VFMM_EINVAL;
+    if (p->p < 1 || p->p > VFMM_PMAX) return VFMM_EINVAL;
+    if (p->depth < 0 || p->depth > 10) return VFMM_EINVAL;
+    if (p->image_levels < 0 || p->image_levels > 6) return VFMM_EINVAL;
+    if (p->scheme != 0 && p->scheme != 1) return VFMM_EINVAL;
+    if (p->mode < 0 || p->mode > 3) return VFMM_EINVAL;
+    if (!finite_pos(p->sigma) || !finite_pos(p->box_len) || !std::isfinite(p->box_lo))
+        return VFMM_EINVAL;
+    return VFMM_OK;
+}
+
+int auto_depth(const vfmm_params& p, int64_t n) {
+    int L = (int)std::lround(std::log((double)n / 64.0) / std::log(8.0));
+    if (L < 1) L = 1;
+    if (L > 10) L = 10;
+    // far field omits the cutoff: keep the leaf width >= 4 sigma (reading R3)
+    while (L > 1 && (double)p.box_len / (double)(1 << L) < 4.0 * (double)p.sigma * (1.0 - 1e-6))
+        --L;
+    return L;
+}
+
+template <class T>
+void dfree(T*& p) {
+    if (p) cudaFree((void*)p);
+    p = nullptr;
+}
+
+vfmm_status ensure_ops(vfmm_ctx* c) {
+    if (c->ops_p == c->prm.p && c->ops_levels == c->prm.image_levels) return VFMM_OK;
+    build_host_ops(c->prm.p, c->prm.image_levels, &c->hops);
+    dfree(c->d_m2m);
+    dfree(c->d_l2l);
+    dfree(c->d_m2l);
+    dfree(c->d_per);
+    auto up = [&](const std::vector<float>& h, float** d) -> cudaError_t {
+        cudaError_t e = cudaMalloc((void**)d, h.size() * sizeof(float));
+        if (e != cudaSuccess) return e;
+        return cudaMemcpy(*d, h.data(), h.size() * sizeof(float), cudaMemcpyHostToDevice);
+    };
+    CK(up(c->hops.m2m, &c->d_m2m), "upload m2m");
+    CK(up(c->hops.l2l, &c->d_l2l), "upload l2l");
+    CK(up(c->hops.m2l, &c->d_m2l), "upload m2l");
+    CK(up(c->hops.per, &c->d_per), "upload periodic");
+    if (!c->d_slots) {
+        // interaction list per parity: o_a in {-2-b_a .. 3-b_a}, minus |o|inf <= 1 (189 cells)
+        std::vector<int> slots;
+        for (int par = 0; par < 8; ++par) {
+            const int bx = par & 1, by = (par >> 1) & 1, bz = (par >> 2) & 1;
+            int cnt = 0;
+            for (int ox = -2 - bx; ox <= 3 - bx; ++ox)
+                for (int oy = -2 - by; oy <= 3 - by; ++oy)
+                    for (int oz = -2 - bz; oz <= 3 - bz; ++oz) {
+                        if (std::abs(ox) <= 1 && std::abs(oy) <= 1 && std::abs(oz) <= 1) continue;
+                        slots.push_back(m2l_slot(ox, oy, oz));
+                        ++cnt;
+                    }
+            if (cnt != 189) return VFMM_EINVAL;
+        }
+        CK(cudaMalloc((void**)&c->d_slots, slots.size() * sizeof(int)), "alloc slots");
+        CK(cudaMemcpy(c->d_slots, slots.data(), slots.size() * sizeof(int),
+                      cudaMemcpyHostToDevice),
+           "upload slots");
+    }
+    c->ops_p = c->prm.p;
+    c->ops_levels = c->prm.image_levels;
+    return VFMM_OK;
+}
+
+vfmm_status ensure_ws(vfmm_ctx* c, int64_t n, int depth) {
+    if (n > c->cap_n) {
+        for (int b = 0; b < 2; ++b) {
+            dfree(c->keys[b]);
+            dfree(c->vals[b]);
+        }
+        dfree(c->sorted6);
+        dfree(c->near6);
+        dfree(c->radix_tmp);
+        c->cap_n = 0;
+        for (int b = 0; b < 2; ++b) {
+            CK(cudaMalloc((void**)&c->keys[b], n * sizeof(uint32_t)), "alloc keys");
+            CK(cudaMalloc((void**)&c->vals[b], n * sizeof(uint32_t)), "alloc vals");
+        }
+        CK(cudaMalloc((void**)&c->sorted6, 6 * n * sizeof(float)), "alloc sorted");
+        CK(cudaMalloc((void**)&c->near6, 6 * n * sizeof(float)), "alloc near");
+        c->radix_tmp_bytes = radix_temp_bytes(n);
+        CK(cudaMalloc(&c->radix_tmp, c->radix_tmp_bytes), "alloc radix");
+        c->cap_n = n;
+    }
+    if (depth != c->cap_depth || c->prm.p != c->cap_p) {
+        dfree(c->leaf_start);
+        dfree(c->Mall);
+        dfree(c->Lall);
+        c->cap_depth = -1;
+        const int64_t nleaf = (int64_t)1 << (3 * depth);
+        const int64_t cells = level_offset(depth + 1);
+        const int nc = ncoef(c->prm.p);
+        CK(cudaMalloc((void**)&c->leaf_start, (nleaf + 1) * sizeof(int)), "alloc leaf_start");
+        CK(cudaMalloc((void**)&c->Mall, cells * 3 * nc * sizeof(float)), "alloc M");
+        CK(cudaMalloc((void**)&c->Lall, cells * 3 * nc * sizeof(float)), "alloc L");
+        c->cap_depth = depth;
+        c->cap_p = c->prm.p;
+    }
+    return VFMM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t vfmm_abi_version(void) { return VFMM_ABI_VERSION; }
+
+void vfmm_params_default(vfmm_params* prm) {
+    if (!prm) return;
+    prm->p = 10;
+    prm->depth = 0;
+    prm->image_levels = 3;
+    prm->scheme = VFMM_STRETCH_CLASSICAL;
+    prm->mode = VFMM_MODE_FMM;
+    prm->sigma = (float)(2.0 * M_PI / 256.0);
+    prm->box_lo = (float)(-M_PI);
+    prm->box_len = (float)(2.0 * M_PI);
+}
+
+const char* vfmm_strerror(vfmm_status s) {
+    switch (s) {
+        case VFMM_OK: return "VFMM_OK";
+        case VFMM_EINVAL: return "VFMM_EINVAL: invalid parameter";
+        case VFMM_EDOMAIN: return "VFMM_EDOMAIN: position outside the box or non-finite input";
+        case VFMM_ENOMEM: return "VFMM_ENOMEM: device allocation failed";
+        case VFMM_ECUDA: return "VFMM_ECUDA: CUDA error";
+        case VFMM_ENCCL: return "VFMM_ENCCL: NCCL error";
+        case VFMM_ESTATE: return "VFMM_ESTATE: invalid state";
+    }
+    return "unknown vfmm_status";
+}
+
+const char* vfmm_last_error_message(const vfmm_ctx* c) { return c ? c->err.c_str() : ""; }
+
+vfmm_status vfmm_create(vfmm_ctx** out, const vfmm_params* prm, int device) {
+    if (!out) return VFMM_EINVAL;
+    *out = nullptr;
+    vfmm_status s = validate(prm);
+    if (s != VFMM_OK) return s;
+    vfmm_ctx* c = new vfmm_ctx();
+    c->prm = *prm;
+    c->device = device;
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) {
+        delete c;
+        return VFMM_ECUDA;
+    }
+    s = ensure_ops(c);
+    if (s == VFMM_OK) {
+        cudaError_t e2 = cudaMalloc((void**)&c->d_err, sizeof(int));
+        if (e2 == cudaSuccess) e2 = cudaMemset(c->d_err, 0, sizeof(int));
+        if (e2 == cudaSuccess) e2 = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
+        for (int i = 0; i < 8 && e2 == cudaSuccess; ++i) e2 = cudaEventCreate(&c->ev[i]);
+        if (e2 != cudaSuccess) s = cuda_fail(c, e2, "create");
+    }
+    if (s != VFMM_OK) {
+        vfmm_destroy(c);
+        return s;
+    }
+    *out = c;
+    return VFMM_OK;
+}
+
+vfmm_status vfmm_set_params(vfmm_ctx* c, const vfmm_params* prm) {
+    if (!c) return VFMM_EINVAL;
+    vfmm_status s = validate(prm);
+    if (s != VFMM_OK) return s;
+    CK(cudaSetDevice(c->device), "set device");
+    if (c->last_stream) CK(cudaStreamSynchronize(c->last_stream), "sync");
+    c->prm = *prm;
+    c->have_exp = false;
+    return ensure_ops(c);
+}
+
+vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float* gamma,
+                          float* vel, float* dgamma, void* stream) {
+    if (!c || n < 1 || !pos || !gamma || !vel || !dgamma) return VFMM_EINVAL;
+    if (n > ((int64_t)1 << 31) - 1) return VFMM_EINVAL;
+    // outputs must not alias inputs or each other
+    auto overlap = [n](const void* a, const void* b) {
+        const char* x = (const char*)a;
+        const char* y = (const char*)b;
+        const size_t L = 3 * (size_t)n * sizeof(float);
+        return x < y + L && y < x + L;
+    };
+    if (overlap(vel, dgamma) || overlap(vel, pos) || overlap(vel, gamma) ||
+        overlap(dgamma, pos) || overlap(dgamma, gamma))
+        return VFMM_EINVAL;
+    CK(cudaSetDevice(c->device), "set device");
+    cudaStream_t st = (cudaStream_t)stream;
+    const vfmm_params& P = c->prm;
+    vfmm_stats& S = c->stats;
+    memset(&S, 0, sizeof(S));
+    c->last_stream = st;
+    c->last_n = n;
+    const KernelConsts kc = make_kernel_consts(P.sigma);
+    CK(cudaEventRecord(c->ev[0], st), "event");
+    if (P.mode == VFMM_MODE_DIRECT) {
+        launch_direct(pos, gamma, n, P.box_len, P.image_levels, P.scheme, kc, vel, dgamma, st);
+        CK(cudaGetLastError(), "direct kernel");
+        for (int i = 1; i < 8; ++i) CK(cudaEventRecord(c->ev[i], st), "event");
+        int m = 0;
+        for (int l = 0; l < P.image_levels; ++l) m = 3 * m + 1;
+        S.n_p2p_pairs = n * n * (int64_t)((2 * m + 1) * (2 * m + 1) * (2 * m + 1));
+        S.n_kernel_launches = 1;
+        c->have_tree = false;
+        c->have_exp = false;
+        return VFMM_OK;
+    }
+    const int depth = P.depth > 0 ? P.depth : auto_depth(P, n);
+    vfmm_status s = ensure_ws(c, n, depth);
+    if (s != VFMM_OK) return s;
+    c->last_depth = depth;
+    S.depth_used = depth;
+    Geom g{P.box_lo, P.box_len, (double)P.box_lo, (double)P.box_len, depth, P.image_levels > 0};
+    const float a = (float)((double)P.box_len / (double)(1 << depth));  // exact in float
+    int nl = 0;
+    // ---- tree ----
+    launch_keys(pos, n, g, c->keys[0], c->vals[0], c->d_err, st);
+    ++nl;
+    CK(cudaEventRecord(c->ev[1], st), "event");
+    launch_radix_sort(c->keys[0], c->vals[0], c->keys[1], c->vals[1], n, 3 * depth, c->radix_tmp,
+                      st, &c->keys_sorted, &c->perm, &nl);
+    CK(cudaEventRecord(c->ev[2], st), "event");
+    launch_leaf_ranges(c->keys_sorted, n, depth, c->leaf_start, st);
+    launch_gather(pos, gamma, c->perm, c->keys_sorted, n, g, c->sorted6, st);
+    nl += 2;
+    CK(cudaGetLastError(), "tree kernels");
+    CK(cudaEventRecord(c->ev[3], st), "event");
+    c->have_tree = true;
+    const bool use_far = P.mode == VFMM_MODE_FMM || P.mode == VFMM_MODE_FAR_ONLY;
+    const bool use_near = P.mode == VFMM_MODE_FMM || P.mode == VFMM_MODE_NEAR_ONLY;
+    const int p = P.p, nc = ncoef(p);
+    const HostOps& H = c->hops;
+    auto Mlev = [&](int l) { return c->Mall + level_offset(l) * 3 * nc; };
+    auto Llev = [&](int l) { return c->Lall + level_offset(l) * 3 * nc; };
+    // ---- upward pass ----
+    if (use_far) {
+        launch_p2m(c->sorted6, n, c->leaf_start, depth, p, 1.f / a, Mlev(depth), st);
+        ++nl;
+        for (int l = depth - 1; l >= 0; --l) {
+            launch_m2m(c->d_m2m, p, H.KP, H.NR, Mlev(l + 1), Mlev(l), l, st);
+            ++nl;
+            S.n_m2m += (int64_t)8 << (3 * l);
+        }
+        CK(cudaGetLastError(), "upward kernels");
+    }
+    CK(cudaEventRecord(c->ev[4], st), "event");
+    // ---- periodic images + downward pass ----
+    if (use_far) {
+        CK(cudaMemsetAsync(Llev(0), 0, 3 * nc * sizeof(float), st), "memset L0");
+        if (P.image_levels >= 2) {
+            launch_periodic(c->d_per, p, H.KP, H.NR, Mlev(0), Llev(0), st);
+            ++nl;
+        }
+        for (int l = 1; l <= depth; ++l) {
+            launch_l2l(c->d_l2l, p, H.KP, H.NR, Llev(l - 1), Llev(l), l, st);
+            launch_m2l(c->d_m2l, c->d_slots, p, H.KP, H.NR, Mlev(l), Llev(l), l,
+                       P.image_levels > 0, st);
+            nl += 2;
+            S.n_l2l += (int64_t)1 << (3 * l);
+            S.n_m2l += (int64_t)189 << (3 * l);
+        }
+        CK(cudaGetLastError(), "downward kernels");
+        c->have_exp = true;
+    }
+    CK(cudaEventRecord(c->ev[5], st), "event");
+    // ---- near field ----
+    if (use_near) {
+        launch_p2p(c->sorted6, n, c->leaf_start, depth, a, P.image_levels > 0, P.scheme, kc,
+                   c->near6, st);
+        ++nl;
+        CK(cudaGetLastError(), "p2p kernel");
+    }
+    CK(cudaEventRecord(c->ev[6], st), "event");
+    launch_l2p_combine(c->sorted6, c->near6, c->perm, n, c->leaf_start, depth, p, a,
+                       Llev(depth), P.scheme, use_near, use_far, vel, dgamma, st);
+    ++nl;
+    CK(cudaGetLastError(), "l2p kernel");
+    CK(cudaEventRecord(c->ev[7], st), "event");
+    S.n_kernel_launches = nl;
+    return VFMM_OK;
+}
+
+vfmm_status vfmm_evaluate_host(vfmm_ctx* c, int64_t n, const float* pos_h, const float* gamma_h,
+                               float* vel_h, float* dgamma_h) {
+    if (!c || n < 1 || !pos_h || !gamma_h || !vel_h || !dgamma_h) return VFMM_EINVAL;
+    CK(cudaSetDevice(c->device), "set device");
+    if (n > c->cap_host_n) {
+        dfree(c->hbuf);
+        c->cap_host_n = 0;
+        CK(cudaMalloc((void**)&c->hbuf, 12 * n * sizeof(float)), "alloc host staging");
+        c->cap_host_n = n;
+    }
+    float* dp = c->hbuf;
+    float* dg = dp + 3 * n;
+    float* dv = dg + 3 * n;
+    float* ds = dv + 3 * n;
+    cudaStream_t st = c->own_stream;
+    CK(cudaMemcpyAsync(dp, pos_h, 3 * n * sizeof(float), cudaMemcpyHostToDevice, st), "h2d");
+    CK(cudaMemcpyAsync(dg, gamma_h, 3 * n * sizeof(float), cudaMemcpyHostToDevice, st), "h2d");
+    vfmm_status s = vfmm_evaluate(c, n, dp, dg, dv, ds, st);
+    if (s != VFMM_OK) return s;
+    CK(cudaMemcpyAsync(vel_h, dv, 3 * n * sizeof(float), cudaMemcpyDeviceToHost, st), "d2h");
+    CK(cudaMemcpyAsync(dgamma_h, ds, 3 * n * sizeof(float), cudaMemcpyDeviceToHost, st), "d2h");
+    return vfmm_sync_status(c);
+}
+
+vfmm_status vfmm_sync_status(vfmm_ctx* c) {
+    if (!c) return VFMM_EINVAL;
+    CK(cudaSetDevice(c->device), "set device");
+    CK(cudaStreamSynchronize(c->last_stream), "sync");
+    int flag = 0;
+    CK(cudaMemcpy(&flag, c->d_err, sizeof(int), cudaMemcpyDeviceToHost), "read flag");
+    if (flag) {
+        CK(cudaMemset(c->d_err, 0, sizeof(int)), "clear flag");
+        c->err = "input position outside [lo, lo+len)^3 or non-finite";
+        return VFMM_EDOMAIN;
+    }
+    return VFMM_OK;
+}
+
+vfmm_status vfmm_get_stats(vfmm_ctx* c, vfmm_stats* out) {
+    if (!c || !out) return VFMM_EINVAL;
+    CK(cudaSetDevice(c->device), "set device");
+    CK(cudaStreamSynchronize(c->last_stream), "sync");
+    vfmm_stats& S = c->stats;
+    float ms[8] = {0};
+    for (int i = 1; i < 8; ++i) CK(cudaEventElapsedTime(&ms[i], c->ev[i - 1], c->ev[i]), "elapsed");
+    S.ms_keys = ms[1];
+    S.ms_sort = ms[2];
+    S.ms_tree = ms[3];
+    S.ms_p2m = 0;
+    S.ms_m2m = ms[4];  // P2M + M2M
+    S.ms_m2l = ms[5];  // periodic + L2L + M2L
+    S.ms_l2l = 0;
+    S.ms_p2p = ms[6];
+    S.ms_l2p = ms[7];
+    float tot = 0;
+    CK(cudaEventElapsedTime(&tot, c->ev[0], c->ev[7]), "elapsed");
+    S.ms_total = tot;
+    if (c->prm.mode != VFMM_MODE_DIRECT && (c->prm.mode != VFMM_MODE_FAR_ONLY)) {
+        // near-field pair count: sum over leaves of n_t * (sum of 27 neighbour counts)
+        const int depth = c->last_depth;
+        const int64_t nleaf = (int64_t)1 << (3 * depth);
+        std::vector<int> ls(nleaf + 1);
+        CK(cudaMemcpy(ls.data(), c->leaf_start, (nleaf + 1) * sizeof(int), cudaMemcpyDeviceToHost),
+           "copy leaf_start");
+        const int side = 1 << depth;
+        auto enc = [&](int x, int y, int z) {
+            int64_t k = 0;
+            for (int b = 0; b < depth; ++b)
+                k |= ((int64_t)((x >> b) & 1) << (3 * b)) | ((int64_t)((y >> b) & 1) << (3 * b + 1)) |
+                     ((int64_t)((z >> b) & 1) << (3 * b + 2));
+            return k;
+        };
+        int64_t pairs = 0;
+        const bool per = c->prm.image_levels > 0;
+        for (int x = 0; x < side; ++x)
+            for (int y = 0; y < side; ++y)
+                for (int z = 0; z < side; ++z) {
+                    const int64_t t = enc(x, y, z);
+                    const int64_t nt = ls[t + 1] - ls[t];
+                    if (!nt) continue;
+                    int64_t ns = 0;
+                    for (int o = 0; o < 27; ++o) {
+                        int nx = x + o % 3 - 1, ny = y + (o / 3) % 3 - 1, nz = z + o / 9 - 1;
+                        if (!per && (nx < 0 || ny < 0 || nz < 0 || nx >= side || ny >= side ||
+                                     nz >= side))
+                            continue;
+                        nx &= side - 1;
+                        ny &= side - 1;
+                        nz &= side - 1;
+                        const int64_t sc = enc(nx, ny, nz);
+                        ns += ls[sc + 1] - ls[sc];
+                    }
+                    pairs += nt * ns;
+                }
+        S.n_p2p_pairs = pairs;
+    }
+    *out = S;
+    return VFMM_OK;
+}
+
+vfmm_status vfmm_debug_tree(vfmm_ctx* c, uint32_t* keys_sorted, uint32_t* perm,
+                            int32_t* leaf_start) {
+    if (!c) return VFMM_EINVAL;
+    if (!c->have_tree) return VFMM_ESTATE;
+    CK(cudaSetDevice(c->device), "set device");
+    CK(cudaStreamSynchronize(c->last_stream), "sync");
+    const int64_t n = c->last_n;
+    if (keys_sorted)
+        CK(cudaMemcpy(keys_sorted, c->keys_sorted, n * 4, cudaMemcpyDeviceToHost), "copy keys");
+    if (perm) CK(cudaMemcpy(perm, c->perm, n * 4, cudaMemcpyDeviceToHost), "copy perm");
+    if (leaf_start)
+        CK(cudaMemcpy(leaf_start, c->leaf_start, (((int64_t)1 << (3 * c->last_depth)) + 1) * 4,
+                      cudaMemcpyDeviceToHost),
+           "copy leaf_start");
+    return VFMM_OK;
+}
+
+vfmm_status vfmm_debug_expansions(vfmm_ctx* c, int kind, int level, float* out) {
+    if (!c || !out || (kind != 0 && kind != 1)) return VFMM_EINVAL;
+    if (!c->have_exp) return VFMM_ESTATE;
+    if (level < 0 || level > c->last_depth) return VFMM_EINVAL;
+    CK(cudaSetDevice(c->device), "set device");
+    CK(cudaStreamSynchronize(c->last_stream), "sync");
+    const int nc = ncoef(c->prm.p);
+    const float* base = (kind == 0 ? c->Mall : c->Lall) + level_offset(level) * 3 * nc;
+    CK(cudaMemcpy(out, base, ((size_t)1 << (3 * level)) * 3 * nc * sizeof(float),
+                  cudaMemcpyDeviceToHost),
+       "copy expansions");
+    return VFMM_OK;
+}
+
+void vfmm_destroy(vfmm_ctx* c) {
+    if (!c) return;
+    cudaSetDevice(c->device);
+    if (c->last_stream) cudaStreamSynchronize(c->last_stream);
+    dfree(c->d_m2m);
+    dfree(c->d_l2l);
+    dfree(c->d_m2l);
+    dfree(c->d_per);
+    dfree(c->d_slots);
+    for (int b = 0; b < 2; ++b) {
+        dfree(c->keys[b]);
+        dfree(c->vals[b]);
+    }
+    dfree(c->radix_tmp);
+    dfree(c->sorted6);
+    dfree(c->near6);
+    dfree(c->leaf_start);
+    dfree(c->Mall);
+    dfree(c->Lall);
+    dfree(c->d_err);
+    dfree(c->hbuf);
+    for (int i = 0; i < 8; ++i)
+        if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+    if (c->own_stream) cudaStreamDestroy(c->own_stream);
+    delete c;
+}
+
+}  // extern "C"

@@ -1,0 +1,554 @@
+// expansions.cu -- P2M, M2M, periodic images, M2L, L2L and L2P (+ near/far combine).
+//
+// PAPER.md section 3.1: multipole (Eq. 10, PAPER.md:123) and local (Eq. 11, PAPER.md:128)
+// expansions of the three Laplace potentials phi_c = sum_j gamma_{j,c} / |x - x_j|; the far
+// velocity u = curl(phi)/4pi (Eqs. 12-13, PAPER.md:133-134) and the far stretching
+// (gamma_i . grad) u from the Hessian of the local expansions (Eqs. 14-15, PAPER.md:140-141,
+// reading R10).  The far field omits the cutoff g (PAPER.md:138).
+//
+// Coefficients are the packed real form of DESIGN.md, scaled per level (Mt = M/a^n,
+// Lt = L a^(n+1)) so every translation operator is level independent.  Per-level arrays:
+// [cell (Morton order)][component][nc], nc = (p+1)^2.
+//
+// M2M, L2L and M2L all run through one batched "gather GEMM" on the FP32 pipe:
+//   C[nc x (3*32 cols)] (+)= sum_ops T_op[nc x nc] * B_op[nc x (3*32)],
+// 32 target cells x 3 strength components per block; every target in a block shares the
+// same operator sequence (same parity for M2L / L2L), B_op gathers the source cell of each
+// target for operator op.
+#include <cuda_runtime.h>
+
+#include "vfmm_internal.h"
+
+namespace vfmm {
+
+namespace {
+
+__device__ __forceinline__ uint32_t spread3d(uint32_t v) {
+    v &= 0x3ffu;
+    v = (v | (v << 16)) & 0x030000FFu;
+    v = (v | (v << 8)) & 0x0300F00Fu;
+    v = (v | (v << 4)) & 0x030C30C3u;
+    v = (v | (v << 2)) & 0x09249249u;
+    return v;
+}
+__device__ __forceinline__ uint32_t compact3d(uint32_t v) {
+    v &= 0x09249249u;
+    v = (v ^ (v >> 2)) & 0x030C30C3u;
+    v = (v ^ (v >> 4)) & 0x0300F00Fu;
+    v = (v ^ (v >> 8)) & 0x030000FFu;
+    v = (v ^ (v >> 16)) & 0x000003FFu;
+    return v;
+}
+
+// ---------------------------------------------------------------------------
+// P2M (Eq. 10): Mt[c][n,m] = sum_j gamma_{j,c} conj(R_n^m((x_j - centre)/a))
+// one block (64 threads) per leaf; thread j builds conj(R) of particle j in smem,
+// then threads reduce the 3 x nc outputs over particles.
+// ---------------------------------------------------------------------------
+__device__ void solid_R_packed(float x, float y, float z, int p, float* out, int stride,
+                               bool conj_) {
+    // packed real R_n^m for 0 <= m <= n <= p, written to out[k * stride]
+    const float r2 = x * x + y * y + z * z;
+    float dre = 1.f, dim = 0.f;  // R_m^m
+    for (int m = 0; m <= p; ++m) {
+        if (m > 0) {
+            const float s = -0.5f / (float)m;
+            const float nre = s * (x * dre - y * dim);
+            const float nim = s * (x * dim + y * dre);
+            dre = nre;
+            dim = nim;
+        }
+        float p2re = dre, p2im = dim, p1re = 0.f, p1im = 0.f;
+        out[pk_re(m, m) * stride] = dre;
+        if (m > 0) out[pk_im(m, m) * stride] = conj_ ? -dim : dim;
+        if (m + 1 <= p) {
+            p1re = z * dre;
+            p1im = z * dim;
+            out[pk_re(m + 1, m) * stride] = p1re;
+            if (m > 0) out[pk_im(m + 1, m) * stride] = conj_ ? -p1im : p1im;
+        }
+        for (int n = m + 2; n <= p; ++n) {
+            const float inv = 1.f / (float)((n + m) * (n - m));
+            const float a = (2.f * n - 1.f) * z;
+            const float nre = (a * p1re - r2 * p2re) * inv;
+            const float nim = (a * p1im - r2 * p2im) * inv;
+            out[pk_re(n, m) * stride] = nre;
+            if (m > 0) out[pk_im(n, m) * stride] = conj_ ? -nim : nim;
+            p2re = p1re;
+            p2im = p1im;
+            p1re = nre;
+            p1im = nim;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(64) p2m_kernel(const float* __restrict__ s6, int64_t n,
+                                                 const int* __restrict__ leaf_start, int p,
+                                                 float inv_a, float* __restrict__ M) {
+    extern __shared__ float sm[];
+    const int nc = (p + 1) * (p + 1);
+    float* Rs = sm;             // [nc][65]
+    float* gs = sm + nc * 65;   // [3][64]
+    const int leaf = blockIdx.x;
+    const int s = leaf_start[leaf], e = leaf_start[leaf + 1];
+    float acc[3 * kPMax + 12];  // outputs t, t+64, ... ; at most ceil(3*289/64) = 14
+    const int nout = (3 * nc + 63) / 64;
+    for (int i = 0; i < nout; ++i) acc[i] = 0.f;
+    for (int b = s; b < e; b += 64) {
+        const int j = b + threadIdx.x;
+        const int cnt = min(64, e - b);
+        if (threadIdx.x < cnt) {
+            solid_R_packed(s6[j] * inv_a, s6[n + j] * inv_a, s6[2 * n + j] * inv_a, p,
+                           Rs + threadIdx.x, 65, true);
+            gs[threadIdx.x] = s6[3 * n + j];
+            gs[64 + threadIdx.x] = s6[4 * n + j];
+            gs[128 + threadIdx.x] = s6[5 * n + j];
+        }
+        __syncthreads();
+        for (int i = 0; i < nout; ++i) {
+            const int o = threadIdx.x + 64 * i;
+            if (o < 3 * nc) {
+                const int c = o / nc, k = o - c * nc;
+                float a = acc[i];
+                for (int q = 0; q < cnt; ++q) a = fmaf(gs[c * 64 + q], Rs[k * 65 + q], a);
+                acc[i] = a;
+            }
+        }
+        __syncthreads();
+    }
+    float* out = M + (int64_t)leaf * 3 * nc;
+    for (int i = 0; i < nout; ++i) {
+        const int o = threadIdx.x + 64 * i;
+        if (o < 3 * nc) out[o] = acc[i];
+    }
+}
+
+// ---------------------------------------------------------------------------
+// batched gather GEMM for M2M / L2L / M2L
+// ---------------------------------------------------------------------------
+constexpr int TCELLS = 32;
+constexpr int TCOLS = 3 * TCELLS;  // 96
+constexpr int TROWS = 128;
+constexpr int KC = 16;
+constexpr int BSTR = TCOLS + 4;    // smem row stride of B
+constexpr int MAXOPS = 189;
+
+enum { OP_M2M = 0, OP_L2L = 1, OP_M2L = 2 };
+constexpr size_t TRANSLATE_SMEM =
+    sizeof(float) * (2 * KC * TROWS + 2 * KC * BSTR) + sizeof(int) * (MAXOPS * TCELLS + MAXOPS);
+
+// grid.x: column tiles; grid.y: row tiles (nc > 128).  256 threads: 16 x 16, each 8 rows x 6 cols.
+template <int KIND>
+__global__ void __launch_bounds__(256) translate_kernel(
+    const float* __restrict__ mats, const int* __restrict__ slots, int p, int KP, int NR,
+    const float* __restrict__ src, float* __restrict__ dst, int level, int periodic) {
+    extern __shared__ float4 dsm4[];
+    float (*As)[KC][TROWS] = reinterpret_cast<float (*)[KC][TROWS]>(dsm4);
+    float (*Bs)[KC][BSTR] = reinterpret_cast<float (*)[KC][BSTR]>(
+        reinterpret_cast<float*>(dsm4) + 2 * KC * TROWS);
+    int (*srcidx)[TCELLS] = reinterpret_cast<int (*)[TCELLS]>(
+        reinterpret_cast<float*>(dsm4) + 2 * KC * TROWS + 2 * KC * BSTR);
+    int* opmat = &srcidx[MAXOPS][0];
+    const int nc = (p + 1) * (p + 1);
+    const int tid = threadIdx.x;
+    const int ty = tid >> 4, tx = tid & 15;
+    const int row0 = blockIdx.y * TROWS;
+
+    // ---- which target cells / ops ----
+    int nops, ncell_tile, parity = 0, tile0;
+    const int64_t ncells = (int64_t)1 << (3 * level);
+    if (KIND == OP_M2M) {
+        nops = 8;
+        tile0 = blockIdx.x * TCELLS;  // parents at `level`
+        ncell_tile = (int)min((int64_t)TCELLS, ncells - tile0);
+    } else {
+        const int64_t nparents = ncells >> 3;
+        const int64_t ntiles = (nparents + TCELLS - 1) / TCELLS;
+        parity = (int)(blockIdx.x / ntiles);
+        tile0 = (int)(blockIdx.x % ntiles) * TCELLS;  // parent index of first target
+        ncell_tile = (int)min((int64_t)TCELLS, nparents - tile0);
+        nops = KIND == OP_L2L ? 1 : MAXOPS;
+    }
+    auto target_cell = [&](int j) -> int64_t {
+        return KIND == OP_M2M ? (int64_t)(tile0 + j) : ((int64_t)(tile0 + j) << 3) + parity;
+    };
+    // ---- source tables ----
+    for (int i = tid; i < nops * TCELLS; i += 256) {
+        const int op = i / TCELLS, j = i - op * TCELLS;
+        int sidx = -1;
+        if (j < ncell_tile) {
+            const int64_t t = target_cell(j);
+            if (KIND == OP_M2M) {
+                sidx = (int)((t << 3) + op);
+            } else if (KIND == OP_L2L) {
+                sidx = (int)(t >> 3);
+            } else {
+                const int slot = slots[parity * MAXOPS + op];
+                const int oz = slot % 7 - 3, oy = (slot / 7) % 7 - 3, ox = slot / 49 - 3;
+                const uint32_t tt = (uint32_t)t;
+                const int side = 1 << level;
+                int sx = (int)compact3d(tt) + ox, sy = (int)compact3d(tt >> 1) + oy,
+                    sz = (int)compact3d(tt >> 2) + oz;
+                const bool inside = sx >= 0 && sx < side && sy >= 0 && sy < side && sz >= 0 &&
+                                    sz < side;
+                if (periodic || inside) {
+                    sx &= side - 1;
+                    sy &= side - 1;
+                    sz &= side - 1;
+                    sidx = (int)(spread3d(sx) | (spread3d(sy) << 1) | (spread3d(sz) << 2));
+                }
+            }
+        }
+        srcidx[op][j] = sidx;
+    }
+    for (int i = tid; i < nops; i += 256) {
+        if (KIND == OP_M2M) opmat[i] = i;
+        else if (KIND == OP_L2L) opmat[i] = parity;
+        else opmat[i] = slots[parity * MAXOPS + i];
+    }
+    __syncthreads();
+
+    float acc[8][6];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 6; ++j) acc[i][j] = 0.f;
+
+    const int nkc = KP / KC;
+    const int niter = nops * nkc;
+    const size_t msz = (size_t)KP * NR;
+    // register staging for the next chunk
+    float4 ra[2];
+    float rb[6];
+    auto load_regs = [&](int it) {
+        const int op = it / nkc, kc = it - op * nkc;
+        const float* A = mats + (size_t)opmat[op] * msz + (size_t)(kc * KC) * NR + row0;
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int e = (tid + q * 256) * 4;  // 0..2047 in [KC][128]
+            const int kk = e >> 7, r = e & 127;
+            ra[q] = *reinterpret_cast<const float4*>(A + (size_t)kk * NR + r);
+        }
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+            const int e = tid + q * 256;  // 0..1535 in [col][KC]
+            const int col = e >> 4, kk = e & 15;
+            const int cell = col / 3, comp = col - cell * 3;
+            const int k = kc * KC + kk;
+            const int sidx = srcidx[op][cell];
+            rb[q] = (sidx >= 0 && k < nc) ? __ldg(src + ((int64_t)sidx * 3 + comp) * nc + k) : 0.f;
+        }
+    };
+    auto store_smem = [&](int buf) {
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+            const int e = (tid + q * 256) * 4;
+            const int kk = e >> 7, r = e & 127;
+            *reinterpret_cast<float4*>(&As[buf][kk][r]) = ra[q];
+        }
+#pragma unroll
+        for (int q = 0; q < 6; ++q) {
+            const int e = tid + q * 256;
+            const int col = e >> 4, kk = e & 15;
+            Bs[buf][kk][col] = rb[q];
+        }
+    };
+    load_regs(0);
+    store_smem(0);
+    __syncthreads();
+    for (int it = 0; it < niter; ++it) {
+        const int buf = it & 1;
+        if (it + 1 < niter) load_regs(it + 1);
+#pragma unroll
+        for (int kk = 0; kk < KC; ++kk) {
+            const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 8]);
+            const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 8 + 4]);
+            const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+            float b[6];
+#pragma unroll
+            for (int j = 0; j < 6; ++j) b[j] = Bs[buf][kk][tx * 6 + j];
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+#pragma unroll
+                for (int j = 0; j < 6; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+        }
+        if (it + 1 < niter) store_smem(buf ^ 1);
+        __syncthreads();
+    }
+    // ---- epilogue ----
+#pragma unroll
+    for (int j = 0; j < 6; ++j) {
+        const int col = tx * 6 + j;
+        const int cell = col / 3, comp = col - cell * 3;
+        if (cell >= ncell_tile) continue;
+        float* out = dst + (target_cell(cell) * 3 + comp) * nc;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+            const int r = row0 + ty * 8 + i;
+            if (r < nc) {
+                if (KIND == OP_M2L) out[r] += acc[i][j];
+                else out[r] = acc[i][j];
+            }
+        }
+    }
+}
+
+// periodic far field: L0 += P M0 (3 columns); one block
+__global__ void periodic_kernel(const float* __restrict__ P, int KP, int NR, int nc,
+                                const float* __restrict__ M0, float* __restrict__ L0) {
+    for (int o = threadIdx.x; o < 3 * nc; o += blockDim.x) {
+        const int c = o / nc, r = o - c * nc;
+        float a = 0.f;
+        for (int k = 0; k < nc; ++k) a = fmaf(P[(size_t)k * NR + r], M0[c * nc + k], a);
+        L0[c * nc + r] += a;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// L2P + combine: far field from the leaf's local expansion, plus the P2P near field,
+// scattered back to input order.  One block (64 threads) per leaf.
+//   phi_c(x) = (1/a) sum Lt_c[n,m] R_n^m(z/a);  grad: 1/a^2 sum Lt dR;  hess: 1/a^3 ...
+//   u_a = eps_abc d_b phi_c / 4pi;  classical sdot_a = eps_abc g_k d_k d_b phi_c / 4pi
+//   transpose sdot_a = eps_kbc g_k d_a d_b phi_c / 4pi
+// Derivative expansions (DESIGN.md): d_z D[n,m] = L[n+1,m],
+//   d_x D[n,m] = (-L[n+1,m+1] + L[n+1,m-1])/2,  d_y D[n,m] = -i (L[n+1,m+1] + L[n+1,m-1])/2
+// ---------------------------------------------------------------------------
+struct cf {
+    float re, im;
+};
+__device__ __forceinline__ cf getc(const float* L, int n, int m) {
+    // complex coefficient (n, m) of a packed real expansion, any |m| <= n; 0 outside
+    if (m > n || -m > n || n < 0) return {0.f, 0.f};
+    if (m == 0) return {L[pk_re(n, 0)], 0.f};
+    const int am = m < 0 ? -m : m;
+    cf v{L[pk_re(n, am)], L[pk_im(n, am)]};
+    if (m < 0) {  // (-1)^m conj
+        v.im = -v.im;
+        if (am & 1) {
+            v.re = -v.re;
+            v.im = -v.im;
+        }
+    }
+    return v;
+}
+// derivative of expansion `in` (degree <= pin) along axis -> `out` (degree pin-1), packed
+__device__ void deriv_expansion(const float* in, int pin, int axis, float* out, int tid, int nthr) {
+    const int ncout = pin * pin;
+    for (int k = tid; k < ncout; k += nthr) {
+        const int n = (int)sqrtf((float)k + 0.5f);
+        const int j = k - n * n;
+        const int m = (j + 1) >> 1;
+        const bool isim = j > 0 && (j & 1) == 0;
+        cf v;
+        if (axis == 2) {
+            v = getc(in, n + 1, m);
+        } else {
+            const cf up = getc(in, n + 1, m + 1), dn = getc(in, n + 1, m - 1);
+            if (axis == 0) v = {0.5f * (dn.re - up.re), 0.5f * (dn.im - up.im)};
+            else v = {0.5f * (up.im + dn.im), -0.5f * (up.re + dn.re)};  // -i/2 (up + dn)
+        }
+        out[k] = isim ? v.im : v.re;
+    }
+}
+
+template <int SCHEME>
+__global__ void __launch_bounds__(64) l2p_combine_kernel(
+    const float* __restrict__ s6, const float* __restrict__ near6,
+    const uint32_t* __restrict__ perm, int64_t n, const int* __restrict__ leaf_start, int p,
+    float inv_a, const float* __restrict__ Lleaf, int use_near, int use_far,
+    float* __restrict__ vel, float* __restrict__ dgam) {
+    extern __shared__ float sm[];
+    const int nc = (p + 1) * (p + 1);
+    const int ng = p * p, nh = (p - 1) * (p - 1);
+    float* Ls = sm;                    // [3][nc]
+    float* G = Ls + 3 * nc;            // [3 comp][3 axis][ng]
+    float* H = G + 9 * ng;             // [3 comp][6 pair][nh]  pairs: xx xy xz yy yz zz
+    float* Rw = H + 18 * (nh > 0 ? nh : 1);  // [ng][65]
+    const int leaf = blockIdx.x;
+    const int s = leaf_start[leaf], e = leaf_start[leaf + 1];
+    if (e == s) return;
+    const float inv4pi = 0.0795774715459476679f;
+    if (use_far) {
+        for (int i = threadIdx.x; i < 3 * nc; i += 64) Ls[i] = Lleaf[(int64_t)leaf * 3 * nc + i];
+        __syncthreads();
+        for (int c = 0; c < 3; ++c)
+            for (int ax = 0; ax < 3; ++ax)
+                deriv_expansion(Ls + c * nc, p, ax, G + (c * 3 + ax) * ng, threadIdx.x, 64);
+        __syncthreads();
+        if (p >= 2) {
+            const int pa[6] = {0, 0, 0, 1, 1, 2}, pb[6] = {0, 1, 2, 1, 2, 2};
+            for (int c = 0; c < 3; ++c)
+                for (int q = 0; q < 6; ++q)
+                    deriv_expansion(G + (c * 3 + pb[q]) * ng, p - 1, pa[q], H + (c * 6 + q) * nh,
+                                    threadIdx.x, 64);
+        }
+        __syncthreads();
+    }
+    for (int b = s; b < e; b += 64) {
+        const int j = b + threadIdx.x;
+        const bool act = j < e;
+        float u[3] = {0.f, 0.f, 0.f}, sd[3] = {0.f, 0.f, 0.f};
+        float gi[3] = {0.f, 0.f, 0.f};
+        if (act) {
+            gi[0] = s6[3 * n + j];
+            gi[1] = s6[4 * n + j];
+            gi[2] = s6[5 * n + j];
+        }
+        if (use_far && act) {
+            float* R = Rw + threadIdx.x;
+            solid_R_packed(s6[j] * inv_a, s6[n + j] * inv_a, s6[2 * n + j] * inv_a, p - 1, R, 65,
+                           false);
+            // weights: Re(n,0) x1, Re(n,m) x2, Im(n,m) x(-2)  ->  value = sum D[k] * Rw[k]
+            for (int k = 1; k < ng; ++k) {
+                const int nn = (int)sqrtf((float)k + 0.5f);
+                const int jj = k - nn * nn;
+                if (jj > 0) R[k * 65] *= (jj & 1) ? 2.f : -2.f;
+            }
+            float gr[3][3];  // gr[c][axis] = d_axis phi_c (scaled form)
+            for (int c = 0; c < 3; ++c)
+                for (int ax = 0; ax < 3; ++ax) {
+                    const float* D = G + (c * 3 + ax) * ng;
+                    float a = 0.f;
+                    for (int k = 0; k < ng; ++k) a = fmaf(D[k], R[k * 65], a);
+                    gr[c][ax] = a;
+                }
+            float hs[3][6];
+            for (int c = 0; c < 3; ++c)
+                for (int q = 0; q < 6; ++q) {
+                    const float* D = H + (c * 6 + q) * nh;
+                    float a = 0.f;
+                    for (int k = 0; k < nh; ++k) a = fmaf(D[k], R[k * 65], a);
+                    hs[c][q] = a;
+                }
+            const float sg = inv4pi * inv_a * inv_a;        // grad scale
+            const float sh = sg * inv_a;                    // hessian scale
+            // u = curl(phi)/4pi
+            u[0] = sg * (gr[2][1] - gr[1][2]);
+            u[1] = sg * (gr[0][2] - gr[2][0]);
+            u[2] = sg * (gr[1][0] - gr[0][1]);
+            // Hessian h[c][a][b]
+            auto h = [&](int c, int a, int b2) -> float {
+                const int lo = a < b2 ? a : b2, hi = a < b2 ? b2 : a;
+                const int q = lo == 0 ? hi : (lo == 1 ? 2 + hi : 5);
+                return hs[c][q];
+            };
+            if (SCHEME == 0) {
+                // sdot_a = eps_abc g_k d_k d_b phi_c : J[a][k] = d_k u_a
+                float J[3][3];
+                for (int k = 0; k < 3; ++k) {
+                    J[0][k] = h(2, k, 1) - h(1, k, 2);
+                    J[1][k] = h(0, k, 2) - h(2, k, 0);
+                    J[2][k] = h(1, k, 0) - h(0, k, 1);
+                }
+                for (int a = 0; a < 3; ++a)
+                    sd[a] = sh * (J[a][0] * gi[0] + J[a][1] * gi[1] + J[a][2] * gi[2]);
+            } else {
+                float J[3][3];
+                for (int k = 0; k < 3; ++k) {
+                    J[0][k] = h(2, k, 1) - h(1, k, 2);
+                    J[1][k] = h(0, k, 2) - h(2, k, 0);
+                    J[2][k] = h(1, k, 0) - h(0, k, 1);
+                }
+                for (int a = 0; a < 3; ++a)  // (grad u)^T g : sum_k J[k][a] g_k
+                    sd[a] = sh * (J[0][a] * gi[0] + J[1][a] * gi[1] + J[2][a] * gi[2]);
+            }
+        }
+        if (act) {
+            if (use_near) {
+                for (int a = 0; a < 3; ++a) {
+                    u[a] += near6[a * n + j];
+                    sd[a] += near6[(3 + a) * n + j];
+                }
+            }
+            const int64_t i = perm[j];
+            for (int a = 0; a < 3; ++a) {
+                vel[a * n + i] = u[a];
+                dgam[a * n + i] = sd[a];
+            }
+        }
+    }
+}
+
+void translate_attrs() {
+    static bool done = false;
+    if (done) return;
+    cudaFuncSetAttribute(translate_kernel<OP_M2M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)TRANSLATE_SMEM);
+    cudaFuncSetAttribute(translate_kernel<OP_L2L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)TRANSLATE_SMEM);
+    cudaFuncSetAttribute(translate_kernel<OP_M2L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)TRANSLATE_SMEM);
+    done = true;
+}
+
+}  // namespace
+
+void launch_p2m(const float* sorted6, int64_t n, const int* leaf_start, int depth, int p,
+                float inv_a, float* M_leaf, cudaStream_t st) {
+    const int nc = (p + 1) * (p + 1);
+    const size_t smem = sizeof(float) * (nc * 65 + 3 * 64);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(p2m_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        attr = true;
+    }
+    const int64_t nleaf = (int64_t)1 << (3 * depth);
+    p2m_kernel<<<(unsigned)nleaf, 64, smem, st>>>(sorted6, n, leaf_start, p, inv_a, M_leaf);
+}
+
+void launch_m2m(const float* ops_m2m, int p, int KP, int NR, const float* M_child, float* M_par,
+                int level_par, cudaStream_t st) {
+    const int64_t ncells = (int64_t)1 << (3 * level_par);
+    dim3 grid((unsigned)((ncells + TCELLS - 1) / TCELLS), NR / TROWS);
+    translate_attrs();
+    translate_kernel<OP_M2M><<<grid, 256, TRANSLATE_SMEM, st>>>(ops_m2m, nullptr, p, KP, NR, M_child, M_par,
+                                                   level_par, 0);
+}
+
+void launch_l2l(const float* ops_l2l, int p, int KP, int NR, const float* L_par, float* L_child,
+                int level_child, cudaStream_t st) {
+    const int64_t nparents = (int64_t)1 << (3 * (level_child - 1));
+    dim3 grid((unsigned)(8 * ((nparents + TCELLS - 1) / TCELLS)), NR / TROWS);
+    translate_attrs();
+    translate_kernel<OP_L2L><<<grid, 256, TRANSLATE_SMEM, st>>>(ops_l2l, nullptr, p, KP, NR, L_par, L_child,
+                                                   level_child, 0);
+}
+
+void launch_m2l(const float* ops_m2l, const int* il_slots, int p, int KP, int NR,
+                const float* M_l, float* L_l, int level, int periodic, cudaStream_t st) {
+    const int64_t nparents = (int64_t)1 << (3 * (level - 1));
+    dim3 grid((unsigned)(8 * ((nparents + TCELLS - 1) / TCELLS)), NR / TROWS);
+    translate_attrs();
+    translate_kernel<OP_M2L><<<grid, 256, TRANSLATE_SMEM, st>>>(ops_m2l, il_slots, p, KP, NR, M_l, L_l, level,
+                                                   periodic);
+}
+
+void launch_periodic(const float* ops_per, int p, int KP, int NR, const float* M0, float* L0,
+                     cudaStream_t st) {
+    periodic_kernel<<<1, 256, 0, st>>>(ops_per, KP, NR, (p + 1) * (p + 1), M0, L0);
+}
+
+void launch_l2p_combine(const float* sorted6, const float* near6, const uint32_t* perm,
+                        int64_t n, const int* leaf_start, int depth, int p, float a,
+                        const float* L_leaf, int scheme, int use_near, int use_far,
+                        float* vel, float* dgam, cudaStream_t st) {
+    const int nc = (p + 1) * (p + 1), ng = p * p, nh = (p - 1) * (p - 1);
+    const size_t smem = sizeof(float) * (3 * nc + 9 * ng + 18 * (nh > 0 ? nh : 1) + ng * 65);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(l2p_combine_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             200 * 1024);
+        cudaFuncSetAttribute(l2p_combine_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             200 * 1024);
+        attr = true;
+    }
+    const int64_t nleaf = (int64_t)1 << (3 * depth);
+    if (scheme == 0)
+        l2p_combine_kernel<0><<<(unsigned)nleaf, 64, smem, st>>>(
+            sorted6, near6, perm, n, leaf_start, p, 1.f / a, L_leaf, use_near, use_far, vel, dgam);
+    else
+        l2p_combine_kernel<1><<<(unsigned)nleaf, 64, smem, st>>>(
+            sorted6, near6, perm, n, leaf_start, p, 1.f / a, L_leaf, use_near, use_far, vel, dgam);
+}
+
+}  // namespace vfmm

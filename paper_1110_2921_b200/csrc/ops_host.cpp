@@ -1,0 +1,251 @@
+// ops_host.cpp -- translation operators of the FMM, built once per context in double
+// precision on the host ("nomenclature of Cheng et al."; Eqs. (10)-(11),
+// PAPER.md:123-128), then rounded to float32 and uploaded.
+//
+// Solid harmonics, complex, m >= 0, by recurrence:
+//   R_0^0 = 1, R_m^m = -(x+iy)/(2m) R_{m-1}^{m-1}, R_{m+1}^m = z R_m^m,
+//   (n+m)(n-m) R_n^m = (2n-1) z R_{n-1}^m - r^2 R_{n-2}^m
+//   I_0^0 = 1/r, I_m^m = -(2m-1)(x+iy)/r^2 I_{m-1}^{m-1}, I_{m+1}^m = (2m+1) z/r^2 I_m^m,
+//   r^2 I_n^m = (2n-1) z I_{n-1}^m - (n-1-m)(n-1+m) I_{n-2}^m
+//   R_n^{-m} = (-1)^m conj(R_n^m), I_n^{-m} = (-1)^m conj(I_n^m)
+// with 1/|x-y| = sum conj(R_n^m(y)) I_n^m(x) (Eq. 10's M_j = rho^n Y_n^{-m}, S = r^{-n-1} Y_n^m).
+//
+// Scaled (level-independent) operators, cell width a:  Mt = M / a^n, Lt = L a^(n+1)
+//   M2M (child c' -> parent c, d = (c'-c)/a_p):   Mt_p[n,m] = sum conj(R_k^l(d)) 2^-(n-k) Mt_c[n-k,m-l]
+//   M2L (source at c_t + o a):                   Lt[n,m]   = sum (-1)^(n+m) I_{n+k}^{l-m}(-o) Mt[k,l]
+//   L2L (parent c -> child c', d = (c'-c)/a_p):   Lt_c[n,m] = sum_{k>=n} 2^-(n+1) R_{k-n}^{l-m}(d) Lt_p[k,l]
+//   periodic (unit box, rings of 3x supercells): see build_periodic below.
+#include <cmath>
+#include <complex>
+#include <vector>
+
+#include "vfmm_internal.h"
+
+namespace vfmm {
+namespace {
+
+using cd = std::complex<double>;
+
+inline int fidx(int n, int m) { return n * n + n + m; }  // full complex index, |m| <= n
+
+// regular solid harmonics R_n^m(x) for all |m| <= n <= p
+void solid_R(double x, double y, double z, int p, std::vector<cd>& out) {
+    out.assign((p + 1) * (p + 1), cd(0, 0));
+    const double r2 = x * x + y * y + z * z;
+    const cd xy(x, y);
+    cd diag(1.0, 0.0);  // R_m^m
+    for (int m = 0; m <= p; ++m) {
+        if (m > 0) diag = -xy / (2.0 * m) * diag;
+        cd rm2 = diag, rm1(0, 0);
+        out[fidx(m, m)] = diag;
+        if (m + 1 <= p) {
+            rm1 = z * diag;
+            out[fidx(m + 1, m)] = rm1;
+        }
+        for (int n = m + 2; n <= p; ++n) {
+            cd rn = ((2.0 * n - 1.0) * z * rm1 - r2 * rm2) / double((n + m) * (n - m));
+            out[fidx(n, m)] = rn;
+            rm2 = rm1;
+            rm1 = rn;
+        }
+    }
+    for (int n = 1; n <= p; ++n)
+        for (int m = 1; m <= n; ++m)
+            out[fidx(n, -m)] = ((m & 1) ? -1.0 : 1.0) * std::conj(out[fidx(n, m)]);
+}
+
+// irregular solid harmonics I_n^m(x) for all |m| <= n <= p
+void solid_I(double x, double y, double z, int p, std::vector<cd>& out) {
+    out.assign((p + 1) * (p + 1), cd(0, 0));
+    const double r2 = x * x + y * y + z * z;
+    const double ir2 = 1.0 / r2;
+    const cd xy(x, y);
+    cd diag(1.0 / std::sqrt(r2), 0.0);  // I_m^m
+    for (int m = 0; m <= p; ++m) {
+        if (m > 0) diag = -(2.0 * m - 1.0) * xy * ir2 * diag;
+        cd im2 = diag, im1(0, 0);
+        out[fidx(m, m)] = diag;
+        if (m + 1 <= p) {
+            im1 = (2.0 * m + 1.0) * z * ir2 * diag;
+            out[fidx(m + 1, m)] = im1;
+        }
+        for (int n = m + 2; n <= p; ++n) {
+            cd in = ((2.0 * n - 1.0) * z * im1 - double((n - 1 - m) * (n - 1 + m)) * im2) * ir2;
+            out[fidx(n, m)] = in;
+            im2 = im1;
+            im1 = in;
+        }
+    }
+    for (int n = 1; n <= p; ++n)
+        for (int m = 1; m <= n; ++m)
+            out[fidx(n, -m)] = ((m & 1) ? -1.0 : 1.0) * std::conj(out[fidx(n, m)]);
+}
+
+// A: full complex matrix (nc x nc, row-major, acting on full coefficient vectors).
+// Returns the packed real matrix P (nc x nc row-major): P = pack o A o unpack.
+std::vector<double> pack_matrix(const std::vector<cd>& A, int p) {
+    const int nc = (p + 1) * (p + 1);
+    std::vector<double> P((size_t)nc * nc, 0.0);
+    for (int n = 0; n <= p; ++n) {
+        for (int m = 0; m <= n; ++m) {
+            // unpacked images of the packed basis vectors (Re / Im of coefficient (n,m))
+            for (int part = 0; part < (m == 0 ? 1 : 2); ++part) {
+                const int j = part == 0 ? pk_re(n, m) : pk_im(n, m);
+                std::vector<cd> col(nc, cd(0, 0));
+                const double sg = (m & 1) ? -1.0 : 1.0;
+                for (int r = 0; r < nc; ++r) {
+                    cd v = A[(size_t)r * nc + fidx(n, m)] * (part == 0 ? cd(1, 0) : cd(0, 1));
+                    if (m > 0)
+                        v += A[(size_t)r * nc + fidx(n, -m)] * sg * (part == 0 ? cd(1, 0) : cd(0, -1));
+                    col[r] = v;
+                }
+                for (int nn = 0; nn <= p; ++nn) {
+                    P[(size_t)pk_re(nn, 0) * nc + j] = col[fidx(nn, 0)].real();
+                    for (int mm = 1; mm <= nn; ++mm) {
+                        P[(size_t)pk_re(nn, mm) * nc + j] = col[fidx(nn, mm)].real();
+                        P[(size_t)pk_im(nn, mm) * nc + j] = col[fidx(nn, mm)].imag();
+                    }
+                }
+            }
+        }
+    }
+    return P;
+}
+
+// full complex M2M matrix: M_parent[n,m] += conj(R_k^l(d)) s^(n-k) M_child[n-k, m-l]
+std::vector<cd> m2m_full(double dx, double dy, double dz, int p, double s) {
+    const int nc = (p + 1) * (p + 1);
+    std::vector<cd> R;
+    solid_R(dx, dy, dz, p, R);
+    std::vector<cd> A((size_t)nc * nc, cd(0, 0));
+    for (int n = 0; n <= p; ++n)
+        for (int m = -n; m <= n; ++m)
+            for (int k = 0; k <= n; ++k)
+                for (int l = -k; l <= k; ++l) {
+                    const int nn = n - k, mm = m - l;
+                    if (std::abs(mm) > nn) continue;
+                    A[(size_t)fidx(n, m) * nc + fidx(nn, mm)] +=
+                        std::conj(R[fidx(k, l)]) * std::pow(s, nn);
+                }
+    return A;
+}
+
+// full complex M2L matrix: L[n,m] = sum (-1)^(n+m) I_{n+k}^{l-m}(D) M[k,l]
+std::vector<cd> m2l_full(double Dx, double Dy, double Dz, int p) {
+    const int nc = (p + 1) * (p + 1);
+    std::vector<cd> I;
+    solid_I(Dx, Dy, Dz, 2 * p, I);
+    std::vector<cd> A((size_t)nc * nc, cd(0, 0));
+    for (int n = 0; n <= p; ++n)
+        for (int m = -n; m <= n; ++m) {
+            const double sg = ((n + m) & 1) ? -1.0 : 1.0;
+            for (int k = 0; k <= p; ++k)
+                for (int l = -k; l <= k; ++l)
+                    A[(size_t)fidx(n, m) * nc + fidx(k, l)] = sg * I[fidx(n + k, l - m)];
+        }
+    return A;
+}
+
+// full complex L2L matrix: L_child[n,m] = sum_{k>=n} s^(n+1) R_{k-n}^{l-m}(d) L_parent[k,l]
+std::vector<cd> l2l_full(double dx, double dy, double dz, int p, double s) {
+    const int nc = (p + 1) * (p + 1);
+    std::vector<cd> R;
+    solid_R(dx, dy, dz, p, R);
+    std::vector<cd> A((size_t)nc * nc, cd(0, 0));
+    for (int n = 0; n <= p; ++n)
+        for (int m = -n; m <= n; ++m)
+            for (int k = n; k <= p; ++k)
+                for (int l = -k; l <= k; ++l) {
+                    const int j = k - n, t = l - m;
+                    if (std::abs(t) > j) continue;
+                    A[(size_t)fidx(n, m) * nc + fidx(k, l)] += std::pow(s, n + 1) * R[fidx(j, t)];
+                }
+    return A;
+}
+
+std::vector<double> matmul(const std::vector<double>& A, const std::vector<double>& B, int nc) {
+    std::vector<double> C((size_t)nc * nc, 0.0);
+    for (int i = 0; i < nc; ++i)
+        for (int k = 0; k < nc; ++k) {
+            const double a = A[(size_t)i * nc + k];
+            if (a == 0.0) continue;
+            for (int j = 0; j < nc; ++j) C[(size_t)i * nc + j] += a * B[(size_t)k * nc + j];
+        }
+    return C;
+}
+
+// Periodic far-field operator in unit-box scaled form: Lt_0 += P Mt_0, covering all
+// images of the image cube {-m..m}^3 outside the near 3^3 block (reading R5):
+//   ring k = 0..levels-2: supercells of width 3^k at offsets 3^k n, n in {-4..4}^3 \ {-1..1}^3
+//   supercell_{k+1} = sum over d in {-1,0,1}^3 of M2M(shift d 3^k) supercell_k
+std::vector<double> build_periodic(int p, int levels) {
+    const int nc = (p + 1) * (p + 1);
+    std::vector<double> P((size_t)nc * nc, 0.0);
+    if (levels < 2) return P;
+    std::vector<double> S((size_t)nc * nc, 0.0);  // supercell_k = S * Mt_0
+    for (int i = 0; i < nc; ++i) S[(size_t)i * nc + i] = 1.0;
+    for (int k = 0; k <= levels - 2; ++k) {
+        const double w = std::pow(3.0, k);
+        std::vector<double> ring((size_t)nc * nc, 0.0);
+        for (int a = -4; a <= 4; ++a)
+            for (int b = -4; b <= 4; ++b)
+                for (int c = -4; c <= 4; ++c) {
+                    if (std::max(std::abs(a), std::max(std::abs(b), std::abs(c))) <= 1) continue;
+                    auto T = pack_matrix(m2l_full(-a * w, -b * w, -c * w, p), p);
+                    for (size_t i = 0; i < T.size(); ++i) ring[i] += T[i];
+                }
+        auto RS = matmul(ring, S, nc);
+        for (size_t i = 0; i < P.size(); ++i) P[i] += RS[i];
+        if (k == levels - 2) break;
+        std::vector<double> up((size_t)nc * nc, 0.0);
+        for (int a = -1; a <= 1; ++a)
+            for (int b = -1; b <= 1; ++b)
+                for (int c = -1; c <= 1; ++c) {
+                    auto T = pack_matrix(m2m_full(a * w, b * w, c * w, p, 1.0), p);
+                    for (size_t i = 0; i < T.size(); ++i) up[i] += T[i];
+                }
+        S = matmul(up, S, nc);
+    }
+    return P;
+}
+
+// store a packed row-major matrix A (nc x nc) transposed + padded at slot `slot`
+void store_t(std::vector<float>& dst, int slot, const std::vector<double>& A, int nc, int KP,
+             int NR) {
+    float* base = dst.data() + (size_t)slot * KP * NR;
+    for (int r = 0; r < nc; ++r)
+        for (int k = 0; k < nc; ++k) base[(size_t)k * NR + r] = (float)A[(size_t)r * nc + k];
+}
+
+}  // namespace
+
+void build_host_ops(int p, int image_levels, HostOps* out) {
+    const int nc = (p + 1) * (p + 1);
+    out->p = p;
+    out->nc = nc;
+    out->KP = (nc + 15) / 16 * 16;
+    out->NR = (nc + 127) / 128 * 128;
+    const size_t msz = (size_t)out->KP * out->NR;
+    out->m2m.assign(8 * msz, 0.f);
+    out->l2l.assign(8 * msz, 0.f);
+    out->m2l.assign(343 * msz, 0.f);
+    out->per.assign(msz, 0.f);
+    for (int ch = 0; ch < 8; ++ch) {
+        const double dx = (((ch >> 0) & 1) - 0.5) * 0.5;
+        const double dy = (((ch >> 1) & 1) - 0.5) * 0.5;
+        const double dz = (((ch >> 2) & 1) - 0.5) * 0.5;
+        store_t(out->m2m, ch, pack_matrix(m2m_full(dx, dy, dz, p, 0.5), p), nc, out->KP, out->NR);
+        store_t(out->l2l, ch, pack_matrix(l2l_full(dx, dy, dz, p, 0.5), p), nc, out->KP, out->NR);
+    }
+    for (int ox = -3; ox <= 3; ++ox)
+        for (int oy = -3; oy <= 3; ++oy)
+            for (int oz = -3; oz <= 3; ++oz) {
+                if (std::max(std::abs(ox), std::max(std::abs(oy), std::abs(oz))) <= 1) continue;
+                store_t(out->m2l, m2l_slot(ox, oy, oz),
+                        pack_matrix(m2l_full(-ox, -oy, -oz, p), p), nc, out->KP, out->NR);
+            }
+    out->per_d = build_periodic(p, image_levels);
+    store_t(out->per, 0, out->per_d, nc, out->KP, out->NR);
+}
+
+}  // namespace vfmm

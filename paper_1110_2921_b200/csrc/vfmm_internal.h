@@ -1,0 +1,102 @@
+// vfmm_internal.h -- internal declarations of libvfmm (not part of the ABI).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "../../include/vfmm.h"
+
+namespace vfmm {
+
+constexpr int kPMax = VFMM_PMAX;
+
+inline int ncoef(int p) { return (p + 1) * (p + 1); }
+
+// Packed real coefficient index:
+// Re(n,0) -> n^2 ; Re(n,m) -> n^2 + 2m - 1 ; Im(n,m) -> n^2 + 2m   (m >= 1)
+__host__ __device__ inline int pk_re(int n, int m) { return n * n + (m == 0 ? 0 : 2 * m - 1); }
+__host__ __device__ inline int pk_im(int n, int m) { return n * n + 2 * m; }
+
+// cells at level l start at (8^l - 1) / 7 in the concatenated per-level arrays
+inline int64_t level_offset(int l) { return ((int64_t(1) << (3 * l)) - 1) / 7; }
+
+// ---------------------------------------------------------------------------
+// host operator tables (ops_host.cpp), double precision, packed real form
+// ---------------------------------------------------------------------------
+struct HostOps {
+    int p = 0, nc = 0;
+    int KP = 0;  // K padded to a multiple of 16
+    int NR = 0;  // rows padded to a multiple of 128
+    // all matrices stored transposed+padded: T[k * NR + r] = A[r][k]  (float32 upload)
+    std::vector<float> m2m;  // 8 child matrices   [8][KP][NR]
+    std::vector<float> l2l;  // 8 child matrices   [8][KP][NR]
+    std::vector<float> m2l;  // 343 offset slots   [343][KP][NR] (|o|inf <= 1 slots zero)
+    std::vector<float> per;  // periodic operator  [1][KP][NR]
+    std::vector<double> per_d;  // periodic operator row-major [nc][nc] (double, for tests)
+};
+
+// Build all operator tables for order p and image_levels (periodic operator is zero for
+// image_levels < 2).  Deterministic, double precision.
+void build_host_ops(int p, int image_levels, HostOps* out);
+
+// M2L offset slot of o in {-3..3}^3
+__host__ __device__ inline int m2l_slot(int ox, int oy, int oz) {
+    return ((ox + 3) * 7 + (oy + 3)) * 7 + (oz + 3);
+}
+
+// ---------------------------------------------------------------------------
+// kernels' launch wrappers (defined in .cu files); all async on `st`
+// ---------------------------------------------------------------------------
+struct Geom {
+    float lo, len;   // box
+    double lo_d, len_d;
+    int depth;       // L
+    int periodic;    // image_levels > 0
+};
+
+// tree.cu
+void launch_keys(const float* pos, int64_t n, Geom g, uint32_t* keys, uint32_t* vals,
+                 int* err_flag, cudaStream_t st);
+size_t radix_temp_bytes(int64_t n);
+void launch_radix_sort(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint32_t* vals_alt,
+                       int64_t n, int key_bits, void* temp, cudaStream_t st,
+                       uint32_t** keys_out, uint32_t** vals_out, int* n_launch);
+void launch_leaf_ranges(const uint32_t* keys_sorted, int64_t n, int depth, int* leaf_start,
+                        cudaStream_t st);
+void launch_gather(const float* pos, const float* gamma, const uint32_t* perm,
+                   const uint32_t* keys_sorted, int64_t n, Geom g, float* sorted6,
+                   cudaStream_t st);
+
+// expansions.cu
+void launch_p2m(const float* sorted6, int64_t n, const int* leaf_start, int depth, int p,
+                float inv_a, float* M_leaf, cudaStream_t st);
+void launch_m2m(const float* ops_m2m, int p, int KP, int NR, const float* M_child, float* M_par,
+                int level_par, cudaStream_t st);
+void launch_l2l(const float* ops_l2l, int p, int KP, int NR, const float* L_par, float* L_child,
+                int level_child, cudaStream_t st);
+void launch_m2l(const float* ops_m2l, const int* il_slots, int p, int KP, int NR,
+                const float* M_l, float* L_l, int level, int periodic, cudaStream_t st);
+void launch_periodic(const float* ops_per, int p, int KP, int NR, const float* M0, float* L0,
+                     cudaStream_t st);
+void launch_l2p_combine(const float* sorted6, const float* near6, const uint32_t* perm,
+                        int64_t n, const int* leaf_start, int depth, int p, float a,
+                        const float* L_leaf, int scheme, int use_near, int use_far,
+                        float* vel, float* dgam, cudaStream_t st);
+
+// p2p.cu
+struct KernelConsts {
+    float inv2s2;        // 1 / (2 sigma^2)
+    float neg_l2e_inv2s2;// -log2(e) / (2 sigma^2)
+    float inv_s_sqrt2;   // 1 / (sqrt(2) sigma)
+    float zeta0;         // (2 pi sigma^2)^(-3/2)
+    float zeta0_over_s2; // zeta0 / sigma^2
+};
+KernelConsts make_kernel_consts(float sigma);
+void launch_p2p(const float* sorted6, int64_t n, const int* leaf_start, int depth, float a,
+                int periodic, int scheme, KernelConsts kc, float* near6, cudaStream_t st);
+void launch_direct(const float* pos, const float* gamma, int64_t n, float len, int image_levels,
+                   int scheme, KernelConsts kc, float* vel, float* dgam, cudaStream_t st);
+
+}  // namespace vfmm

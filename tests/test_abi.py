@@ -1,0 +1,59 @@
+"""CPU-side checks of the C ABI boundary: the library builds, loads and exports every
+function include/vfmm.h declares; host-only entry points behave (no GPU needed)."""
+import ctypes
+import os
+import re
+
+import pytest
+
+import paper_1110_2921_b200 as vf
+
+
+def _declared():
+    src = open(vf.HEADER_PATH).read()
+    return sorted(set(re.findall(r"\b(vfmm_[a-z_]+)\s*\(", src)))
+
+
+def test_header_declares_the_documented_entry_points():
+    names = _declared()
+    for f in vf.EXPORTS:
+        assert f in names
+
+
+def test_library_exports_every_declared_symbol():
+    L = vf.load_library()
+    for name in _declared():
+        assert hasattr(L, name), name
+
+
+def test_host_only_functions():
+    L = vf.load_library()
+    assert L.vfmm_abi_version() == 1
+    p = vf.c_params()
+    L.vfmm_params_default(ctypes.byref(p))
+    assert p.p == 10 and p.image_levels == 3 and p.depth == 0
+    assert abs(p.box_len - 6.2831855) < 1e-6 and abs(p.box_lo + 3.1415927) < 1e-6
+    assert L.vfmm_strerror(-2).decode().startswith("VFMM_EDOMAIN")
+    assert L.vfmm_strerror(0).decode() == "VFMM_OK"
+
+
+def test_create_rejects_bad_params_without_touching_the_gpu():
+    L = vf.load_library()
+    ctx = ctypes.c_void_p()
+    for bad in (dict(p=0), dict(p=17), dict(sigma=0.0), dict(sigma=float("nan")),
+                dict(depth=11), dict(image_levels=7), dict(scheme=2), dict(mode=9),
+                dict(box_len=-1.0)):
+        prm = vf.Params(**bad).to_c()
+        assert L.vfmm_create(ctypes.byref(ctx), ctypes.byref(prm), 0) == vf.VFMM_EINVAL
+        assert not ctx.value
+
+
+def test_no_oracle_in_product_path():
+    """The product package must not import or link the oracle."""
+    pkg = os.path.dirname(vf.__file__)
+    for root, _, files in os.walk(pkg):
+        for fn in files:
+            if fn.endswith((".py", ".cu", ".cpp", ".h")):
+                txt = open(os.path.join(root, fn)).read()
+                assert "import oracle" not in txt and "liboracle" not in txt, fn
+                assert "from oracle" not in txt, fn

@@ -1,0 +1,241 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle.
+
+* tree: Morton keys, stable sort and leaf ranges bit-exact vs oracle.morton
+* DIRECT mode vs the direct-sum oracle O1 (FP32 kernel arithmetic vs float64)
+* NEAR_ONLY / FAR_ONLY structure; NEAR_ONLY at depth 1 free space == O1
+* FMM vs the float64 step-by-step FMM oracle (same algorithm: FP32 rounding only),
+  including per-stage multipole / local expansions
+* FMM vs O1 at the frozen per-p tolerances (tests/tolerances.py), p sweep decreasing
+* edge cases: ragged N, single particle, empty leaves, free space, jittered, bad input
+* full size (256^3, the bench configuration) on sampled targets
+"""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import synthgen
+from oracle import fmm_ref as F
+from tests import tolerances as TOL
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_1110_2921_b200 as vf  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / np.linalg.norm(b))
+
+
+def run(field, **kw):
+    ev = vf.Evaluator(sigma=field.sigma, box_lo=field.box_lo, box_len=field.box_len, **kw)
+    pos = torch.from_numpy(np.ascontiguousarray(field.pos)).to(DEV)
+    gam = torch.from_numpy(np.ascontiguousarray(field.gamma)).to(DEV)
+    v, s = ev.evaluate(pos, gam)
+    ev.sync_status()
+    torch.cuda.synchronize()
+    return v.cpu().numpy().astype(np.float64), s.cpu().numpy().astype(np.float64), ev
+
+
+def random_field(n, seed=0, sigma=0.3):
+    rng = np.random.default_rng(seed)
+    lo, ln = synthgen.BOX_LO, synthgen.BOX_LEN
+    pos = rng.uniform(float(lo), float(lo + ln), (3, n)).astype(np.float32)
+    pos = np.minimum(pos, np.nextafter(np.float32(lo + ln), np.float32(0)))
+    gam = rng.normal(size=(3, n)).astype(np.float32) * 1e-3
+    return synthgen.Field(pos, gam, sigma, float(lo), float(ln), 0, f"random{n}")
+
+
+# ------------------------------------------------------------------ tree (bit-exact)
+
+@pytest.mark.parametrize("case", ["c1", "c2", "c1j", "rand", "ragged"])
+def test_tree_bit_exact(case):
+    if case == "c1":
+        f, depth = synthgen.make("c1"), 2
+    elif case == "c2":
+        f, depth = synthgen.make("c2"), 4
+    elif case == "c1j":
+        f, depth = synthgen.jitter(synthgen.make("c1")), 3
+    elif case == "rand":
+        f, depth = random_field(100000, 1), 5
+    else:
+        f, depth = random_field(12345, 2), 3
+    _, _, ev = run(f, p=2, depth=depth, image_levels=1, mode=vf.MODE_NEAR_ONLY)
+    keys, perm, ls = ev.debug_tree(depth)
+    k_o, p_o, ls_o, rc = oracle.morton(f.pos, depth, f.box_lo, f.box_len)
+    assert rc == 0
+    assert np.array_equal(keys, k_o)
+    assert np.array_equal(perm, p_o)
+    assert np.array_equal(ls, ls_o)
+    ev.close()
+
+
+def test_bad_input_is_flagged():
+    f = random_field(1000, 3)
+    f.pos[1, 17] = np.float32(f.box_lo + f.box_len)  # upper face is outside [lo, lo+len)
+    ev = vf.Evaluator(sigma=f.sigma, p=2, depth=2, image_levels=1)
+    pos = torch.from_numpy(f.pos).to(DEV)
+    gam = torch.from_numpy(f.gamma).to(DEV)
+    ev.evaluate(pos, gam)
+    with pytest.raises(vf.VfmmError) as e:
+        ev.sync_status()
+    assert e.value.status == vf.VFMM_EDOMAIN
+    ev.sync_status()  # sticky flag was cleared
+    with pytest.raises(vf.VfmmError):
+        ev.evaluate_into(pos, gam, pos, gam)  # outputs aliasing inputs
+    ev.close()
+
+
+# ------------------------------------------------------------------ DIRECT / NEAR vs O1
+
+@pytest.mark.parametrize("lam,scheme", [(0, 0), (1, 0), (1, 1), (3, 0)])
+def test_direct_mode_vs_oracle(lam, scheme):
+    f = synthgen.make("c1") if lam != 0 else random_field(3000, 4)
+    v, s, ev = run(f, p=2, image_levels=lam, scheme=scheme, mode=vf.MODE_DIRECT)
+    tg = synthgen.sample_targets(f.pos.shape[1], 64, n_lattice=f.n or None)
+    vo, so = oracle.direct(f.pos, f.gamma, f.sigma, f.box_lo, f.box_len, lam, scheme, targets=tg)
+    assert rel(v[:, tg], vo) < TOL.DIRECT_VS_ORACLE[0]
+    assert rel(s[:, tg], so) < TOL.DIRECT_VS_ORACLE[1]
+    ev.close()
+
+
+@pytest.mark.parametrize("scheme", [0, 1])
+def test_near_only_depth1_free_space_equals_direct(scheme):
+    """Depth 1, free space: all octants are neighbours, so P2P alone is the whole sum."""
+    f = synthgen.jitter(synthgen.taylor_green(12), seed=5)
+    v, s, ev = run(f, p=2, depth=1, image_levels=0, scheme=scheme, mode=vf.MODE_NEAR_ONLY)
+    vo, so = oracle.direct(f.pos, f.gamma, f.sigma, f.box_lo, f.box_len, 0, scheme)
+    assert rel(v, vo) < TOL.NEAR_VS_ORACLE[0] and rel(s, so) < TOL.NEAR_VS_ORACLE[1]
+    ev.close()
+
+
+def test_near_plus_far_equals_fmm():
+    f = synthgen.isotropic(16, seed=7)
+    v, s, ev = run(f, p=6, depth=2, image_levels=3)
+    vn, sn, _ = run(f, p=6, depth=2, image_levels=3, mode=vf.MODE_NEAR_ONLY)
+    vf_, sf_, _ = run(f, p=6, depth=2, image_levels=3, mode=vf.MODE_FAR_ONLY)
+    assert np.abs(vn + vf_ - v).max() <= 1e-6 * np.abs(v).max()
+    assert np.abs(sn + sf_ - s).max() <= 1e-6 * np.abs(s).max()
+    ev.close()
+
+
+# ------------------------------------------------------------------ FMM vs fp64 FMM oracle
+
+def _fmm_oracle(f, depth, p, lam, scheme=0):
+    return F.evaluate(f.pos, f.gamma, f.sigma, f.box_lo, f.box_len, depth, p, lam, scheme,
+                      return_stages=True)
+
+
+@pytest.mark.parametrize("name,depth,p,lam,scheme", [
+    ("c1", 2, 4, 3, 0),
+    ("iso16", 2, 6, 2, 0),
+    ("iso16", 2, 6, 2, 1),
+    ("iso16", 3, 3, 0, 0),
+    ("c1j", 2, 5, 1, 0),
+])
+def test_fmm_vs_fmm_oracle(name, depth, p, lam, scheme):
+    f = {"c1": lambda: synthgen.make("c1"), "iso16": lambda: synthgen.isotropic(16, seed=9),
+         "c1j": lambda: synthgen.jitter(synthgen.make("c1"))}[name]()
+    v, s, ev = run(f, p=p, depth=depth, image_levels=lam, scheme=scheme)
+    vo, so, st = _fmm_oracle(f, depth, p, lam, scheme)
+    assert rel(v, vo) < TOL.FMM_VS_FMM_ORACLE[0], rel(v, vo)
+    assert rel(s, so) < TOL.FMM_VS_FMM_ORACLE[1], rel(s, so)
+    # per-stage: leaf multipoles, and local expansions at every level (scaled, packed)
+    a = f.box_len / (1 << depth)
+    for l in range(depth + 1):
+        al = f.box_len / (1 << l)
+        for kind, C, scale in ((0, st["M"][l], al ** -np.arange(p + 1.0)),
+                               (1, st["L"][l], al ** (np.arange(p + 1.0) + 1))):
+            got = ev.debug_expansions(kind, l)
+            want = _pack(C, p, scale)
+            if np.abs(want).max() == 0:
+                continue
+            assert rel(got, want) < 1e-5, (kind, l, rel(got, want))
+    ev.close()
+
+
+def _pack(C, p, scale_n):
+    """complex coefficients [cell][comp][(n,m) full] -> packed real, times scale_n[n]."""
+    out = np.zeros(C.shape[:2] + ((p + 1) ** 2,))
+    for n in range(p + 1):
+        out[..., n * n] = C[..., F.kidx(n, 0)].real * scale_n[n]
+        for m in range(1, n + 1):
+            out[..., n * n + 2 * m - 1] = C[..., F.kidx(n, m)].real * scale_n[n]
+            out[..., n * n + 2 * m] = C[..., F.kidx(n, m)].imag * scale_n[n]
+    return out
+
+
+# ------------------------------------------------------------------ FMM vs direct sum
+
+def test_c1_fmm_vs_direct_oracle():
+    f = synthgen.make("c1")
+    v, s, ev = run(f, p=4, depth=2, image_levels=3)
+    vo, so = oracle.direct(f.pos, f.gamma, f.sigma, f.box_lo, f.box_len, 3, 0)
+    tu, ts = TOL.FMM_VS_DIRECT[4]
+    assert rel(v, vo) < tu and rel(s, so) < ts
+    ev.close()
+
+
+def test_p_sweep_error_decreases():
+    f = synthgen.isotropic(32, seed=12)
+    tg = synthgen.sample_targets(32 ** 3, 48, n_lattice=32)
+    vo, so = oracle.direct(f.pos, f.gamma, f.sigma, f.box_lo, f.box_len, 1, 0, targets=tg)
+    errs = []
+    for p in (4, 6, 8, 10):
+        v, s, ev = run(f, p=p, depth=3, image_levels=1)
+        errs.append((rel(v[:, tg], vo), rel(s[:, tg], so)))
+        tu, ts = TOL.FMM_VS_DIRECT[p]
+        assert errs[-1][0] < tu and errs[-1][1] < ts, (p, errs[-1])
+        ev.close()
+    for a, b in zip(errs, errs[1:]):
+        assert b[0] < a[0] and b[1] < a[1], errs
+
+
+# ------------------------------------------------------------------ edge cases
+
+def test_single_particle_periodic_is_at_rest():
+    f = random_field(1, 5)
+    v, s, ev = run(f, p=6, depth=2, image_levels=3)
+    # a lone particle feels no velocity from its own images (cube symmetry); FMM to tolerance
+    assert np.abs(v).max() < 1e-6 * abs(f.gamma).max() / f.sigma ** 2
+    ev.close()
+
+
+def test_ragged_random_points_vs_direct():
+    f = random_field(5003, 6, sigma=0.2)
+    tg = np.arange(0, 5003, 97)
+    v, s, ev = run(f, p=8, depth=3, image_levels=1)
+    vo, so = oracle.direct(f.pos, f.gamma, f.sigma, f.box_lo, f.box_len, 1, 0, targets=tg)
+    tu, ts = TOL.FMM_VS_DIRECT[8]
+    assert rel(v[:, tg], vo) < tu and rel(s[:, tg], so) < ts
+    ev.close()
+
+
+def test_zero_strengths_give_zero():
+    f = synthgen.make("c1")
+    f.gamma[:] = 0
+    v, s, ev = run(f, p=4, depth=2, image_levels=3)
+    assert np.all(v == 0) and np.all(s == 0)
+    ev.close()
+
+
+# ------------------------------------------------------------------ full size (bench config)
+
+@pytest.mark.slow
+def test_c4_full_size_sampled_targets():
+    """256^3 (the bench workload, p = 10, depth 6): lambda = 1 so the oracle finishes in
+    seconds per target; the lambda = 3 far-image operator is covered at c1/c2 sizes."""
+    f = synthgen.make("c4")
+    v, s, ev = run(f, p=10, depth=6, image_levels=1)
+    tg = synthgen.sample_targets(f.pos.shape[1], 8, n_lattice=f.n)
+    vo, so = oracle.direct(f.pos, f.gamma, f.sigma, f.box_lo, f.box_len, 1, 0, targets=tg)
+    tu, ts = TOL.FMM_VS_DIRECT[10]
+    assert rel(v[:, tg], vo) < tu and rel(s[:, tg], so) < ts, (rel(v[:, tg], vo), rel(s[:, tg], so))
+    ev.close()
