@@ -34,6 +34,7 @@ struct vfmm_ctx {
     int* leaf_start = nullptr;
     float *Mall = nullptr, *Lall = nullptr;
     int* d_err = nullptr;
+    unsigned long long* d_pairs = nullptr;  // P2P pair counter of the last evaluate
     // host-API staging
     int64_t cap_host_n = 0;
     float* hbuf = nullptr;  // 12 x n
@@ -45,7 +46,8 @@ struct vfmm_ctx {
     int last_depth = 0;
     bool have_tree = false, have_exp = false;
     vfmm_stats stats{};
-    cudaEvent_t ev[8] = {};
+    static constexpr int NEV = 10;
+    cudaEvent_t ev[NEV] = {};
 };
 
 namespace {
@@ -218,9 +220,10 @@ vfmm_status vfmm_create(vfmm_ctx** out, const vfmm_params* prm, int device) {
     s = ensure_ops(c);
     if (s == VFMM_OK) {
         cudaError_t e2 = cudaMalloc((void**)&c->d_err, sizeof(int));
+        if (e2 == cudaSuccess) e2 = cudaMalloc((void**)&c->d_pairs, sizeof(unsigned long long));
         if (e2 == cudaSuccess) e2 = cudaMemset(c->d_err, 0, sizeof(int));
         if (e2 == cudaSuccess) e2 = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
-        for (int i = 0; i < 8 && e2 == cudaSuccess; ++i) e2 = cudaEventCreate(&c->ev[i]);
+        for (int i = 0; i < vfmm_ctx::NEV && e2 == cudaSuccess; ++i) e2 = cudaEventCreate(&c->ev[i]);
         if (e2 != cudaSuccess) s = cuda_fail(c, e2, "create");
     }
     if (s != VFMM_OK) {
@@ -268,7 +271,7 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
     if (P.mode == VFMM_MODE_DIRECT) {
         launch_direct(pos, gamma, n, P.box_len, P.image_levels, P.scheme, kc, vel, dgamma, st);
         CK(cudaGetLastError(), "direct kernel");
-        for (int i = 1; i < 8; ++i) CK(cudaEventRecord(c->ev[i], st), "event");
+        for (int i = 1; i < vfmm_ctx::NEV; ++i) CK(cudaEventRecord(c->ev[i], st), "event");
         int m = 0;
         for (int l = 0; l < P.image_levels; ++l) m = 3 * m + 1;
         S.n_p2p_pairs = n * n * (int64_t)((2 * m + 1) * (2 * m + 1) * (2 * m + 1));
@@ -308,6 +311,9 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
     if (use_far) {
         launch_p2m(c->sorted6, n, c->leaf_start, depth, p, 1.f / a, Mlev(depth), st);
         ++nl;
+    }
+    CK(cudaEventRecord(c->ev[4], st), "event");
+    if (use_far) {
         for (int l = depth - 1; l >= 0; --l) {
             launch_m2m(c->d_m2m, p, H.KP, H.NR, Mlev(l + 1), Mlev(l), l, st);
             ++nl;
@@ -315,39 +321,48 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
         }
         CK(cudaGetLastError(), "upward kernels");
     }
-    CK(cudaEventRecord(c->ev[4], st), "event");
-    // ---- periodic images + downward pass ----
+    CK(cudaEventRecord(c->ev[5], st), "event");
+    // ---- M2L at every level (writes L_l), then periodic images + L2L top-down (adds) ----
     if (use_far) {
-        CK(cudaMemsetAsync(Llev(0), 0, 3 * nc * sizeof(float), st), "memset L0");
+        for (int l = 1; l <= depth; ++l) {
+            launch_m2l(c->d_m2l, c->d_slots, p, H.KP, H.NR, Mlev(l), Llev(l), l,
+                       P.image_levels > 0, st);
+            ++nl;
+            S.n_m2l += (int64_t)189 << (3 * l);
+        }
+        CK(cudaGetLastError(), "m2l kernels");
+    }
+    CK(cudaEventRecord(c->ev[6], st), "event");
+    if (use_far) {
         if (P.image_levels >= 2) {
             launch_periodic(c->d_per, p, H.KP, H.NR, Mlev(0), Llev(0), st);
             ++nl;
+        } else {
+            CK(cudaMemsetAsync(Llev(0), 0, 3 * nc * sizeof(float), st), "memset L0");
         }
         for (int l = 1; l <= depth; ++l) {
             launch_l2l(c->d_l2l, p, H.KP, H.NR, Llev(l - 1), Llev(l), l, st);
-            launch_m2l(c->d_m2l, c->d_slots, p, H.KP, H.NR, Mlev(l), Llev(l), l,
-                       P.image_levels > 0, st);
-            nl += 2;
+            ++nl;
             S.n_l2l += (int64_t)1 << (3 * l);
-            S.n_m2l += (int64_t)189 << (3 * l);
         }
         CK(cudaGetLastError(), "downward kernels");
         c->have_exp = true;
     }
-    CK(cudaEventRecord(c->ev[5], st), "event");
+    CK(cudaEventRecord(c->ev[7], st), "event");
     // ---- near field ----
     if (use_near) {
+        CK(cudaMemsetAsync(c->d_pairs, 0, sizeof(unsigned long long), st), "memset pairs");
         launch_p2p(c->sorted6, n, c->leaf_start, depth, a, P.image_levels > 0, P.scheme, kc,
-                   c->near6, st);
+                   c->near6, c->d_pairs, st);
         ++nl;
         CK(cudaGetLastError(), "p2p kernel");
     }
-    CK(cudaEventRecord(c->ev[6], st), "event");
+    CK(cudaEventRecord(c->ev[8], st), "event");
     launch_l2p_combine(c->sorted6, c->near6, c->perm, n, c->leaf_start, depth, p, a,
                        Llev(depth), P.scheme, use_near, use_far, vel, dgamma, st);
     ++nl;
     CK(cudaGetLastError(), "l2p kernel");
-    CK(cudaEventRecord(c->ev[7], st), "event");
+    CK(cudaEventRecord(c->ev[9], st), "event");
     S.n_kernel_launches = nl;
     return VFMM_OK;
 }
@@ -395,58 +410,25 @@ vfmm_status vfmm_get_stats(vfmm_ctx* c, vfmm_stats* out) {
     CK(cudaSetDevice(c->device), "set device");
     CK(cudaStreamSynchronize(c->last_stream), "sync");
     vfmm_stats& S = c->stats;
-    float ms[8] = {0};
-    for (int i = 1; i < 8; ++i) CK(cudaEventElapsedTime(&ms[i], c->ev[i - 1], c->ev[i]), "elapsed");
+    float ms[vfmm_ctx::NEV] = {0};
+    for (int i = 1; i < vfmm_ctx::NEV; ++i)
+        CK(cudaEventElapsedTime(&ms[i], c->ev[i - 1], c->ev[i]), "elapsed");
     S.ms_keys = ms[1];
     S.ms_sort = ms[2];
-    S.ms_tree = ms[3];
-    S.ms_p2m = 0;
-    S.ms_m2m = ms[4];  // P2M + M2M
-    S.ms_m2l = ms[5];  // periodic + L2L + M2L
-    S.ms_l2l = 0;
-    S.ms_p2p = ms[6];
-    S.ms_l2p = ms[7];
+    S.ms_tree = ms[3];  // leaf ranges + gather
+    S.ms_p2m = ms[4];
+    S.ms_m2m = ms[5];
+    S.ms_m2l = ms[6];
+    S.ms_l2l = ms[7];   // periodic images + L2L
+    S.ms_p2p = ms[8];
+    S.ms_l2p = ms[9];   // L2P + near/far combine + un-permute
     float tot = 0;
-    CK(cudaEventElapsedTime(&tot, c->ev[0], c->ev[7]), "elapsed");
+    CK(cudaEventElapsedTime(&tot, c->ev[0], c->ev[vfmm_ctx::NEV - 1]), "elapsed");
     S.ms_total = tot;
-    if (c->prm.mode != VFMM_MODE_DIRECT && (c->prm.mode != VFMM_MODE_FAR_ONLY)) {
-        // near-field pair count: sum over leaves of n_t * (sum of 27 neighbour counts)
-        const int depth = c->last_depth;
-        const int64_t nleaf = (int64_t)1 << (3 * depth);
-        std::vector<int> ls(nleaf + 1);
-        CK(cudaMemcpy(ls.data(), c->leaf_start, (nleaf + 1) * sizeof(int), cudaMemcpyDeviceToHost),
-           "copy leaf_start");
-        const int side = 1 << depth;
-        auto enc = [&](int x, int y, int z) {
-            int64_t k = 0;
-            for (int b = 0; b < depth; ++b)
-                k |= ((int64_t)((x >> b) & 1) << (3 * b)) | ((int64_t)((y >> b) & 1) << (3 * b + 1)) |
-                     ((int64_t)((z >> b) & 1) << (3 * b + 2));
-            return k;
-        };
-        int64_t pairs = 0;
-        const bool per = c->prm.image_levels > 0;
-        for (int x = 0; x < side; ++x)
-            for (int y = 0; y < side; ++y)
-                for (int z = 0; z < side; ++z) {
-                    const int64_t t = enc(x, y, z);
-                    const int64_t nt = ls[t + 1] - ls[t];
-                    if (!nt) continue;
-                    int64_t ns = 0;
-                    for (int o = 0; o < 27; ++o) {
-                        int nx = x + o % 3 - 1, ny = y + (o / 3) % 3 - 1, nz = z + o / 9 - 1;
-                        if (!per && (nx < 0 || ny < 0 || nz < 0 || nx >= side || ny >= side ||
-                                     nz >= side))
-                            continue;
-                        nx &= side - 1;
-                        ny &= side - 1;
-                        nz &= side - 1;
-                        const int64_t sc = enc(nx, ny, nz);
-                        ns += ls[sc + 1] - ls[sc];
-                    }
-                    pairs += nt * ns;
-                }
-        S.n_p2p_pairs = pairs;
+    if (c->prm.mode == VFMM_MODE_FMM || c->prm.mode == VFMM_MODE_NEAR_ONLY) {
+        unsigned long long pairs = 0;
+        CK(cudaMemcpy(&pairs, c->d_pairs, sizeof(pairs), cudaMemcpyDeviceToHost), "copy pairs");
+        S.n_p2p_pairs = (int64_t)pairs;
     }
     *out = S;
     return VFMM_OK;
@@ -503,8 +485,9 @@ void vfmm_destroy(vfmm_ctx* c) {
     dfree(c->Mall);
     dfree(c->Lall);
     dfree(c->d_err);
+    dfree(c->d_pairs);
     dfree(c->hbuf);
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < vfmm_ctx::NEV; ++i)
         if (c->ev[i]) cudaEventDestroy(c->ev[i]);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     delete c;

@@ -286,21 +286,21 @@ __global__ void __launch_bounds__(256) translate_kernel(
         for (int i = 0; i < 8; ++i) {
             const int r = row0 + ty * 8 + i;
             if (r < nc) {
-                if (KIND == OP_M2L) out[r] += acc[i][j];
+                if (KIND == OP_L2L) out[r] += acc[i][j];  // L2L accumulates onto M2L
                 else out[r] = acc[i][j];
             }
         }
     }
 }
 
-// periodic far field: L0 += P M0 (3 columns); one block
+// periodic far field: L0 = P M0 (3 columns); one block
 __global__ void periodic_kernel(const float* __restrict__ P, int KP, int NR, int nc,
                                 const float* __restrict__ M0, float* __restrict__ L0) {
     for (int o = threadIdx.x; o < 3 * nc; o += blockDim.x) {
         const int c = o / nc, r = o - c * nc;
         float a = 0.f;
         for (int k = 0; k < nc; ++k) a = fmaf(P[(size_t)k * NR + r], M0[c * nc + k], a);
-        L0[c * nc + r] += a;
+        L0[c * nc + r] = a;
     }
 }
 

