@@ -7,6 +7,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -23,6 +24,9 @@ struct vfmm_ctx {
     int ops_p = -1, ops_levels = -1;
     HostOps hops;
     float *d_m2m = nullptr, *d_l2l = nullptr, *d_m2l = nullptr, *d_per = nullptr;
+    float *d_tc_hi = nullptr, *d_tc_lo = nullptr;  // tensor-core M2L operators
+    float *g_hi = nullptr, *g_lo = nullptr;        // tensor-core M2L staged source grid
+    size_t g_cap = 0;
     int* d_slots = nullptr;  // [8][189]
     // workspace
     int64_t cap_n = 0;
@@ -109,6 +113,12 @@ vfmm_status ensure_ops(vfmm_ctx* c) {
     CK(up(c->hops.l2l, &c->d_l2l), "upload l2l");
     CK(up(c->hops.m2l, &c->d_m2l), "upload m2l");
     CK(up(c->hops.per, &c->d_per), "upload periodic");
+    dfree(c->d_tc_hi);
+    dfree(c->d_tc_lo);
+    if (!c->hops.m2l_tc_hi.empty()) {
+        CK(up(c->hops.m2l_tc_hi, &c->d_tc_hi), "upload m2l tc hi");
+        CK(up(c->hops.m2l_tc_lo, &c->d_tc_lo), "upload m2l tc lo");
+    }
     if (!c->d_slots) {
         // interaction list per parity: o_a in {-2-b_a .. 3-b_a}, minus |o|inf <= 1 (189 cells)
         std::vector<int> slots;
@@ -324,10 +334,31 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
     CK(cudaEventRecord(c->ev[5], st), "event");
     // ---- M2L at every level (writes L_l), then periodic images + L2L top-down (adds) ----
     if (use_far) {
+        const char* m2l_env = getenv("VFMM_M2L");
+        const bool allow_tc = !(m2l_env && strcmp(m2l_env, "simt") == 0) && c->d_tc_hi;
         for (int l = 1; l <= depth; ++l) {
-            launch_m2l(c->d_m2l, c->d_slots, p, H.KP, H.NR, Mlev(l), Llev(l), l,
-                       P.image_levels > 0, st);
-            ++nl;
+            if (allow_tc && m2l_tc_supported(p, l)) {
+                const size_t need = m2l_tc_grid_floats(l);
+                if (need > c->g_cap) {
+                    dfree(c->g_hi);
+                    dfree(c->g_lo);
+                    c->g_cap = 0;
+                    CK(cudaMalloc((void**)&c->g_hi, need * sizeof(float)), "alloc m2l grid");
+                    CK(cudaMalloc((void**)&c->g_lo, need * sizeof(float)), "alloc m2l grid");
+                    c->g_cap = need;
+                }
+                const int rc = launch_m2l_tc(c->d_tc_hi, c->d_tc_lo, c->d_slots, p, Mlev(l),
+                                             Llev(l), l, P.image_levels > 0, c->g_hi, c->g_lo, st);
+                if (rc != 0) {
+                    c->err = "tensor-map encode failed for tcgen05 M2L";
+                    return VFMM_ECUDA;
+                }
+                nl += 2;
+            } else {
+                launch_m2l(c->d_m2l, c->d_slots, p, H.KP, H.NR, Mlev(l), Llev(l), l,
+                           P.image_levels > 0, st);
+                ++nl;
+            }
             S.n_m2l += (int64_t)189 << (3 * l);
         }
         CK(cudaGetLastError(), "m2l kernels");
@@ -474,6 +505,10 @@ void vfmm_destroy(vfmm_ctx* c) {
     dfree(c->d_m2l);
     dfree(c->d_per);
     dfree(c->d_slots);
+    dfree(c->d_tc_hi);
+    dfree(c->d_tc_lo);
+    dfree(c->g_hi);
+    dfree(c->g_lo);
     for (int b = 0; b < 2; ++b) {
         dfree(c->keys[b]);
         dfree(c->vals[b]);

@@ -357,13 +357,15 @@ __global__ void __launch_bounds__(64) l2p_combine_kernel(
     const uint32_t* __restrict__ perm, int64_t n, const int* __restrict__ leaf_start, int p,
     float inv_a, const float* __restrict__ Lleaf, int use_near, int use_far,
     float* __restrict__ vel, float* __restrict__ dgam) {
-    extern __shared__ float sm[];
+    // smem: D [ng][28] (q: 9 gradients then 18 Hessian entries, pad); Ls [3][nc]; G; H
+    extern __shared__ float4 l2p_sm4[];
+    float* sm = reinterpret_cast<float*>(l2p_sm4);
     const int nc = (p + 1) * (p + 1);
     const int ng = p * p, nh = (p - 1) * (p - 1);
-    float* Ls = sm;                    // [3][nc]
-    float* G = Ls + 3 * nc;            // [3 comp][3 axis][ng]
-    float* H = G + 9 * ng;             // [3 comp][6 pair][nh]  pairs: xx xy xz yy yz zz
-    float* Rw = H + 18 * (nh > 0 ? nh : 1);  // [ng][65]
+    const float4* D4 = l2p_sm4;
+    float* Ls = sm + ng * 28;
+    float* G = Ls + 3 * nc;
+    float* H = G + 9 * ng;
     const int leaf = blockIdx.x;
     const int s = leaf_start[leaf], e = leaf_start[leaf + 1];
     if (e == s) return;
@@ -383,6 +385,15 @@ __global__ void __launch_bounds__(64) l2p_combine_kernel(
                                     threadIdx.x, 64);
         }
         __syncthreads();
+        // transpose into D[k][q]: q < 9 -> G[q][k]; 9 <= q < 27 -> H[q-9][k] (0 beyond nh)
+        for (int i = threadIdx.x; i < ng * 28; i += 64) {
+            const int k = i / 28, q = i - k * 28;
+            float v = 0.f;
+            if (q < 9) v = G[q * ng + k];
+            else if (q < 27 && k < nh) v = H[(q - 9) * nh + k];
+            sm[i] = v;
+        }
+        __syncthreads();
     }
     for (int b = s; b < e; b += 64) {
         const int j = b + threadIdx.x;
@@ -395,75 +406,103 @@ __global__ void __launch_bounds__(64) l2p_combine_kernel(
             gi[2] = s6[5 * n + j];
         }
         if (use_far && act) {
-            float* R = Rw + threadIdx.x;
-            solid_R_packed(s6[j] * inv_a, s6[n + j] * inv_a, s6[2 * n + j] * inv_a, p - 1, R, 65,
-                           false);
-            // weights: Re(n,0) x1, Re(n,m) x2, Im(n,m) x(-2)  ->  value = sum D[k] * Rw[k]
-            for (int k = 1; k < ng; ++k) {
-                const int nn = (int)sqrtf((float)k + 0.5f);
-                const int jj = k - nn * nn;
-                if (jj > 0) R[k * 65] *= (jj & 1) ? 2.f : -2.f;
+            const float x = s6[j] * inv_a, y = s6[n + j] * inv_a, z = s6[2 * n + j] * inv_a;
+            float acc[28];
+#pragma unroll
+            for (int q = 0; q < 28; ++q) acc[q] = 0.f;
+            // R_n^m(z/a) by recurrence (m outer, n inner, n <= p-1), accumulated on the fly:
+            // value_q = sum_k D[k][q] w_k, w = R_re (m = 0); 2 R_re, -2 R_im (m > 0)
+            const float r2 = x * x + y * y + z * z;
+            float dre = 1.f, dim = 0.f;
+            const int pm = p - 1;
+            for (int m = 0; m <= pm; ++m) {
+                if (m > 0) {
+                    const float sc = -0.5f / (float)m;
+                    const float nre = sc * (x * dre - y * dim);
+                    const float nim = sc * (x * dim + y * dre);
+                    dre = nre;
+                    dim = nim;
+                }
+                float p2re = 0.f, p2im = 0.f, p1re = 0.f, p1im = 0.f;
+                for (int nn = m; nn <= pm; ++nn) {
+                    float cre, cim;
+                    if (nn == m) {
+                        cre = dre;
+                        cim = dim;
+                    } else if (nn == m + 1) {
+                        cre = z * dre;
+                        cim = z * dim;
+                    } else {
+                        const float inv = 1.f / (float)((nn + m) * (nn - m));
+                        const float aa = (2.f * nn - 1.f) * z;
+                        cre = (aa * p1re - r2 * p2re) * inv;
+                        cim = (aa * p1im - r2 * p2im) * inv;
+                    }
+                    p2re = p1re;
+                    p2im = p1im;
+                    p1re = cre;
+                    p1im = cim;
+                    const float4* Dr = D4 + pk_re(nn, m) * 7;
+                    if (m == 0) {
+#pragma unroll
+                        for (int q4 = 0; q4 < 7; ++q4) {
+                            const float4 d = Dr[q4];
+                            acc[4 * q4 + 0] = fmaf(d.x, cre, acc[4 * q4 + 0]);
+                            acc[4 * q4 + 1] = fmaf(d.y, cre, acc[4 * q4 + 1]);
+                            acc[4 * q4 + 2] = fmaf(d.z, cre, acc[4 * q4 + 2]);
+                            acc[4 * q4 + 3] = fmaf(d.w, cre, acc[4 * q4 + 3]);
+                        }
+                    } else {
+                        const float4* Di = D4 + pk_im(nn, m) * 7;
+                        const float wr = 2.f * cre, wi = -2.f * cim;
+#pragma unroll
+                        for (int q4 = 0; q4 < 7; ++q4) {
+                            const float4 d = Dr[q4], f = Di[q4];
+                            acc[4 * q4 + 0] = fmaf(d.x, wr, fmaf(f.x, wi, acc[4 * q4 + 0]));
+                            acc[4 * q4 + 1] = fmaf(d.y, wr, fmaf(f.y, wi, acc[4 * q4 + 1]));
+                            acc[4 * q4 + 2] = fmaf(d.z, wr, fmaf(f.z, wi, acc[4 * q4 + 2]));
+                            acc[4 * q4 + 3] = fmaf(d.w, wr, fmaf(f.w, wi, acc[4 * q4 + 3]));
+                        }
+                    }
+                }
             }
-            float gr[3][3];  // gr[c][axis] = d_axis phi_c (scaled form)
-            for (int c = 0; c < 3; ++c)
-                for (int ax = 0; ax < 3; ++ax) {
-                    const float* D = G + (c * 3 + ax) * ng;
-                    float a = 0.f;
-                    for (int k = 0; k < ng; ++k) a = fmaf(D[k], R[k * 65], a);
-                    gr[c][ax] = a;
-                }
-            float hs[3][6];
-            for (int c = 0; c < 3; ++c)
-                for (int q = 0; q < 6; ++q) {
-                    const float* D = H + (c * 6 + q) * nh;
-                    float a = 0.f;
-                    for (int k = 0; k < nh; ++k) a = fmaf(D[k], R[k * 65], a);
-                    hs[c][q] = a;
-                }
-            const float sg = inv4pi * inv_a * inv_a;        // grad scale
-            const float sh = sg * inv_a;                    // hessian scale
-            // u = curl(phi)/4pi
-            u[0] = sg * (gr[2][1] - gr[1][2]);
-            u[1] = sg * (gr[0][2] - gr[2][0]);
-            u[2] = sg * (gr[1][0] - gr[0][1]);
-            // Hessian h[c][a][b]
+            // acc[c*3 + axis] = d_axis phi_c ; acc[9 + c*6 + q] = Hessian pair q of phi_c
+            const float sg = inv4pi * inv_a * inv_a;  // gradient scale
+            const float sh = sg * inv_a;              // Hessian scale
+            u[0] = sg * (acc[2 * 3 + 1] - acc[1 * 3 + 2]);
+            u[1] = sg * (acc[0 * 3 + 2] - acc[2 * 3 + 0]);
+            u[2] = sg * (acc[1 * 3 + 0] - acc[0 * 3 + 1]);
             auto h = [&](int c, int a, int b2) -> float {
                 const int lo = a < b2 ? a : b2, hi = a < b2 ? b2 : a;
                 const int q = lo == 0 ? hi : (lo == 1 ? 2 + hi : 5);
-                return hs[c][q];
+                return acc[9 + c * 6 + q];
             };
-            if (SCHEME == 0) {
-                // sdot_a = eps_abc g_k d_k d_b phi_c : J[a][k] = d_k u_a
-                float J[3][3];
-                for (int k = 0; k < 3; ++k) {
-                    J[0][k] = h(2, k, 1) - h(1, k, 2);
-                    J[1][k] = h(0, k, 2) - h(2, k, 0);
-                    J[2][k] = h(1, k, 0) - h(0, k, 1);
-                }
-                for (int a = 0; a < 3; ++a)
-                    sd[a] = sh * (J[a][0] * gi[0] + J[a][1] * gi[1] + J[a][2] * gi[2]);
-            } else {
-                float J[3][3];
-                for (int k = 0; k < 3; ++k) {
-                    J[0][k] = h(2, k, 1) - h(1, k, 2);
-                    J[1][k] = h(0, k, 2) - h(2, k, 0);
-                    J[2][k] = h(1, k, 0) - h(0, k, 1);
-                }
-                for (int a = 0; a < 3; ++a)  // (grad u)^T g : sum_k J[k][a] g_k
-                    sd[a] = sh * (J[0][a] * gi[0] + J[1][a] * gi[1] + J[2][a] * gi[2]);
+            float J[3][3];  // J[a][k] = d_k u_a / sh
+#pragma unroll
+            for (int k = 0; k < 3; ++k) {
+                J[0][k] = h(2, k, 1) - h(1, k, 2);
+                J[1][k] = h(0, k, 2) - h(2, k, 0);
+                J[2][k] = h(1, k, 0) - h(0, k, 1);
+            }
+#pragma unroll
+            for (int a2 = 0; a2 < 3; ++a2) {
+                if (SCHEME == 0)
+                    sd[a2] = sh * (J[a2][0] * gi[0] + J[a2][1] * gi[1] + J[a2][2] * gi[2]);
+                else
+                    sd[a2] = sh * (J[0][a2] * gi[0] + J[1][a2] * gi[1] + J[2][a2] * gi[2]);
             }
         }
         if (act) {
             if (use_near) {
-                for (int a = 0; a < 3; ++a) {
-                    u[a] += near6[a * n + j];
-                    sd[a] += near6[(3 + a) * n + j];
+                for (int a2 = 0; a2 < 3; ++a2) {
+                    u[a2] += near6[a2 * n + j];
+                    sd[a2] += near6[(3 + a2) * n + j];
                 }
             }
             const int64_t i = perm[j];
-            for (int a = 0; a < 3; ++a) {
-                vel[a * n + i] = u[a];
-                dgam[a * n + i] = sd[a];
+            for (int a2 = 0; a2 < 3; ++a2) {
+                vel[a2 * n + i] = u[a2];
+                dgam[a2 * n + i] = sd[a2];
             }
         }
     }
@@ -533,7 +572,7 @@ void launch_l2p_combine(const float* sorted6, const float* near6, const uint32_t
                         const float* L_leaf, int scheme, int use_near, int use_far,
                         float* vel, float* dgam, cudaStream_t st) {
     const int nc = (p + 1) * (p + 1), ng = p * p, nh = (p - 1) * (p - 1);
-    const size_t smem = sizeof(float) * (3 * nc + 9 * ng + 18 * (nh > 0 ? nh : 1) + ng * 65);
+    const size_t smem = sizeof(float) * (ng * 28 + 3 * nc + 9 * ng + 18 * (nh > 0 ? nh : 1));
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(l2p_combine_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,

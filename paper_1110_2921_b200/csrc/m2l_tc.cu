@@ -1,0 +1,432 @@
+// m2l_tc.cu -- M2L (Eq. 11; operators of Cheng et al.) on the
+// 5th-generation tensor cores: tcgen05.mma kind::tf32 with a 3xTF32 split
+// (A_hi B_hi + A_hi B_lo + A_lo B_hi) so the result keeps FP32 accuracy, operands staged by
+// TMA (SWIZZLE_128B, K-major), accumulators in TMEM.
+//
+// The M2L of level l is a batch of dense GEMMs, one per (target parity pi, offset o):
+//   D[r][(px,c)] += sum_k T_o[r][k] * Msrc[(px + dx, c)][k]
+// A = T_o (128 output coefficients r x 128 input coefficients k, zero padded, one per slot),
+// B = a "slab" of source multipoles: one x-row of XT <= 32 parent cells x 3 strength
+// components = N <= 96 rows, read from a parity-major, halo-padded copy of the level's
+// multipoles (m2l_stage_kernel) so every (target row, offset) maps to one TMA box.
+// A CTA owns T = 4 target rows (Py, Pz) of one parity: 4 accumulators of 128 x N fp32 in
+// TMEM; operators are loaded once per CTA per offset and reused by the 4 rows.
+//
+// Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM alloc + MMA issuer,
+// warps 2-5 = epilogue (TMEM -> registers -> L in Morton order).
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include "vfmm_internal.h"
+
+namespace vfmm {
+
+namespace {
+
+constexpr int TC_T = 4;        // target rows per CTA
+constexpr int TC_NKC = 4;      // K chunks of 32 floats (128 B)
+constexpr int TC_AST = 2;      // A (operator) pipeline stages
+constexpr int TC_BST = 4;      // B (slab) pipeline stages
+constexpr int A_BYTES = 128 * 128;  // one K chunk of one operator half (hi or lo): 16 KB
+constexpr int B_BYTES = 96 * 128;   // one K chunk of one slab half: <= 12 KB
+constexpr int TC_THREADS = 192;
+constexpr size_t TC_SMEM = 1024 + (size_t)TC_AST * 2 * A_BYTES + (size_t)TC_BST * 2 * B_BYTES + 256;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    const uint32_t a = smem_u32(b);
+    uint32_t done = 0;
+    uint32_t spins = 0;
+    while (!done) {
+        if (++spins == (1u << 30)) asm volatile("trap;");  // watchdog: never hang the GPU
+        asm volatile(
+            "{\n\t.reg .pred p;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(done)
+            : "r"(a), "r"(parity)
+            : "memory");
+    }
+}
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int c0, int c1, int c2, int c3, int c4) {
+    asm volatile(
+        "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
+        "[%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(c3), "r"(c4),
+        "r"(smem_u32(bar))
+        : "memory");
+}
+// shared-memory matrix descriptor: K-major, SWIZZLE_128B, 8-row atoms of 1024 B
+__device__ __forceinline__ uint64_t sw128_desc(const void* p) {
+    const uint64_t addr = smem_u32(p);
+    uint64_t d = (addr >> 4) & 0x3FFFull;  // start address
+    d |= 1ull << 16;                        // LBO (unused for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;       // SBO = 1024 B between 8-row groups
+    d |= 1ull << 46;                        // version (sm_100)
+    d |= 2ull << 61;                        // SWIZZLE_128B
+    return d;
+}
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                         uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::
+                     "r"(smem_u32(bar))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+
+__device__ __forceinline__ uint32_t spread3t(uint32_t v) {
+    v &= 0x3ffu;
+    v = (v | (v << 16)) & 0x030000FFu;
+    v = (v | (v << 8)) & 0x0300F00Fu;
+    v = (v | (v << 4)) & 0x030C30C3u;
+    v = (v | (v << 2)) & 0x09249249u;
+    return v;
+}
+
+struct TcParams {
+    int nP;     // parent cells per axis at this level (2^(l-1))
+    int XT;     // parents per B tile row (<= 32)
+    int ntx;    // x tiles per row (nP / XT)
+    int N;      // 3 * XT
+    int rows;   // target rows per parity = nP * nP * ntx
+    int nc;     // (p+1)^2 <= 128
+    int level;
+    const int* slots;  // [8][189] M2L slot per target parity
+    float* L;          // local expansions of this level, Morton [cell][3][nc]
+};
+
+__global__ void __launch_bounds__(TC_THREADS, 1)
+    m2l_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant__ CUtensorMap tmA_lo,
+                  const __grid_constant__ CUtensorMap tmB_hi, const __grid_constant__ CUtensorMap tmB_lo,
+                  TcParams P) {
+    extern __shared__ uint8_t tc_raw[];
+    uint8_t* sm = reinterpret_cast<uint8_t*>(((uintptr_t)tc_raw + 1023) & ~(uintptr_t)1023);
+    uint8_t* Abuf = sm;                                  // [AST][hi|lo][16 KB]
+    uint8_t* Bbuf = sm + TC_AST * 2 * A_BYTES;           // [BST][hi|lo][12 KB]
+    uint64_t* bars = reinterpret_cast<uint64_t*>(Bbuf + TC_BST * 2 * B_BYTES);
+    uint64_t* a_full = bars;
+    uint64_t* a_empty = bars + TC_AST;
+    uint64_t* b_full = bars + 2 * TC_AST;
+    uint64_t* b_empty = bars + 2 * TC_AST + TC_BST;
+    uint64_t* acc_full = bars + 2 * TC_AST + 2 * TC_BST;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int groups = P.rows / TC_T;
+    const int pi = blockIdx.x / groups;
+    const int g = blockIdx.x - pi * groups;
+    const int pix = pi & 1, piy = (pi >> 1) & 1, piz = (pi >> 2) & 1;
+    const uint32_t tmem_cols = TC_T * P.N <= 256 ? 256u : 512u;
+
+    if (warp == 0 && lane == 0) {
+        for (int i = 0; i < TC_AST; ++i) {
+            mbar_init(&a_full[i], 1);
+            mbar_init(&a_empty[i], 1);
+        }
+        for (int i = 0; i < TC_BST; ++i) {
+            mbar_init(&b_full[i], 1);
+            mbar_init(&b_empty[i], 1);
+        }
+        mbar_init(acc_full, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 1) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                         smem_u32(tmem_slot)),
+                     "r"(tmem_cols));
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ===================== TMA producer =====================
+        if (lane == 0) {
+            int sa = 0, sb = 0;
+            uint32_t pa = 0, pb = 0;
+            const uint32_t b_tx = 2u * (uint32_t)P.N * 128u;
+            for (int oi = 0; oi < 189; ++oi) {
+                const int slot = P.slots[pi * 189 + oi];
+                const int ox = slot / 49 - 3, oy = (slot / 7) % 7 - 3, oz = slot % 7 - 3;
+                const int sx = pix + ox, sy = piy + oy, sz = piz + oz;
+                const int dx = sx >> 1, dy = sy >> 1, dz = sz >> 1;  // floor division
+                const int pis = (sx & 1) | ((sy & 1) << 1) | ((sz & 1) << 2);
+                for (int kc = 0; kc < TC_NKC; ++kc) {
+                    mbar_wait(&a_empty[sa], pa ^ 1);
+                    mbar_expect_tx(&a_full[sa], 2u * A_BYTES);
+                    tma_load_3d(Abuf + (sa * 2 + 0) * A_BYTES, &tmA_hi, &a_full[sa], kc * 32, 0, slot);
+                    tma_load_3d(Abuf + (sa * 2 + 1) * A_BYTES, &tmA_lo, &a_full[sa], kc * 32, 0, slot);
+                    if (++sa == TC_AST) {
+                        sa = 0;
+                        pa ^= 1;
+                    }
+                    for (int t = 0; t < TC_T; ++t) {
+                        const int row = g * TC_T + t;
+                        const int tx = row % P.ntx, rest = row / P.ntx;
+                        const int py = rest % P.nP, pz = rest / P.nP;
+                        mbar_wait(&b_empty[sb], pb ^ 1);
+                        mbar_expect_tx(&b_full[sb], b_tx);
+                        const int c1 = 3 * (2 + tx * P.XT + dx);
+                        tma_load_5d(Bbuf + (sb * 2 + 0) * B_BYTES, &tmB_hi, &b_full[sb], kc * 32, c1,
+                                    2 + py + dy, 2 + pz + dz, pis);
+                        tma_load_5d(Bbuf + (sb * 2 + 1) * B_BYTES, &tmB_lo, &b_full[sb], kc * 32, c1,
+                                    2 + py + dy, 2 + pz + dz, pis);
+                        if (++sb == TC_BST) {
+                            sb = 0;
+                            pb ^= 1;
+                        }
+                    }
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ===================== MMA issuer =====================
+        // instruction descriptor: D f32, A/B tf32, both K-major, N, M = 128
+        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(P.N >> 3) << 17) |
+                               ((uint32_t)(128 >> 4) << 24);
+        int sa = 0, sb = 0;
+        uint32_t pa = 0, pb = 0;
+        for (int oi = 0; oi < 189; ++oi) {
+            for (int kc = 0; kc < TC_NKC; ++kc) {
+                mbar_wait(&a_full[sa], pa);
+                tc_fence_after();
+                const uint64_t ahi = sw128_desc(Abuf + (sa * 2 + 0) * A_BYTES);
+                const uint64_t alo = sw128_desc(Abuf + (sa * 2 + 1) * A_BYTES);
+                for (int t = 0; t < TC_T; ++t) {
+                    mbar_wait(&b_full[sb], pb);
+                    tc_fence_after();
+                    const uint64_t bhi = sw128_desc(Bbuf + (sb * 2 + 0) * B_BYTES);
+                    const uint64_t blo = sw128_desc(Bbuf + (sb * 2 + 1) * B_BYTES);
+                    const uint32_t d = tmem + (uint32_t)(t * P.N);
+                    if (lane == 0) {
+#pragma unroll
+                        for (int ks = 0; ks < 4; ++ks) {  // K = 8 tf32 = 32 B per MMA
+                            const uint64_t adv = (uint64_t)(ks * 2);
+                            const uint32_t acc = (oi | kc | ks) != 0 ? 1u : 0u;
+                            mma_tf32(d, ahi + adv, bhi + adv, idesc, acc);
+                            mma_tf32(d, ahi + adv, blo + adv, idesc, 1u);
+                            mma_tf32(d, alo + adv, bhi + adv, idesc, 1u);
+                        }
+                        mma_commit(&b_empty[sb]);
+                    }
+                    __syncwarp();
+                    if (++sb == TC_BST) {
+                        sb = 0;
+                        pb ^= 1;
+                    }
+                }
+                if (lane == 0) mma_commit(&a_empty[sa]);
+                __syncwarp();
+                if (++sa == TC_AST) {
+                    sa = 0;
+                    pa ^= 1;
+                }
+            }
+        }
+        if (lane == 0) mma_commit(acc_full);
+        __syncwarp();
+    } else {
+        // ===================== epilogue: TMEM -> L (Morton) =====================
+        mbar_wait(acc_full, 0);
+        tc_fence_after();
+        const int quarter = warp & 3;  // TMEM lanes [32 quarter, 32 quarter + 32)
+        const int r = quarter * 32 + lane;
+        for (int t = 0; t < TC_T; ++t) {
+            const int row = g * TC_T + t;
+            const int tx = row % P.ntx, rest = row / P.ntx;
+            const int py = rest % P.nP, pz = rest / P.nP;
+            const uint32_t cy = spread3t(2 * py + piy) << 1, cz = spread3t(2 * pz + piz) << 2;
+            for (int c0 = 0; c0 < P.N; c0 += 16) {
+                uint32_t v[16];
+                const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(t * P.N + c0);
+                asm volatile(
+                    "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, "
+                    "%9, %10, %11, %12, %13, %14, %15}, [%16];"
+                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                      "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+                      "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                    : "r"(taddr));
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+                if (r < P.nc) {
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const int col = c0 + j;
+                        const int px = tx * P.XT + col / 3, comp = col % 3;
+                        const uint32_t cell = spread3t(2 * px + pix) | cy | cz;
+                        P.L[((int64_t)cell * 3 + comp) * P.nc + r] = __uint_as_float(v[j]);
+                    }
+                }
+            }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    if (warp == 1)
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
+                     "r"(tmem_cols));
+}
+
+// Morton level multipoles -> parity-major halo-padded grid (hi = tf32 part, lo = rest):
+// grid[pi'][Z][Y][X][comp][128], parent coords (X-2, Y-2, Z-2) wrapped (periodic) or zero.
+__global__ void m2l_stage_kernel(const float* __restrict__ M, int nP, int periodic, int nc,
+                                 float* __restrict__ ghi, float* __restrict__ glo) {
+    const int Xp = nP + 4;
+    const int64_t total = (int64_t)8 * Xp * Xp * Xp * 3 * 128;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int k = (int)(i & 127);
+        int64_t q = i >> 7;
+        const int comp = (int)(q % 3);
+        q /= 3;
+        const int X = (int)(q % Xp);
+        q /= Xp;
+        const int Y = (int)(q % Xp);
+        q /= Xp;
+        const int Z = (int)(q % Xp);
+        const int ps = (int)(q / Xp);
+        int px = X - 2, py = Y - 2, pz = Z - 2;
+        float v = 0.f;
+        const bool inside = px >= 0 && px < nP && py >= 0 && py < nP && pz >= 0 && pz < nP;
+        if (k < nc && (periodic || inside)) {
+            px = (px + nP) % nP;
+            py = (py + nP) % nP;
+            pz = (pz + nP) % nP;
+            const uint32_t cell = spread3t(2 * px + (ps & 1)) | (spread3t(2 * py + ((ps >> 1) & 1)) << 1) |
+                                  (spread3t(2 * pz + ((ps >> 2) & 1)) << 2);
+            v = M[((int64_t)cell * 3 + comp) * nc + k];
+        }
+        const float hi = __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+        ghi[i] = hi;
+        glo[i] = v - hi;
+    }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    if (!fn) {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (PFN_cuTensorMapEncodeTiled_v12000)p;
+    }
+    return fn;
+}
+
+}  // namespace
+
+bool m2l_tc_supported(int p, int level) {
+    return (p + 1) * (p + 1) <= 128 && level >= 5 && get_encode() != nullptr;
+}
+
+size_t m2l_tc_grid_floats(int level) {
+    const int64_t nP = (int64_t)1 << (level - 1), Xp = nP + 4;
+    return (size_t)(8 * Xp * Xp * Xp * 3 * 128);
+}
+
+int launch_m2l_tc(const float* ops_hi, const float* ops_lo, const int* il_slots, int p,
+                  const float* M_l, float* L_l, int level, int periodic, float* ghi, float* glo,
+                  cudaStream_t st) {
+    const int nc = (p + 1) * (p + 1);
+    const int nP = 1 << (level - 1);
+    const int Xp = nP + 4;
+    // 1) stage the level's multipoles into the halo-padded parity-major grid
+    {
+        const int64_t total = (int64_t)8 * Xp * Xp * Xp * 3 * 128;
+        int64_t blocks = (total + 255) / 256;
+        if (blocks > 148 * 64) blocks = 148 * 64;
+        m2l_stage_kernel<<<(unsigned)blocks, 256, 0, st>>>(M_l, nP, periodic, nc, ghi, glo);
+    }
+    // 2) tensor maps
+    auto enc = get_encode();
+    if (!enc) return -1;
+    CUtensorMap mAh, mAl, mBh, mBl;
+    {
+        cuuint64_t dims[3] = {128, 128, 343};
+        cuuint64_t strides[2] = {128 * 4, 128 * 128 * 4};
+        cuuint32_t box[3] = {32, 128, 1};
+        cuuint32_t es[3] = {1, 1, 1};
+        if (enc(&mAh, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)ops_hi, dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return -2;
+        if (enc(&mAl, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)ops_lo, dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return -2;
+    }
+    const int XT = nP < 32 ? nP : 32;
+    const int N = 3 * XT;
+    {
+        cuuint64_t dims[5] = {128, (cuuint64_t)3 * Xp, (cuuint64_t)Xp, (cuuint64_t)Xp, 8};
+        cuuint64_t strides[4] = {128 * 4, (cuuint64_t)3 * Xp * 128 * 4,
+                                 (cuuint64_t)Xp * 3 * Xp * 128 * 4,
+                                 (cuuint64_t)Xp * Xp * 3 * Xp * 128 * 4};
+        cuuint32_t box[5] = {32, (cuuint32_t)N, 1, 1, 1};
+        cuuint32_t es[5] = {1, 1, 1, 1, 1};
+        if (enc(&mBh, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, (void*)ghi, dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return -3;
+        if (enc(&mBl, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, (void*)glo, dims, strides, box, es,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return -3;
+    }
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(m2l_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC_SMEM);
+        attr = true;
+    }
+    TcParams P;
+    P.nP = nP;
+    P.XT = XT;
+    P.ntx = nP / XT;
+    P.N = N;
+    P.rows = nP * nP * P.ntx;
+    P.nc = nc;
+    P.level = level;
+    P.slots = il_slots;
+    P.L = L_l;
+    const unsigned grid = (unsigned)(8 * (P.rows / TC_T));
+    m2l_tc_kernel<<<grid, TC_THREADS, TC_SMEM, st>>>(mAh, mAl, mBh, mBl, P);
+    return 0;
+}
+
+}  // namespace vfmm

@@ -16,6 +16,7 @@
 //   L2L (parent c -> child c', d = (c'-c)/a_p):   Lt_c[n,m] = sum_{k>=n} 2^-(n+1) R_{k-n}^{l-m}(d) Lt_p[k,l]
 //   periodic (unit box, rings of 3x supercells): see build_periodic below.
 #include <cmath>
+#include <cstring>
 #include <complex>
 #include <vector>
 
@@ -210,6 +211,24 @@ std::vector<double> build_periodic(int p, int levels) {
 }
 
 // store a packed row-major matrix A (nc x nc) transposed + padded at slot `slot`
+// row-major [slot][128][128] tf32 hi part (low 13 mantissa bits cleared) and FP32 remainder
+void store_tc(std::vector<float>& hi, std::vector<float>& lo, int slot,
+              const std::vector<double>& A, int nc) {
+    float* H = hi.data() + (size_t)slot * 128 * 128;
+    float* Lo = lo.data() + (size_t)slot * 128 * 128;
+    for (int r = 0; r < nc; ++r)
+        for (int k = 0; k < nc; ++k) {
+            const float v = (float)A[(size_t)r * nc + k];
+            uint32_t u;
+            memcpy(&u, &v, 4);
+            u &= 0xFFFFE000u;
+            float h;
+            memcpy(&h, &u, 4);
+            H[(size_t)r * 128 + k] = h;
+            Lo[(size_t)r * 128 + k] = v - h;
+        }
+}
+
 void store_t(std::vector<float>& dst, int slot, const std::vector<double>& A, int nc, int KP,
              int NR) {
     float* base = dst.data() + (size_t)slot * KP * NR;
@@ -230,6 +249,9 @@ void build_host_ops(int p, int image_levels, HostOps* out) {
     out->l2l.assign(8 * msz, 0.f);
     out->m2l.assign(343 * msz, 0.f);
     out->per.assign(msz, 0.f);
+    const bool tc = nc <= 128;
+    out->m2l_tc_hi.assign(tc ? (size_t)343 * 128 * 128 : 0, 0.f);
+    out->m2l_tc_lo.assign(tc ? (size_t)343 * 128 * 128 : 0, 0.f);
     for (int ch = 0; ch < 8; ++ch) {
         const double dx = (((ch >> 0) & 1) - 0.5) * 0.5;
         const double dy = (((ch >> 1) & 1) - 0.5) * 0.5;
@@ -241,8 +263,9 @@ void build_host_ops(int p, int image_levels, HostOps* out) {
         for (int oy = -3; oy <= 3; ++oy)
             for (int oz = -3; oz <= 3; ++oz) {
                 if (std::max(std::abs(ox), std::max(std::abs(oy), std::abs(oz))) <= 1) continue;
-                store_t(out->m2l, m2l_slot(ox, oy, oz),
-                        pack_matrix(m2l_full(-ox, -oy, -oz, p), p), nc, out->KP, out->NR);
+                const auto T = pack_matrix(m2l_full(-ox, -oy, -oz, p), p);
+                store_t(out->m2l, m2l_slot(ox, oy, oz), T, nc, out->KP, out->NR);
+                if (tc) store_tc(out->m2l_tc_hi, out->m2l_tc_lo, m2l_slot(ox, oy, oz), T, nc);
             }
     out->per_d = build_periodic(p, image_levels);
     store_t(out->per, 0, out->per_d, nc, out->KP, out->NR);

@@ -38,6 +38,11 @@ __device__ __forceinline__ float ex2_approx(float x) {
     asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
     return y;
 }
+__device__ __forceinline__ float rsqrt_approx(float x) {
+    float y;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
 __device__ __forceinline__ float rcp_approx(float x) {
     float y;
     asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
@@ -74,22 +79,23 @@ __device__ __forceinline__ void pair(float dx, float dy, float dz, float gjx, fl
         f = kc.zeta0 * pf;
         q = kc.zeta0_over_s2 * pq;
     } else {
-        const float rinv = rsqrtf(r2);
+        const float rinv = rsqrt_approx(r2);
         const float e = ex2_approx(r2 * kc.neg_l2e_inv2s2);
         const float rho = r2 * rinv * kc.inv_s_sqrt2;
         const float t = rcp_approx(fmaf(0.5f, rho, 1.f)) - 0.5f;
-        float E = 7.796925861e-02f;
-        E = fmaf(E, t, -2.091334887e-02f);
-        E = fmaf(E, t, -2.338621977e-01f);
-        E = fmaf(E, t, 6.124646918e-02f);
-        E = fmaf(E, t, 6.317173519e-01f);
-        E = fmaf(E, t, 9.666348646e-01f);
-        E = fmaf(E, t, 8.543718279e-01f);
-        E = fmaf(E, t, 2.553956723e-01f);
-        const float Q = fmaf(1.1283791670955126f, rho, E);  // + 2 rho / sqrt(pi)
-        const float g = fmaf(-e, Q, 1.f);
+        // (1/4pi) erfcx(rho) as a polynomial in t, and (1/4pi)(1 - g) = e (E + 2 rho/(4pi sqrt(pi)))
+        float E = 6.204596458e-03f;
+        E = fmaf(E, t, -1.664231425e-03f);
+        E = fmaf(E, t, -1.861016238e-02f);
+        E = fmaf(E, t, 4.873839158e-03f);
+        E = fmaf(E, t, 5.027046960e-02f);
+        E = fmaf(E, t, 7.692235843e-02f);
+        E = fmaf(E, t, 6.798874982e-02f);
+        E = fmaf(E, t, 2.032374185e-02f);
+        const float Q = fmaf(0.0897935610625833f, rho, E);  // 2/(4 pi sqrt(pi)) = 0.0897935...
+        const float g4pi = fmaf(-e, Q, 0.0795774715459476679f);  // g / (4 pi)
         const float rinv2 = rinv * rinv;
-        f = g * rinv2 * rinv * 0.0795774715459476679f;
+        f = g4pi * (rinv2 * rinv);
         q = fmaf(kc.zeta0, e, -3.f * f) * rinv2;
     }
     // c = gamma_j x d

@@ -35,6 +35,8 @@ struct HostOps {
     std::vector<float> m2l;  // 343 offset slots   [343][KP][NR] (|o|inf <= 1 slots zero)
     std::vector<float> per;  // periodic operator  [1][KP][NR]
     std::vector<double> per_d;  // periodic operator row-major [nc][nc] (double, for tests)
+    // tensor-core M2L operands (nc <= 128): row-major [343][128 r][128 k], 3xTF32 split
+    std::vector<float> m2l_tc_hi, m2l_tc_lo;
 };
 
 // Build all operator tables for order p and image_levels (periodic operator is zero for
@@ -84,6 +86,13 @@ void launch_l2p_combine(const float* sorted6, const float* near6, const uint32_t
                         int64_t n, const int* leaf_start, int depth, int p, float a,
                         const float* L_leaf, int scheme, int use_near, int use_far,
                         float* vel, float* dgam, cudaStream_t st);
+
+// m2l_tc.cu (tcgen05, 3xTF32)
+bool m2l_tc_supported(int p, int level);
+size_t m2l_tc_grid_floats(int level);
+int launch_m2l_tc(const float* ops_hi, const float* ops_lo, const int* il_slots, int p,
+                  const float* M_l, float* L_l, int level, int periodic, float* ghi, float* glo,
+                  cudaStream_t st);
 
 // p2p.cu
 struct KernelConsts {

@@ -16,3 +16,5 @@ g = erf(x) - 2.0 / np.sqrt(np.pi) * x * np.exp(-x * x)
 w = np.exp(-x * x) / g
 c = P.polyfit(t - 0.5, erfcx(x), 7, w=w)
 print(", ".join("%.9ef" % v for v in c))
+# p2p.cu folds 1/(4 pi) into the coefficients: (1/4pi)(1 - g) = e (E/4pi + rho 2/(4 pi sqrt(pi)))
+print(", ".join("%.9ef" % (v / (4 * np.pi)) for v in c))
