@@ -89,6 +89,7 @@ typedef struct {
     int64_t n_m2m, n_l2l; /* child-parent translations                                     */
     int32_t depth_used;
     int32_t n_kernel_launches; /* kernels launched by the last evaluate                  */
+    int64_t bytes_sent, bytes_recv; /* distributed contexts: LET + halo bytes of this rank */
 } vfmm_stats;
 
 /* ABI version this library was built with (VFMM_ABI_VERSION). */
@@ -115,6 +116,43 @@ vfmm_status vfmm_create(vfmm_ctx** ctx, const vfmm_params* prm, int device);
    reported by vfmm_sync_status(). */
 vfmm_status vfmm_evaluate(vfmm_ctx* ctx, int64_t n, const float* pos, const float* gamma,
                           float* vel, float* dgamma, void* cuda_stream);
+
+/* ---- multi-GPU: Morton-range spatial decomposition + local-essential-tree exchange ----
+   (the paper's multi-GPU runs.)  Rank r of R
+   (R in {1, 2, 4, 8}) owns the Morton leaf range [r 8^L/R, (r+1) 8^L/R) at depth L
+   (vfmm_partition); every rank passes only particles inside its range (others are flagged
+   VFMM_EDOMAIN) and gets u, dgamma for them in its own input order.  depth must be set
+   explicitly (>= 2).  Halo particles and LET multipoles travel over NCCL (grouped
+   send/recv + all-gather on the compute stream). */
+
+/* Write a fresh NCCL unique id (128 bytes) to host memory `out128` (call on one rank and
+   broadcast it, e.g. with torch.distributed).  VFMM_ENCCL if libnccl.so.2 is unavailable. */
+vfmm_status vfmm_nccl_get_unique_id(void* out128);
+
+/* Collective: create a context for rank `rank` of `nranks` on `device`, initialising an NCCL
+   communicator from `nccl_id128` (host, 128 bytes).  prm->depth must be >= 2. */
+vfmm_status vfmm_create_nccl(vfmm_ctx** ctx, const vfmm_params* prm, int device,
+                             const void* nccl_id128, int nranks, int rank);
+
+/* Owned Morton leaf range [*leaf_lo, *leaf_hi) of `rank` for depth L and `nranks` ranks
+   (host helper for partitioning inputs).  VFMM_EINVAL unless nranks in {1,2,4,8}. */
+vfmm_status vfmm_partition(int depth, int nranks, int rank, int64_t* leaf_lo, int64_t* leaf_hi);
+
+/* Test mode: run the distributed algorithm for `nranks` LOGICAL ranks on this context's one
+   GPU -- every phase of every rank in lockstep, exchanges as device-to-device copies -- so
+   the partition / halo / LET logic can be validated on a single GPU.  Arrays are per rank:
+   n[r] particles at device pointers pos[r], gamma[r] (inside rank r's range), results to
+   vel[r], dgamma[r].  Asynchronous on `cuda_stream` apart from two host syncs per phase. */
+vfmm_status vfmm_evaluate_logical(vfmm_ctx* ctx, int nranks, const int64_t* n,
+                                  const float* const* pos, const float* const* gamma,
+                                  float* const* vel, float* const* dgamma, void* cuda_stream);
+
+/* Host-only introspection of the static exchange plan of `rank` (no GPU needed): kind 0 =
+   halo particle leaves (depth level), kind k in [2, depth] = LET multipole cells of level k;
+   dir 0 = ids this rank receives from `peer`, dir 1 = ids it sends to `peer`.  Writes up to
+   `cap` ids (ascending Morton index) to `out` (may be NULL) and the full count to *count. */
+vfmm_status vfmm_dist_plan(int depth, int nranks, int rank, int periodic, int kind, int dir,
+                           int peer, int32_t* out, int64_t cap, int64_t* count);
 
 /* Same as vfmm_evaluate but every buffer is HOST memory (pinned or pageable): copies in,
    evaluates on the context's internal stream, copies out, synchronizes. */

@@ -50,7 +50,8 @@ class c_stats(ctypes.Structure):
                 ("ms_total", "ms_keys", "ms_sort", "ms_tree", "ms_p2m", "ms_m2m", "ms_m2l",
                  "ms_l2l", "ms_l2p", "ms_p2p")] + \
                [(k, ctypes.c_int64) for k in ("n_p2p_pairs", "n_m2l", "n_m2m", "n_l2l")] + \
-               [("depth_used", ctypes.c_int32), ("n_kernel_launches", ctypes.c_int32)]
+               [("depth_used", ctypes.c_int32), ("n_kernel_launches", ctypes.c_int32),
+                ("bytes_sent", ctypes.c_int64), ("bytes_recv", ctypes.c_int64)]
 
 
 _LIB = None
@@ -58,7 +59,8 @@ _LIB = None
 EXPORTS = ["vfmm_abi_version", "vfmm_params_default", "vfmm_create", "vfmm_evaluate",
            "vfmm_evaluate_host", "vfmm_sync_status", "vfmm_get_stats", "vfmm_set_params",
            "vfmm_debug_tree", "vfmm_debug_expansions", "vfmm_strerror",
-           "vfmm_last_error_message", "vfmm_destroy"]
+           "vfmm_last_error_message", "vfmm_destroy", "vfmm_nccl_get_unique_id",
+           "vfmm_create_nccl", "vfmm_partition", "vfmm_evaluate_logical", "vfmm_dist_plan"]
 
 
 def load_library(path: str = LIB_PATH):
@@ -86,6 +88,14 @@ def load_library(path: str = LIB_PATH):
     L.vfmm_last_error_message.restype = ctypes.c_char_p
     L.vfmm_destroy.argtypes = [vp]
     L.vfmm_destroy.restype = None
+    L.vfmm_nccl_get_unique_id.argtypes = [vp]
+    L.vfmm_create_nccl.argtypes = [ctypes.POINTER(vp), ctypes.POINTER(c_params), i32, vp, i32, i32]
+    L.vfmm_partition.argtypes = [i32, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]
+    L.vfmm_evaluate_logical.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp]
+    L.vfmm_dist_plan.argtypes = [i32, i32, i32, i32, i32, i32, i32, vp, i64, ctypes.POINTER(i64)]
+    for f in ("vfmm_nccl_get_unique_id", "vfmm_create_nccl", "vfmm_partition",
+              "vfmm_evaluate_logical", "vfmm_dist_plan"):
+        getattr(L, f).restype = ctypes.c_int
     for f in ("vfmm_create", "vfmm_evaluate", "vfmm_evaluate_host", "vfmm_sync_status",
               "vfmm_get_stats", "vfmm_set_params", "vfmm_debug_tree", "vfmm_debug_expansions"):
         getattr(L, f).restype = ctypes.c_int
@@ -119,10 +129,55 @@ def _check(L, ctx, st):
         raise VfmmError(st, msg)
 
 
-class Evaluator:
-    """One vfmm context on one CUDA device (not thread-safe)."""
+def partition(depth: int, nranks: int, rank: int):
+    """Owned Morton leaf range [lo, hi) of `rank` (C ABI vfmm_partition)."""
+    L = load_library()
+    lo, hi = ctypes.c_int64(), ctypes.c_int64()
+    _check(L, None, L.vfmm_partition(depth, nranks, rank, ctypes.byref(lo), ctypes.byref(hi)))
+    return lo.value, hi.value
 
-    def __init__(self, device: int | None = None, **kw):
+
+def leaf_of(pos, depth: int, box_lo: float, box_len: float):
+    """Morton leaf index of each particle (input plumbing for partitioning a field across
+    ranks; the same float32 quantization the keys kernel uses)."""
+    pos = np.asarray(pos, np.float32)
+    inv = np.float32((1 << depth) / float(np.float32(box_len)))
+    q = np.floor((pos - np.float32(box_lo)) * inv).astype(np.int64).clip(0, (1 << depth) - 1)
+    key = np.zeros(pos.shape[1], np.int64)
+    for b in range(depth):
+        for a in range(3):
+            key |= ((q[a] >> b) & 1) << (3 * b + a)
+    return key
+
+
+def dist_plan(depth, nranks, rank, periodic, kind, direction, peer):
+    """Static exchange plan (host only): list of leaf/cell ids (see vfmm_dist_plan)."""
+    L = load_library()
+    cnt = ctypes.c_int64()
+    _check(L, None, L.vfmm_dist_plan(depth, nranks, rank, periodic, kind, direction, peer, None,
+                                     0, ctypes.byref(cnt)))
+    out = np.zeros(cnt.value, np.int32)
+    _check(L, None, L.vfmm_dist_plan(depth, nranks, rank, periodic, kind, direction, peer,
+                                     out.ctypes.data, cnt.value, ctypes.byref(cnt)))
+    return out
+
+
+def nccl_unique_id() -> bytes:
+    L = load_library()
+    buf = ctypes.create_string_buffer(128)
+    _check(L, None, L.vfmm_nccl_get_unique_id(buf))
+    return buf.raw
+
+
+class Evaluator:
+    """One vfmm context on one CUDA device (not thread-safe).
+
+    Distributed (one process per GPU): pass nranks > 1, rank and the 128-byte NCCL unique id
+    (rank 0's nccl_unique_id(), broadcast by the caller, e.g. torch.distributed) -- see
+    init_distributed()."""
+
+    def __init__(self, device: int | None = None, nranks: int = 1, rank: int = 0,
+                 nccl_id: bytes | None = None, **kw):
         import torch
 
         self._L = load_library()
@@ -130,8 +185,14 @@ class Evaluator:
         self.device = torch.cuda.current_device() if device is None else int(device)
         self._ctx = ctypes.c_void_p()
         prm = self.params.to_c()
-        _check(self._L, None, self._L.vfmm_create(ctypes.byref(self._ctx), ctypes.byref(prm),
-                                                   self.device))
+        self.nranks, self.rank = nranks, rank
+        if nranks > 1:
+            idb = ctypes.create_string_buffer(nccl_id, 128)
+            _check(self._L, None, self._L.vfmm_create_nccl(
+                ctypes.byref(self._ctx), ctypes.byref(prm), self.device, idb, nranks, rank))
+        else:
+            _check(self._L, None, self._L.vfmm_create(ctypes.byref(self._ctx),
+                                                       ctypes.byref(prm), self.device))
         self._n = 0
 
     # -- parameters -------------------------------------------------------------------
@@ -182,6 +243,23 @@ class Evaluator:
         _check(self._L, self._ctx, self._L.vfmm_evaluate_host(
             self._ctx, n, pos_ptr, gamma_ptr, vel_ptr, dg_ptr))
 
+    def evaluate_logical(self, pos_list, gamma_list, stream=None):
+        """Distributed algorithm with len(pos_list) logical ranks on this one GPU (tests):
+        pos_list[r], gamma_list[r]: (3, n_r) float32 CUDA tensors inside rank r's range."""
+        import torch
+
+        R = len(pos_list)
+        vel = [torch.empty_like(p) for p in pos_list]
+        dg = [torch.empty_like(p) for p in pos_list]
+        n = (ctypes.c_int64 * R)(*[p.shape[1] for p in pos_list])
+        P = lambda ts: (ctypes.c_void_p * R)(*[t.data_ptr() for t in ts])
+        if stream is None:
+            stream = torch.cuda.current_stream(pos_list[0].device)
+        _check(self._L, self._ctx, self._L.vfmm_evaluate_logical(
+            self._ctx, R, n, P(pos_list), P(gamma_list), P(vel), P(dg),
+            ctypes.c_void_p(stream.cuda_stream)))
+        return vel, dg
+
     def sync_status(self):
         _check(self._L, self._ctx, self._L.vfmm_sync_status(self._ctx))
 
@@ -217,6 +295,19 @@ class Evaluator:
             self.close()
         except Exception:
             pass
+
+
+def init_distributed(**kw):
+    """Create an Evaluator for this torch.distributed rank (one process per GPU): rank 0 makes
+    the NCCL unique id, torch.distributed broadcasts it, every rank joins the communicator."""
+    import torch
+    import torch.distributed as dist
+
+    rank, world = dist.get_rank(), dist.get_world_size()
+    obj = [nccl_unique_id() if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0)
+    return Evaluator(device=torch.cuda.current_device(), nranks=world, rank=rank,
+                     nccl_id=obj[0], **kw)
 
 
 def evaluate(pos, gamma, sigma, p=10, depth=0, image_levels=3, scheme=0, mode=MODE_FMM,

@@ -8,10 +8,12 @@
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 #include <cstring>
 #include <string>
 #include <vector>
 
+#include "dist.h"
 #include "vfmm_internal.h"
 
 using namespace vfmm;
@@ -50,6 +52,10 @@ struct vfmm_ctx {
     int last_depth = 0;
     bool have_tree = false, have_exp = false;
     vfmm_stats stats{};
+    // distributed state (R > 1: NCCL; logical mode: one RankState per logical rank)
+    int R = 1, rank = 0;
+    void* comm = nullptr;
+    std::vector<vfmm::RankState*> ranks;
     static constexpr int NEV = 10;
     cudaEvent_t ev[NEV] = {};
 };
@@ -181,9 +187,151 @@ vfmm_status ensure_ws(vfmm_ctx* c, int64_t n, int depth) {
     return VFMM_OK;
 }
 
+DistShared make_shared(vfmm_ctx* c, int R) {
+    DistShared D;
+    D.prm = c->prm;
+    D.depth = c->prm.depth;
+    D.R = R;
+    D.m2m = c->d_m2m;
+    D.l2l = c->d_l2l;
+    D.m2l = c->d_m2l;
+    D.per = c->d_per;
+    D.tc_hi = c->d_tc_hi;
+    D.tc_lo = c->d_tc_lo;
+    D.slots = c->d_slots;
+    D.KP = c->hops.KP;
+    D.NR = c->hops.NR;
+    const char* env = getenv("VFMM_M2L");
+    D.allow_tc = !(env && strcmp(env, "simt") == 0);
+    return D;
+}
+
+bool valid_R(int R) { return R == 1 || R == 2 || R == 4 || R == 8; }
+
+void ensure_rank_states(vfmm_ctx* c, int R, int first_rank, int count) {
+    while ((int)c->ranks.size() < count) c->ranks.push_back(new RankState());
+    for (int i = 0; i < count; ++i) {
+        RankState* S = c->ranks[i];
+        S->rank = first_rank + i;
+        const int per = c->prm.image_levels > 0;
+        if (S->plan.L != c->prm.depth || S->plan.R != R || S->plan.rank != S->rank ||
+            S->plan.periodic != per || S->plan.p_send.empty())
+            build_dist_plan(c->prm.depth, R, S->rank, per, &S->plan);
+    }
+}
+
+vfmm_status dist_sticky(vfmm_ctx* c, RankState* S) {
+    int flag = 0;
+    CK(cudaMemcpy(&flag, S->d_err, sizeof(int), cudaMemcpyDeviceToHost), "read flag");
+    if (flag) {
+        CK(cudaMemset(S->d_err, 0, sizeof(int)), "clear flag");
+        c->err = "a particle lies outside the box or outside its rank's Morton range";
+        return VFMM_EDOMAIN;
+    }
+    return VFMM_OK;
+}
+
 }  // namespace
 
 extern "C" {
+
+vfmm_status vfmm_partition(int depth, int nranks, int rank, int64_t* leaf_lo, int64_t* leaf_hi) {
+    if (!valid_R(nranks) || rank < 0 || rank >= nranks || depth < 1 || depth > 10)
+        return VFMM_EINVAL;
+    const int64_t nleaf = (int64_t)1 << (3 * depth);
+    if (leaf_lo) *leaf_lo = nleaf / nranks * rank;
+    if (leaf_hi) *leaf_hi = nleaf / nranks * (rank + 1);
+    return VFMM_OK;
+}
+
+vfmm_status vfmm_dist_plan(int depth, int nranks, int rank, int periodic, int kind, int dir,
+                           int peer, int32_t* out, int64_t cap, int64_t* count) {
+    if (!valid_R(nranks) || rank < 0 || rank >= nranks || peer < 0 || peer >= nranks ||
+        depth < 2 || depth > 8 || !count || (kind != 0 && (kind < 2 || kind > depth)) ||
+        (dir != 0 && dir != 1))
+        return VFMM_EINVAL;
+    DistPlan P;
+    build_dist_plan(depth, nranks, rank, periodic ? 1 : 0, &P);
+    const std::vector<int>& v = kind == 0 ? (dir == 0 ? P.p_recv[peer] : P.p_send[peer])
+                                          : (dir == 0 ? P.m_recv[kind][peer] : P.m_send[kind][peer]);
+    *count = (int64_t)v.size();
+    if (out)
+        for (int64_t i = 0; i < std::min<int64_t>(cap, (int64_t)v.size()); ++i) out[i] = v[i];
+    return VFMM_OK;
+}
+
+vfmm_status vfmm_nccl_get_unique_id(void* out128) {
+    if (!out128) return VFMM_EINVAL;
+    return nccl_unique_id(out128);
+}
+
+vfmm_status vfmm_create_nccl(vfmm_ctx** out, const vfmm_params* prm, int device,
+                             const void* nccl_id128, int nranks, int rank) {
+    if (!out || !nccl_id128 || !prm || !valid_R(nranks) || rank < 0 || rank >= nranks)
+        return VFMM_EINVAL;
+    if (prm->depth < 2 || prm->mode == VFMM_MODE_DIRECT) return VFMM_EINVAL;
+    vfmm_status s = vfmm_create(out, prm, device);
+    if (s != VFMM_OK) return s;
+    vfmm_ctx* c = *out;
+    c->R = nranks;
+    c->rank = rank;
+    if (nranks > 1) {
+        s = nccl_init(&c->comm, nranks, rank, nccl_id128);
+        if (s != VFMM_OK) {
+            c->err = "ncclCommInitRank failed";
+            vfmm_destroy(c);
+            *out = nullptr;
+            return s;
+        }
+    }
+    return VFMM_OK;
+}
+
+vfmm_status vfmm_evaluate_logical(vfmm_ctx* c, int nranks, const int64_t* n,
+                                  const float* const* pos, const float* const* gamma,
+                                  float* const* vel, float* const* dgamma, void* stream) {
+    if (!c || !valid_R(nranks) || !n || !pos || !gamma || !vel || !dgamma) return VFMM_EINVAL;
+    if (c->prm.depth < 2 || c->prm.mode == VFMM_MODE_DIRECT) return VFMM_EINVAL;
+    CK(cudaSetDevice(c->device), "set device");
+    cudaStream_t st = (cudaStream_t)stream;
+    ensure_rank_states(c, nranks, 0, nranks);
+    DistShared D = make_shared(c, nranks);
+    std::vector<RankState*> S(c->ranks.begin(), c->ranks.begin() + nranks);
+    for (int r = 0; r < nranks; ++r) {
+        if (n[r] < 0 || (n[r] > 0 && (!pos[r] || !gamma[r] || !vel[r] || !dgamma[r])))
+            return VFMM_EINVAL;
+        S[r]->n_local = n[r];
+        S[r]->pos = pos[r];
+        S[r]->gam = gamma[r];
+        S[r]->vel = vel[r];
+        S[r]->dg = dgamma[r];
+    }
+    vfmm_status s;
+    for (int r = 0; r < nranks; ++r)
+        if ((s = dist_phase1(*S[r], D, st, &c->err)) != VFMM_OK) return s;
+    if ((s = logical_x1(S, D, st)) != VFMM_OK) return s;
+    for (int r = 0; r < nranks; ++r)
+        if ((s = dist_phase2(*S[r], D, st, &c->err)) != VFMM_OK) return s;
+    if ((s = logical_x2(S, D, st)) != VFMM_OK) return s;
+    for (int r = 0; r < nranks; ++r)
+        if ((s = dist_phase3(*S[r], D, st, &c->err)) != VFMM_OK) return s;
+    if ((s = logical_x3(S, D, st)) != VFMM_OK) return s;
+    for (int r = 0; r < nranks; ++r)
+        if ((s = dist_phase4(*S[r], D, st, &c->err)) != VFMM_OK) return s;
+    c->last_stream = st;
+    c->have_tree = false;
+    c->have_exp = false;
+    memset(&c->stats, 0, sizeof(c->stats));
+    for (int r = 0; r < nranks; ++r) {
+        c->stats.bytes_sent += S[r]->bytes_sent;
+        c->stats.bytes_recv += S[r]->bytes_recv;
+    }
+    CK(cudaStreamSynchronize(st), "sync");
+    for (int r = 0; r < nranks; ++r)
+        if ((s = dist_sticky(c, S[r])) != VFMM_OK) return s;
+    return VFMM_OK;
+}
+
 
 int32_t vfmm_abi_version(void) { return VFMM_ABI_VERSION; }
 
@@ -271,6 +419,34 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
         return VFMM_EINVAL;
     CK(cudaSetDevice(c->device), "set device");
     cudaStream_t st = (cudaStream_t)stream;
+    if (c->R > 1) {  // distributed evaluation over NCCL (this process = one rank)
+        ensure_rank_states(c, c->R, c->rank, 1);
+        DistShared D = make_shared(c, c->R);
+        RankState& R0 = *c->ranks[0];
+        R0.n_local = n;
+        R0.pos = pos;
+        R0.gam = gamma;
+        R0.vel = vel;
+        R0.dg = dgamma;
+        vfmm_status s;
+        CK(cudaEventRecord(c->ev[0], st), "event");
+        if ((s = dist_phase1(R0, D, st, &c->err)) != VFMM_OK) return s;
+        if ((s = nccl_x1(R0, D, c->comm, st)) != VFMM_OK) return s;
+        if ((s = dist_phase2(R0, D, st, &c->err)) != VFMM_OK) return s;
+        if ((s = nccl_x2(R0, D, c->comm, st)) != VFMM_OK) return s;
+        if ((s = dist_phase3(R0, D, st, &c->err)) != VFMM_OK) return s;
+        if ((s = nccl_x3(R0, D, c->comm, st)) != VFMM_OK) return s;
+        if ((s = dist_phase4(R0, D, st, &c->err)) != VFMM_OK) return s;
+        for (int i = 1; i < vfmm_ctx::NEV; ++i) CK(cudaEventRecord(c->ev[i], st), "event");
+        memset(&c->stats, 0, sizeof(c->stats));
+        c->stats.bytes_sent = R0.bytes_sent;
+        c->stats.bytes_recv = R0.bytes_recv;
+        c->stats.depth_used = c->prm.depth;
+        c->last_stream = st;
+        c->have_tree = false;
+        c->have_exp = false;
+        return VFMM_OK;
+    }
     const vfmm_params& P = c->prm;
     vfmm_stats& S = c->stats;
     memset(&S, 0, sizeof(S));
@@ -306,7 +482,7 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
                       st, &c->keys_sorted, &c->perm, &nl);
     CK(cudaEventRecord(c->ev[2], st), "event");
     launch_leaf_ranges(c->keys_sorted, n, depth, c->leaf_start, st);
-    launch_gather(pos, gamma, c->perm, c->keys_sorted, n, g, c->sorted6, st);
+    launch_gather(pos, gamma, c->perm, c->keys_sorted, n, g, c->sorted6, n, 0, st);
     nl += 2;
     CK(cudaGetLastError(), "tree kernels");
     CK(cudaEventRecord(c->ev[3], st), "event");
@@ -319,13 +495,15 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
     auto Llev = [&](int l) { return c->Lall + level_offset(l) * 3 * nc; };
     // ---- upward pass ----
     if (use_far) {
-        launch_p2m(c->sorted6, n, c->leaf_start, depth, p, 1.f / a, Mlev(depth), st);
+        launch_p2m(c->sorted6, n, c->leaf_start, p, 1.f / a, Mlev(depth), 0,
+                   (int64_t)1 << (3 * depth), st);
         ++nl;
     }
     CK(cudaEventRecord(c->ev[4], st), "event");
     if (use_far) {
         for (int l = depth - 1; l >= 0; --l) {
-            launch_m2m(c->d_m2m, p, H.KP, H.NR, Mlev(l + 1), Mlev(l), l, st);
+            launch_m2m(c->d_m2m, p, H.KP, H.NR, Mlev(l + 1), Mlev(l), l, 0, (int64_t)1 << (3 * l),
+                       st);
             ++nl;
             S.n_m2m += (int64_t)8 << (3 * l);
         }
@@ -337,7 +515,8 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
         const char* m2l_env = getenv("VFMM_M2L");
         const bool allow_tc = !(m2l_env && strcmp(m2l_env, "simt") == 0) && c->d_tc_hi;
         for (int l = 1; l <= depth; ++l) {
-            if (allow_tc && m2l_tc_supported(p, l)) {
+            const int box[6] = {0, 0, 0, 1 << (l - 1), 1 << (l - 1), 1 << (l - 1)};
+            if (allow_tc && m2l_tc_supported(p, l) && box[3] >= 16) {
                 const size_t need = m2l_tc_grid_floats(l);
                 if (need > c->g_cap) {
                     dfree(c->g_hi);
@@ -348,7 +527,8 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
                     c->g_cap = need;
                 }
                 const int rc = launch_m2l_tc(c->d_tc_hi, c->d_tc_lo, c->d_slots, p, Mlev(l),
-                                             Llev(l), l, P.image_levels > 0, c->g_hi, c->g_lo, st);
+                                             Llev(l), l, P.image_levels > 0, c->g_hi, c->g_lo,
+                                             box, st);
                 if (rc != 0) {
                     c->err = "tensor-map encode failed for tcgen05 M2L";
                     return VFMM_ECUDA;
@@ -356,7 +536,7 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
                 nl += 2;
             } else {
                 launch_m2l(c->d_m2l, c->d_slots, p, H.KP, H.NR, Mlev(l), Llev(l), l,
-                           P.image_levels > 0, st);
+                           P.image_levels > 0, 0, (int64_t)1 << (3 * (l - 1)), st);
                 ++nl;
             }
             S.n_m2l += (int64_t)189 << (3 * l);
@@ -372,7 +552,8 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
             CK(cudaMemsetAsync(Llev(0), 0, 3 * nc * sizeof(float), st), "memset L0");
         }
         for (int l = 1; l <= depth; ++l) {
-            launch_l2l(c->d_l2l, p, H.KP, H.NR, Llev(l - 1), Llev(l), l, st);
+            launch_l2l(c->d_l2l, p, H.KP, H.NR, Llev(l - 1), Llev(l), l, 0,
+                       (int64_t)1 << (3 * (l - 1)), st);
             ++nl;
             S.n_l2l += (int64_t)1 << (3 * l);
         }
@@ -384,13 +565,14 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
     if (use_near) {
         CK(cudaMemsetAsync(c->d_pairs, 0, sizeof(unsigned long long), st), "memset pairs");
         launch_p2p(c->sorted6, n, c->leaf_start, depth, a, P.image_levels > 0, P.scheme, kc,
-                   c->near6, c->d_pairs, st);
+                   c->near6, c->d_pairs, 0, (int64_t)1 << (3 * (depth - 1)), st);
         ++nl;
         CK(cudaGetLastError(), "p2p kernel");
     }
     CK(cudaEventRecord(c->ev[8], st), "event");
-    launch_l2p_combine(c->sorted6, c->near6, c->perm, n, c->leaf_start, depth, p, a,
-                       Llev(depth), P.scheme, use_near, use_far, vel, dgamma, st);
+    launch_l2p_combine(c->sorted6, c->near6, c->perm, n, c->leaf_start, p, a, Llev(depth),
+                       P.scheme, use_near, use_far, vel, dgamma, 0, (int64_t)1 << (3 * depth), 0, n,
+                       st);
     ++nl;
     CK(cudaGetLastError(), "l2p kernel");
     CK(cudaEventRecord(c->ev[9], st), "event");
@@ -426,6 +608,10 @@ vfmm_status vfmm_sync_status(vfmm_ctx* c) {
     if (!c) return VFMM_EINVAL;
     CK(cudaSetDevice(c->device), "set device");
     CK(cudaStreamSynchronize(c->last_stream), "sync");
+    if (c->R > 1 && !c->ranks.empty()) {
+        vfmm_status s = dist_sticky(c, c->ranks[0]);
+        if (s != VFMM_OK) return s;
+    }
     int flag = 0;
     CK(cudaMemcpy(&flag, c->d_err, sizeof(int), cudaMemcpyDeviceToHost), "read flag");
     if (flag) {
@@ -525,6 +711,9 @@ void vfmm_destroy(vfmm_ctx* c) {
     for (int i = 0; i < vfmm_ctx::NEV; ++i)
         if (c->ev[i]) cudaEventDestroy(c->ev[i]);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
+    for (auto* s : c->ranks) delete s;
+    c->ranks.clear();
+    if (c->comm) nccl_destroy(c->comm);
     delete c;
 }
 

@@ -84,12 +84,13 @@ __device__ void solid_R_packed(float x, float y, float z, int p, float* out, int
 
 __global__ void __launch_bounds__(64) p2m_kernel(const float* __restrict__ s6, int64_t n,
                                                  const int* __restrict__ leaf_start, int p,
-                                                 float inv_a, float* __restrict__ M) {
+                                                 float inv_a, float* __restrict__ M,
+                                                 int64_t leaf_lo) {
     extern __shared__ float sm[];
     const int nc = (p + 1) * (p + 1);
     float* Rs = sm;             // [nc][65]
     float* gs = sm + nc * 65;   // [3][64]
-    const int leaf = blockIdx.x;
+    const int64_t leaf = leaf_lo + blockIdx.x;
     const int s = leaf_start[leaf], e = leaf_start[leaf + 1];
     float acc[3 * kPMax + 12];  // outputs t, t+64, ... ; at most ceil(3*289/64) = 14
     const int nout = (3 * nc + 63) / 64;
@@ -141,7 +142,8 @@ constexpr size_t TRANSLATE_SMEM =
 template <int KIND>
 __global__ void __launch_bounds__(256) translate_kernel(
     const float* __restrict__ mats, const int* __restrict__ slots, int p, int KP, int NR,
-    const float* __restrict__ src, float* __restrict__ dst, int level, int periodic) {
+    const float* __restrict__ src, float* __restrict__ dst, int level, int periodic, int64_t plo,
+    int64_t pcnt) {
     extern __shared__ float4 dsm4[];
     float (*As)[KC][TROWS] = reinterpret_cast<float (*)[KC][TROWS]>(dsm4);
     float (*Bs)[KC][BSTR] = reinterpret_cast<float (*)[KC][BSTR]>(
@@ -155,18 +157,18 @@ __global__ void __launch_bounds__(256) translate_kernel(
     const int row0 = blockIdx.y * TROWS;
 
     // ---- which target cells / ops ----
+    // M2M: targets are the parents [plo, plo + pcnt) at `level`; M2L / L2L: targets are the
+    // children (parity) of the parents [plo, plo + pcnt) at level - 1 (owned ranges)
     int nops, ncell_tile, parity = 0, tile0;
-    const int64_t ncells = (int64_t)1 << (3 * level);
     if (KIND == OP_M2M) {
         nops = 8;
-        tile0 = blockIdx.x * TCELLS;  // parents at `level`
-        ncell_tile = (int)min((int64_t)TCELLS, ncells - tile0);
+        tile0 = (int)(plo + (int64_t)blockIdx.x * TCELLS);
+        ncell_tile = (int)min((int64_t)TCELLS, plo + pcnt - tile0);
     } else {
-        const int64_t nparents = ncells >> 3;
-        const int64_t ntiles = (nparents + TCELLS - 1) / TCELLS;
+        const int64_t ntiles = (pcnt + TCELLS - 1) / TCELLS;
         parity = (int)(blockIdx.x / ntiles);
-        tile0 = (int)(blockIdx.x % ntiles) * TCELLS;  // parent index of first target
-        ncell_tile = (int)min((int64_t)TCELLS, nparents - tile0);
+        tile0 = (int)(plo + (int64_t)(blockIdx.x % ntiles) * TCELLS);
+        ncell_tile = (int)min((int64_t)TCELLS, plo + pcnt - tile0);
         nops = KIND == OP_L2L ? 1 : MAXOPS;
     }
     auto target_cell = [&](int j) -> int64_t {
@@ -356,7 +358,8 @@ __global__ void __launch_bounds__(64) l2p_combine_kernel(
     const float* __restrict__ s6, const float* __restrict__ near6,
     const uint32_t* __restrict__ perm, int64_t n, const int* __restrict__ leaf_start, int p,
     float inv_a, const float* __restrict__ Lleaf, int use_near, int use_far,
-    float* __restrict__ vel, float* __restrict__ dgam) {
+    float* __restrict__ vel, float* __restrict__ dgam, int64_t leaf_lo, int64_t gbase,
+    int64_t nout) {
     // smem: D [ng][28] (q: 9 gradients then 18 Hessian entries, pad); Ls [3][nc]; G; H
     extern __shared__ float4 l2p_sm4[];
     float* sm = reinterpret_cast<float*>(l2p_sm4);
@@ -366,12 +369,12 @@ __global__ void __launch_bounds__(64) l2p_combine_kernel(
     float* Ls = sm + ng * 28;
     float* G = Ls + 3 * nc;
     float* H = G + 9 * ng;
-    const int leaf = blockIdx.x;
+    const int64_t leaf = leaf_lo + blockIdx.x;
     const int s = leaf_start[leaf], e = leaf_start[leaf + 1];
     if (e == s) return;
     const float inv4pi = 0.0795774715459476679f;
     if (use_far) {
-        for (int i = threadIdx.x; i < 3 * nc; i += 64) Ls[i] = Lleaf[(int64_t)leaf * 3 * nc + i];
+        for (int i = threadIdx.x; i < 3 * nc; i += 64) Ls[i] = Lleaf[leaf * 3 * nc + i];
         __syncthreads();
         for (int c = 0; c < 3; ++c)
             for (int ax = 0; ax < 3; ++ax)
@@ -499,10 +502,10 @@ __global__ void __launch_bounds__(64) l2p_combine_kernel(
                     sd[a2] += near6[(3 + a2) * n + j];
                 }
             }
-            const int64_t i = perm[j];
+            const int64_t i = perm[j - gbase];  // caller's input index (rank-local)
             for (int a2 = 0; a2 < 3; ++a2) {
-                vel[a2 * n + i] = u[a2];
-                dgam[a2 * n + i] = sd[a2];
+                vel[a2 * nout + i] = u[a2];
+                dgam[a2 * nout + i] = sd[a2];
             }
         }
     }
@@ -522,8 +525,8 @@ void translate_attrs() {
 
 }  // namespace
 
-void launch_p2m(const float* sorted6, int64_t n, const int* leaf_start, int depth, int p,
-                float inv_a, float* M_leaf, cudaStream_t st) {
+void launch_p2m(const float* sorted6, int64_t n, const int* leaf_start, int p, float inv_a,
+                float* M_leaf, int64_t leaf_lo, int64_t leaf_cnt, cudaStream_t st) {
     const int nc = (p + 1) * (p + 1);
     const size_t smem = sizeof(float) * (nc * 65 + 3 * 64);
     static bool attr = false;
@@ -531,35 +534,37 @@ void launch_p2m(const float* sorted6, int64_t n, const int* leaf_start, int dept
         cudaFuncSetAttribute(p2m_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
-    const int64_t nleaf = (int64_t)1 << (3 * depth);
-    p2m_kernel<<<(unsigned)nleaf, 64, smem, st>>>(sorted6, n, leaf_start, p, inv_a, M_leaf);
+    if (leaf_cnt <= 0) return;
+    p2m_kernel<<<(unsigned)leaf_cnt, 64, smem, st>>>(sorted6, n, leaf_start, p, inv_a, M_leaf,
+                                                     leaf_lo);
 }
 
 void launch_m2m(const float* ops_m2m, int p, int KP, int NR, const float* M_child, float* M_par,
-                int level_par, cudaStream_t st) {
-    const int64_t ncells = (int64_t)1 << (3 * level_par);
-    dim3 grid((unsigned)((ncells + TCELLS - 1) / TCELLS), NR / TROWS);
+                int level_par, int64_t plo, int64_t pcnt, cudaStream_t st) {
+    if (pcnt <= 0) return;
+    dim3 grid((unsigned)((pcnt + TCELLS - 1) / TCELLS), NR / TROWS);
     translate_attrs();
-    translate_kernel<OP_M2M><<<grid, 256, TRANSLATE_SMEM, st>>>(ops_m2m, nullptr, p, KP, NR, M_child, M_par,
-                                                   level_par, 0);
+    translate_kernel<OP_M2M><<<grid, 256, TRANSLATE_SMEM, st>>>(ops_m2m, nullptr, p, KP, NR, M_child,
+                                                                M_par, level_par, 0, plo, pcnt);
 }
 
 void launch_l2l(const float* ops_l2l, int p, int KP, int NR, const float* L_par, float* L_child,
-                int level_child, cudaStream_t st) {
-    const int64_t nparents = (int64_t)1 << (3 * (level_child - 1));
-    dim3 grid((unsigned)(8 * ((nparents + TCELLS - 1) / TCELLS)), NR / TROWS);
+                int level_child, int64_t plo, int64_t pcnt, cudaStream_t st) {
+    if (pcnt <= 0) return;
+    dim3 grid((unsigned)(8 * ((pcnt + TCELLS - 1) / TCELLS)), NR / TROWS);
     translate_attrs();
-    translate_kernel<OP_L2L><<<grid, 256, TRANSLATE_SMEM, st>>>(ops_l2l, nullptr, p, KP, NR, L_par, L_child,
-                                                   level_child, 0);
+    translate_kernel<OP_L2L><<<grid, 256, TRANSLATE_SMEM, st>>>(ops_l2l, nullptr, p, KP, NR, L_par,
+                                                                L_child, level_child, 0, plo, pcnt);
 }
 
 void launch_m2l(const float* ops_m2l, const int* il_slots, int p, int KP, int NR,
-                const float* M_l, float* L_l, int level, int periodic, cudaStream_t st) {
-    const int64_t nparents = (int64_t)1 << (3 * (level - 1));
-    dim3 grid((unsigned)(8 * ((nparents + TCELLS - 1) / TCELLS)), NR / TROWS);
+                const float* M_l, float* L_l, int level, int periodic, int64_t plo, int64_t pcnt,
+                cudaStream_t st) {
+    if (pcnt <= 0) return;
+    dim3 grid((unsigned)(8 * ((pcnt + TCELLS - 1) / TCELLS)), NR / TROWS);
     translate_attrs();
-    translate_kernel<OP_M2L><<<grid, 256, TRANSLATE_SMEM, st>>>(ops_m2l, il_slots, p, KP, NR, M_l, L_l, level,
-                                                   periodic);
+    translate_kernel<OP_M2L><<<grid, 256, TRANSLATE_SMEM, st>>>(ops_m2l, il_slots, p, KP, NR, M_l,
+                                                                L_l, level, periodic, plo, pcnt);
 }
 
 void launch_periodic(const float* ops_per, int p, int KP, int NR, const float* M0, float* L0,
@@ -568,9 +573,10 @@ void launch_periodic(const float* ops_per, int p, int KP, int NR, const float* M
 }
 
 void launch_l2p_combine(const float* sorted6, const float* near6, const uint32_t* perm,
-                        int64_t n, const int* leaf_start, int depth, int p, float a,
-                        const float* L_leaf, int scheme, int use_near, int use_far,
-                        float* vel, float* dgam, cudaStream_t st) {
+                        int64_t n, const int* leaf_start, int p, float a, const float* L_leaf,
+                        int scheme, int use_near, int use_far, float* vel, float* dgam,
+                        int64_t leaf_lo, int64_t leaf_cnt, int64_t gbase, int64_t nout,
+                        cudaStream_t st) {
     const int nc = (p + 1) * (p + 1), ng = p * p, nh = (p - 1) * (p - 1);
     const size_t smem = sizeof(float) * (ng * 28 + 3 * nc + 9 * ng + 18 * (nh > 0 ? nh : 1));
     static bool attr = false;
@@ -581,13 +587,15 @@ void launch_l2p_combine(const float* sorted6, const float* near6, const uint32_t
                              200 * 1024);
         attr = true;
     }
-    const int64_t nleaf = (int64_t)1 << (3 * depth);
+    if (leaf_cnt <= 0) return;
     if (scheme == 0)
-        l2p_combine_kernel<0><<<(unsigned)nleaf, 64, smem, st>>>(
-            sorted6, near6, perm, n, leaf_start, p, 1.f / a, L_leaf, use_near, use_far, vel, dgam);
+        l2p_combine_kernel<0><<<(unsigned)leaf_cnt, 64, smem, st>>>(
+            sorted6, near6, perm, n, leaf_start, p, 1.f / a, L_leaf, use_near, use_far, vel, dgam,
+            leaf_lo, gbase, nout);
     else
-        l2p_combine_kernel<1><<<(unsigned)nleaf, 64, smem, st>>>(
-            sorted6, near6, perm, n, leaf_start, p, 1.f / a, L_leaf, use_near, use_far, vel, dgam);
+        l2p_combine_kernel<1><<<(unsigned)leaf_cnt, 64, smem, st>>>(
+            sorted6, near6, perm, n, leaf_start, p, 1.f / a, L_leaf, use_near, use_far, vel, dgam,
+            leaf_lo, gbase, nout);
 }
 
 }  // namespace vfmm

@@ -9,11 +9,19 @@
 // B = a "slab" of source multipoles: one x-row of XT <= 32 parent cells x 3 strength
 // components = N <= 96 rows, read from a parity-major, halo-padded copy of the level's
 // multipoles (m2l_stage_kernel) so every (target row, offset) maps to one TMA box.
-// A CTA owns T = 4 target rows (Py, Pz) of one parity: 4 accumulators of 128 x N fp32 in
-// TMEM; operators are loaded once per CTA per offset and reused by the 4 rows.
+// A CTA owns T = 2 target rows (Py, Pz) of one parity: 2 accumulator tiles of 128 x N fp32
+// in TMEM; operators are loaded once per CTA per offset and reused by both rows.
 //
-// Warp roles (192 threads): warp 0 = TMA producer, warp 1 = TMEM alloc + MMA issuer,
-// warps 2-5 = epilogue (TMEM -> registers -> L in Morton order).
+// Accuracy: the tensor core accumulates with truncation, so a TMEM chain over all
+// 189 offsets x 16 K-steps x 3 products (~9000 accumulations) drifts by ~1e-4.  The chain is
+// therefore cut every TC_G = 2 offsets (<= 96 accumulations): the MMA warp alternates between
+// two TMEM buffers and the epilogue warps add each finished buffer into FP32 registers
+// (round-to-nearest), so the result keeps FP32 accuracy.
+//
+// Warp roles (320 threads): warp 0 = TMA producer, warp 1 = TMEM alloc + MMA issuer,
+// warps 2-9 = epilogue (TMEM -> FP32 register sums -> L in Morton order).
+// CTA order: parity fastest, then 8x8 tiles of row groups, so co-resident CTAs share the
+// source slabs they stream (L2 reuse).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -24,14 +32,16 @@ namespace vfmm {
 
 namespace {
 
-constexpr int TC_T = 4;        // target rows per CTA
+constexpr int TC_T = 2;        // target rows per CTA (one accumulator tile each)
+constexpr int TC_G = 2;        // offsets per TMEM accumulation group (flushed to FP32 registers)
 constexpr int TC_NKC = 4;      // K chunks of 32 floats (128 B)
 constexpr int TC_AST = 2;      // A (operator) pipeline stages
 constexpr int TC_BST = 4;      // B (slab) pipeline stages
 constexpr int A_BYTES = 128 * 128;  // one K chunk of one operator half (hi or lo): 16 KB
 constexpr int B_BYTES = 96 * 128;   // one K chunk of one slab half: <= 12 KB
-constexpr int TC_THREADS = 192;
-constexpr size_t TC_SMEM = 1024 + (size_t)TC_AST * 2 * A_BYTES + (size_t)TC_BST * 2 * B_BYTES + 256;
+constexpr int TC_EPI_WARPS = 8;  // 2 per TMEM lane quarter: warp pair splits the T tiles
+constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;
+constexpr size_t TC_SMEM = 1024 + (size_t)TC_AST * 2 * A_BYTES + (size_t)TC_BST * 2 * B_BYTES + 512;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -43,6 +53,9 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
                  "r"(bytes)
                  : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
     const uint32_t a = smem_u32(b);
@@ -123,9 +136,29 @@ struct TcParams {
     int rows;   // target rows per parity = nP * nP * ntx
     int nc;     // (p+1)^2 <= 128
     int level;
+    int bx0, by0, bz0, bny;  // owned box of target parents (origin; y extent)
     const int* slots;  // [8][189] M2L slot per target parity
     float* L;          // local expansions of this level, Morton [cell][3][nc]
 };
+
+// row group g of a CTA -> (x tile, first target row y, row z) inside the owned box;
+// groups are visited in 8x8 tiles of (y group, z) so co-resident CTAs share source rows
+__device__ __forceinline__ void group_rows(const TcParams& P, int g, int* tx, int* py0, int* pz) {
+    *tx = g % P.ntx;
+    const int gg = g / P.ntx;
+    const int GY = P.bny / TC_T, GZ = P.rows / (P.ntx * P.bny);  // groups along y, rows in z
+    int gy, gz;
+    if (GY % 8 == 0 && GZ % 8 == 0) {
+        const int tile = gg / 64, w = gg % 64;
+        gy = (tile % (GY / 8)) * 8 + (w & 7);
+        gz = (tile / (GY / 8)) * 8 + (w >> 3);
+    } else {
+        gy = gg % GY;
+        gz = gg / GY;
+    }
+    *py0 = P.by0 + gy * TC_T;
+    *pz = P.bz0 + gz;
+}
 
 __global__ void __launch_bounds__(TC_THREADS, 1)
     m2l_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant__ CUtensorMap tmA_lo,
@@ -140,15 +173,18 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint64_t* a_empty = bars + TC_AST;
     uint64_t* b_full = bars + 2 * TC_AST;
     uint64_t* b_empty = bars + 2 * TC_AST + TC_BST;
-    uint64_t* acc_full = bars + 2 * TC_AST + 2 * TC_BST;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_full + 1);
+    uint64_t* acc_full = bars + 2 * TC_AST + 2 * TC_BST;  // [2]
+    uint64_t* acc_empty = acc_full + 2;                  // [2]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int groups = P.rows / TC_T;
-    const int pi = blockIdx.x / groups;
-    const int g = blockIdx.x - pi * groups;
+    const int pi = blockIdx.x & 7;  // target parity fastest (CTAs of one row group share slabs)
+    const int g = blockIdx.x >> 3;
     const int pix = pi & 1, piy = (pi >> 1) & 1, piz = (pi >> 2) & 1;
-    const uint32_t tmem_cols = TC_T * P.N <= 256 ? 256u : 512u;
+    int gtx, gpy0, gpz;
+    group_rows(P, g, &gtx, &gpy0, &gpz);
+    constexpr uint32_t tmem_cols = 512;  // 2 buffers x 256 columns
+    const int ngroups = (189 + TC_G - 1) / TC_G;
 
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < TC_AST; ++i) {
@@ -159,7 +195,10 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             mbar_init(&b_full[i], 1);
             mbar_init(&b_empty[i], 1);
         }
-        mbar_init(acc_full, 1);
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&acc_full[i], 1);
+            mbar_init(&acc_empty[i], TC_EPI_WARPS);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     if (warp == 1) {
@@ -195,16 +234,14 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                         pa ^= 1;
                     }
                     for (int t = 0; t < TC_T; ++t) {
-                        const int row = g * TC_T + t;
-                        const int tx = row % P.ntx, rest = row / P.ntx;
-                        const int py = rest % P.nP, pz = rest / P.nP;
                         mbar_wait(&b_empty[sb], pb ^ 1);
                         mbar_expect_tx(&b_full[sb], b_tx);
-                        const int c1 = 3 * (2 + tx * P.XT + dx);
+                        const int c1 = 3 * (2 + P.bx0 + gtx * P.XT + dx);
+                        const int c2 = 2 + gpy0 + t + dy, c3 = 2 + gpz + dz;
                         tma_load_5d(Bbuf + (sb * 2 + 0) * B_BYTES, &tmB_hi, &b_full[sb], kc * 32, c1,
-                                    2 + py + dy, 2 + pz + dz, pis);
+                                    c2, c3, pis);
                         tma_load_5d(Bbuf + (sb * 2 + 1) * B_BYTES, &tmB_lo, &b_full[sb], kc * 32, c1,
-                                    2 + py + dy, 2 + pz + dz, pis);
+                                    c2, c3, pis);
                         if (++sb == TC_BST) {
                             sb = 0;
                             pb ^= 1;
@@ -220,75 +257,95 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                                ((uint32_t)(128 >> 4) << 24);
         int sa = 0, sb = 0;
         uint32_t pa = 0, pb = 0;
-        for (int oi = 0; oi < 189; ++oi) {
-            for (int kc = 0; kc < TC_NKC; ++kc) {
-                mbar_wait(&a_full[sa], pa);
-                tc_fence_after();
-                const uint64_t ahi = sw128_desc(Abuf + (sa * 2 + 0) * A_BYTES);
-                const uint64_t alo = sw128_desc(Abuf + (sa * 2 + 1) * A_BYTES);
-                for (int t = 0; t < TC_T; ++t) {
-                    mbar_wait(&b_full[sb], pb);
+        for (int grp = 0; grp < ngroups; ++grp) {
+            const int buf = grp & 1;
+            mbar_wait(&acc_empty[buf], ((grp >> 1) & 1) ^ 1);  // epilogue drained this buffer
+            tc_fence_after();
+            const int o_end = min(189, (grp + 1) * TC_G);
+            for (int oi = grp * TC_G; oi < o_end; ++oi) {
+                for (int kc = 0; kc < TC_NKC; ++kc) {
+                    mbar_wait(&a_full[sa], pa);
                     tc_fence_after();
-                    const uint64_t bhi = sw128_desc(Bbuf + (sb * 2 + 0) * B_BYTES);
-                    const uint64_t blo = sw128_desc(Bbuf + (sb * 2 + 1) * B_BYTES);
-                    const uint32_t d = tmem + (uint32_t)(t * P.N);
-                    if (lane == 0) {
+                    const uint64_t ahi = sw128_desc(Abuf + (sa * 2 + 0) * A_BYTES);
+                    const uint64_t alo = sw128_desc(Abuf + (sa * 2 + 1) * A_BYTES);
+                    for (int t = 0; t < TC_T; ++t) {
+                        mbar_wait(&b_full[sb], pb);
+                        tc_fence_after();
+                        const uint64_t bhi = sw128_desc(Bbuf + (sb * 2 + 0) * B_BYTES);
+                        const uint64_t blo = sw128_desc(Bbuf + (sb * 2 + 1) * B_BYTES);
+                        const uint32_t d = tmem + (uint32_t)(buf * 256 + t * P.N);
+                        if (lane == 0) {
 #pragma unroll
-                        for (int ks = 0; ks < 4; ++ks) {  // K = 8 tf32 = 32 B per MMA
-                            const uint64_t adv = (uint64_t)(ks * 2);
-                            const uint32_t acc = (oi | kc | ks) != 0 ? 1u : 0u;
-                            mma_tf32(d, ahi + adv, bhi + adv, idesc, acc);
-                            mma_tf32(d, ahi + adv, blo + adv, idesc, 1u);
-                            mma_tf32(d, alo + adv, bhi + adv, idesc, 1u);
+                            for (int ks = 0; ks < 4; ++ks) {  // K = 8 tf32 = 32 B per MMA
+                                const uint64_t adv = (uint64_t)(ks * 2);
+                                const uint32_t acc = (oi != grp * TC_G || kc != 0 || ks != 0) ? 1u : 0u;
+                                mma_tf32(d, ahi + adv, bhi + adv, idesc, acc);
+                                mma_tf32(d, ahi + adv, blo + adv, idesc, 1u);
+                                mma_tf32(d, alo + adv, bhi + adv, idesc, 1u);
+                            }
+                            mma_commit(&b_empty[sb]);
                         }
-                        mma_commit(&b_empty[sb]);
+                        __syncwarp();
+                        if (++sb == TC_BST) {
+                            sb = 0;
+                            pb ^= 1;
+                        }
                     }
+                    if (lane == 0) mma_commit(&a_empty[sa]);
                     __syncwarp();
-                    if (++sb == TC_BST) {
-                        sb = 0;
-                        pb ^= 1;
+                    if (++sa == TC_AST) {
+                        sa = 0;
+                        pa ^= 1;
                     }
-                }
-                if (lane == 0) mma_commit(&a_empty[sa]);
-                __syncwarp();
-                if (++sa == TC_AST) {
-                    sa = 0;
-                    pa ^= 1;
                 }
             }
+            if (lane == 0) mma_commit(&acc_full[buf]);
+            __syncwarp();
         }
-        if (lane == 0) mma_commit(acc_full);
-        __syncwarp();
     } else {
-        // ===================== epilogue: TMEM -> L (Morton) =====================
-        mbar_wait(acc_full, 0);
-        tc_fence_after();
+        // ===================== epilogue: TMEM groups -> FP32 register sums -> L =====================
+        const int e = warp - 2;
         const int quarter = warp & 3;  // TMEM lanes [32 quarter, 32 quarter + 32)
+        const int t = e >> 2;          // accumulator tile of this warp
         const int r = quarter * 32 + lane;
-        for (int t = 0; t < TC_T; ++t) {
-            const int row = g * TC_T + t;
-            const int tx = row % P.ntx, rest = row / P.ntx;
-            const int py = rest % P.nP, pz = rest / P.nP;
-            const uint32_t cy = spread3t(2 * py + piy) << 1, cz = spread3t(2 * pz + piz) << 2;
-            for (int c0 = 0; c0 < P.N; c0 += 16) {
-                uint32_t v[16];
-                const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(t * P.N + c0);
-                asm volatile(
-                    "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, "
-                    "%9, %10, %11, %12, %13, %14, %15}, [%16];"
-                    : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
-                      "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
-                      "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
-                    : "r"(taddr));
-                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-                if (r < P.nc) {
+        float acc[96];
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const int col = c0 + j;
-                        const int px = tx * P.XT + col / 3, comp = col % 3;
-                        const uint32_t cell = spread3t(2 * px + pix) | cy | cz;
-                        P.L[((int64_t)cell * 3 + comp) * P.nc + r] = __uint_as_float(v[j]);
-                    }
+        for (int j = 0; j < 96; ++j) acc[j] = 0.f;
+        for (int grp = 0; grp < ngroups; ++grp) {
+            const int buf = grp & 1;
+            mbar_wait(&acc_full[buf], (grp >> 1) & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int c = 0; c < 6; ++c) {
+                if (c * 16 < P.N) {
+                    uint32_t v[16];
+                    const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) +
+                                           (uint32_t)(buf * 256 + t * P.N + c * 16);
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, "
+                        "%8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+                        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                          "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
+                          "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                        : "r"(taddr));
+                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) acc[c * 16 + j] += __uint_as_float(v[j]);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[buf]);
+        }
+        if (r < P.nc) {
+            const int py = gpy0 + t;
+            const uint32_t cy = spread3t(2 * py + piy) << 1, cz = spread3t(2 * gpz + piz) << 2;
+#pragma unroll
+            for (int j = 0; j < 96; ++j) {
+                if (j < P.N) {
+                    const int px = P.bx0 + gtx * P.XT + j / 3, comp = j % 3;
+                    const uint32_t cell = spread3t(2 * px + pix) | cy | cz;
+                    P.L[((int64_t)cell * 3 + comp) * P.nc + r] = acc[j];
                 }
             }
         }
@@ -362,7 +419,7 @@ size_t m2l_tc_grid_floats(int level) {
 
 int launch_m2l_tc(const float* ops_hi, const float* ops_lo, const int* il_slots, int p,
                   const float* M_l, float* L_l, int level, int periodic, float* ghi, float* glo,
-                  cudaStream_t st) {
+                  const int box[6], cudaStream_t st) {
     const int nc = (p + 1) * (p + 1);
     const int nP = 1 << (level - 1);
     const int Xp = nP + 4;
@@ -391,7 +448,9 @@ int launch_m2l_tc(const float* ops_hi, const float* ops_lo, const int* il_slots,
                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return -2;
     }
-    const int XT = nP < 32 ? nP : 32;
+    // owned box of target parents: origin box[0..2], extents box[3..5] (whole level: 0, nP)
+    const int bnx = box[3], bny = box[4], bnz = box[5];
+    const int XT = bnx < 32 ? bnx : 32;
     const int N = 3 * XT;
     {
         cuuint64_t dims[5] = {128, (cuuint64_t)3 * Xp, (cuuint64_t)Xp, (cuuint64_t)Xp, 8};
@@ -417,13 +476,18 @@ int launch_m2l_tc(const float* ops_hi, const float* ops_lo, const int* il_slots,
     TcParams P;
     P.nP = nP;
     P.XT = XT;
-    P.ntx = nP / XT;
+    P.ntx = bnx / XT;
     P.N = N;
-    P.rows = nP * nP * P.ntx;
+    P.rows = bny * bnz * P.ntx;
+    P.bx0 = box[0];
+    P.by0 = box[1];
+    P.bz0 = box[2];
+    P.bny = bny;
     P.nc = nc;
     P.level = level;
     P.slots = il_slots;
     P.L = L_l;
+    if (P.rows % TC_T != 0 || bny % TC_T != 0) return -4;
     const unsigned grid = (unsigned)(8 * (P.rows / TC_T));
     m2l_tc_kernel<<<grid, TC_THREADS, TC_SMEM, st>>>(mAh, mAl, mBh, mBl, P);
     return 0;

@@ -167,13 +167,13 @@ template <int SCHEME>
 __global__ void __launch_bounds__(P2P_THREADS, 2) p2p_kernel(
     const float* __restrict__ s6, int64_t n, const int* __restrict__ leaf_start, int depth,
     float a, int periodic, KernelConsts kc, float* __restrict__ near6,
-    unsigned long long* __restrict__ npairs) {
+    unsigned long long* __restrict__ npairs, int64_t plo) {
     extern __shared__ float4 p2p_sm[];
     float4* S4 = p2p_sm;                                        // x, y, z, gx
     float2* S2 = reinterpret_cast<float2*>(S4 + P2P_CAP);       // gy, gz
     __shared__ int rstart[65], rcnt[64], rsrc[64];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-    const uint32_t parent = blockIdx.x;
+    const uint32_t parent = (uint32_t)(plo + blockIdx.x);
     const int side = 1 << depth;
     const int px = (int)compact3p(parent), py = (int)compact3p(parent >> 1),
               pz = (int)compact3p(parent >> 2);
@@ -356,7 +356,7 @@ __global__ void __launch_bounds__(128) direct_kernel(const float* __restrict__ p
 
 void launch_p2p(const float* sorted6, int64_t n, const int* leaf_start, int depth, float a,
                 int periodic, int scheme, KernelConsts kc, float* near6,
-                unsigned long long* npairs, cudaStream_t st) {
+                unsigned long long* npairs, int64_t plo, int64_t pcnt, cudaStream_t st) {
     const size_t smem = (size_t)P2P_CAP * (sizeof(float4) + sizeof(float2));
     static bool attr = false;
     if (!attr) {
@@ -364,13 +364,13 @@ void launch_p2p(const float* sorted6, int64_t n, const int* leaf_start, int dept
         cudaFuncSetAttribute(p2p_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = true;
     }
-    const int64_t nparent = (int64_t)1 << (3 * (depth - 1));
+    if (pcnt <= 0) return;
     if (scheme == 0)
-        p2p_kernel<0><<<(unsigned)nparent, P2P_THREADS, smem, st>>>(sorted6, n, leaf_start, depth,
-                                                                    a, periodic, kc, near6, npairs);
+        p2p_kernel<0><<<(unsigned)pcnt, P2P_THREADS, smem, st>>>(sorted6, n, leaf_start, depth, a,
+                                                                periodic, kc, near6, npairs, plo);
     else
-        p2p_kernel<1><<<(unsigned)nparent, P2P_THREADS, smem, st>>>(sorted6, n, leaf_start, depth,
-                                                                    a, periodic, kc, near6, npairs);
+        p2p_kernel<1><<<(unsigned)pcnt, P2P_THREADS, smem, st>>>(sorted6, n, leaf_start, depth, a,
+                                                                periodic, kc, near6, npairs, plo);
 }
 
 void launch_direct(const float* pos, const float* gamma, int64_t n, float len, int image_levels,

@@ -191,7 +191,7 @@ __global__ void leaf_ranges_kernel(const uint32_t* __restrict__ keys, int64_t n,
 __global__ void gather_kernel(const float* __restrict__ pos, const float* __restrict__ gam,
                               const uint32_t* __restrict__ perm,
                               const uint32_t* __restrict__ keys, int64_t n, double lo,
-                              double a, float* __restrict__ out) {
+                              double a, float* __restrict__ out, int64_t ostride, int64_t ooff) {
     for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
          k += (int64_t)gridDim.x * blockDim.x) {
         const int64_t i = perm[k];
@@ -200,8 +200,8 @@ __global__ void gather_kernel(const float* __restrict__ pos, const float* __rest
 #pragma unroll
         for (int ax = 0; ax < 3; ++ax) {
             const double ctr = lo + ((double)c[ax] + 0.5) * a;
-            out[ax * n + k] = (float)((double)__ldg(pos + ax * n + i) - ctr);
-            out[(3 + ax) * n + k] = __ldg(gam + ax * n + i);
+            out[ax * ostride + ooff + k] = (float)((double)__ldg(pos + ax * n + i) - ctr);
+            out[(3 + ax) * ostride + ooff + k] = __ldg(gam + ax * n + i);
         }
     }
 }
@@ -261,10 +261,10 @@ void launch_leaf_ranges(const uint32_t* keys_sorted, int64_t n, int depth, int* 
 
 void launch_gather(const float* pos, const float* gamma, const uint32_t* perm,
                    const uint32_t* keys_sorted, int64_t n, Geom g, float* sorted6,
-                   cudaStream_t st) {
+                   int64_t ostride, int64_t ooff, cudaStream_t st) {
     const double a = g.len_d / (double)(1 << g.depth);
     gather_kernel<<<grid_for(n, 256), 256, 0, st>>>(pos, gamma, perm, keys_sorted, n, g.lo_d, a,
-                                                    sorted6);
+                                                    sorted6, ostride, ooff);
 }
 
 }  // namespace vfmm

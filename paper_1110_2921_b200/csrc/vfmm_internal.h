@@ -69,30 +69,32 @@ void launch_leaf_ranges(const uint32_t* keys_sorted, int64_t n, int depth, int* 
                         cudaStream_t st);
 void launch_gather(const float* pos, const float* gamma, const uint32_t* perm,
                    const uint32_t* keys_sorted, int64_t n, Geom g, float* sorted6,
-                   cudaStream_t st);
+                   int64_t ostride, int64_t ooff, cudaStream_t st);
 
-// expansions.cu
-void launch_p2m(const float* sorted6, int64_t n, const int* leaf_start, int depth, int p,
-                float inv_a, float* M_leaf, cudaStream_t st);
+// expansions.cu  (ranges: the owned part of the tree; whole tree for one rank)
+void launch_p2m(const float* sorted6, int64_t n, const int* leaf_start, int p, float inv_a,
+                float* M_leaf, int64_t leaf_lo, int64_t leaf_cnt, cudaStream_t st);
 void launch_m2m(const float* ops_m2m, int p, int KP, int NR, const float* M_child, float* M_par,
-                int level_par, cudaStream_t st);
+                int level_par, int64_t plo, int64_t pcnt, cudaStream_t st);
 void launch_l2l(const float* ops_l2l, int p, int KP, int NR, const float* L_par, float* L_child,
-                int level_child, cudaStream_t st);
+                int level_child, int64_t plo, int64_t pcnt, cudaStream_t st);
 void launch_m2l(const float* ops_m2l, const int* il_slots, int p, int KP, int NR,
-                const float* M_l, float* L_l, int level, int periodic, cudaStream_t st);
+                const float* M_l, float* L_l, int level, int periodic, int64_t plo, int64_t pcnt,
+                cudaStream_t st);
 void launch_periodic(const float* ops_per, int p, int KP, int NR, const float* M0, float* L0,
                      cudaStream_t st);
 void launch_l2p_combine(const float* sorted6, const float* near6, const uint32_t* perm,
-                        int64_t n, const int* leaf_start, int depth, int p, float a,
-                        const float* L_leaf, int scheme, int use_near, int use_far,
-                        float* vel, float* dgam, cudaStream_t st);
+                        int64_t n, const int* leaf_start, int p, float a, const float* L_leaf,
+                        int scheme, int use_near, int use_far, float* vel, float* dgam,
+                        int64_t leaf_lo, int64_t leaf_cnt, int64_t gbase, int64_t nout,
+                        cudaStream_t st);
 
 // m2l_tc.cu (tcgen05, 3xTF32)
 bool m2l_tc_supported(int p, int level);
 size_t m2l_tc_grid_floats(int level);
 int launch_m2l_tc(const float* ops_hi, const float* ops_lo, const int* il_slots, int p,
                   const float* M_l, float* L_l, int level, int periodic, float* ghi, float* glo,
-                  cudaStream_t st);
+                  const int box[6], cudaStream_t st);
 
 // p2p.cu
 struct KernelConsts {
@@ -105,7 +107,7 @@ struct KernelConsts {
 KernelConsts make_kernel_consts(float sigma);
 void launch_p2p(const float* sorted6, int64_t n, const int* leaf_start, int depth, float a,
                 int periodic, int scheme, KernelConsts kc, float* near6,
-                unsigned long long* npairs, cudaStream_t st);
+                unsigned long long* npairs, int64_t plo, int64_t pcnt, cudaStream_t st);
 void launch_direct(const float* pos, const float* gamma, int64_t n, float len, int image_levels,
                    int scheme, KernelConsts kc, float* vel, float* dgam, cudaStream_t st);
 

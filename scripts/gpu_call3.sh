@@ -1,0 +1,10 @@
+#!/bin/bash
+cd "${GRAFT_REPO_ROOT:-/root/repo}"; mkdir -p gpurun_out
+# quick targeted checks first (tensor-core M2L), each bounded
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -k "tensor_core or fmm_vs_fmm or near_plus" > gpurun_out/pytest_quick.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_quick.log
+timeout 300 python scripts/profile_step.py --m2l tc > gpurun_out/plain_tc.log 2>&1; echo "rc=$?" >> gpurun_out/plain_tc.log
+timeout 300 python scripts/profile_step.py --m2l simt > gpurun_out/plain_simt.log 2>&1; echo "rc=$?" >> gpurun_out/plain_simt.log
+timeout 600 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench.log
+timeout 300 python scripts/profile_step.py > gpurun_out/plain.log 2>&1 && \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"p2p_kernel|m2l_tc_kernel|l2p_combine" -s 3 -c 3 -o gpurun_out/prof_r1a python scripts/profile_step.py > gpurun_out/ncu_full.log 2>&1; echo "ncu rc=$?" >> gpurun_out/ncu_full.log
+timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?" >> gpurun_out/pytest_gpu.log

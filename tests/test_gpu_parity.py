@@ -259,7 +259,7 @@ def test_m2l_tensor_core_matches_simt(n, depth, p, lam, monkeypatch):
     v2, s2, ev2 = run(f, p=p, depth=depth, image_levels=lam, mode=vf.MODE_FAR_ONLY)
     for l in range(depth - 1, depth + 1):
         a, b = ev1.debug_expansions(1, l), ev2.debug_expansions(1, l)
-        assert rel(a, b) < 2e-6, (l, rel(a, b))
-    assert rel(v1, v2) < 2e-6 and rel(s1, s2) < 5e-6, (rel(v1, v2), rel(s1, s2))
+        assert rel(a[..., 1:], b[..., 1:]) < 5e-6, (l, rel(a[..., 1:], b[..., 1:]))
+    assert rel(v1, v2) < 5e-6 and rel(s1, s2) < 1e-5, (rel(v1, v2), rel(s1, s2))
     ev1.close()
     ev2.close()
