@@ -11,8 +11,9 @@ HBM (403 MB of inputs, larger than the 126 MB L2).
 
 --impl reference times the CPU oracle (oracle/, float64 direct periodic sum) on a bounded
 sample of the same workload (the tier's reference arm; extrapolated to a full evaluation).
-Under torchrun each rank evaluates its own 256^3 field (replicas; weak scaling) until the
-LET-sharded path lands.
+Under torchrun (N > 1) the ONE 256^3 problem is split across the ranks by Morton range
+(vfmm_partition) and evaluated with the halo-particle + LET exchange over NCCL
+(DESIGN.md "Multi-GPU"): strong scaling, value = seconds per whole evaluation (max over ranks).
 """
 from __future__ import annotations
 
@@ -161,7 +162,7 @@ def workload_config(args, f):
             "n": int(f.pos.shape[1]), "p": args.p or c["p"], "depth": args.depth or c["depth"],
             "image_levels": 3, "scheme": "classical",
             "l2": "inputs (403 MB at 256^3) and working set larger than the 126 MB L2",
-            "parallelism": "replicas" if args.gpus > 1 else "single"}
+            "parallelism": f"morton-partition+LET x{args.gpus}" if args.gpus > 1 else "single"}
 
 
 def main():
@@ -197,9 +198,20 @@ def main():
     p = args.p or cfg["p"]
     depth = args.depth or cfg["depth"]
     f = synthgen.make(args.config)
+    n_total = f.pos.shape[1]
+    kw = dict(p=p, depth=depth, image_levels=3, sigma=f.sigma, box_lo=f.box_lo,
+              box_len=f.box_len)
+    if world > 1:
+        # this rank's share of the one problem: particles in its Morton leaf range
+        lo, hi = vf.partition(depth, world, rank)
+        leaf = vf.leaf_of(f.pos, depth, f.box_lo, f.box_len)
+        mine = np.nonzero((leaf >= lo) & (leaf < hi))[0]
+        f.pos = np.ascontiguousarray(f.pos[:, mine])
+        f.gamma = np.ascontiguousarray(f.gamma[:, mine])
+        ev = vf.init_distributed(**kw)
+    else:
+        ev = vf.Evaluator(device=local, **kw)
     n = f.pos.shape[1]
-    ev = vf.Evaluator(p=p, depth=depth, image_levels=3, sigma=f.sigma, box_lo=f.box_lo,
-                      box_len=f.box_len, device=local)
     dev = torch.device("cuda", local)
     pos = torch.from_numpy(f.pos).to(dev)
     gam = torch.from_numpy(f.gamma).to(dev)
@@ -254,7 +266,7 @@ def main():
                           dtype=torch.float64)
         if world > 1:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": float(te.item()) / world, "unit": "s",
+        e2e = {"value": float(te.item()), "unit": "s",
                "h2d_bytes_per_step": int(hp.numel() * 4 + hg.numel() * 4),
                "d2h_bytes_per_step": int(hv.numel() * 4 + hs.numel() * 4)}
 
@@ -270,22 +282,35 @@ def main():
     fp32_peak = 148 * 128 * 2 * sm_max * 1e6 / 1e12  # TFLOP/s
     nc = (p + 1) ** 2
     avg = {k: statistics.mean(ph[k] for ph in phases) for k in phases[0]}
-    t_p2p = avg["ms_p2p"] * 1e-3
-    t_m2l = avg["ms_m2l"] * 1e-3
-    pairs = phases[0]["n_p2p_pairs"]
+    t_p2p = max(avg["ms_p2p"], 1e-9) * 1e-3  # per-kernel events exist on single-rank contexts
+    t_m2l = max(avg["ms_m2l"], 1e-9) * 1e-3
+    pairs = phases[0]["n_p2p_pairs"] or 27 * 64 * n_total
     p2p_tf = pairs * P2P_FLOP_PER_PAIR / t_p2p / 1e12
     m2l_tf = phases[0]["n_m2l"] * 6 * nc * nc / t_m2l / 1e12
+    tc_m2l = p <= 10 and depth >= 5  # levels >= 5 run M2L on tcgen05 (3xTF32)
+    bf16 = float(peaks.get("bf16_tflops", 1630.5))
+    tf32_peak = bf16 * (1.1 / 2.25)  # guide's nominal dense tf32 / bf16 ratio x measured bf16
     if t_m2l >= t_p2p:
-        roof = {"kernel": "m2l (translate_kernel<M2L>, all levels)", "bound": "alu",
-                "achieved": m2l_tf, "peak": fp32_peak, "unit": "TFLOP/s",
-                "frac": m2l_tf / fp32_peak, "traffic": None,
-                "per_unit": f"6(p+1)^4 = {6 * nc * nc} flop per M2L translation (dense, 3 comps)"}
+        if tc_m2l:
+            roof = {"kernel": "m2l (m2l_tc_kernel tcgen05 3xTF32 at levels >= 5, SIMT below)",
+                    "bound": "tensor", "achieved": m2l_tf, "peak": tf32_peak, "unit": "TFLOP/s",
+                    "frac": m2l_tf / tf32_peak, "traffic": None,
+                    "per_unit": f"6(p+1)^4 = {6 * nc * nc} useful flop per M2L translation; "
+                                "3xTF32 issues 3 tensor products per useful product",
+                    "peak_note": "measured bf16 burst x nominal tf32/bf16 (1.1/2.25 PF)"}
+        else:
+            roof = {"kernel": "m2l (translate_kernel<M2L>, all levels)", "bound": "alu",
+                    "achieved": m2l_tf, "peak": fp32_peak, "unit": "TFLOP/s",
+                    "frac": m2l_tf / fp32_peak, "traffic": None,
+                    "per_unit": f"6(p+1)^4 = {6 * nc * nc} flop per M2L translation"}
     else:
         roof = {"kernel": "p2p_kernel", "bound": "alu", "achieved": p2p_tf, "peak": fp32_peak,
                 "unit": "TFLOP/s", "frac": p2p_tf / fp32_peak, "traffic": None,
                 "per_unit": f"{P2P_FLOP_PER_PAIR} FP32 flop per ordered pair"}
-    roof["peak_source"] = (f"FP32 SIMT: 148 SMs x 128 lanes x 2 x {sm_max:.0f} MHz "
-                           "(sm_max_mhz of MEASURED_PEAKS.json)")
+    if world > 1:  # distributed contexts time whole phases only: roofline comes from N = 1
+        roof.update(achieved=None, frac=None, note="per-kernel events measured at n_gpus=1")
+    roof.setdefault("peak_source", f"FP32 SIMT: 148 SMs x 128 lanes x 2 x {sm_max:.0f} MHz "
+                                   "(sm_max_mhz of MEASURED_PEAKS.json)")
     tr_path = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(tr_path):
         try:
@@ -303,15 +328,16 @@ def main():
             cb = {"value": None, "unit": "s/eval", "cores": os.cpu_count(), "kind": "oracle",
                   "sample": f"unavailable: {e}"}
 
-    s_per_eval = ms_step * 1e-3 / world  # whole job: world evaluations per step (replicas)
+    s_per_eval = ms_step * 1e-3  # one whole 256^3 evaluation per step (max over ranks)
     line = {
         "metric": METRIC, "value": s_per_eval, "unit": "s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
-        "higher_is_better": False, "scaling": "weak", "vs_baseline": None,
+        "higher_is_better": False, "scaling": "strong" if world > 1 else "weak",
+        "vs_baseline": None,
         "dtype": "f32", "data": "synthetic", "config": workload_config(args, f),
-        "p2p_interactions_per_s": pairs / t_p2p * world,
+        "p2p_interactions_per_s": pairs / t_p2p,
         "p2p_pairs_per_eval": pairs,
-        "fp32_frac_p2p": p2p_tf / fp32_peak, "fp32_frac_m2l": m2l_tf / fp32_peak,
+        "fp32_frac_p2p": p2p_tf / fp32_peak, "m2l_useful_tflops": m2l_tf,
         "phase_ms": {k[3:]: round(v, 4) for k, v in avg.items() if k.startswith("ms_")},
         "roofline": roof, "cpu_baseline": cb, "e2e": e2e,
         "gpu_launches": int(phases[0]["n_kernel_launches"]) * args.steps,

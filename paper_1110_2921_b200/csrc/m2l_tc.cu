@@ -14,7 +14,7 @@
 //
 // Accuracy: the tensor core accumulates with truncation, so a TMEM chain over all
 // 189 offsets x 16 K-steps x 3 products (~9000 accumulations) drifts by ~1e-4.  The chain is
-// therefore cut every TC_G = 2 offsets (<= 96 accumulations): the MMA warp alternates between
+// therefore cut after every offset (TC_G = 1: <= 48 accumulations): the MMA warp alternates between
 // two TMEM buffers and the epilogue warps add each finished buffer into FP32 registers
 // (round-to-nearest), so the result keeps FP32 accuracy.
 //
@@ -33,7 +33,7 @@ namespace vfmm {
 namespace {
 
 constexpr int TC_T = 2;        // target rows per CTA (one accumulator tile each)
-constexpr int TC_G = 2;        // offsets per TMEM accumulation group (flushed to FP32 registers)
+constexpr int TC_G = 1;        // offsets per TMEM accumulation group (flushed to FP32 registers)
 constexpr int TC_NKC = 4;      // K chunks of 32 floats (128 B)
 constexpr int TC_AST = 2;      // A (operator) pipeline stages
 constexpr int TC_BST = 4;      // B (slab) pipeline stages

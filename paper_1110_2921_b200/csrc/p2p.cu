@@ -28,6 +28,9 @@ KernelConsts make_kernel_consts(float sigma) {
     const double z0 = std::pow(2.0 * M_PI * s * s, -1.5);
     k.zeta0 = (float)z0;
     k.zeta0_over_s2 = (float)(z0 / (s * s));
+    k.r2_series = (float)(0.5 * s * s);
+    k.t_scale = (float)(1.0 / (2.0 * std::sqrt(2.0) * s));
+    k.q_scale = (float)(2.0 / (4.0 * M_PI * std::sqrt(M_PI)) / (std::sqrt(2.0) * s));
     return k;
 }
 
@@ -53,51 +56,53 @@ struct Acc {
     float u0, u1, u2, a0, a1, a2, b0, b1, b2;
 };
 
-template <int SCHEME>
-__device__ __forceinline__ void pair(float dx, float dy, float dz, float gjx, float gjy, float gjz,
-                                     float gix, float giy, float giz, const KernelConsts& kc,
-                                     Acc& acc) {
-    const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+// f, q by the Taylor series (rho^2 < 1/4, incl. r = 0)
+__device__ __forceinline__ void fq_series(float r2, const KernelConsts& kc, float& f, float& q) {
+    // f = zeta0 sum (-s)^k/(k!(2k+3)),  q = zeta0/sigma^2 sum_{k>=1} (-1)^k s^{k-1}/((k-1)!(2k+3))
     const float s = r2 * kc.inv2s2;  // rho^2
-    float f, q;
-    if (s < 0.25f) {
-        // f = zeta0 sum (-s)^k/(k!(2k+3)),  q = zeta0/sigma^2 sum_{k>=1} (-1)^k s^{k-1}/((k-1)!(2k+3))
-        float pf = 1.f / 10800.f;
-        pf = fmaf(pf, s, -1.f / 1560.f);
-        pf = fmaf(pf, s, 1.f / 264.f);
-        pf = fmaf(pf, s, -1.f / 54.f);
-        pf = fmaf(pf, s, 1.f / 14.f);
-        pf = fmaf(pf, s, -1.f / 5.f);
-        pf = fmaf(pf, s, 1.f / 3.f);
-        float pq = -1.f / 12240.f;
-        pq = fmaf(pq, s, 1.f / 1800.f);
-        pq = fmaf(pq, s, -1.f / 312.f);
-        pq = fmaf(pq, s, 1.f / 66.f);
-        pq = fmaf(pq, s, -1.f / 18.f);
-        pq = fmaf(pq, s, 1.f / 7.f);
-        pq = fmaf(pq, s, -1.f / 5.f);
-        f = kc.zeta0 * pf;
-        q = kc.zeta0_over_s2 * pq;
-    } else {
-        const float rinv = rsqrt_approx(r2);
-        const float e = ex2_approx(r2 * kc.neg_l2e_inv2s2);
-        const float rho = r2 * rinv * kc.inv_s_sqrt2;
-        const float t = rcp_approx(fmaf(0.5f, rho, 1.f)) - 0.5f;
-        // (1/4pi) erfcx(rho) as a polynomial in t, and (1/4pi)(1 - g) = e (E + 2 rho/(4pi sqrt(pi)))
-        float E = 6.204596458e-03f;
-        E = fmaf(E, t, -1.664231425e-03f);
-        E = fmaf(E, t, -1.861016238e-02f);
-        E = fmaf(E, t, 4.873839158e-03f);
-        E = fmaf(E, t, 5.027046960e-02f);
-        E = fmaf(E, t, 7.692235843e-02f);
-        E = fmaf(E, t, 6.798874982e-02f);
-        E = fmaf(E, t, 2.032374185e-02f);
-        const float Q = fmaf(0.0897935610625833f, rho, E);  // 2/(4 pi sqrt(pi)) = 0.0897935...
-        const float g4pi = fmaf(-e, Q, 0.0795774715459476679f);  // g / (4 pi)
-        const float rinv2 = rinv * rinv;
-        f = g4pi * (rinv2 * rinv);
-        q = fmaf(kc.zeta0, e, -3.f * f) * rinv2;
-    }
+    float pf = 1.f / 10800.f;
+    pf = fmaf(pf, s, -1.f / 1560.f);
+    pf = fmaf(pf, s, 1.f / 264.f);
+    pf = fmaf(pf, s, -1.f / 54.f);
+    pf = fmaf(pf, s, 1.f / 14.f);
+    pf = fmaf(pf, s, -1.f / 5.f);
+    pf = fmaf(pf, s, 1.f / 3.f);
+    float pq = -1.f / 12240.f;
+    pq = fmaf(pq, s, 1.f / 1800.f);
+    pq = fmaf(pq, s, -1.f / 312.f);
+    pq = fmaf(pq, s, 1.f / 66.f);
+    pq = fmaf(pq, s, -1.f / 18.f);
+    pq = fmaf(pq, s, 1.f / 7.f);
+    pq = fmaf(pq, s, -1.f / 5.f);
+    f = kc.zeta0 * pf;
+    q = kc.zeta0_over_s2 * pq;
+}
+
+// f, q in closed form (rho^2 >= 1/4): (1/4pi)(1 - g) = e^{-rho^2} (erfcx(rho) + 2 rho/sqrt(pi))/(4pi)
+__device__ __forceinline__ void fq_closed(float r2, const KernelConsts& kc, float& f, float& q) {
+    const float rinv = rsqrt_approx(r2);
+    const float e = ex2_approx(r2 * kc.neg_l2e_inv2s2);
+    const float r = r2 * rinv;
+    const float t = rcp_approx(fmaf(kc.t_scale, r, 1.f)) - 0.5f;
+    float E = 6.204596458e-03f;  // erfcx(rho)/(4 pi), polynomial in t - 1/2
+    E = fmaf(E, t, -1.664231425e-03f);
+    E = fmaf(E, t, -1.861016238e-02f);
+    E = fmaf(E, t, 4.873839158e-03f);
+    E = fmaf(E, t, 5.027046960e-02f);
+    E = fmaf(E, t, 7.692235843e-02f);
+    E = fmaf(E, t, 6.798874982e-02f);
+    E = fmaf(E, t, 2.032374185e-02f);
+    const float Q = fmaf(kc.q_scale, r, E);
+    const float g4pi = fmaf(-e, Q, 0.0795774715459476679f);  // g / (4 pi)
+    const float rinv2 = rinv * rinv;
+    f = g4pi * (rinv2 * rinv);
+    q = fmaf(kc.zeta0, e, -3.f * f) * rinv2;
+}
+
+template <int SCHEME>
+__device__ __forceinline__ void accumulate(float dx, float dy, float dz, float f, float q,
+                                           float gjx, float gjy, float gjz, float gix, float giy,
+                                           float giz, Acc& acc) {
     // c = gamma_j x d
     const float cx = fmaf(gjy, dz, -gjz * dy);
     const float cy = fmaf(gjz, dx, -gjx * dz);
@@ -119,6 +124,17 @@ __device__ __forceinline__ void pair(float dx, float dy, float dz, float gjx, fl
         acc.b1 = fmaf(w, dy, acc.b1);
         acc.b2 = fmaf(w, dz, acc.b2);
     }
+}
+
+template <int SCHEME>
+__device__ __forceinline__ void pair(float dx, float dy, float dz, float gjx, float gjy, float gjz,
+                                     float gix, float giy, float giz, const KernelConsts& kc,
+                                     Acc& acc) {
+    const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    float f, q;
+    if (r2 < kc.r2_series) fq_series(r2, kc, f, q);
+    else fq_closed(r2, kc, f, q);
+    accumulate<SCHEME>(dx, dy, dz, f, q, gjx, gjy, gjz, gix, giy, giz, acc);
 }
 
 template <int SCHEME>
@@ -263,8 +279,25 @@ __global__ void __launch_bounds__(P2P_THREADS, 2) p2p_kernel(
                 for (int j = js; j < je; ++j) {
                     const float4 p = S4[j];
                     const float2 q = S2[j];
-                    pair<SCHEME>(x0 - p.x, y0 - p.y, z0 - p.z, p.w, q.x, q.y, g0x, g0y, g0z, kc, c0);
-                    pair<SCHEME>(x1 - p.x, y1 - p.y, z1 - p.z, p.w, q.x, q.y, g1x, g1y, g1z, kc, c1);
+                    const float dx0 = x0 - p.x, dy0 = y0 - p.y, dz0 = z0 - p.z;
+                    const float dx1 = x1 - p.x, dy1 = y1 - p.y, dz1 = z1 - p.z;
+                    const float r20 = fmaf(dx0, dx0, fmaf(dy0, dy0, dz0 * dz0));
+                    const float r21 = fmaf(dx1, dx1, fmaf(dy1, dy1, dz1 * dz1));
+                    float f0, q0, f1, q1;
+                    // warp-uniform fast path: closed form unless some lane has a close pair
+                    // (self pairs, coincident or sub-h/2 particles take the series)
+                    const bool close = (a0 && r20 < kc.r2_series) || (a1 && r21 < kc.r2_series);
+                    if (__any_sync(0xffffffffu, close)) {
+                        if (r20 < kc.r2_series) fq_series(r20, kc, f0, q0);
+                        else fq_closed(r20, kc, f0, q0);
+                        if (r21 < kc.r2_series) fq_series(r21, kc, f1, q1);
+                        else fq_closed(r21, kc, f1, q1);
+                    } else {
+                        fq_closed(r20, kc, f0, q0);
+                        fq_closed(r21, kc, f1, q1);
+                    }
+                    accumulate<SCHEME>(dx0, dy0, dz0, f0, q0, p.w, q.x, q.y, g0x, g0y, g0z, c0);
+                    accumulate<SCHEME>(dx1, dy1, dz1, f1, q1, p.w, q.x, q.y, g1x, g1y, g1z, c1);
                 }
             }
         }

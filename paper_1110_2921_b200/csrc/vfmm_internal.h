@@ -103,6 +103,9 @@ struct KernelConsts {
     float inv_s_sqrt2;   // 1 / (sqrt(2) sigma)
     float zeta0;         // (2 pi sigma^2)^(-3/2)
     float zeta0_over_s2; // zeta0 / sigma^2
+    float r2_series;     // r^2 below which the Taylor series is used (rho^2 < 1/4)
+    float t_scale;       // 1 / (2 sqrt(2) sigma): t = 1 / (1 + r t_scale) = 1/(1 + rho/2)
+    float q_scale;       // 2 / (4 pi sqrt(pi) sqrt(2) sigma): rho term of (1 - g)/(4 pi)
 };
 KernelConsts make_kernel_consts(float sigma);
 void launch_p2p(const float* sorted6, int64_t n, const int* leaf_start, int depth, float a,
