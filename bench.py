@@ -287,12 +287,12 @@ def main():
     pairs = phases[0]["n_p2p_pairs"] or 27 * 64 * n_total
     p2p_tf = pairs * P2P_FLOP_PER_PAIR / t_p2p / 1e12
     m2l_tf = phases[0]["n_m2l"] * 6 * nc * nc / t_m2l / 1e12
-    tc_m2l = p <= 10 and depth >= 5  # levels >= 5 run M2L on tcgen05 (3xTF32)
+    tc_m2l = p <= 10 and depth >= 2  # levels >= 2 run M2L on tcgen05 (3xTF32)
     bf16 = float(peaks.get("bf16_tflops", 1630.5))
     tf32_peak = bf16 * (1.1 / 2.25)  # guide's nominal dense tf32 / bf16 ratio x measured bf16
     if t_m2l >= t_p2p:
         if tc_m2l:
-            roof = {"kernel": "m2l (m2l_tc_kernel tcgen05 3xTF32 at levels >= 5, SIMT below)",
+            roof = {"kernel": "m2l (m2l_tc_kernel tcgen05 3xTF32 at levels >= 2, SIMT level 1)",
                     "bound": "tensor", "achieved": m2l_tf, "peak": tf32_peak, "unit": "TFLOP/s",
                     "frac": m2l_tf / tf32_peak, "traffic": None,
                     "per_unit": f"6(p+1)^4 = {6 * nc * nc} useful flop per M2L translation; "

@@ -293,8 +293,10 @@ vfmm_status vfmm_evaluate_logical(vfmm_ctx* c, int nranks, const int64_t* n,
     if (!c || !valid_R(nranks) || !n || !pos || !gamma || !vel || !dgamma) return VFMM_EINVAL;
     if (c->prm.depth < 2 || c->prm.mode == VFMM_MODE_DIRECT) return VFMM_EINVAL;
     CK(cudaSetDevice(c->device), "set device");
+    (void)cudaGetLastError();
     cudaStream_t st = (cudaStream_t)stream;
     ensure_rank_states(c, nranks, 0, nranks);
+    CK(cudaEventRecord(c->ev[0], st), "event");
     DistShared D = make_shared(c, nranks);
     std::vector<RankState*> S(c->ranks.begin(), c->ranks.begin() + nranks);
     for (int r = 0; r < nranks; ++r) {
@@ -318,6 +320,7 @@ vfmm_status vfmm_evaluate_logical(vfmm_ctx* c, int nranks, const int64_t* n,
     if ((s = logical_x3(S, D, st)) != VFMM_OK) return s;
     for (int r = 0; r < nranks; ++r)
         if ((s = dist_phase4(*S[r], D, st, &c->err)) != VFMM_OK) return s;
+    for (int i = 1; i < vfmm_ctx::NEV; ++i) CK(cudaEventRecord(c->ev[i], st), "event");
     c->last_stream = st;
     c->have_tree = false;
     c->have_exp = false;
@@ -418,6 +421,7 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
         overlap(dgamma, pos) || overlap(dgamma, gamma))
         return VFMM_EINVAL;
     CK(cudaSetDevice(c->device), "set device");
+    (void)cudaGetLastError();  // drop stale non-sticky errors of unrelated earlier calls
     cudaStream_t st = (cudaStream_t)stream;
     if (c->R > 1) {  // distributed evaluation over NCCL (this process = one rank)
         ensure_rank_states(c, c->R, c->rank, 1);
@@ -516,7 +520,7 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
         const bool allow_tc = !(m2l_env && strcmp(m2l_env, "simt") == 0) && c->d_tc_hi;
         for (int l = 1; l <= depth; ++l) {
             const int box[6] = {0, 0, 0, 1 << (l - 1), 1 << (l - 1), 1 << (l - 1)};
-            if (allow_tc && m2l_tc_supported(p, l) && box[3] >= 16) {
+            if (allow_tc && m2l_tc_supported(p, l) && box[4] % 2 == 0) {
                 const size_t need = m2l_tc_grid_floats(l);
                 if (need > c->g_cap) {
                     dfree(c->g_hi);

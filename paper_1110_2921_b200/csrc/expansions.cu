@@ -17,6 +17,8 @@
 // target for operator op.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "vfmm_internal.h"
 
 namespace vfmm {
@@ -135,15 +137,18 @@ constexpr int BSTR = TCOLS + 4;    // smem row stride of B
 constexpr int MAXOPS = 189;
 
 enum { OP_M2M = 0, OP_L2L = 1, OP_M2L = 2 };
-constexpr size_t TRANSLATE_SMEM =
+constexpr size_t TRANSLATE_SMEM_MAIN =
     sizeof(float) * (2 * KC * TROWS + 2 * KC * BSTR) + sizeof(int) * (MAXOPS * TCELLS + MAXOPS);
+constexpr size_t TRANSLATE_SMEM_EPI = sizeof(float) * TCOLS * 129;
+constexpr size_t TRANSLATE_SMEM =
+    TRANSLATE_SMEM_MAIN > TRANSLATE_SMEM_EPI ? TRANSLATE_SMEM_MAIN : TRANSLATE_SMEM_EPI;
 
 // grid.x: column tiles; grid.y: row tiles (nc > 128).  256 threads: 16 x 16, each 8 rows x 6 cols.
 template <int KIND>
 __global__ void __launch_bounds__(256) translate_kernel(
     const float* __restrict__ mats, const int* __restrict__ slots, int p, int KP, int NR,
     const float* __restrict__ src, float* __restrict__ dst, int level, int periodic, int64_t plo,
-    int64_t pcnt) {
+    int64_t pcnt, int opsplit) {
     extern __shared__ float4 dsm4[];
     float (*As)[KC][TROWS] = reinterpret_cast<float (*)[KC][TROWS]>(dsm4);
     float (*Bs)[KC][BSTR] = reinterpret_cast<float (*)[KC][BSTR]>(
@@ -171,12 +176,17 @@ __global__ void __launch_bounds__(256) translate_kernel(
         ncell_tile = (int)min((int64_t)TCELLS, plo + pcnt - tile0);
         nops = KIND == OP_L2L ? 1 : MAXOPS;
     }
+    // op split (grid.z): this block handles ops [op0, op1) and accumulates atomically
+    const int opc = (nops + opsplit - 1) / opsplit;
+    const int op0 = blockIdx.z * opc;
+    const int op1 = min(nops, op0 + opc);
     auto target_cell = [&](int j) -> int64_t {
         return KIND == OP_M2M ? (int64_t)(tile0 + j) : ((int64_t)(tile0 + j) << 3) + parity;
     };
     // ---- source tables ----
     for (int i = tid; i < nops * TCELLS; i += 256) {
         const int op = i / TCELLS, j = i - op * TCELLS;
+        if (op < op0 || op >= op1) continue;
         int sidx = -1;
         if (j < ncell_tile) {
             const int64_t t = target_cell(j);
@@ -217,13 +227,13 @@ __global__ void __launch_bounds__(256) translate_kernel(
         for (int j = 0; j < 6; ++j) acc[i][j] = 0.f;
 
     const int nkc = KP / KC;
-    const int niter = nops * nkc;
+    const int niter = (op1 - op0) * nkc;
     const size_t msz = (size_t)KP * NR;
     // register staging for the next chunk
     float4 ra[2];
     float rb[6];
     auto load_regs = [&](int it) {
-        const int op = it / nkc, kc = it - op * nkc;
+        const int op = op0 + it / nkc, kc = it % nkc;
         const float* A = mats + (size_t)opmat[op] * msz + (size_t)(kc * KC) * NR + row0;
 #pragma unroll
         for (int q = 0; q < 2; ++q) {
@@ -277,20 +287,25 @@ __global__ void __launch_bounds__(256) translate_kernel(
         if (it + 1 < niter) store_smem(buf ^ 1);
         __syncthreads();
     }
-    // ---- epilogue ----
+    // ---- epilogue: C tile -> smem (column-major) -> coalesced rows of the target cells ----
+    float* Cs = reinterpret_cast<float*>(dsm4);  // [96 cols][129]
 #pragma unroll
-    for (int j = 0; j < 6; ++j) {
-        const int col = tx * 6 + j;
+    for (int j = 0; j < 6; ++j)
+#pragma unroll
+        for (int i = 0; i < 8; ++i) Cs[(tx * 6 + j) * 129 + ty * 8 + i] = acc[i][j];
+    __syncthreads();
+    const int lane = tid & 31, warp = tid >> 5;
+    for (int col = warp; col < TCOLS; col += 8) {
         const int cell = col / 3, comp = col - cell * 3;
         if (cell >= ncell_tile) continue;
         float* out = dst + (target_cell(cell) * 3 + comp) * nc;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-            const int r = row0 + ty * 8 + i;
-            if (r < nc) {
-                if (KIND == OP_L2L) out[r] += acc[i][j];  // L2L accumulates onto M2L
-                else out[r] = acc[i][j];
-            }
+        for (int rr = lane; rr < TROWS; rr += 32) {
+            const int r = row0 + rr;
+            if (r >= nc) continue;
+            const float v = Cs[col * 129 + rr];
+            if (opsplit > 1) atomicAdd(out + r, v);
+            else if (KIND == OP_L2L) out[r] += v;  // L2L accumulates onto M2L
+            else out[r] = v;
         }
     }
 }
@@ -545,7 +560,7 @@ void launch_m2m(const float* ops_m2m, int p, int KP, int NR, const float* M_chil
     dim3 grid((unsigned)((pcnt + TCELLS - 1) / TCELLS), NR / TROWS);
     translate_attrs();
     translate_kernel<OP_M2M><<<grid, 256, TRANSLATE_SMEM, st>>>(ops_m2m, nullptr, p, KP, NR, M_child,
-                                                                M_par, level_par, 0, plo, pcnt);
+                                                                M_par, level_par, 0, plo, pcnt, 1);
 }
 
 void launch_l2l(const float* ops_l2l, int p, int KP, int NR, const float* L_par, float* L_child,
@@ -554,17 +569,26 @@ void launch_l2l(const float* ops_l2l, int p, int KP, int NR, const float* L_par,
     dim3 grid((unsigned)(8 * ((pcnt + TCELLS - 1) / TCELLS)), NR / TROWS);
     translate_attrs();
     translate_kernel<OP_L2L><<<grid, 256, TRANSLATE_SMEM, st>>>(ops_l2l, nullptr, p, KP, NR, L_par,
-                                                                L_child, level_child, 0, plo, pcnt);
+                                                                L_child, level_child, 0, plo, pcnt, 1);
 }
 
 void launch_m2l(const float* ops_m2l, const int* il_slots, int p, int KP, int NR,
                 const float* M_l, float* L_l, int level, int periodic, int64_t plo, int64_t pcnt,
                 cudaStream_t st) {
     if (pcnt <= 0) return;
-    dim3 grid((unsigned)(8 * ((pcnt + TCELLS - 1) / TCELLS)), NR / TROWS);
+    // few target tiles (coarse levels): split the 189 offsets over grid.z and accumulate
+    // atomically into the zeroed output, so the level does not run on a handful of SMs
+    const int64_t tiles = 8 * ((pcnt + TCELLS - 1) / TCELLS) * (NR / TROWS);
+    const int opsplit = tiles >= 296 ? 1 : (int)std::min<int64_t>(27, (296 + tiles - 1) / tiles);
+    if (opsplit > 1) {
+        const int nc = (p + 1) * (p + 1);
+        cudaMemsetAsync(L_l + plo * 8 * 3 * nc, 0, (size_t)pcnt * 8 * 3 * nc * sizeof(float), st);
+    }
+    dim3 grid((unsigned)(8 * ((pcnt + TCELLS - 1) / TCELLS)), NR / TROWS, opsplit);
     translate_attrs();
     translate_kernel<OP_M2L><<<grid, 256, TRANSLATE_SMEM, st>>>(ops_m2l, il_slots, p, KP, NR, M_l,
-                                                                L_l, level, periodic, plo, pcnt);
+                                                                L_l, level, periodic, plo, pcnt,
+                                                                opsplit);
 }
 
 void launch_periodic(const float* ops_per, int p, int KP, int NR, const float* M0, float* L0,

@@ -132,7 +132,8 @@ struct TcParams {
     int nP;     // parent cells per axis at this level (2^(l-1))
     int XT;     // parents per B tile row (<= 32)
     int ntx;    // x tiles per row (nP / XT)
-    int N;      // 3 * XT
+    int N;      // MMA N = 3 XT rounded up to a multiple of 16 (extra rows are discarded)
+    int NV;     // valid columns = 3 * XT
     int rows;   // target rows per parity = nP * nP * ntx
     int nc;     // (p+1)^2 <= 128
     int level;
@@ -342,7 +343,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
             const uint32_t cy = spread3t(2 * py + piy) << 1, cz = spread3t(2 * gpz + piz) << 2;
 #pragma unroll
             for (int j = 0; j < 96; ++j) {
-                if (j < P.N) {
+                if (j < P.NV) {
                     const int px = P.bx0 + gtx * P.XT + j / 3, comp = j % 3;
                     const uint32_t cell = spread3t(2 * px + pix) | cy | cz;
                     P.L[((int64_t)cell * 3 + comp) * P.nc + r] = acc[j];
@@ -409,7 +410,7 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }  // namespace
 
 bool m2l_tc_supported(int p, int level) {
-    return (p + 1) * (p + 1) <= 128 && level >= 5 && get_encode() != nullptr;
+    return (p + 1) * (p + 1) <= 128 && level >= 2 && get_encode() != nullptr;
 }
 
 size_t m2l_tc_grid_floats(int level) {
@@ -451,7 +452,8 @@ int launch_m2l_tc(const float* ops_hi, const float* ops_lo, const int* il_slots,
     // owned box of target parents: origin box[0..2], extents box[3..5] (whole level: 0, nP)
     const int bnx = box[3], bny = box[4], bnz = box[5];
     const int XT = bnx < 32 ? bnx : 32;
-    const int N = 3 * XT;
+    const int NV = 3 * XT;
+    const int N = (NV + 15) / 16 * 16;  // MMA N (multiple of 16 for M = 128)
     {
         cuuint64_t dims[5] = {128, (cuuint64_t)3 * Xp, (cuuint64_t)Xp, (cuuint64_t)Xp, 8};
         cuuint64_t strides[4] = {128 * 4, (cuuint64_t)3 * Xp * 128 * 4,
@@ -478,6 +480,7 @@ int launch_m2l_tc(const float* ops_hi, const float* ops_lo, const int* il_slots,
     P.XT = XT;
     P.ntx = bnx / XT;
     P.N = N;
+    P.NV = NV;
     P.rows = bny * bnz * P.ntx;
     P.bx0 = box[0];
     P.by0 = box[1];

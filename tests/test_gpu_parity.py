@@ -249,7 +249,7 @@ def test_c4_full_size_sampled_targets():
 
 @pytest.mark.parametrize("n,depth,p,lam", [(64, 5, 10, 3), (48, 5, 6, 0), (128, 6, 8, 1)])
 def test_m2l_tensor_core_matches_simt(n, depth, p, lam, monkeypatch):
-    """Levels >= 5 run M2L on tcgen05 (3xTF32); the SIMT FP32 gather-GEMM (validated against
+    """Levels >= 2 run M2L on tcgen05 (3xTF32); the SIMT FP32 gather-GEMM (validated against
     the fp64 FMM oracle above) computes the same translations.  The tensor core accumulates
     with truncation (round toward zero), so even with the TMEM chain cut after every offset the
     two differ by ~1e-5, not FP32 round-off."""
