@@ -36,7 +36,7 @@ constexpr int TC_T = 2;        // target rows per CTA (one accumulator tile each
 constexpr int TC_G = 1;        // offsets per TMEM accumulation group (flushed to FP32 registers)
 constexpr int TC_NKC = 4;      // K chunks of 32 floats (128 B)
 constexpr int TC_AST = 2;      // A (operator) pipeline stages
-constexpr int TC_BST = 4;      // B (slab) pipeline stages
+constexpr int TC_BST = 6;      // B (slab) pipeline stages (TMA latency ~ several MMA groups)
 constexpr int A_BYTES = 128 * 128;  // one K chunk of one operator half (hi or lo): 16 KB
 constexpr int B_BYTES = 96 * 128;   // one K chunk of one slab half: <= 12 KB
 constexpr int TC_EPI_WARPS = 8;  // 2 per TMEM lane quarter: warp pair splits the T tiles

@@ -276,28 +276,43 @@ __global__ void __launch_bounds__(P2P_THREADS, 2) p2p_kernel(
                 const int rx = bx + nb % 3, ry = by + (nb / 3) % 3, rz = bz + nb / 9;
                 const int rl = rx + 4 * ry + 16 * rz;
                 const int js = max(rstart[rl], w0) - w0, je = min(rstart[rl + 1], w1) - w0;
-                for (int j = js; j < je; ++j) {
+                // two sources per iteration (4 pairs per lane): one vote, one loop test
+                int j = js;
+                for (; j + 1 < je; j += 2) {
+                    const float4 pa = S4[j], pb = S4[j + 1];
+                    const float2 qa = S2[j], qb = S2[j + 1];
+                    const float dxa0 = x0 - pa.x, dya0 = y0 - pa.y, dza0 = z0 - pa.z;
+                    const float dxa1 = x1 - pa.x, dya1 = y1 - pa.y, dza1 = z1 - pa.z;
+                    const float dxb0 = x0 - pb.x, dyb0 = y0 - pb.y, dzb0 = z0 - pb.z;
+                    const float dxb1 = x1 - pb.x, dyb1 = y1 - pb.y, dzb1 = z1 - pb.z;
+                    const float ra0 = fmaf(dxa0, dxa0, fmaf(dya0, dya0, dza0 * dza0));
+                    const float ra1 = fmaf(dxa1, dxa1, fmaf(dya1, dya1, dza1 * dza1));
+                    const float rb0 = fmaf(dxb0, dxb0, fmaf(dyb0, dyb0, dzb0 * dzb0));
+                    const float rb1 = fmaf(dxb1, dxb1, fmaf(dyb1, dyb1, dzb1 * dzb1));
+                    float fa0, qa0, fa1, qa1, fb0, qb0, fb1, qb1;
+                    const float thr = kc.r2_series;
+                    const bool close = (a0 && (ra0 < thr || rb0 < thr)) || (a1 && (ra1 < thr || rb1 < thr));
+                    if (__any_sync(0xffffffffu, close)) {
+                        if (ra0 < thr) fq_series(ra0, kc, fa0, qa0); else fq_closed(ra0, kc, fa0, qa0);
+                        if (ra1 < thr) fq_series(ra1, kc, fa1, qa1); else fq_closed(ra1, kc, fa1, qa1);
+                        if (rb0 < thr) fq_series(rb0, kc, fb0, qb0); else fq_closed(rb0, kc, fb0, qb0);
+                        if (rb1 < thr) fq_series(rb1, kc, fb1, qb1); else fq_closed(rb1, kc, fb1, qb1);
+                    } else {
+                        fq_closed(ra0, kc, fa0, qa0);
+                        fq_closed(ra1, kc, fa1, qa1);
+                        fq_closed(rb0, kc, fb0, qb0);
+                        fq_closed(rb1, kc, fb1, qb1);
+                    }
+                    accumulate<SCHEME>(dxa0, dya0, dza0, fa0, qa0, pa.w, qa.x, qa.y, g0x, g0y, g0z, c0);
+                    accumulate<SCHEME>(dxa1, dya1, dza1, fa1, qa1, pa.w, qa.x, qa.y, g1x, g1y, g1z, c1);
+                    accumulate<SCHEME>(dxb0, dyb0, dzb0, fb0, qb0, pb.w, qb.x, qb.y, g0x, g0y, g0z, c0);
+                    accumulate<SCHEME>(dxb1, dyb1, dzb1, fb1, qb1, pb.w, qb.x, qb.y, g1x, g1y, g1z, c1);
+                }
+                if (j < je) {
                     const float4 p = S4[j];
                     const float2 q = S2[j];
-                    const float dx0 = x0 - p.x, dy0 = y0 - p.y, dz0 = z0 - p.z;
-                    const float dx1 = x1 - p.x, dy1 = y1 - p.y, dz1 = z1 - p.z;
-                    const float r20 = fmaf(dx0, dx0, fmaf(dy0, dy0, dz0 * dz0));
-                    const float r21 = fmaf(dx1, dx1, fmaf(dy1, dy1, dz1 * dz1));
-                    float f0, q0, f1, q1;
-                    // warp-uniform fast path: closed form unless some lane has a close pair
-                    // (self pairs, coincident or sub-h/2 particles take the series)
-                    const bool close = (a0 && r20 < kc.r2_series) || (a1 && r21 < kc.r2_series);
-                    if (__any_sync(0xffffffffu, close)) {
-                        if (r20 < kc.r2_series) fq_series(r20, kc, f0, q0);
-                        else fq_closed(r20, kc, f0, q0);
-                        if (r21 < kc.r2_series) fq_series(r21, kc, f1, q1);
-                        else fq_closed(r21, kc, f1, q1);
-                    } else {
-                        fq_closed(r20, kc, f0, q0);
-                        fq_closed(r21, kc, f1, q1);
-                    }
-                    accumulate<SCHEME>(dx0, dy0, dz0, f0, q0, p.w, q.x, q.y, g0x, g0y, g0z, c0);
-                    accumulate<SCHEME>(dx1, dy1, dz1, f1, q1, p.w, q.x, q.y, g1x, g1y, g1z, c1);
+                    pair<SCHEME>(x0 - p.x, y0 - p.y, z0 - p.z, p.w, q.x, q.y, g0x, g0y, g0z, kc, c0);
+                    pair<SCHEME>(x1 - p.x, y1 - p.y, z1 - p.z, p.w, q.x, q.y, g1x, g1y, g1z, kc, c1);
                 }
             }
         }
