@@ -388,7 +388,7 @@ __device__ void deriv_expansion(const float* in, int pin, int axis, float* out, 
 }
 
 template <int SCHEME>
-__global__ void __launch_bounds__(32) l2p_combine_kernel(
+__global__ void __launch_bounds__(64) l2p_combine_kernel(
     const float* __restrict__ s6, const float* __restrict__ near6,
     const uint32_t* __restrict__ perm, int64_t n, const int* __restrict__ leaf_start, int p,
     float inv_a, const float* __restrict__ Lleaf, int use_near, int use_far,
@@ -408,22 +408,22 @@ __global__ void __launch_bounds__(32) l2p_combine_kernel(
     if (e == s) return;
     const float inv4pi = 0.0795774715459476679f;
     if (use_far) {
-        for (int i = threadIdx.x; i < 3 * nc; i += blockDim.x) Ls[i] = Lleaf[leaf * 3 * nc + i];
+        for (int i = threadIdx.x; i < 3 * nc; i += 64) Ls[i] = Lleaf[leaf * 3 * nc + i];
         __syncthreads();
         for (int c = 0; c < 3; ++c)
             for (int ax = 0; ax < 3; ++ax)
-                deriv_expansion(Ls + c * nc, p, ax, G + (c * 3 + ax) * ng, threadIdx.x, blockDim.x);
+                deriv_expansion(Ls + c * nc, p, ax, G + (c * 3 + ax) * ng, threadIdx.x, 64);
         __syncthreads();
         if (p >= 2) {
             const int pa[6] = {0, 0, 0, 1, 1, 2}, pb[6] = {0, 1, 2, 1, 2, 2};
             for (int c = 0; c < 3; ++c)
                 for (int q = 0; q < 6; ++q)
                     deriv_expansion(G + (c * 3 + pb[q]) * ng, p - 1, pa[q], H + (c * 6 + q) * nh,
-                                    threadIdx.x, blockDim.x);
+                                    threadIdx.x, 64);
         }
         __syncthreads();
         // transpose into D[k][q]: q < 9 -> G[q][k]; 9 <= q < 27 -> H[q-9][k] (0 beyond nh)
-        for (int i = threadIdx.x; i < ng * 28; i += blockDim.x) {
+        for (int i = threadIdx.x; i < ng * 28; i += 64) {
             const int k = i / 28, q = i - k * 28;
             float v = 0.f;
             if (q < 9) v = G[q * ng + k];
@@ -432,106 +432,73 @@ __global__ void __launch_bounds__(32) l2p_combine_kernel(
         }
         __syncthreads();
     }
-    // two particles per thread (j, j + 32): every vector load of derivative coefficients
-    // feeds 2 x 8 FMAs
     for (int b = s; b < e; b += 64) {
-        const int jj[2] = {b + (int)threadIdx.x, b + (int)threadIdx.x + 32};
-        bool act[2];
-        float gi[2][3], xs[2][3];
-#pragma unroll
-        for (int w = 0; w < 2; ++w) {
-            act[w] = jj[w] < e;
-            const int j = act[w] ? jj[w] : s;
-            gi[w][0] = s6[3 * n + j];
-            gi[w][1] = s6[4 * n + j];
-            gi[w][2] = s6[5 * n + j];
-            xs[w][0] = s6[j] * inv_a;
-            xs[w][1] = s6[n + j] * inv_a;
-            xs[w][2] = s6[2 * n + j] * inv_a;
+        const int j = b + threadIdx.x;
+        const bool act = j < e;
+        float u[3] = {0.f, 0.f, 0.f}, sd[3] = {0.f, 0.f, 0.f};
+        float gi[3] = {0.f, 0.f, 0.f};
+        if (act) {
+            gi[0] = s6[3 * n + j];
+            gi[1] = s6[4 * n + j];
+            gi[2] = s6[5 * n + j];
         }
-        float u[2][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
-        float sd[2][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
-        if (use_far) {
-            float acc[2][28];
+        if (use_far && act) {
+            const float x = s6[j] * inv_a, y = s6[n + j] * inv_a, z = s6[2 * n + j] * inv_a;
+            float acc[28];
 #pragma unroll
-            for (int w = 0; w < 2; ++w)
-#pragma unroll
-                for (int q = 0; q < 28; ++q) acc[w][q] = 0.f;
+            for (int q = 0; q < 28; ++q) acc[q] = 0.f;
             // R_n^m(z/a) by recurrence (m outer, n inner, n <= p-1), accumulated on the fly:
             // value_q = sum_k D[k][q] w_k, w = R_re (m = 0); 2 R_re, -2 R_im (m > 0)
-            float r2[2], dre[2], dim[2];
-#pragma unroll
-            for (int w = 0; w < 2; ++w) {
-                r2[w] = xs[w][0] * xs[w][0] + xs[w][1] * xs[w][1] + xs[w][2] * xs[w][2];
-                dre[w] = 1.f;
-                dim[w] = 0.f;
-            }
+            const float r2 = x * x + y * y + z * z;
+            float dre = 1.f, dim = 0.f;
             const int pm = p - 1;
             for (int m = 0; m <= pm; ++m) {
-                float p1re[2], p1im[2], p2re[2], p2im[2];
-#pragma unroll
-                for (int w = 0; w < 2; ++w) {
-                    if (m > 0) {
-                        const float sc = -0.5f / (float)m;
-                        const float nre = sc * (xs[w][0] * dre[w] - xs[w][1] * dim[w]);
-                        const float nim = sc * (xs[w][0] * dim[w] + xs[w][1] * dre[w]);
-                        dre[w] = nre;
-                        dim[w] = nim;
-                    }
-                    p1re[w] = p1im[w] = p2re[w] = p2im[w] = 0.f;
+                if (m > 0) {
+                    const float sc = -0.5f / (float)m;
+                    const float nre = sc * (x * dre - y * dim);
+                    const float nim = sc * (x * dim + y * dre);
+                    dre = nre;
+                    dim = nim;
                 }
+                float p2re = 0.f, p2im = 0.f, p1re = 0.f, p1im = 0.f;
                 for (int nn = m; nn <= pm; ++nn) {
-                    float cre[2], cim[2];
-#pragma unroll
-                    for (int w = 0; w < 2; ++w) {
-                        if (nn == m) {
-                            cre[w] = dre[w];
-                            cim[w] = dim[w];
-                        } else if (nn == m + 1) {
-                            cre[w] = xs[w][2] * dre[w];
-                            cim[w] = xs[w][2] * dim[w];
-                        } else {
-                            const float inv = 1.f / (float)((nn + m) * (nn - m));
-                            const float aa = (2.f * nn - 1.f) * xs[w][2];
-                            cre[w] = (aa * p1re[w] - r2[w] * p2re[w]) * inv;
-                            cim[w] = (aa * p1im[w] - r2[w] * p2im[w]) * inv;
-                        }
-                        p2re[w] = p1re[w];
-                        p2im[w] = p1im[w];
-                        p1re[w] = cre[w];
-                        p1im[w] = cim[w];
+                    float cre, cim;
+                    if (nn == m) {
+                        cre = dre;
+                        cim = dim;
+                    } else if (nn == m + 1) {
+                        cre = z * dre;
+                        cim = z * dim;
+                    } else {
+                        const float inv = 1.f / (float)((nn + m) * (nn - m));
+                        const float aa = (2.f * nn - 1.f) * z;
+                        cre = (aa * p1re - r2 * p2re) * inv;
+                        cim = (aa * p1im - r2 * p2im) * inv;
                     }
+                    p2re = p1re;
+                    p2im = p1im;
+                    p1re = cre;
+                    p1im = cim;
                     const float4* Dr = D4 + pk_re(nn, m) * 7;
                     if (m == 0) {
 #pragma unroll
                         for (int q4 = 0; q4 < 7; ++q4) {
                             const float4 d = Dr[q4];
-#pragma unroll
-                            for (int w = 0; w < 2; ++w) {
-                                acc[w][4 * q4 + 0] = fmaf(d.x, cre[w], acc[w][4 * q4 + 0]);
-                                acc[w][4 * q4 + 1] = fmaf(d.y, cre[w], acc[w][4 * q4 + 1]);
-                                acc[w][4 * q4 + 2] = fmaf(d.z, cre[w], acc[w][4 * q4 + 2]);
-                                acc[w][4 * q4 + 3] = fmaf(d.w, cre[w], acc[w][4 * q4 + 3]);
-                            }
+                            acc[4 * q4 + 0] = fmaf(d.x, cre, acc[4 * q4 + 0]);
+                            acc[4 * q4 + 1] = fmaf(d.y, cre, acc[4 * q4 + 1]);
+                            acc[4 * q4 + 2] = fmaf(d.z, cre, acc[4 * q4 + 2]);
+                            acc[4 * q4 + 3] = fmaf(d.w, cre, acc[4 * q4 + 3]);
                         }
                     } else {
                         const float4* Di = D4 + pk_im(nn, m) * 7;
-                        float wr[2], wi[2];
-#pragma unroll
-                        for (int w = 0; w < 2; ++w) {
-                            wr[w] = 2.f * cre[w];
-                            wi[w] = -2.f * cim[w];
-                        }
+                        const float wr = 2.f * cre, wi = -2.f * cim;
 #pragma unroll
                         for (int q4 = 0; q4 < 7; ++q4) {
                             const float4 d = Dr[q4], f = Di[q4];
-#pragma unroll
-                            for (int w = 0; w < 2; ++w) {
-                                acc[w][4 * q4 + 0] = fmaf(d.x, wr[w], fmaf(f.x, wi[w], acc[w][4 * q4 + 0]));
-                                acc[w][4 * q4 + 1] = fmaf(d.y, wr[w], fmaf(f.y, wi[w], acc[w][4 * q4 + 1]));
-                                acc[w][4 * q4 + 2] = fmaf(d.z, wr[w], fmaf(f.z, wi[w], acc[w][4 * q4 + 2]));
-                                acc[w][4 * q4 + 3] = fmaf(d.w, wr[w], fmaf(f.w, wi[w], acc[w][4 * q4 + 3]));
-                            }
+                            acc[4 * q4 + 0] = fmaf(d.x, wr, fmaf(f.x, wi, acc[4 * q4 + 0]));
+                            acc[4 * q4 + 1] = fmaf(d.y, wr, fmaf(f.y, wi, acc[4 * q4 + 1]));
+                            acc[4 * q4 + 2] = fmaf(d.z, wr, fmaf(f.z, wi, acc[4 * q4 + 2]));
+                            acc[4 * q4 + 3] = fmaf(d.w, wr, fmaf(f.w, wi, acc[4 * q4 + 3]));
                         }
                     }
                 }
@@ -539,47 +506,40 @@ __global__ void __launch_bounds__(32) l2p_combine_kernel(
             // acc[c*3 + axis] = d_axis phi_c ; acc[9 + c*6 + q] = Hessian pair q of phi_c
             const float sg = inv4pi * inv_a * inv_a;  // gradient scale
             const float sh = sg * inv_a;              // Hessian scale
+            u[0] = sg * (acc[2 * 3 + 1] - acc[1 * 3 + 2]);
+            u[1] = sg * (acc[0 * 3 + 2] - acc[2 * 3 + 0]);
+            u[2] = sg * (acc[1 * 3 + 0] - acc[0 * 3 + 1]);
+            auto h = [&](int c, int a, int b2) -> float {
+                const int lo = a < b2 ? a : b2, hi = a < b2 ? b2 : a;
+                const int q = lo == 0 ? hi : (lo == 1 ? 2 + hi : 5);
+                return acc[9 + c * 6 + q];
+            };
+            float J[3][3];  // J[a][k] = d_k u_a / sh
 #pragma unroll
-            for (int w = 0; w < 2; ++w) {
-                const float* A = acc[w];
-                u[w][0] = sg * (A[2 * 3 + 1] - A[1 * 3 + 2]);
-                u[w][1] = sg * (A[0 * 3 + 2] - A[2 * 3 + 0]);
-                u[w][2] = sg * (A[1 * 3 + 0] - A[0 * 3 + 1]);
-                auto h = [&](int c, int a, int b2) -> float {
-                    const int lo = a < b2 ? a : b2, hi = a < b2 ? b2 : a;
-                    const int q = lo == 0 ? hi : (lo == 1 ? 2 + hi : 5);
-                    return A[9 + c * 6 + q];
-                };
-                float J[3][3];  // J[a][k] = d_k u_a / sh
+            for (int k = 0; k < 3; ++k) {
+                J[0][k] = h(2, k, 1) - h(1, k, 2);
+                J[1][k] = h(0, k, 2) - h(2, k, 0);
+                J[2][k] = h(1, k, 0) - h(0, k, 1);
+            }
 #pragma unroll
-                for (int k = 0; k < 3; ++k) {
-                    J[0][k] = h(2, k, 1) - h(1, k, 2);
-                    J[1][k] = h(0, k, 2) - h(2, k, 0);
-                    J[2][k] = h(1, k, 0) - h(0, k, 1);
-                }
-#pragma unroll
-                for (int a2 = 0; a2 < 3; ++a2) {
-                    if (SCHEME == 0)
-                        sd[w][a2] = sh * (J[a2][0] * gi[w][0] + J[a2][1] * gi[w][1] + J[a2][2] * gi[w][2]);
-                    else
-                        sd[w][a2] = sh * (J[0][a2] * gi[w][0] + J[1][a2] * gi[w][1] + J[2][a2] * gi[w][2]);
-                }
+            for (int a2 = 0; a2 < 3; ++a2) {
+                if (SCHEME == 0)
+                    sd[a2] = sh * (J[a2][0] * gi[0] + J[a2][1] * gi[1] + J[a2][2] * gi[2]);
+                else
+                    sd[a2] = sh * (J[0][a2] * gi[0] + J[1][a2] * gi[1] + J[2][a2] * gi[2]);
             }
         }
-#pragma unroll
-        for (int w = 0; w < 2; ++w) {
-            if (!act[w]) continue;
-            const int j = jj[w];
+        if (act) {
             if (use_near) {
                 for (int a2 = 0; a2 < 3; ++a2) {
-                    u[w][a2] += near6[a2 * n + j];
-                    sd[w][a2] += near6[(3 + a2) * n + j];
+                    u[a2] += near6[a2 * n + j];
+                    sd[a2] += near6[(3 + a2) * n + j];
                 }
             }
             const int64_t i = perm[j - gbase];  // caller's input index (rank-local)
             for (int a2 = 0; a2 < 3; ++a2) {
-                vel[a2 * nout + i] = u[w][a2];
-                dgam[a2 * nout + i] = sd[w][a2];
+                vel[a2 * nout + i] = u[a2];
+                dgam[a2 * nout + i] = sd[a2];
             }
         }
     }
@@ -672,11 +632,11 @@ void launch_l2p_combine(const float* sorted6, const float* near6, const uint32_t
     }
     if (leaf_cnt <= 0) return;
     if (scheme == 0)
-        l2p_combine_kernel<0><<<(unsigned)leaf_cnt, 32, smem, st>>>(
+        l2p_combine_kernel<0><<<(unsigned)leaf_cnt, 64, smem, st>>>(
             sorted6, near6, perm, n, leaf_start, p, 1.f / a, L_leaf, use_near, use_far, vel, dgam,
             leaf_lo, gbase, nout);
     else
-        l2p_combine_kernel<1><<<(unsigned)leaf_cnt, 32, smem, st>>>(
+        l2p_combine_kernel<1><<<(unsigned)leaf_cnt, 64, smem, st>>>(
             sorted6, near6, perm, n, leaf_start, p, 1.f / a, L_leaf, use_near, use_far, vel, dgam,
             leaf_lo, gbase, nout);
 }

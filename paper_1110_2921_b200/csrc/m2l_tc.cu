@@ -21,7 +21,9 @@
 // Warp roles (320 threads): warp 0 = TMA producer, warp 1 = TMEM alloc + MMA issuer,
 // warps 2-9 = epilogue (TMEM -> FP32 register sums -> L in Morton order).
 // CTA order: parity fastest, then 8x8 tiles of row groups, so co-resident CTAs share the
-// source slabs they stream (L2 reuse).
+// source slabs they stream (L2 reuse).  CTAs run in 2-CTA clusters (same parity, adjacent
+// row groups): each loads one half (hi or lo) of an operator chunk with TMA multicast into
+// both CTAs, halving operator traffic; operator stages are released by both MMA warps.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
@@ -72,14 +74,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
             : "memory");
     }
 }
-__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
-                                            int c0, int c1, int c2) {
-    asm volatile(
-        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes "
-        "[%0], [%1, {%2, %3, %4}], [%5];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar))
-        : "memory");
-}
 __device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, uint64_t* bar,
                                             int c0, int c1, int c2, int c3, int c4) {
     asm volatile(
@@ -89,6 +83,32 @@ __device__ __forceinline__ void tma_load_5d(void* dst, const CUtensorMap* map, u
         "r"(smem_u32(bar))
         : "memory");
 }
+__device__ __forceinline__ void tma_load_3d_mc(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                               int c0, int c1, int c2, uint16_t mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        ".multicast::cluster [%0], [%1, {%2, %3, %4}], [%5], %6;" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
+    asm volatile(
+        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;" ::"r"(smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_rank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+__device__ __forceinline__ void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                     : "memory");
+}
+
 // shared-memory matrix descriptor: K-major, SWIZZLE_128B, 8-row atoms of 1024 B
 __device__ __forceinline__ uint64_t sw128_desc(const void* p) {
     const uint64_t addr = smem_u32(p);
@@ -161,7 +181,7 @@ __device__ __forceinline__ void group_rows(const TcParams& P, int g, int* tx, in
     *pz = P.bz0 + gz;
 }
 
-__global__ void __launch_bounds__(TC_THREADS, 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     m2l_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant__ CUtensorMap tmA_lo,
                   const __grid_constant__ CUtensorMap tmB_hi, const __grid_constant__ CUtensorMap tmB_lo,
                   TcParams P) {
@@ -179,8 +199,12 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int pi = blockIdx.x & 7;  // target parity fastest (CTAs of one row group share slabs)
-    const int g = blockIdx.x >> 3;
+    // 2-CTA clusters: both CTAs take the same parity (same operator sequence) and adjacent row
+    // groups; each loads one half (hi / lo) of every operator chunk and multicasts it to both
+    const uint32_t crank = cluster_rank();
+    const int cidx = blockIdx.x >> 1;
+    const int pi = cidx & 7;  // target parity fastest (co-resident clusters share slabs)
+    const int g = ((cidx >> 3) << 1) | (int)crank;
     const int pix = pi & 1, piy = (pi >> 1) & 1, piz = (pi >> 2) & 1;
     int gtx, gpy0, gpz;
     group_rows(P, g, &gtx, &gpy0, &gpz);
@@ -190,7 +214,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < TC_AST; ++i) {
             mbar_init(&a_full[i], 1);
-            mbar_init(&a_empty[i], 1);
+            mbar_init(&a_empty[i], 2);  // both CTAs' MMA warps release a shared operator stage
         }
         for (int i = 0; i < TC_BST; ++i) {
             mbar_init(&b_full[i], 1);
@@ -210,6 +234,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     tc_fence_before();
     __syncthreads();
+    cluster_sync();  // peer barriers initialised before any multicast lands
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
@@ -227,9 +252,13 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                 const int pis = (sx & 1) | ((sy & 1) << 1) | ((sz & 1) << 2);
                 for (int kc = 0; kc < TC_NKC; ++kc) {
                     mbar_wait(&a_empty[sa], pa ^ 1);
-                    mbar_expect_tx(&a_full[sa], 2u * A_BYTES);
-                    tma_load_3d(Abuf + (sa * 2 + 0) * A_BYTES, &tmA_hi, &a_full[sa], kc * 32, 0, slot);
-                    tma_load_3d(Abuf + (sa * 2 + 1) * A_BYTES, &tmA_lo, &a_full[sa], kc * 32, 0, slot);
+                    mbar_expect_tx(&a_full[sa], 2u * A_BYTES);  // hi from rank 0, lo from rank 1
+                    if (crank == 0)
+                        tma_load_3d_mc(Abuf + (sa * 2 + 0) * A_BYTES, &tmA_hi, &a_full[sa], kc * 32, 0,
+                                       slot, (uint16_t)3);
+                    else
+                        tma_load_3d_mc(Abuf + (sa * 2 + 1) * A_BYTES, &tmA_lo, &a_full[sa], kc * 32, 0,
+                                       slot, (uint16_t)3);
                     if (++sa == TC_AST) {
                         sa = 0;
                         pa ^= 1;
@@ -292,7 +321,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
                             pb ^= 1;
                         }
                     }
-                    if (lane == 0) mma_commit(&a_empty[sa]);
+                    if (lane == 0) mma_commit_mc(&a_empty[sa], (uint16_t)3);  // release in both CTAs
                     __syncwarp();
                     if (++sa == TC_AST) {
                         sa = 0;
@@ -353,6 +382,7 @@ __global__ void __launch_bounds__(TC_THREADS, 1)
     }
     tc_fence_before();
     __syncthreads();
+    cluster_sync();  // the peer may still multicast into / arrive on this CTA until here
     tc_fence_after();
     if (warp == 1)
         asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem),
@@ -490,7 +520,7 @@ int launch_m2l_tc(const float* ops_hi, const float* ops_lo, const int* il_slots,
     P.level = level;
     P.slots = il_slots;
     P.L = L_l;
-    if (P.rows % TC_T != 0 || bny % TC_T != 0) return -4;
+    if (P.rows % TC_T != 0 || bny % TC_T != 0 || (P.rows / TC_T) % 2 != 0) return -4;
     const unsigned grid = (unsigned)(8 * (P.rows / TC_T));
     m2l_tc_kernel<<<grid, TC_THREADS, TC_SMEM, st>>>(mAh, mAl, mBh, mBl, P);
     return 0;
