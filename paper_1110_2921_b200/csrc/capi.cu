@@ -520,7 +520,7 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
         const bool allow_tc = !(m2l_env && strcmp(m2l_env, "simt") == 0) && c->d_tc_hi;
         for (int l = 1; l <= depth; ++l) {
             const int box[6] = {0, 0, 0, 1 << (l - 1), 1 << (l - 1), 1 << (l - 1)};
-            if (allow_tc && m2l_tc_supported(p, l) && box[4] % 2 == 0) {
+            if (allow_tc && m2l_tc_supported(p, l) && m2l_tc_shape_ok(box)) {
                 const size_t need = m2l_tc_grid_floats(l);
                 if (need > c->g_cap) {
                     dfree(c->g_hi);

@@ -37,8 +37,8 @@ namespace {
 constexpr int TC_T = 2;        // target rows per CTA (one accumulator tile each)
 constexpr int TC_G = 1;        // offsets per TMEM accumulation group (flushed to FP32 registers)
 constexpr int TC_NKC = 4;      // K chunks of 32 floats (128 B)
-constexpr int TC_AST = 2;      // A (operator) pipeline stages
-constexpr int TC_BST = 6;      // B (slab) pipeline stages (TMA latency ~ several MMA groups)
+constexpr int TC_AST = 4;      // A (operator) pipeline stages
+constexpr int TC_BST = 4;      // B (slab) pipeline stages
 constexpr int A_BYTES = 128 * 128;  // one K chunk of one operator half (hi or lo): 16 KB
 constexpr int B_BYTES = 96 * 128;   // one K chunk of one slab half: <= 12 KB
 constexpr int TC_EPI_WARPS = 8;  // 2 per TMEM lane quarter: warp pair splits the T tiles
@@ -438,6 +438,15 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 }
 
 }  // namespace
+
+bool m2l_tc_shape_ok(const int box[6]) {
+    // 2 target rows per CTA and CTA pairs (clusters): rows / 2 must be even
+    const int bnx = box[3], bny = box[4], bnz = box[5];
+    const int XT = bnx < 32 ? bnx : 32;
+    if (bny % TC_T != 0 || bnx % XT != 0) return false;
+    const int rows = bny * bnz * (bnx / XT);
+    return (rows / TC_T) % 2 == 0;
+}
 
 bool m2l_tc_supported(int p, int level) {
     return (p + 1) * (p + 1) <= 128 && level >= 2 && get_encode() != nullptr;

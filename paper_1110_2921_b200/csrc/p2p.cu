@@ -56,6 +56,41 @@ struct Acc {
     float u0, u1, u2, a0, a1, a2, b0, b1, b2;
 };
 
+// ---- packed FP32x2 (Blackwell FFMA2 / FMUL2 / FADD2): lane's two targets in .lo / .hi ----
+typedef unsigned long long f2;
+__device__ __forceinline__ f2 pk(float a, float b) {
+    f2 r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ f2 bc(float a) { return pk(a, a); }
+__device__ __forceinline__ void upk(f2 v, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ f2 add2(f2 a, f2 b) {
+    f2 r;
+    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2 sub2(f2 a, f2 b) {
+    f2 r;
+    asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2 mul2(f2 a, f2 b) {
+    f2 r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
+    f2 r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+struct Acc2 {
+    f2 u0, u1, u2, a0, a1, a2, b0, b1, b2;
+};
+
 // f, q by the Taylor series (rho^2 < 1/4, incl. r = 0)
 __device__ __forceinline__ void fq_series(float r2, const KernelConsts& kc, float& f, float& q) {
     // f = zeta0 sum (-s)^k/(k!(2k+3)),  q = zeta0/sigma^2 sum_{k>=1} (-1)^k s^{k-1}/((k-1)!(2k+3))
@@ -97,6 +132,59 @@ __device__ __forceinline__ void fq_closed(float r2, const KernelConsts& kc, floa
     const float rinv2 = rinv * rinv;
     f = g4pi * (rinv2 * rinv);
     q = fmaf(kc.zeta0, e, -3.f * f) * rinv2;
+}
+
+// f, q for two pairs at once (closed form)
+__device__ __forceinline__ void fq_closed2(f2 r2, const KernelConsts& kc, f2& f, f2& q) {
+    float ra, rb;
+    upk(r2, ra, rb);
+    const f2 rinv = pk(rsqrt_approx(ra), rsqrt_approx(rb));
+    float ea, eb;
+    upk(mul2(r2, bc(kc.neg_l2e_inv2s2)), ea, eb);
+    const f2 e = pk(ex2_approx(ea), ex2_approx(eb));
+    const f2 r = mul2(r2, rinv);
+    float da, db;
+    upk(fma2(r, bc(kc.t_scale), bc(1.f)), da, db);
+    const f2 t = add2(pk(rcp_approx(da), rcp_approx(db)), bc(-0.5f));
+    f2 E = bc(6.204596458e-03f);
+    E = fma2(E, t, bc(-1.664231425e-03f));
+    E = fma2(E, t, bc(-1.861016238e-02f));
+    E = fma2(E, t, bc(4.873839158e-03f));
+    E = fma2(E, t, bc(5.027046960e-02f));
+    E = fma2(E, t, bc(7.692235843e-02f));
+    E = fma2(E, t, bc(6.798874982e-02f));
+    E = fma2(E, t, bc(2.032374185e-02f));
+    const f2 Q = fma2(bc(kc.q_scale), r, E);
+    const f2 g4pi = sub2(bc(0.0795774715459476679f), mul2(e, Q));  // g / (4 pi)
+    const f2 rinv2 = mul2(rinv, rinv);
+    f = mul2(g4pi, mul2(rinv2, rinv));
+    q = mul2(sub2(mul2(bc(kc.zeta0), e), mul2(bc(3.f), f)), rinv2);
+}
+
+template <int SCHEME>
+__device__ __forceinline__ void accumulate2(f2 dx, f2 dy, f2 dz, f2 f, f2 q, float gjx,
+                                            float gjy, float gjz, f2 gix, f2 giy, f2 giz,
+                                            Acc2& acc) {
+    const f2 cx = sub2(mul2(bc(gjy), dz), mul2(bc(gjz), dy));  // gamma_j x d
+    const f2 cy = sub2(mul2(bc(gjz), dx), mul2(bc(gjx), dz));
+    const f2 cz = sub2(mul2(bc(gjx), dy), mul2(bc(gjy), dx));
+    acc.u0 = fma2(f, cx, acc.u0);
+    acc.u1 = fma2(f, cy, acc.u1);
+    acc.u2 = fma2(f, cz, acc.u2);
+    acc.a0 = fma2(f, bc(gjx), acc.a0);
+    acc.a1 = fma2(f, bc(gjy), acc.a1);
+    acc.a2 = fma2(f, bc(gjz), acc.a2);
+    if (SCHEME == 0) {
+        const f2 w = mul2(q, fma2(gix, dx, fma2(giy, dy, mul2(giz, dz))));
+        acc.b0 = fma2(w, cx, acc.b0);
+        acc.b1 = fma2(w, cy, acc.b1);
+        acc.b2 = fma2(w, cz, acc.b2);
+    } else {
+        const f2 w = mul2(q, fma2(gix, cx, fma2(giy, cy, mul2(giz, cz))));
+        acc.b0 = fma2(w, dx, acc.b0);
+        acc.b1 = fma2(w, dy, acc.b1);
+        acc.b2 = fma2(w, dz, acc.b2);
+    }
 }
 
 template <int SCHEME>
@@ -253,7 +341,13 @@ __global__ void __launch_bounds__(P2P_THREADS, 2) p2p_kernel(
             x1 = s6[i1] + tox; y1 = s6[n + i1] + toy; z1 = s6[2 * n + i1] + toz;
             g1x = s6[3 * n + i1]; g1y = s6[4 * n + i1]; g1z = s6[5 * n + i1];
         }
-        Acc c0 = {0, 0, 0, 0, 0, 0, 0, 0, 0}, c1 = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+        // targets (i0, i1) packed in the two halves of f2 registers
+        const f2 X = pk(x0, x1), Y = pk(y0, y1), Z = pk(z0, z1);
+        const f2 GX = pk(g0x, g1x), GY = pk(g0y, g1y), GZ = pk(g0z, g1z);
+        const f2 z2 = pk(0.f, 0.f);
+        Acc2 C = {z2, z2, z2, z2, z2, z2, z2, z2, z2};
+        const f2 thr = bc(kc.r2_series);
+        (void)thr;
         // windows [w0, w1) of the concatenated region sources, P2P_CAP at a time
         for (int w0 = 0; w0 < total; w0 += P2P_CAP) {
             const int w1 = min(w0 + P2P_CAP, total);
@@ -276,46 +370,54 @@ __global__ void __launch_bounds__(P2P_THREADS, 2) p2p_kernel(
                 const int rx = bx + nb % 3, ry = by + (nb / 3) % 3, rz = bz + nb / 9;
                 const int rl = rx + 4 * ry + 16 * rz;
                 const int js = max(rstart[rl], w0) - w0, je = min(rstart[rl + 1], w1) - w0;
-                // two sources per iteration (4 pairs per lane): one vote, one loop test
-                int j = js;
-                for (; j + 1 < je; j += 2) {
-                    const float4 pa = S4[j], pb = S4[j + 1];
-                    const float2 qa = S2[j], qb = S2[j + 1];
-                    const float dxa0 = x0 - pa.x, dya0 = y0 - pa.y, dza0 = z0 - pa.z;
-                    const float dxa1 = x1 - pa.x, dya1 = y1 - pa.y, dza1 = z1 - pa.z;
-                    const float dxb0 = x0 - pb.x, dyb0 = y0 - pb.y, dzb0 = z0 - pb.z;
-                    const float dxb1 = x1 - pb.x, dyb1 = y1 - pb.y, dzb1 = z1 - pb.z;
-                    const float ra0 = fmaf(dxa0, dxa0, fmaf(dya0, dya0, dza0 * dza0));
-                    const float ra1 = fmaf(dxa1, dxa1, fmaf(dya1, dya1, dza1 * dza1));
-                    const float rb0 = fmaf(dxb0, dxb0, fmaf(dyb0, dyb0, dzb0 * dzb0));
-                    const float rb1 = fmaf(dxb1, dxb1, fmaf(dyb1, dyb1, dzb1 * dzb1));
-                    float fa0, qa0, fa1, qa1, fb0, qb0, fb1, qb1;
-                    const float thr = kc.r2_series;
-                    const bool close = (a0 && (ra0 < thr || rb0 < thr)) || (a1 && (ra1 < thr || rb1 < thr));
+                // two sources per iteration; each source x two targets = one packed pair
+                for (int j = js; j < je; j += 2) {
+                    const bool two = j + 1 < je;
+                    const float4 pa = S4[j];
+                    const float2 qa = S2[j];
+                    const float4 pb = two ? S4[j + 1] : pa;
+                    const float2 qb = two ? S2[j + 1] : make_float2(0.f, 0.f);
+                    const float gbx = two ? pb.w : 0.f;  // a missing 2nd source has zero strength
+                    const f2 dxa = sub2(X, bc(pa.x)), dya = sub2(Y, bc(pa.y)), dza = sub2(Z, bc(pa.z));
+                    const f2 dxb = sub2(X, bc(pb.x)), dyb = sub2(Y, bc(pb.y)), dzb = sub2(Z, bc(pb.z));
+                    const f2 r2a = fma2(dxa, dxa, fma2(dya, dya, mul2(dza, dza)));
+                    const f2 r2b = fma2(dxb, dxb, fma2(dyb, dyb, mul2(dzb, dzb)));
+                    float ra0, ra1, rb0, rb1;
+                    upk(r2a, ra0, ra1);
+                    upk(r2b, rb0, rb1);
+                    const float th = kc.r2_series;
+                    const bool close = (a0 && (ra0 < th || rb0 < th)) || (a1 && (ra1 < th || rb1 < th));
+                    f2 fa, qa2, fb, qb2;
                     if (__any_sync(0xffffffffu, close)) {
-                        if (ra0 < thr) fq_series(ra0, kc, fa0, qa0); else fq_closed(ra0, kc, fa0, qa0);
-                        if (ra1 < thr) fq_series(ra1, kc, fa1, qa1); else fq_closed(ra1, kc, fa1, qa1);
-                        if (rb0 < thr) fq_series(rb0, kc, fb0, qb0); else fq_closed(rb0, kc, fb0, qb0);
-                        if (rb1 < thr) fq_series(rb1, kc, fb1, qb1); else fq_closed(rb1, kc, fb1, qb1);
+                        // rare path (self pairs, close particles): per pair, series or closed form
+                        float f0, q0, f1, q1;
+                        if (ra0 < th) fq_series(ra0, kc, f0, q0); else fq_closed(ra0, kc, f0, q0);
+                        if (ra1 < th) fq_series(ra1, kc, f1, q1); else fq_closed(ra1, kc, f1, q1);
+                        fa = pk(f0, f1);
+                        qa2 = pk(q0, q1);
+                        if (rb0 < th) fq_series(rb0, kc, f0, q0); else fq_closed(rb0, kc, f0, q0);
+                        if (rb1 < th) fq_series(rb1, kc, f1, q1); else fq_closed(rb1, kc, f1, q1);
+                        fb = pk(f0, f1);
+                        qb2 = pk(q0, q1);
                     } else {
-                        fq_closed(ra0, kc, fa0, qa0);
-                        fq_closed(ra1, kc, fa1, qa1);
-                        fq_closed(rb0, kc, fb0, qb0);
-                        fq_closed(rb1, kc, fb1, qb1);
+                        fq_closed2(r2a, kc, fa, qa2);
+                        fq_closed2(r2b, kc, fb, qb2);
                     }
-                    accumulate<SCHEME>(dxa0, dya0, dza0, fa0, qa0, pa.w, qa.x, qa.y, g0x, g0y, g0z, c0);
-                    accumulate<SCHEME>(dxa1, dya1, dza1, fa1, qa1, pa.w, qa.x, qa.y, g1x, g1y, g1z, c1);
-                    accumulate<SCHEME>(dxb0, dyb0, dzb0, fb0, qb0, pb.w, qb.x, qb.y, g0x, g0y, g0z, c0);
-                    accumulate<SCHEME>(dxb1, dyb1, dzb1, fb1, qb1, pb.w, qb.x, qb.y, g1x, g1y, g1z, c1);
-                }
-                if (j < je) {
-                    const float4 p = S4[j];
-                    const float2 q = S2[j];
-                    pair<SCHEME>(x0 - p.x, y0 - p.y, z0 - p.z, p.w, q.x, q.y, g0x, g0y, g0z, kc, c0);
-                    pair<SCHEME>(x1 - p.x, y1 - p.y, z1 - p.z, p.w, q.x, q.y, g1x, g1y, g1z, kc, c1);
+                    accumulate2<SCHEME>(dxa, dya, dza, fa, qa2, pa.w, qa.x, qa.y, GX, GY, GZ, C);
+                    accumulate2<SCHEME>(dxb, dyb, dzb, fb, qb2, gbx, qb.x, qb.y, GX, GY, GZ, C);
                 }
             }
         }
+        Acc c0, c1;
+        upk(C.u0, c0.u0, c1.u0);
+        upk(C.u1, c0.u1, c1.u1);
+        upk(C.u2, c0.u2, c1.u2);
+        upk(C.a0, c0.a0, c1.a0);
+        upk(C.a1, c0.a1, c1.a1);
+        upk(C.a2, c0.a2, c1.a2);
+        upk(C.b0, c0.b0, c1.b0);
+        upk(C.b1, c0.b1, c1.b1);
+        upk(C.b2, c0.b2, c1.b2);
         float o[6];
         if (a0) {
             finish<SCHEME>(c0, g0x, g0y, g0z, o);

@@ -91,6 +91,7 @@ void launch_l2p_combine(const float* sorted6, const float* near6, const uint32_t
 
 // m2l_tc.cu (tcgen05, 3xTF32)
 bool m2l_tc_supported(int p, int level);
+bool m2l_tc_shape_ok(const int box[6]);
 size_t m2l_tc_grid_floats(int level);
 int launch_m2l_tc(const float* ops_hi, const float* ops_lo, const int* il_slots, int p,
                   const float* M_l, float* L_l, int level, int periodic, float* ghi, float* glo,
