@@ -57,3 +57,21 @@ def test_no_oracle_in_product_path():
                 txt = open(os.path.join(root, fn)).read()
                 assert "import oracle" not in txt and "liboracle" not in txt, fn
                 assert "from oracle" not in txt, fn
+
+
+def test_missing_library_fails_loudly(tmp_path):
+    """No CPU fallback: without libvfmm.so the binding raises instead of computing."""
+    import importlib
+
+    mod = importlib.reload(vf)
+    try:
+        mod._LIB = None
+        with pytest.raises(OSError):
+            mod.load_library(str(tmp_path / "missing.so"))
+    finally:
+        importlib.reload(vf)
+
+
+def test_partition_helper_without_gpu():
+    lo, hi = vf.partition(6, 8, 7)
+    assert hi == 1 << 18 and lo == 7 * (1 << 15)
