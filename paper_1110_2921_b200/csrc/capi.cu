@@ -565,6 +565,7 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
         c->have_exp = true;
     }
     CK(cudaEventRecord(c->ev[7], st), "event");
+    if (getenv("VFMM_DEBUG_SYNC")) CK(cudaStreamSynchronize(st), "debug sync");
     // ---- near field ----
     if (use_near) {
         CK(cudaMemsetAsync(c->d_pairs, 0, sizeof(unsigned long long), st), "memset pairs");

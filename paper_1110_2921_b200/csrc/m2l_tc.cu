@@ -9,8 +9,9 @@
 // B = a "slab" of source multipoles: one x-row of XT <= 32 parent cells x 3 strength
 // components = N <= 96 rows, read from a parity-major, halo-padded copy of the level's
 // multipoles (m2l_stage_kernel) so every (target row, offset) maps to one TMA box.
-// A CTA owns T = 2 target rows (Py, Pz) of one parity: 2 accumulator tiles of 128 x N fp32
-// in TMEM; operators are loaded once per CTA per offset and reused by both rows.
+// A CTA owns T = 2 target rows (Py, Pz) of one parity; their slabs are stacked in one B
+// stage so a single MMA (N' = 2N <= 192) serves both rows: the operator is read from shared
+// memory once per K-step for both (2 accumulator tiles side by side in TMEM).
 //
 // Accuracy: the tensor core accumulates with truncation, so a TMEM chain over all
 // 189 offsets x 16 K-steps x 3 products (~9000 accumulations) drifts by ~1e-4.  The chain is
@@ -37,10 +38,10 @@ namespace {
 constexpr int TC_T = 2;        // target rows per CTA (one accumulator tile each)
 constexpr int TC_G = 1;        // offsets per TMEM accumulation group (flushed to FP32 registers)
 constexpr int TC_NKC = 4;      // K chunks of 32 floats (128 B)
-constexpr int TC_AST = 4;      // A (operator) pipeline stages
-constexpr int TC_BST = 4;      // B (slab) pipeline stages
+constexpr int TC_AST = 2;      // A (operator) pipeline stages
+constexpr int TC_BST = 3;      // B pipeline stages (each holds the slabs of all T rows)
 constexpr int A_BYTES = 128 * 128;  // one K chunk of one operator half (hi or lo): 16 KB
-constexpr int B_BYTES = 96 * 128;   // one K chunk of one slab half: <= 12 KB
+constexpr int B_BYTES = 2 * 96 * 128;  // one K chunk of the T = 2 stacked slabs, one half: <= 24 KB
 constexpr int TC_EPI_WARPS = 8;  // 2 per TMEM lane quarter: warp pair splits the T tiles
 constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;
 constexpr size_t TC_SMEM = 1024 + (size_t)TC_AST * 2 * A_BYTES + (size_t)TC_BST * 2 * B_BYTES + 512;
@@ -263,19 +264,20 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
                         sa = 0;
                         pa ^= 1;
                     }
+                    // both rows' slabs stacked in one stage: rows [t N, (t+1) N) of the B operand
+                    mbar_wait(&b_empty[sb], pb ^ 1);
+                    mbar_expect_tx(&b_full[sb], (uint32_t)TC_T * b_tx);
                     for (int t = 0; t < TC_T; ++t) {
-                        mbar_wait(&b_empty[sb], pb ^ 1);
-                        mbar_expect_tx(&b_full[sb], b_tx);
                         const int c1 = 3 * (2 + P.bx0 + gtx * P.XT + dx);
                         const int c2 = 2 + gpy0 + t + dy, c3 = 2 + gpz + dz;
-                        tma_load_5d(Bbuf + (sb * 2 + 0) * B_BYTES, &tmB_hi, &b_full[sb], kc * 32, c1,
-                                    c2, c3, pis);
-                        tma_load_5d(Bbuf + (sb * 2 + 1) * B_BYTES, &tmB_lo, &b_full[sb], kc * 32, c1,
-                                    c2, c3, pis);
-                        if (++sb == TC_BST) {
-                            sb = 0;
-                            pb ^= 1;
-                        }
+                        uint8_t* bh = Bbuf + (sb * 2 + 0) * B_BYTES + t * P.N * 128;
+                        uint8_t* bl = Bbuf + (sb * 2 + 1) * B_BYTES + t * P.N * 128;
+                        tma_load_5d(bh, &tmB_hi, &b_full[sb], kc * 32, c1, c2, c3, pis);
+                        tma_load_5d(bl, &tmB_lo, &b_full[sb], kc * 32, c1, c2, c3, pis);
+                    }
+                    if (++sb == TC_BST) {
+                        sb = 0;
+                        pb ^= 1;
                     }
                 }
             }
@@ -283,8 +285,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     } else if (warp == 1) {
         // ===================== MMA issuer =====================
         // instruction descriptor: D f32, A/B tf32, both K-major, N, M = 128
-        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(P.N >> 3) << 17) |
-                               ((uint32_t)(128 >> 4) << 24);
+        // one MMA covers both rows: N' = T N columns (tile t at columns [t N, (t+1) N))
+        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) |
+                               ((uint32_t)((TC_T * P.N) >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
         int sa = 0, sb = 0;
         uint32_t pa = 0, pb = 0;
         for (int grp = 0; grp < ngroups; ++grp) {
@@ -298,28 +301,26 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
                     tc_fence_after();
                     const uint64_t ahi = sw128_desc(Abuf + (sa * 2 + 0) * A_BYTES);
                     const uint64_t alo = sw128_desc(Abuf + (sa * 2 + 1) * A_BYTES);
-                    for (int t = 0; t < TC_T; ++t) {
-                        mbar_wait(&b_full[sb], pb);
-                        tc_fence_after();
-                        const uint64_t bhi = sw128_desc(Bbuf + (sb * 2 + 0) * B_BYTES);
-                        const uint64_t blo = sw128_desc(Bbuf + (sb * 2 + 1) * B_BYTES);
-                        const uint32_t d = tmem + (uint32_t)(buf * 256 + t * P.N);
-                        if (lane == 0) {
+                    mbar_wait(&b_full[sb], pb);
+                    tc_fence_after();
+                    const uint64_t bhi = sw128_desc(Bbuf + (sb * 2 + 0) * B_BYTES);
+                    const uint64_t blo = sw128_desc(Bbuf + (sb * 2 + 1) * B_BYTES);
+                    const uint32_t d = tmem + (uint32_t)(buf * 256);
+                    if (lane == 0) {
 #pragma unroll
-                            for (int ks = 0; ks < 4; ++ks) {  // K = 8 tf32 = 32 B per MMA
-                                const uint64_t adv = (uint64_t)(ks * 2);
-                                const uint32_t acc = (oi != grp * TC_G || kc != 0 || ks != 0) ? 1u : 0u;
-                                mma_tf32(d, ahi + adv, bhi + adv, idesc, acc);
-                                mma_tf32(d, ahi + adv, blo + adv, idesc, 1u);
-                                mma_tf32(d, alo + adv, bhi + adv, idesc, 1u);
-                            }
-                            mma_commit(&b_empty[sb]);
+                        for (int ks = 0; ks < 4; ++ks) {  // K = 8 tf32 = 32 B per MMA
+                            const uint64_t adv = (uint64_t)(ks * 2);
+                            const uint32_t acc = (oi != grp * TC_G || kc != 0 || ks != 0) ? 1u : 0u;
+                            mma_tf32(d, ahi + adv, bhi + adv, idesc, acc);
+                            mma_tf32(d, ahi + adv, blo + adv, idesc, 1u);
+                            mma_tf32(d, alo + adv, bhi + adv, idesc, 1u);
                         }
-                        __syncwarp();
-                        if (++sb == TC_BST) {
-                            sb = 0;
-                            pb ^= 1;
-                        }
+                        mma_commit(&b_empty[sb]);
+                    }
+                    __syncwarp();
+                    if (++sb == TC_BST) {
+                        sb = 0;
+                        pb ^= 1;
                     }
                     if (lane == 0) mma_commit_mc(&a_empty[sa], (uint16_t)3);  // release in both CTAs
                     __syncwarp();
