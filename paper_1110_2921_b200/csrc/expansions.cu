@@ -42,6 +42,10 @@ __device__ __forceinline__ uint32_t compact3d(uint32_t v) {
     return v;
 }
 
+// recurrence constants of the solid harmonics: 1/((n+m)(n-m)) [n][m] and -1/(2m)
+__constant__ float c_rinv[17 * 17] = {0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 2.500000000e-01f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 1.111111111e-01f, 1.250000000e-01f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 6.250000000e-02f, 6.666666667e-02f, 8.333333333e-02f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 4.000000000e-02f, 4.166666667e-02f, 4.761904762e-02f, 6.250000000e-02f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 2.777777778e-02f, 2.857142857e-02f, 3.125000000e-02f, 3.703703704e-02f, 5.000000000e-02f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 2.040816327e-02f, 2.083333333e-02f, 2.222222222e-02f, 2.500000000e-02f, 3.030303030e-02f, 4.166666667e-02f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 1.562500000e-02f, 1.587301587e-02f, 1.666666667e-02f, 1.818181818e-02f, 2.083333333e-02f, 2.564102564e-02f, 3.571428571e-02f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 1.234567901e-02f, 1.250000000e-02f, 1.298701299e-02f, 1.388888889e-02f, 1.538461538e-02f, 1.785714286e-02f, 2.222222222e-02f, 3.125000000e-02f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 1.000000000e-02f, 1.010101010e-02f, 1.041666667e-02f, 1.098901099e-02f, 1.190476190e-02f, 1.333333333e-02f, 1.562500000e-02f, 1.960784314e-02f, 2.777777778e-02f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 8.264462810e-03f, 8.333333333e-03f, 8.547008547e-03f, 8.928571429e-03f, 9.523809524e-03f, 1.041666667e-02f, 1.176470588e-02f, 1.388888889e-02f, 1.754385965e-02f, 2.500000000e-02f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 6.944444444e-03f, 6.993006993e-03f, 7.142857143e-03f, 7.407407407e-03f, 7.812500000e-03f, 8.403361345e-03f, 9.259259259e-03f, 1.052631579e-02f, 1.250000000e-02f, 1.587301587e-02f, 2.272727273e-02f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 5.917159763e-03f, 5.952380952e-03f, 6.060606061e-03f, 6.250000000e-03f, 6.535947712e-03f, 6.944444444e-03f, 7.518796992e-03f, 8.333333333e-03f, 9.523809524e-03f, 1.136363636e-02f, 1.449275362e-02f, 2.083333333e-02f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 5.102040816e-03f, 5.128205128e-03f, 5.208333333e-03f, 5.347593583e-03f, 5.555555556e-03f, 5.847953216e-03f, 6.250000000e-03f, 6.802721088e-03f, 7.575757576e-03f, 8.695652174e-03f, 1.041666667e-02f, 1.333333333e-02f, 1.923076923e-02f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 4.444444444e-03f, 4.464285714e-03f, 4.524886878e-03f, 4.629629630e-03f, 4.784688995e-03f, 5.000000000e-03f, 5.291005291e-03f, 5.681818182e-03f, 6.211180124e-03f, 6.944444444e-03f, 8.000000000e-03f, 9.615384615e-03f, 1.234567901e-02f, 1.785714286e-02f, 0.000000000e+00f, 0.000000000e+00f, 0.000000000e+00f, 3.906250000e-03f, 3.921568627e-03f, 3.968253968e-03f, 4.048582996e-03f, 4.166666667e-03f, 4.329004329e-03f, 4.545454545e-03f, 4.830917874e-03f, 5.208333333e-03f, 5.714285714e-03f, 6.410256410e-03f, 7.407407407e-03f, 8.928571429e-03f, 1.149425287e-02f, 1.666666667e-02f, 0.000000000e+00f, 0.000000000e+00f};
+__constant__ float c_mhalf[17] = {0.000000000e+00f, -5.000000000e-01f, -2.500000000e-01f, -1.666666667e-01f, -1.250000000e-01f, -1.000000000e-01f, -8.333333333e-02f, -7.142857143e-02f, -6.250000000e-02f, -5.555555556e-02f, -5.000000000e-02f, -4.545454545e-02f, -4.166666667e-02f, -3.846153846e-02f, -3.571428571e-02f, -3.333333333e-02f, -3.125000000e-02f};
+
 // ---------------------------------------------------------------------------
 // P2M (Eq. 10): Mt[c][n,m] = sum_j gamma_{j,c} conj(R_n^m((x_j - centre)/a))
 // one block (64 threads) per leaf; thread j builds conj(R) of particle j in smem,
@@ -54,7 +58,7 @@ __device__ void solid_R_packed(float x, float y, float z, int p, float* out, int
     float dre = 1.f, dim = 0.f;  // R_m^m
     for (int m = 0; m <= p; ++m) {
         if (m > 0) {
-            const float s = -0.5f / (float)m;
+            const float s = c_mhalf[m];
             const float nre = s * (x * dre - y * dim);
             const float nim = s * (x * dim + y * dre);
             dre = nre;
@@ -70,7 +74,7 @@ __device__ void solid_R_packed(float x, float y, float z, int p, float* out, int
             if (m > 0) out[pk_im(m + 1, m) * stride] = conj_ ? -p1im : p1im;
         }
         for (int n = m + 2; n <= p; ++n) {
-            const float inv = 1.f / (float)((n + m) * (n - m));
+            const float inv = c_rinv[n * 17 + m];
             const float a = (2.f * n - 1.f) * z;
             const float nre = (a * p1re - r2 * p2re) * inv;
             const float nim = (a * p1im - r2 * p2im) * inv;
@@ -454,7 +458,7 @@ __global__ void __launch_bounds__(64) l2p_combine_kernel(
             const int pm = p - 1;
             for (int m = 0; m <= pm; ++m) {
                 if (m > 0) {
-                    const float sc = -0.5f / (float)m;
+                    const float sc = c_mhalf[m];
                     const float nre = sc * (x * dre - y * dim);
                     const float nim = sc * (x * dim + y * dre);
                     dre = nre;
@@ -470,7 +474,7 @@ __global__ void __launch_bounds__(64) l2p_combine_kernel(
                         cre = z * dre;
                         cim = z * dim;
                     } else {
-                        const float inv = 1.f / (float)((nn + m) * (nn - m));
+                        const float inv = c_rinv[nn * 17 + m];
                         const float aa = (2.f * nn - 1.f) * z;
                         cre = (aa * p1re - r2 * p2re) * inv;
                         cim = (aa * p1im - r2 * p2im) * inv;
