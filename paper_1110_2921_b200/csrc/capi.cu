@@ -29,6 +29,10 @@ struct vfmm_ctx {
     float *d_tc_hi = nullptr, *d_tc_lo = nullptr;  // tensor-core M2L operators
     float *g_hi = nullptr, *g_lo = nullptr;        // tensor-core M2L staged source grid
     size_t g_cap = 0;
+    float *g2_hi = nullptr, *g2_lo = nullptr;      // staging for the side stream (levels < L)
+    size_t g2_cap = 0;
+    cudaStream_t side = nullptr;                   // coarse M2L levels run here, joined by events
+    cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int* d_slots = nullptr;  // [8][189]
     // workspace
     int64_t cap_n = 0;
@@ -384,6 +388,9 @@ vfmm_status vfmm_create(vfmm_ctx** out, const vfmm_params* prm, int device) {
         if (e2 == cudaSuccess) e2 = cudaMalloc((void**)&c->d_pairs, sizeof(unsigned long long));
         if (e2 == cudaSuccess) e2 = cudaMemset(c->d_err, 0, sizeof(int));
         if (e2 == cudaSuccess) e2 = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
+        if (e2 == cudaSuccess) e2 = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+        if (e2 == cudaSuccess) e2 = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
+        if (e2 == cudaSuccess) e2 = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
         for (int i = 0; i < vfmm_ctx::NEV && e2 == cudaSuccess; ++i) e2 = cudaEventCreate(&c->ev[i]);
         if (e2 != cudaSuccess) s = cuda_fail(c, e2, "create");
     }
@@ -515,24 +522,33 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
     }
     CK(cudaEventRecord(c->ev[5], st), "event");
     // ---- M2L at every level (writes L_l), then periodic images + L2L top-down (adds) ----
+    // The levels are independent: levels 1..L-1 (few CTAs each, latency bound) and the
+    // periodic-image operator run on a side stream concurrently with level L (fork/join by
+    // events), each stream with its own tensor-core staging buffer.
     if (use_far) {
         const char* m2l_env = getenv("VFMM_M2L");
         const bool allow_tc = !(m2l_env && strcmp(m2l_env, "simt") == 0) && c->d_tc_hi;
-        for (int l = 1; l <= depth; ++l) {
+        CK(cudaEventRecord(c->ev_fork, st), "fork");
+        CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0), "fork");
+        for (int l = depth; l >= 1; --l) {
+            cudaStream_t sl = l == depth ? st : c->side;
+            float** ghi = l == depth ? &c->g_hi : &c->g2_hi;
+            float** glo = l == depth ? &c->g_lo : &c->g2_lo;
+            size_t* gcap = l == depth ? &c->g_cap : &c->g2_cap;
             const int box[6] = {0, 0, 0, 1 << (l - 1), 1 << (l - 1), 1 << (l - 1)};
             if (allow_tc && m2l_tc_supported(p, l) && m2l_tc_shape_ok(box)) {
                 const size_t need = m2l_tc_grid_floats(l);
-                if (need > c->g_cap) {
-                    dfree(c->g_hi);
-                    dfree(c->g_lo);
-                    c->g_cap = 0;
-                    CK(cudaMalloc((void**)&c->g_hi, need * sizeof(float)), "alloc m2l grid");
-                    CK(cudaMalloc((void**)&c->g_lo, need * sizeof(float)), "alloc m2l grid");
-                    c->g_cap = need;
+                if (need > *gcap) {
+                    CK(cudaStreamSynchronize(sl), "sync before grid realloc");
+                    dfree(*ghi);
+                    dfree(*glo);
+                    *gcap = 0;
+                    CK(cudaMalloc((void**)ghi, need * sizeof(float)), "alloc m2l grid");
+                    CK(cudaMalloc((void**)glo, need * sizeof(float)), "alloc m2l grid");
+                    *gcap = need;
                 }
                 const int rc = launch_m2l_tc(c->d_tc_hi, c->d_tc_lo, c->d_slots, p, Mlev(l),
-                                             Llev(l), l, P.image_levels > 0, c->g_hi, c->g_lo,
-                                             box, st);
+                                             Llev(l), l, P.image_levels > 0, *ghi, *glo, box, sl);
                 if (rc != 0) {
                     c->err = "tensor-map encode failed for tcgen05 M2L";
                     return VFMM_ECUDA;
@@ -540,21 +556,23 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
                 nl += 2;
             } else {
                 launch_m2l(c->d_m2l, c->d_slots, p, H.KP, H.NR, Mlev(l), Llev(l), l,
-                           P.image_levels > 0, 0, (int64_t)1 << (3 * (l - 1)), st);
+                           P.image_levels > 0, 0, (int64_t)1 << (3 * (l - 1)), sl);
                 ++nl;
             }
             S.n_m2l += (int64_t)189 << (3 * l);
         }
+        if (P.image_levels >= 2) {
+            launch_periodic(c->d_per, p, H.KP, H.NR, Mlev(0), Llev(0), c->side);
+            ++nl;
+        } else {
+            CK(cudaMemsetAsync(Llev(0), 0, 3 * nc * sizeof(float), c->side), "memset L0");
+        }
+        CK(cudaEventRecord(c->ev_join, c->side), "join");
+        CK(cudaStreamWaitEvent(st, c->ev_join, 0), "join");
         CK(cudaGetLastError(), "m2l kernels");
     }
     CK(cudaEventRecord(c->ev[6], st), "event");
     if (use_far) {
-        if (P.image_levels >= 2) {
-            launch_periodic(c->d_per, p, H.KP, H.NR, Mlev(0), Llev(0), st);
-            ++nl;
-        } else {
-            CK(cudaMemsetAsync(Llev(0), 0, 3 * nc * sizeof(float), st), "memset L0");
-        }
         for (int l = 1; l <= depth; ++l) {
             launch_l2l(c->d_l2l, p, H.KP, H.NR, Llev(l - 1), Llev(l), l, 0,
                        (int64_t)1 << (3 * (l - 1)), st);
@@ -716,6 +734,11 @@ void vfmm_destroy(vfmm_ctx* c) {
     for (int i = 0; i < vfmm_ctx::NEV; ++i)
         if (c->ev[i]) cudaEventDestroy(c->ev[i]);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
+    if (c->side) cudaStreamDestroy(c->side);
+    if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+    if (c->ev_join) cudaEventDestroy(c->ev_join);
+    dfree(c->g2_hi);
+    dfree(c->g2_lo);
     for (auto* s : c->ranks) delete s;
     c->ranks.clear();
     if (c->comm) nccl_destroy(c->comm);
