@@ -26,7 +26,10 @@ struct vfmm_ctx {
     int ops_p = -1, ops_levels = -1;
     HostOps hops;
     float *d_m2m = nullptr, *d_l2l = nullptr, *d_m2l = nullptr, *d_per = nullptr;
-    float *d_tc_hi = nullptr, *d_tc_lo = nullptr;  // tensor-core M2L operators
+    float *d_tc_hi = nullptr, *d_tc_lo = nullptr;  // tensor-core M2L operators (3xTF32)
+    uint16_t *d_h16_hi = nullptr, *d_h16_lo = nullptr;  // balanced 3xFP16 operators
+    float *d_h16_rs = nullptr, *d_h16_cs = nullptr;     // their row / column scales
+    uint32_t* d_tcmax = nullptr;                        // [32] per-level staging max (f16)
     float *g_hi = nullptr, *g_lo = nullptr;        // tensor-core M2L staged source grid
     size_t g_cap = 0;
     float *g2_hi = nullptr, *g2_lo = nullptr;      // staging for the side stream (levels < L)
@@ -65,6 +68,30 @@ struct vfmm_ctx {
 };
 
 namespace {
+
+// VFMM_M2L selects the M2L engine: "simt" (FP32 CUDA cores), "tf32" (tcgen05 3xTF32), default
+// (or "f16") tcgen05 scaled 3xFP16.  0 = simt, 1 = tf32, 2 = f16
+int m2l_env_mode() {
+    const char* e = getenv("VFMM_M2L");
+    if (e && strcmp(e, "simt") == 0) return 0;
+    if (e && strcmp(e, "tf32") == 0) return 1;
+    return 2;
+}
+
+TcOps tc_ops(const vfmm_ctx* c) {
+    TcOps t;
+    if (m2l_env_mode() == 2 && c->d_h16_hi) {
+        t.hi = c->d_h16_hi;
+        t.lo = c->d_h16_lo;
+        t.rs = c->d_h16_rs;
+        t.cs = c->d_h16_cs;
+        t.f16 = true;
+    } else {
+        t.hi = c->d_tc_hi;
+        t.lo = c->d_tc_lo;
+    }
+    return t;
+}
 
 vfmm_status cuda_fail(vfmm_ctx* c, cudaError_t e, const char* where) {
     if (c) c->err = std::string(where) + ": " + cudaGetErrorString(e);
@@ -125,10 +152,24 @@ vfmm_status ensure_ops(vfmm_ctx* c) {
     CK(up(c->hops.per, &c->d_per), "upload periodic");
     dfree(c->d_tc_hi);
     dfree(c->d_tc_lo);
+    dfree(c->d_h16_hi);
+    dfree(c->d_h16_lo);
+    dfree(c->d_h16_rs);
+    dfree(c->d_h16_cs);
     if (!c->hops.m2l_tc_hi.empty()) {
         CK(up(c->hops.m2l_tc_hi, &c->d_tc_hi), "upload m2l tc hi");
         CK(up(c->hops.m2l_tc_lo, &c->d_tc_lo), "upload m2l tc lo");
+        auto up16 = [&](const std::vector<uint16_t>& h, uint16_t** d) -> cudaError_t {
+            cudaError_t e = cudaMalloc((void**)d, h.size() * sizeof(uint16_t));
+            if (e != cudaSuccess) return e;
+            return cudaMemcpy(*d, h.data(), h.size() * sizeof(uint16_t), cudaMemcpyHostToDevice);
+        };
+        CK(up16(c->hops.m2l_h16_hi, &c->d_h16_hi), "upload m2l f16 hi");
+        CK(up16(c->hops.m2l_h16_lo, &c->d_h16_lo), "upload m2l f16 lo");
+        CK(up(c->hops.h16_rs, &c->d_h16_rs), "upload m2l f16 scales");
+        CK(up(c->hops.h16_cs, &c->d_h16_cs), "upload m2l f16 scales");
     }
+    if (!c->d_tcmax) CK(cudaMalloc((void**)&c->d_tcmax, 32 * sizeof(uint32_t)), "alloc tc max");
     if (!c->d_slots) {
         // interaction list per parity: o_a in {-2-b_a .. 3-b_a}, minus |o|inf <= 1 (189 cells)
         std::vector<int> slots;
@@ -200,13 +241,11 @@ DistShared make_shared(vfmm_ctx* c, int R) {
     D.l2l = c->d_l2l;
     D.m2l = c->d_m2l;
     D.per = c->d_per;
-    D.tc_hi = c->d_tc_hi;
-    D.tc_lo = c->d_tc_lo;
+    D.tc = tc_ops(c);
     D.slots = c->d_slots;
     D.KP = c->hops.KP;
     D.NR = c->hops.NR;
-    const char* env = getenv("VFMM_M2L");
-    D.allow_tc = !(env && strcmp(env, "simt") == 0);
+    D.allow_tc = m2l_env_mode() != 0;
     return D;
 }
 
@@ -526,8 +565,9 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
     // periodic-image operator run on a side stream concurrently with level L (fork/join by
     // events), each stream with its own tensor-core staging buffer.
     if (use_far) {
-        const char* m2l_env = getenv("VFMM_M2L");
-        const bool allow_tc = !(m2l_env && strcmp(m2l_env, "simt") == 0) && c->d_tc_hi;
+        const TcOps tco = tc_ops(c);
+        const bool allow_tc = m2l_env_mode() != 0 && tco.hi;
+        CK(cudaMemsetAsync(c->d_tcmax, 0, 32 * sizeof(uint32_t), st), "memset tc max");
         CK(cudaEventRecord(c->ev_fork, st), "fork");
         CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0), "fork");
         for (int l = depth; l >= 1; --l) {
@@ -547,13 +587,14 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
                     CK(cudaMalloc((void**)glo, need * sizeof(float)), "alloc m2l grid");
                     *gcap = need;
                 }
-                const int rc = launch_m2l_tc(c->d_tc_hi, c->d_tc_lo, c->d_slots, p, Mlev(l),
-                                             Llev(l), l, P.image_levels > 0, *ghi, *glo, box, sl);
+                const int rc = launch_m2l_tc(tco, c->d_slots, p, Mlev(l), Llev(l), l,
+                                             P.image_levels > 0, *ghi, *glo, c->d_tcmax + l, box,
+                                             sl);
                 if (rc != 0) {
                     c->err = "tensor-map encode failed for tcgen05 M2L";
                     return VFMM_ECUDA;
                 }
-                nl += 2;
+                nl += tco.f16 ? 3 : 2;
             } else {
                 launch_m2l(c->d_m2l, c->d_slots, p, H.KP, H.NR, Mlev(l), Llev(l), l,
                            P.image_levels > 0, 0, (int64_t)1 << (3 * (l - 1)), sl);
@@ -716,6 +757,11 @@ void vfmm_destroy(vfmm_ctx* c) {
     dfree(c->d_slots);
     dfree(c->d_tc_hi);
     dfree(c->d_tc_lo);
+    dfree(c->d_h16_hi);
+    dfree(c->d_h16_lo);
+    dfree(c->d_h16_rs);
+    dfree(c->d_h16_cs);
+    dfree(c->d_tcmax);
     dfree(c->g_hi);
     dfree(c->g_lo);
     for (int b = 0; b < 2; ++b) {

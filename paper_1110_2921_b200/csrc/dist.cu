@@ -286,6 +286,7 @@ void RankState::release() {
     dfree(d_pairs);
     dfree(g_hi);
     dfree(g_lo);
+    dfree(tcmax);
     cap_local = cap_total = 0;
     cap_send = cap_recv = 0;
     cap_segs = cap_cells = 0;
@@ -571,7 +572,7 @@ vfmm_status dist_phase4(RankState& S, const DistShared& D, cudaStream_t st, std:
             box[4] = k >= 4 ? nP : half;
             box[5] = k >= 8 ? nP : half;
         }
-        if (D.allow_tc && D.tc_hi && m2l_tc_supported(p, l) && m2l_tc_shape_ok(box)) {
+        if (D.allow_tc && D.tc.hi && m2l_tc_supported(p, l) && m2l_tc_shape_ok(box)) {
             const size_t need = m2l_tc_grid_floats(l);
             if (need > S.g_cap) {
                 dfree(S.g_hi);
@@ -581,8 +582,12 @@ vfmm_status dist_phase4(RankState& S, const DistShared& D, cudaStream_t st, std:
                 DCK(cudaMalloc((void**)&S.g_lo, need * 4), "alloc m2l grid");
                 S.g_cap = need;
             }
-            if (launch_m2l_tc(D.tc_hi, D.tc_lo, D.slots, p, Mlev(l), Llev(l), l, periodic, S.g_hi,
-                              S.g_lo, box, st) != 0) {
+            if (!S.tcmax) {
+                DCK(cudaMalloc((void**)&S.tcmax, 32 * sizeof(uint32_t)), "alloc tc max");
+            }
+            DCK(cudaMemsetAsync(S.tcmax + l, 0, sizeof(uint32_t), st), "memset tc max");
+            if (launch_m2l_tc(D.tc, D.slots, p, Mlev(l), Llev(l), l, periodic, S.g_hi, S.g_lo,
+                              S.tcmax + l, box, st) != 0) {
                 if (err) *err = "tensor-map encode failed";
                 return VFMM_ECUDA;
             }

@@ -65,6 +65,7 @@ struct RankState {
     unsigned long long* d_pairs = nullptr;
     float *g_hi = nullptr, *g_lo = nullptr;  // tcgen05 M2L staging
     size_t g_cap = 0;
+    uint32_t* tcmax = nullptr;  // [32] per-level f16 staging max
     int64_t bytes_sent = 0, bytes_recv = 0;
     ~RankState();
     void release();
@@ -75,7 +76,7 @@ struct DistShared {
     vfmm_params prm;
     int depth = 0, R = 1;
     const float *m2m = nullptr, *l2l = nullptr, *m2l = nullptr, *per = nullptr;
-    const float *tc_hi = nullptr, *tc_lo = nullptr;
+    TcOps tc;  // tensor-core M2L operators (3xTF32 or 3xFP16)
     const int* slots = nullptr;
     int KP = 0, NR = 0;
     bool allow_tc = true;

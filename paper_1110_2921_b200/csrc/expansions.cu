@@ -25,22 +25,6 @@ namespace vfmm {
 
 namespace {
 
-// packed FP32x2 helpers (Blackwell FFMA2)
-typedef unsigned long long f2x;
-__device__ __forceinline__ f2x pk2(float a, float b) {
-    f2x r;
-    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
-    return r;
-}
-__device__ __forceinline__ void upk2(f2x v, float& a, float& b) {
-    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-}
-__device__ __forceinline__ f2x ffma2(f2x a, f2x b, f2x c) {
-    f2x r;
-    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
-    return r;
-}
-
 __device__ __forceinline__ uint32_t spread3d(uint32_t v) {
     v &= 0x3ffu;
     v = (v | (v << 16)) & 0x030000FFu;
@@ -210,8 +194,7 @@ __global__ void __launch_bounds__(256) translate_kernel(
         ncell_tile = (int)min((int64_t)TCELLS, plo + pcnt - tile0);
     } else {
         const int64_t ntiles = (pcnt + TCELLS - 1) / TCELLS;
-        // L2L: one block per parent tile handles all 8 child parities (loop below)
-        parity = KIND == OP_L2L ? 0 : (int)(blockIdx.x / ntiles);
+        parity = (int)(blockIdx.x / ntiles);
         tile0 = (int)(plo + (int64_t)(blockIdx.x % ntiles) * TCELLS);
         ncell_tile = (int)min((int64_t)TCELLS, plo + pcnt - tile0);
         nops = KIND == OP_L2L ? 1 : MAXOPS;
@@ -223,9 +206,6 @@ __global__ void __launch_bounds__(256) translate_kernel(
     auto target_cell = [&](int j) -> int64_t {
         return KIND == OP_M2M ? (int64_t)(tile0 + j) : ((int64_t)(tile0 + j) << 3) + parity;
     };
-    const int npar = KIND == OP_L2L ? 8 : 1;
-    for (int pp = 0; pp < npar; ++pp) {
-    if (KIND == OP_L2L) parity = pp;
     // ---- source tables ----
     for (int i = tid; i < nops * TCELLS; i += 256) {
         const int op = i / TCELLS, j = i - op * TCELLS;
@@ -351,8 +331,6 @@ __global__ void __launch_bounds__(256) translate_kernel(
             else out[r] = v;
         }
     }
-    __syncthreads();  // Cs aliases the operand / table buffers of the next parity
-    }  // parity loop (L2L)
 }
 
 // periodic far field: L0 = P M0 (3 columns); one block
@@ -470,9 +448,9 @@ __global__ void __launch_bounds__(64) l2p_combine_kernel(
         }
         if (use_far && act) {
             const float x = s6[j] * inv_a, y = s6[n + j] * inv_a, z = s6[2 * n + j] * inv_a;
-            f2x acc2[14];  // 28 accumulators as packed pairs (q, q+1)
+            float acc[28];
 #pragma unroll
-            for (int q = 0; q < 14; ++q) acc2[q] = pk2(0.f, 0.f);
+            for (int q = 0; q < 28; ++q) acc[q] = 0.f;
             // R_n^m(z/a) by recurrence (m outer, n inner, n <= p-1), accumulated on the fly:
             // value_q = sum_k D[k][q] w_k, w = R_re (m = 0); 2 R_re, -2 R_im (m > 0)
             const float r2 = x * x + y * y + z * z;
@@ -507,30 +485,28 @@ __global__ void __launch_bounds__(64) l2p_combine_kernel(
                     p1im = cim;
                     const float4* Dr = D4 + pk_re(nn, m) * 7;
                     if (m == 0) {
-                        const f2x w2 = pk2(cre, cre);
 #pragma unroll
                         for (int q4 = 0; q4 < 7; ++q4) {
                             const float4 d = Dr[q4];
-                            acc2[2 * q4 + 0] = ffma2(pk2(d.x, d.y), w2, acc2[2 * q4 + 0]);
-                            acc2[2 * q4 + 1] = ffma2(pk2(d.z, d.w), w2, acc2[2 * q4 + 1]);
+                            acc[4 * q4 + 0] = fmaf(d.x, cre, acc[4 * q4 + 0]);
+                            acc[4 * q4 + 1] = fmaf(d.y, cre, acc[4 * q4 + 1]);
+                            acc[4 * q4 + 2] = fmaf(d.z, cre, acc[4 * q4 + 2]);
+                            acc[4 * q4 + 3] = fmaf(d.w, cre, acc[4 * q4 + 3]);
                         }
                     } else {
                         const float4* Di = D4 + pk_im(nn, m) * 7;
-                        const f2x wr = pk2(2.f * cre, 2.f * cre), wi = pk2(-2.f * cim, -2.f * cim);
+                        const float wr = 2.f * cre, wi = -2.f * cim;
 #pragma unroll
                         for (int q4 = 0; q4 < 7; ++q4) {
                             const float4 d = Dr[q4], f = Di[q4];
-                            acc2[2 * q4 + 0] =
-                                ffma2(pk2(d.x, d.y), wr, ffma2(pk2(f.x, f.y), wi, acc2[2 * q4 + 0]));
-                            acc2[2 * q4 + 1] =
-                                ffma2(pk2(d.z, d.w), wr, ffma2(pk2(f.z, f.w), wi, acc2[2 * q4 + 1]));
+                            acc[4 * q4 + 0] = fmaf(d.x, wr, fmaf(f.x, wi, acc[4 * q4 + 0]));
+                            acc[4 * q4 + 1] = fmaf(d.y, wr, fmaf(f.y, wi, acc[4 * q4 + 1]));
+                            acc[4 * q4 + 2] = fmaf(d.z, wr, fmaf(f.z, wi, acc[4 * q4 + 2]));
+                            acc[4 * q4 + 3] = fmaf(d.w, wr, fmaf(f.w, wi, acc[4 * q4 + 3]));
                         }
                     }
                 }
             }
-            float acc[28];
-#pragma unroll
-            for (int q = 0; q < 14; ++q) upk2(acc2[q], acc[2 * q], acc[2 * q + 1]);
             // acc[c*3 + axis] = d_axis phi_c ; acc[9 + c*6 + q] = Hessian pair q of phi_c
             const float sg = inv4pi * inv_a * inv_a;  // gradient scale
             const float sh = sg * inv_a;              // Hessian scale
@@ -613,7 +589,7 @@ void launch_m2m(const float* ops_m2m, int p, int KP, int NR, const float* M_chil
 void launch_l2l(const float* ops_l2l, int p, int KP, int NR, const float* L_par, float* L_child,
                 int level_child, int64_t plo, int64_t pcnt, cudaStream_t st) {
     if (pcnt <= 0) return;
-    dim3 grid((unsigned)((pcnt + TCELLS - 1) / TCELLS), NR / TROWS);  // parities looped inside
+    dim3 grid((unsigned)(8 * ((pcnt + TCELLS - 1) / TCELLS)), NR / TROWS);
     translate_attrs();
     translate_kernel<OP_L2L><<<grid, 256, TRANSLATE_SMEM, st>>>(ops_l2l, nullptr, p, KP, NR, L_par,
                                                                 L_child, level_child, 0, plo, pcnt, 1);

@@ -1,7 +1,15 @@
 // m2l_tc.cu -- M2L (Eq. 11; operators of Cheng et al.) on the
-// 5th-generation tensor cores: tcgen05.mma kind::tf32 with a 3xTF32 split
-// (A_hi B_hi + A_hi B_lo + A_lo B_hi) so the result keeps FP32 accuracy, operands staged by
-// TMA (SWIZZLE_128B, K-major), accumulators in TMEM.
+// 5th-generation tensor cores with a 3-term split (A_hi B_hi + A_hi B_lo + A_lo B_hi) so the
+// result keeps ~FP32 accuracy, operands staged by TMA (SWIZZLE_128B, K-major), accumulators in
+// TMEM.  Two operand formats (same 10+1-bit significand, so the same split accuracy):
+//   * 3xTF32 (tcgen05.mma kind::tf32): hi = v with the low 13 mantissa bits cleared.
+//   * 3xFP16 (kind::f16, twice the tensor rate and half the operand bytes): the operator is
+//     balanced by power-of-2 row/column scales, Ahat = T / (rs[r] cs[k]) (|Ahat| <= 1), and the
+//     multipoles are staged as Mhat_k = M_k cs[k] s with one power-of-2 s per level chosen from
+//     the level's max |cs[k] M_k| (max |Mhat| < 2^14, far from the half overflow); the epilogue
+//     multiplies row r by rs[r] / s.  Every scale is exact, so apart from the half range
+//     (entries below 2^-14 of the scaled max lose significand bits) the split is bit-for-bit
+//     the TF32 one.
 //
 // The M2L of level l is a batch of dense GEMMs, one per (target parity pi, offset o):
 //   D[r][(px,c)] += sum_k T_o[r][k] * Msrc[(px + dx, c)][k]
@@ -27,6 +35,7 @@
 // both CTAs, halving operator traffic; operator stages are released by both MMA warps.
 #include <cuda.h>
 #include <cudaTypedefs.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include "vfmm_internal.h"
@@ -35,13 +44,14 @@ namespace vfmm {
 
 namespace {
 
-constexpr int TC_T = 2;        // target rows per CTA (one accumulator tile each)
 constexpr int TC_G = 1;        // offsets per TMEM accumulation group (flushed to FP32 registers)
-constexpr int TC_NKC = 4;      // K chunks of 32 floats (128 B)
+// K chunks of 128 B: 4 x 32 tf32 or 2 x 64 halves (K = 128)
+template <bool F16> __host__ __device__ constexpr int tc_nkc() { return F16 ? 2 : 4; }
+template <bool F16> __host__ __device__ constexpr int tc_ke() { return F16 ? 64 : 32; }
 constexpr int TC_AST = 2;      // A (operator) pipeline stages
 constexpr int TC_BST = 3;      // B pipeline stages (each holds the slabs of all T rows)
 constexpr int A_BYTES = 128 * 128;  // one K chunk of one operator half (hi or lo): 16 KB
-constexpr int B_BYTES = 2 * 96 * 128;  // one K chunk of the T = 2 stacked slabs, one half: <= 24 KB
+constexpr int B_BYTES = 192 * 128;  // one K chunk of the T stacked slabs (T N <= 192 rows), one half
 constexpr int TC_EPI_WARPS = 8;  // 2 per TMEM lane quarter: warp pair splits the T tiles
 constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;
 constexpr size_t TC_SMEM = 1024 + (size_t)TC_AST * 2 * A_BYTES + (size_t)TC_BST * 2 * B_BYTES + 512;
@@ -128,6 +138,14 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b
         "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
         "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
 }
+__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                        uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
 __device__ __forceinline__ void mma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::
                      "r"(smem_u32(bar))
@@ -155,20 +173,32 @@ struct TcParams {
     int ntx;    // x tiles per row (nP / XT)
     int N;      // MMA N = 3 XT rounded up to a multiple of 16 (extra rows are discarded)
     int NV;     // valid columns = 3 * XT
+    int T;      // target rows per CTA (accumulator tiles), T N <= 192
     int rows;   // target rows per parity = nP * nP * ntx
     int nc;     // (p+1)^2 <= 128
     int level;
     int bx0, by0, bz0, bny;  // owned box of target parents (origin; y extent)
     const int* slots;  // [8][189] M2L slot per target parity
     float* L;          // local expansions of this level, Morton [cell][3][nc]
+    const float* rs;   // f16: row scales [128]
+    const uint32_t* maxbits;  // f16: the level's max |cs[k] M_k| (float bits)
 };
+
+// f16 staging scale s = 2^(14 - e) for the level max m = f 2^e (f in [0.5, 1)): max |Mhat| < 2^14
+__device__ __forceinline__ int h16_scale_exp(uint32_t bits) {
+    const float m = __uint_as_float(bits);
+    if (!(m > 0.f) || !isfinite(m)) return 0;
+    int e;
+    frexpf(m, &e);
+    return min(14 - e, 120);
+}
 
 // row group g of a CTA -> (x tile, first target row y, row z) inside the owned box;
 // groups are visited in 8x8 tiles of (y group, z) so co-resident CTAs share source rows
 __device__ __forceinline__ void group_rows(const TcParams& P, int g, int* tx, int* py0, int* pz) {
     *tx = g % P.ntx;
     const int gg = g / P.ntx;
-    const int GY = P.bny / TC_T, GZ = P.rows / (P.ntx * P.bny);  // groups along y, rows in z
+    const int GY = P.bny / P.T, GZ = P.rows / (P.ntx * P.bny);  // groups along y, rows in z
     int gy, gz;
     if (GY % 8 == 0 && GZ % 8 == 0) {
         const int tile = gg / 64, w = gg % 64;
@@ -178,10 +208,11 @@ __device__ __forceinline__ void group_rows(const TcParams& P, int g, int* tx, in
         gy = gg % GY;
         gz = gg / GY;
     }
-    *py0 = P.by0 + gy * TC_T;
+    *py0 = P.by0 + gy * P.T;
     *pz = P.bz0 + gz;
 }
 
+template <bool F16>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     m2l_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant__ CUtensorMap tmA_lo,
                   const __grid_constant__ CUtensorMap tmB_hi, const __grid_constant__ CUtensorMap tmB_lo,
@@ -251,14 +282,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
                 const int sx = pix + ox, sy = piy + oy, sz = piz + oz;
                 const int dx = sx >> 1, dy = sy >> 1, dz = sz >> 1;  // floor division
                 const int pis = (sx & 1) | ((sy & 1) << 1) | ((sz & 1) << 2);
-                for (int kc = 0; kc < TC_NKC; ++kc) {
+                for (int kc = 0; kc < tc_nkc<F16>(); ++kc) {
                     mbar_wait(&a_empty[sa], pa ^ 1);
                     mbar_expect_tx(&a_full[sa], 2u * A_BYTES);  // hi from rank 0, lo from rank 1
                     if (crank == 0)
-                        tma_load_3d_mc(Abuf + (sa * 2 + 0) * A_BYTES, &tmA_hi, &a_full[sa], kc * 32, 0,
+                        tma_load_3d_mc(Abuf + (sa * 2 + 0) * A_BYTES, &tmA_hi, &a_full[sa], kc * tc_ke<F16>(), 0,
                                        slot, (uint16_t)3);
                     else
-                        tma_load_3d_mc(Abuf + (sa * 2 + 1) * A_BYTES, &tmA_lo, &a_full[sa], kc * 32, 0,
+                        tma_load_3d_mc(Abuf + (sa * 2 + 1) * A_BYTES, &tmA_lo, &a_full[sa], kc * tc_ke<F16>(), 0,
                                        slot, (uint16_t)3);
                     if (++sa == TC_AST) {
                         sa = 0;
@@ -266,14 +297,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
                     }
                     // both rows' slabs stacked in one stage: rows [t N, (t+1) N) of the B operand
                     mbar_wait(&b_empty[sb], pb ^ 1);
-                    mbar_expect_tx(&b_full[sb], (uint32_t)TC_T * b_tx);
-                    for (int t = 0; t < TC_T; ++t) {
+                    mbar_expect_tx(&b_full[sb], (uint32_t)P.T * b_tx);
+                    for (int t = 0; t < P.T; ++t) {
                         const int c1 = 3 * (2 + P.bx0 + gtx * P.XT + dx);
                         const int c2 = 2 + gpy0 + t + dy, c3 = 2 + gpz + dz;
                         uint8_t* bh = Bbuf + (sb * 2 + 0) * B_BYTES + t * P.N * 128;
                         uint8_t* bl = Bbuf + (sb * 2 + 1) * B_BYTES + t * P.N * 128;
-                        tma_load_5d(bh, &tmB_hi, &b_full[sb], kc * 32, c1, c2, c3, pis);
-                        tma_load_5d(bl, &tmB_lo, &b_full[sb], kc * 32, c1, c2, c3, pis);
+                        tma_load_5d(bh, &tmB_hi, &b_full[sb], kc * tc_ke<F16>(), c1, c2, c3, pis);
+                        tma_load_5d(bl, &tmB_lo, &b_full[sb], kc * tc_ke<F16>(), c1, c2, c3, pis);
                     }
                     if (++sb == TC_BST) {
                         sb = 0;
@@ -284,10 +315,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         }
     } else if (warp == 1) {
         // ===================== MMA issuer =====================
-        // instruction descriptor: D f32, A/B tf32, both K-major, N, M = 128
-        // one MMA covers both rows: N' = T N columns (tile t at columns [t N, (t+1) N))
-        const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) |
-                               ((uint32_t)((TC_T * P.N) >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+        // instruction descriptor: D f32, A/B tf32 (2) or f16 (0), both K-major, N, M = 128
+        // one MMA covers all T rows: N' = T N columns (tile t at columns [t N, (t+1) N))
+        const uint32_t ab_fmt = F16 ? 0u : 2u;
+        const uint32_t idesc = (1u << 4) | (ab_fmt << 7) | (ab_fmt << 10) |
+                               ((uint32_t)((P.T * P.N) >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
         int sa = 0, sb = 0;
         uint32_t pa = 0, pb = 0;
         for (int grp = 0; grp < ngroups; ++grp) {
@@ -296,7 +328,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
             tc_fence_after();
             const int o_end = min(189, (grp + 1) * TC_G);
             for (int oi = grp * TC_G; oi < o_end; ++oi) {
-                for (int kc = 0; kc < TC_NKC; ++kc) {
+                for (int kc = 0; kc < tc_nkc<F16>(); ++kc) {
                     mbar_wait(&a_full[sa], pa);
                     tc_fence_after();
                     const uint64_t ahi = sw128_desc(Abuf + (sa * 2 + 0) * A_BYTES);
@@ -308,12 +340,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
                     const uint32_t d = tmem + (uint32_t)(buf * 256);
                     if (lane == 0) {
 #pragma unroll
-                        for (int ks = 0; ks < 4; ++ks) {  // K = 8 tf32 = 32 B per MMA
+                        for (int ks = 0; ks < 4; ++ks) {  // K = 8 tf32 / 16 f16 = 32 B per MMA
                             const uint64_t adv = (uint64_t)(ks * 2);
                             const uint32_t acc = (oi != grp * TC_G || kc != 0 || ks != 0) ? 1u : 0u;
-                            mma_tf32(d, ahi + adv, bhi + adv, idesc, acc);
-                            mma_tf32(d, ahi + adv, blo + adv, idesc, 1u);
-                            mma_tf32(d, alo + adv, bhi + adv, idesc, 1u);
+                            if (F16) {
+                                mma_f16(d, ahi + adv, bhi + adv, idesc, acc);
+                                mma_f16(d, ahi + adv, blo + adv, idesc, 1u);
+                                mma_f16(d, alo + adv, bhi + adv, idesc, 1u);
+                            } else {
+                                mma_tf32(d, ahi + adv, bhi + adv, idesc, acc);
+                                mma_tf32(d, ahi + adv, blo + adv, idesc, 1u);
+                                mma_tf32(d, alo + adv, bhi + adv, idesc, 1u);
+                            }
                         }
                         mma_commit(&b_empty[sb]);
                     }
@@ -337,7 +375,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         // ===================== epilogue: TMEM groups -> FP32 register sums -> L =====================
         const int e = warp - 2;
         const int quarter = warp & 3;  // TMEM lanes [32 quarter, 32 quarter + 32)
-        const int t = e >> 2;          // accumulator tile of this warp
+        const int half = e >> 2;       // this warp owns tiles [half T/2, (half+1) T/2)
+        const int ncol = (P.T / 2) * P.N;  // <= 96 columns per warp
+        const int col0 = half * ncol;
         const int r = quarter * 32 + lane;
         float acc[96];
 #pragma unroll
@@ -348,10 +388,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
             tc_fence_after();
 #pragma unroll
             for (int c = 0; c < 6; ++c) {
-                if (c * 16 < P.N) {
+                if (c * 16 < ncol) {
                     uint32_t v[16];
                     const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) +
-                                           (uint32_t)(buf * 256 + t * P.N + c * 16);
+                                           (uint32_t)(buf * 256 + col0 + c * 16);
                     asm volatile(
                         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, "
                         "%8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
@@ -369,14 +409,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
             if (lane == 0) mbar_arrive(&acc_empty[buf]);
         }
         if (r < P.nc) {
-            const int py = gpy0 + t;
-            const uint32_t cy = spread3t(2 * py + piy) << 1, cz = spread3t(2 * gpz + piz) << 2;
+            if (F16) {  // undo the balancing: row r times rs[r] / s
+                const float f = P.rs[r] * ldexpf(1.f, -h16_scale_exp(*P.maxbits));
+#pragma unroll
+                for (int j = 0; j < 96; ++j) acc[j] *= f;
+            }
+            const uint32_t cz = spread3t(2 * gpz + piz) << 2;
 #pragma unroll
             for (int j = 0; j < 96; ++j) {
-                if (j < P.NV) {
-                    const int px = P.bx0 + gtx * P.XT + j / 3, comp = j % 3;
-                    const uint32_t cell = spread3t(2 * px + pix) | cy | cz;
-                    P.L[((int64_t)cell * 3 + comp) * P.nc + r] = acc[j];
+                if (j < ncol) {
+                    const int t = half * (P.T / 2) + j / P.N, cj = j % P.N;
+                    if (cj < P.NV) {
+                        const int py = gpy0 + t;
+                        const int px = P.bx0 + gtx * P.XT + cj / 3, comp = cj % 3;
+                        const uint32_t cell =
+                            spread3t(2 * px + pix) | (spread3t(2 * py + piy) << 1) | cz;
+                        P.L[((int64_t)cell * 3 + comp) * P.nc + r] = acc[j];
+                    }
                 }
             }
         }
@@ -425,6 +474,62 @@ __global__ void m2l_stage_kernel(const float* __restrict__ M, int nP, int period
     }
 }
 
+// f16 staging, two passes over the same padded grid (blockDim = (128 k, 4 rows)):
+// MAXPASS: max |cs[k] M_k| of the staged values -> atomicMax on the float bits (non-negative);
+// else:    grid[pi'][Z][Y][X][comp][128] = half split of M_k cs[k] s, s = 2^h16_scale_exp(max)
+template <bool MAXPASS>
+__global__ void __launch_bounds__(512) m2l_stage16_kernel(const float* __restrict__ M, int nP,
+                                                          int periodic, int nc,
+                                                          const float* __restrict__ cs,
+                                                          uint32_t* __restrict__ maxbits,
+                                                          __half* __restrict__ ghi,
+                                                          __half* __restrict__ glo) {
+    const int Xp = nP + 4;
+    const int nrows = 8 * Xp * Xp * Xp * 3;
+    const int k = threadIdx.x;
+    const float ck = k < nc ? cs[k] : 0.f;
+    const float s = MAXPASS ? 1.f : ldexpf(1.f, h16_scale_exp(*maxbits));
+    float mx = 0.f;
+    for (int row = blockIdx.x * blockDim.y + threadIdx.y; row < nrows;
+         row += gridDim.x * blockDim.y) {
+        int q = row;
+        const int comp = q % 3;
+        q /= 3;
+        const int X = q % Xp;
+        q /= Xp;
+        const int Y = q % Xp;
+        q /= Xp;
+        const int Z = q % Xp;
+        const int ps = q / Xp;
+        int px = X - 2, py = Y - 2, pz = Z - 2;
+        float v = 0.f;
+        const bool inside = px >= 0 && px < nP && py >= 0 && py < nP && pz >= 0 && pz < nP;
+        if (k < nc && (periodic || inside)) {
+            px = (px + nP) & (nP - 1);
+            py = (py + nP) & (nP - 1);
+            pz = (pz + nP) & (nP - 1);
+            const uint32_t cell = spread3t(2 * px + (ps & 1)) |
+                                  (spread3t(2 * py + ((ps >> 1) & 1)) << 1) |
+                                  (spread3t(2 * pz + ((ps >> 2) & 1)) << 2);
+            v = M[((int64_t)cell * 3 + comp) * nc + k];
+        }
+        if (MAXPASS) {
+            mx = fmaxf(mx, fabsf(v * ck));
+        } else {
+            const float x = v * ck * s;
+            const __half h = __float2half_rn(x);
+            const __half l = __float2half_rn(x - __half2float(h));
+            ghi[(int64_t)row * 128 + k] = h;
+            glo[(int64_t)row * 128 + k] = l;
+        }
+    }
+    if (MAXPASS) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if ((threadIdx.x & 31) == 0 && mx > 0.f) atomicMax(maxbits, __float_as_uint(mx));
+    }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     if (!fn) {
@@ -440,14 +545,20 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 }  // namespace
 
-bool m2l_tc_shape_ok(const int box[6]) {
-    // 2 target rows per CTA and CTA pairs (clusters): rows / 2 must be even
+// rows per CTA for a box: the largest T in {8, 4, 2} with T N <= 192, T | bny and an even
+// number of CTAs (2-CTA clusters); 0 if none
+static int pick_T(const int box[6]) {
     const int bnx = box[3], bny = box[4], bnz = box[5];
     const int XT = bnx < 32 ? bnx : 32;
-    if (bny % TC_T != 0 || bnx % XT != 0) return false;
+    if (bnx % XT != 0) return 0;
+    const int N = (3 * XT + 15) / 16 * 16;
     const int rows = bny * bnz * (bnx / XT);
-    return (rows / TC_T) % 2 == 0;
+    for (int T = 8; T >= 2; T /= 2)
+        if (T * N <= 192 && bny % T == 0 && (rows / T) % 2 == 0) return T;
+    return 0;
 }
+
+bool m2l_tc_shape_ok(const int box[6]) { return pick_T(box) != 0; }
 
 bool m2l_tc_supported(int p, int level) {
     return (p + 1) * (p + 1) <= 128 && level >= 2 && get_encode() != nullptr;
@@ -458,18 +569,34 @@ size_t m2l_tc_grid_floats(int level) {
     return (size_t)(8 * Xp * Xp * Xp * 3 * 128);
 }
 
-int launch_m2l_tc(const float* ops_hi, const float* ops_lo, const int* il_slots, int p,
-                  const float* M_l, float* L_l, int level, int periodic, float* ghi, float* glo,
+int launch_m2l_tc(const TcOps& ops, const int* il_slots, int p, const float* M_l, float* L_l,
+                  int level, int periodic, float* ghi, float* glo, uint32_t* maxbits,
                   const int box[6], cudaStream_t st) {
     const int nc = (p + 1) * (p + 1);
     const int nP = 1 << (level - 1);
     const int Xp = nP + 4;
+    const bool f16 = ops.f16;
+    const size_t esz = f16 ? 2 : 4;
+    const CUtensorMapDataType dt = f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    const cuuint32_t ke = f16 ? 64 : 32;  // K elements per 128-byte chunk
     // 1) stage the level's multipoles into the halo-padded parity-major grid
     {
         const int64_t total = (int64_t)8 * Xp * Xp * Xp * 3 * 128;
-        int64_t blocks = (total + 255) / 256;
-        if (blocks > 148 * 64) blocks = 148 * 64;
-        m2l_stage_kernel<<<(unsigned)blocks, 256, 0, st>>>(M_l, nP, periodic, nc, ghi, glo);
+        if (f16) {
+            const int64_t rows = total / 128;
+            int64_t blocks = (rows + 3) / 4;
+            if (blocks > 148 * 8) blocks = 148 * 8;
+            const dim3 blk(128, 4);
+            m2l_stage16_kernel<true><<<(unsigned)blocks, blk, 0, st>>>(
+                M_l, nP, periodic, nc, ops.cs, maxbits, nullptr, nullptr);
+            m2l_stage16_kernel<false><<<(unsigned)blocks, blk, 0, st>>>(
+                M_l, nP, periodic, nc, ops.cs, maxbits, reinterpret_cast<__half*>(ghi),
+                reinterpret_cast<__half*>(glo));
+        } else {
+            int64_t blocks = (total + 255) / 256;
+            if (blocks > 148 * 64) blocks = 148 * 64;
+            m2l_stage_kernel<<<(unsigned)blocks, 256, 0, st>>>(M_l, nP, periodic, nc, ghi, glo);
+        }
     }
     // 2) tensor maps
     auto enc = get_encode();
@@ -477,14 +604,14 @@ int launch_m2l_tc(const float* ops_hi, const float* ops_lo, const int* il_slots,
     CUtensorMap mAh, mAl, mBh, mBl;
     {
         cuuint64_t dims[3] = {128, 128, 343};
-        cuuint64_t strides[2] = {128 * 4, 128 * 128 * 4};
-        cuuint32_t box[3] = {32, 128, 1};
+        cuuint64_t strides[2] = {128 * esz, 128 * 128 * esz};
+        cuuint32_t bx[3] = {ke, 128, 1};
         cuuint32_t es[3] = {1, 1, 1};
-        if (enc(&mAh, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)ops_hi, dims, strides, box, es,
+        if (enc(&mAh, dt, 3, const_cast<void*>(ops.hi), dims, strides, bx, es,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return -2;
-        if (enc(&mAl, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void*)ops_lo, dims, strides, box, es,
+        if (enc(&mAl, dt, 3, const_cast<void*>(ops.lo), dims, strides, bx, es,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                 CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return -2;
@@ -496,23 +623,26 @@ int launch_m2l_tc(const float* ops_hi, const float* ops_lo, const int* il_slots,
     const int N = (NV + 15) / 16 * 16;  // MMA N (multiple of 16 for M = 128)
     {
         cuuint64_t dims[5] = {128, (cuuint64_t)3 * Xp, (cuuint64_t)Xp, (cuuint64_t)Xp, 8};
-        cuuint64_t strides[4] = {128 * 4, (cuuint64_t)3 * Xp * 128 * 4,
-                                 (cuuint64_t)Xp * 3 * Xp * 128 * 4,
-                                 (cuuint64_t)Xp * Xp * 3 * Xp * 128 * 4};
-        cuuint32_t box[5] = {32, (cuuint32_t)N, 1, 1, 1};
+        cuuint64_t strides[4] = {128 * esz, (cuuint64_t)3 * Xp * 128 * esz,
+                                 (cuuint64_t)Xp * 3 * Xp * 128 * esz,
+                                 (cuuint64_t)Xp * Xp * 3 * Xp * 128 * esz};
+        cuuint32_t bx[5] = {ke, (cuuint32_t)N, 1, 1, 1};
         cuuint32_t es[5] = {1, 1, 1, 1, 1};
-        if (enc(&mBh, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, (void*)ghi, dims, strides, box, es,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        if (enc(&mBh, dt, 5, (void*)ghi, dims, strides, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return -3;
-        if (enc(&mBl, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, (void*)glo, dims, strides, box, es,
-                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+        if (enc(&mBl, dt, 5, (void*)glo, dims, strides, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return -3;
     }
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(m2l_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)TC_SMEM);
+        cudaFuncSetAttribute(m2l_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)TC_SMEM);
+        cudaFuncSetAttribute(m2l_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)TC_SMEM);
         attr = true;
     }
     TcParams P;
@@ -530,9 +660,15 @@ int launch_m2l_tc(const float* ops_hi, const float* ops_lo, const int* il_slots,
     P.level = level;
     P.slots = il_slots;
     P.L = L_l;
-    if (P.rows % TC_T != 0 || bny % TC_T != 0 || (P.rows / TC_T) % 2 != 0) return -4;
-    const unsigned grid = (unsigned)(8 * (P.rows / TC_T));
-    m2l_tc_kernel<<<grid, TC_THREADS, TC_SMEM, st>>>(mAh, mAl, mBh, mBl, P);
+    P.rs = ops.rs;
+    P.maxbits = maxbits;
+    P.T = pick_T(box);
+    if (P.T == 0) return -4;
+    const unsigned grid = (unsigned)(8 * (P.rows / P.T));
+    if (f16)
+        m2l_tc_kernel<true><<<grid, TC_THREADS, TC_SMEM, st>>>(mAh, mAl, mBh, mBl, P);
+    else
+        m2l_tc_kernel<false><<<grid, TC_THREADS, TC_SMEM, st>>>(mAh, mAl, mBh, mBl, P);
     return 0;
 }
 

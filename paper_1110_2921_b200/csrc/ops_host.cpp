@@ -15,6 +15,9 @@
 //   M2L (source at c_t + o a):                   Lt[n,m]   = sum (-1)^(n+m) I_{n+k}^{l-m}(-o) Mt[k,l]
 //   L2L (parent c -> child c', d = (c'-c)/a_p):   Lt_c[n,m] = sum_{k>=n} 2^-(n+1) R_{k-n}^{l-m}(d) Lt_p[k,l]
 //   periodic (unit box, rings of 3x supercells): see build_periodic below.
+#include <cuda_fp16.h>
+
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <complex>
@@ -229,6 +232,43 @@ void store_tc(std::vector<float>& hi, std::vector<float>& lo, int slot,
         }
 }
 
+// 3xFP16 operands: balance the operators by power-of-2 column scales cs[k] (max over slots and
+// rows of |T[r][k]|) and row scales rs[r] (max of |T[r][k]| / cs[k]), so Ahat = T / (rs cs)
+// has |Ahat| <= 1 and no overflow in half; hi = half(Ahat), lo = half(Ahat - hi)
+void store_h16(const std::vector<std::pair<int, std::vector<double>>>& ops, int nc, HostOps* out) {
+    auto pow2_ceil = [](double v) { return v > 0 ? std::exp2(std::ceil(std::log2(v))) : 1.0; };
+    std::vector<double> cs(128, 1.0), rs(128, 1.0);
+    for (int k = 0; k < nc; ++k) {
+        double m = 0;
+        for (const auto& so : ops)
+            for (int r = 0; r < nc; ++r) m = std::max(m, std::fabs(so.second[(size_t)r * nc + k]));
+        cs[k] = pow2_ceil(m);
+    }
+    for (int r = 0; r < nc; ++r) {
+        double m = 0;
+        for (const auto& so : ops)
+            for (int k = 0; k < nc; ++k)
+                m = std::max(m, std::fabs(so.second[(size_t)r * nc + k]) / cs[k]);
+        rs[r] = pow2_ceil(m);
+    }
+    out->m2l_h16_hi.assign((size_t)343 * 128 * 128, 0);
+    out->m2l_h16_lo.assign((size_t)343 * 128 * 128, 0);
+    for (const auto& so : ops) {
+        uint16_t* H = out->m2l_h16_hi.data() + (size_t)so.first * 128 * 128;
+        uint16_t* Lo = out->m2l_h16_lo.data() + (size_t)so.first * 128 * 128;
+        for (int r = 0; r < nc; ++r)
+            for (int k = 0; k < nc; ++k) {
+                const double v = so.second[(size_t)r * nc + k] / (rs[r] * cs[k]);
+                const __half h = __double2half(v);
+                const __half l = __double2half(v - (double)__half2float(h));
+                memcpy(&H[(size_t)r * 128 + k], &h, 2);
+                memcpy(&Lo[(size_t)r * 128 + k], &l, 2);
+            }
+    }
+    out->h16_rs.assign(rs.begin(), rs.end());
+    out->h16_cs.assign(cs.begin(), cs.end());
+}
+
 void store_t(std::vector<float>& dst, int slot, const std::vector<double>& A, int nc, int KP,
              int NR) {
     float* base = dst.data() + (size_t)slot * KP * NR;
@@ -252,6 +292,7 @@ void build_host_ops(int p, int image_levels, HostOps* out) {
     const bool tc = nc <= 128;
     out->m2l_tc_hi.assign(tc ? (size_t)343 * 128 * 128 : 0, 0.f);
     out->m2l_tc_lo.assign(tc ? (size_t)343 * 128 * 128 : 0, 0.f);
+    std::vector<std::pair<int, std::vector<double>>> tc_ops;  // (slot, packed operator)
     for (int ch = 0; ch < 8; ++ch) {
         const double dx = (((ch >> 0) & 1) - 0.5) * 0.5;
         const double dy = (((ch >> 1) & 1) - 0.5) * 0.5;
@@ -265,8 +306,12 @@ void build_host_ops(int p, int image_levels, HostOps* out) {
                 if (std::max(std::abs(ox), std::max(std::abs(oy), std::abs(oz))) <= 1) continue;
                 const auto T = pack_matrix(m2l_full(-ox, -oy, -oz, p), p);
                 store_t(out->m2l, m2l_slot(ox, oy, oz), T, nc, out->KP, out->NR);
-                if (tc) store_tc(out->m2l_tc_hi, out->m2l_tc_lo, m2l_slot(ox, oy, oz), T, nc);
+                if (tc) {
+                    store_tc(out->m2l_tc_hi, out->m2l_tc_lo, m2l_slot(ox, oy, oz), T, nc);
+                    tc_ops.emplace_back(m2l_slot(ox, oy, oz), T);
+                }
             }
+    if (tc) store_h16(tc_ops, nc, out);
     out->per_d = build_periodic(p, image_levels);
     store_t(out->per, 0, out->per_d, nc, out->KP, out->NR);
 }

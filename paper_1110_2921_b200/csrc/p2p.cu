@@ -31,6 +31,23 @@ KernelConsts make_kernel_consts(float sigma) {
     k.r2_series = (float)(0.5 * s * s);
     k.t_scale = (float)(1.0 / (2.0 * std::sqrt(2.0) * s));
     k.q_scale = (float)(2.0 / (4.0 * M_PI * std::sqrt(M_PI)) / (std::sqrt(2.0) * s));
+    // packed path: the degree-7 erfcx/(4 pi) polynomial in (t - 1/2) (coefficients below, as
+    // in fq_closed) re-expanded in powers of t, scaled by -1/zeta0 (folds the zeta0 factor
+    // of the exponential into the ex2 argument and removes the shift and a negation)
+    static const double cp[8] = {2.032374185e-02, 6.798874982e-02,  7.692235843e-02,
+                                 5.027046960e-02, 4.873839158e-03,  -1.861016238e-02,
+                                 -1.664231425e-03, 6.204596458e-03};  // ascending in t - 1/2
+    double ce[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    for (int j = 0; j < 8; ++j) {  // (t - 1/2)^j = sum_i C(j, i) t^i (-1/2)^(j - i)
+        double binom = 1.0;
+        for (int i = 0; i <= j; ++i) {
+            ce[i] += cp[j] * binom * std::pow(-0.5, j - i);
+            binom = binom * (j - i) / (i + 1);
+        }
+    }
+    k.ez_off = (float)std::log2(z0);
+    k.qn_scale = (float)(-(2.0 / (4.0 * M_PI * std::sqrt(M_PI)) / (std::sqrt(2.0) * s)) / z0);
+    for (int i = 0; i < 8; ++i) k.en[i] = (float)(-ce[i] / z0);
     return k;
 }
 
@@ -66,11 +83,6 @@ __device__ __forceinline__ f2 pk(float a, float b) {
 __device__ __forceinline__ f2 bc(float a) { return pk(a, a); }
 __device__ __forceinline__ void upk(f2 v, float& a, float& b) {
     asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
-}
-__device__ __forceinline__ f2 add2(f2 a, f2 b) {
-    f2 r;
-    asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
-    return r;
 }
 __device__ __forceinline__ f2 sub2(f2 a, f2 b) {
     f2 r;
@@ -134,40 +146,47 @@ __device__ __forceinline__ void fq_closed(float r2, const KernelConsts& kc, floa
     q = fmaf(kc.zeta0, e, -3.f * f) * rinv2;
 }
 
-// f, q for two pairs at once (closed form)
+// f, q for two pairs at once (closed form), in the scaled form of KernelConsts::en:
+//   e_z = zeta0 e^{-rho^2},  f = (1/(4 pi) + e_z Qn) / r^3,  q = (e_z - 3 f) / r^2
 __device__ __forceinline__ void fq_closed2(f2 r2, const KernelConsts& kc, f2& f, f2& q) {
     float ra, rb;
     upk(r2, ra, rb);
     const f2 rinv = pk(rsqrt_approx(ra), rsqrt_approx(rb));
     float ea, eb;
-    upk(mul2(r2, bc(kc.neg_l2e_inv2s2)), ea, eb);
-    const f2 e = pk(ex2_approx(ea), ex2_approx(eb));
+    upk(fma2(r2, bc(kc.neg_l2e_inv2s2), bc(kc.ez_off)), ea, eb);
+    const f2 ez = pk(ex2_approx(ea), ex2_approx(eb));
     const f2 r = mul2(r2, rinv);
     float da, db;
     upk(fma2(r, bc(kc.t_scale), bc(1.f)), da, db);
-    const f2 t = add2(pk(rcp_approx(da), rcp_approx(db)), bc(-0.5f));
-    f2 E = bc(6.204596458e-03f);
-    E = fma2(E, t, bc(-1.664231425e-03f));
-    E = fma2(E, t, bc(-1.861016238e-02f));
-    E = fma2(E, t, bc(4.873839158e-03f));
-    E = fma2(E, t, bc(5.027046960e-02f));
-    E = fma2(E, t, bc(7.692235843e-02f));
-    E = fma2(E, t, bc(6.798874982e-02f));
-    E = fma2(E, t, bc(2.032374185e-02f));
-    const f2 Q = fma2(bc(kc.q_scale), r, E);
-    const f2 g4pi = sub2(bc(0.0795774715459476679f), mul2(e, Q));  // g / (4 pi)
+    const f2 t = pk(rcp_approx(da), rcp_approx(db));
+    f2 E = fma2(bc(kc.en[7]), t, bc(kc.en[6]));
+    E = fma2(E, t, bc(kc.en[5]));
+    E = fma2(E, t, bc(kc.en[4]));
+    E = fma2(E, t, bc(kc.en[3]));
+    E = fma2(E, t, bc(kc.en[2]));
+    E = fma2(E, t, bc(kc.en[1]));
+    E = fma2(E, t, bc(kc.en[0]));
+    const f2 Qn = fma2(bc(kc.qn_scale), r, E);
+    const f2 g4pi = fma2(ez, Qn, bc(0.0795774715459476679f));  // g / (4 pi)
     const f2 rinv2 = mul2(rinv, rinv);
     f = mul2(g4pi, mul2(rinv2, rinv));
-    q = mul2(sub2(mul2(bc(kc.zeta0), e), mul2(bc(3.f), f)), rinv2);
+    q = mul2(fma2(bc(-3.f), f, ez), rinv2);
+}
+
+// c = gamma_j x d with the negated products folded into FMUL2 operand modifiers
+__device__ __forceinline__ void cross2(float gjx, float gjy, float gjz, f2 dx, f2 dy, f2 dz,
+                                       f2& cx, f2& cy, f2& cz) {
+    cx = fma2(bc(gjy), dz, mul2(bc(-gjz), dy));
+    cy = fma2(bc(gjz), dx, mul2(bc(-gjx), dz));
+    cz = fma2(bc(gjx), dy, mul2(bc(-gjy), dx));
 }
 
 template <int SCHEME>
 __device__ __forceinline__ void accumulate2(f2 dx, f2 dy, f2 dz, f2 f, f2 q, float gjx,
                                             float gjy, float gjz, f2 gix, f2 giy, f2 giz,
                                             Acc2& acc) {
-    const f2 cx = sub2(mul2(bc(gjy), dz), mul2(bc(gjz), dy));  // gamma_j x d
-    const f2 cy = sub2(mul2(bc(gjz), dx), mul2(bc(gjx), dz));
-    const f2 cz = sub2(mul2(bc(gjx), dy), mul2(bc(gjy), dx));
+    f2 cx, cy, cz;  // gamma_j x d
+    cross2(gjx, gjy, gjz, dx, dy, dz, cx, cy, cz);
     acc.u0 = fma2(f, cx, acc.u0);
     acc.u1 = fma2(f, cy, acc.u1);
     acc.u2 = fma2(f, cz, acc.u2);
@@ -266,6 +285,7 @@ __device__ __forceinline__ uint32_t compact3p(uint32_t v) {
 // staged in passes of consecutive region leaves.
 constexpr int P2P_THREADS = 256;
 constexpr int P2P_CAP = 4352;  // sources per pass (104 KB) -> 2 blocks / SM
+constexpr int P2P_PAD = 4;     // slack after each staged array for the prefetch reads
 
 template <int SCHEME>
 __global__ void __launch_bounds__(P2P_THREADS, 2) p2p_kernel(
@@ -274,7 +294,7 @@ __global__ void __launch_bounds__(P2P_THREADS, 2) p2p_kernel(
     unsigned long long* __restrict__ npairs, int64_t plo) {
     extern __shared__ float4 p2p_sm[];
     float4* S4 = p2p_sm;                                        // x, y, z, gx
-    float2* S2 = reinterpret_cast<float2*>(S4 + P2P_CAP);       // gy, gz
+    float2* S2 = reinterpret_cast<float2*>(S4 + P2P_CAP + P2P_PAD);  // gy, gz
     __shared__ int rstart[65], rcnt[64], rsrc[64];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const uint32_t parent = (uint32_t)(plo + blockIdx.x);
@@ -370,13 +390,21 @@ __global__ void __launch_bounds__(P2P_THREADS, 2) p2p_kernel(
                 const int rx = bx + nb % 3, ry = by + (nb / 3) % 3, rz = bz + nb / 9;
                 const int rl = rx + 4 * ry + 16 * rz;
                 const int js = max(rstart[rl], w0) - w0, je = min(rstart[rl + 1], w1) - w0;
-                // two sources per iteration; each source x two targets = one packed pair
+                // two sources per iteration; each source x two targets = one packed pair.
+                // The next two sources are prefetched from shared memory one iteration ahead
+                // (the buffers are padded, so reads past je stay inside them and are unused)
+                float4 na = S4[js], nbb = S4[js + 1];
+                float2 nqa = S2[js], nqb = S2[js + 1];
                 for (int j = js; j < je; j += 2) {
                     const bool two = j + 1 < je;
-                    const float4 pa = S4[j];
-                    const float2 qa = S2[j];
-                    const float4 pb = two ? S4[j + 1] : pa;
-                    const float2 qb = two ? S2[j + 1] : make_float2(0.f, 0.f);
+                    const float4 pa = na;
+                    const float2 qa = nqa;
+                    const float4 pb = two ? nbb : pa;
+                    const float2 qb = two ? nqb : make_float2(0.f, 0.f);
+                    na = S4[j + 2];
+                    nbb = S4[j + 3];
+                    nqa = S2[j + 2];
+                    nqb = S2[j + 3];
                     const float gbx = two ? pb.w : 0.f;  // a missing 2nd source has zero strength
                     const f2 dxa = sub2(X, bc(pa.x)), dya = sub2(Y, bc(pa.y)), dza = sub2(Z, bc(pa.z));
                     const f2 dxb = sub2(X, bc(pb.x)), dyb = sub2(Y, bc(pb.y)), dzb = sub2(Z, bc(pb.z));
@@ -507,7 +535,7 @@ __global__ void __launch_bounds__(128) direct_kernel(const float* __restrict__ p
 void launch_p2p(const float* sorted6, int64_t n, const int* leaf_start, int depth, float a,
                 int periodic, int scheme, KernelConsts kc, float* near6,
                 unsigned long long* npairs, int64_t plo, int64_t pcnt, cudaStream_t st) {
-    const size_t smem = (size_t)P2P_CAP * (sizeof(float4) + sizeof(float2));
+    const size_t smem = (size_t)(P2P_CAP + P2P_PAD) * (sizeof(float4) + sizeof(float2));
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(p2p_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

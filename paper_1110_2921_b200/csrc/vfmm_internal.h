@@ -37,6 +37,10 @@ struct HostOps {
     std::vector<double> per_d;  // periodic operator row-major [nc][nc] (double, for tests)
     // tensor-core M2L operands (nc <= 128): row-major [343][128 r][128 k], 3xTF32 split
     std::vector<float> m2l_tc_hi, m2l_tc_lo;
+    // 3xFP16 split of the balanced operators Ahat = T / (rs[r] cs[k]) (rs, cs powers of 2,
+    // |Ahat| <= 1), IEEE half bit patterns, same layout
+    std::vector<uint16_t> m2l_h16_hi, m2l_h16_lo;
+    std::vector<float> h16_rs, h16_cs;  // [128] row / column scales
 };
 
 // Build all operator tables for order p and image_levels (periodic operator is zero for
@@ -89,12 +93,20 @@ void launch_l2p_combine(const float* sorted6, const float* near6, const uint32_t
                         int64_t leaf_lo, int64_t leaf_cnt, int64_t gbase, int64_t nout,
                         cudaStream_t st);
 
-// m2l_tc.cu (tcgen05, 3xTF32)
+// m2l_tc.cu (tcgen05: 3xTF32 or scaled 3xFP16)
+struct TcOps {
+    const void* hi = nullptr;  // [343][128][128] operator hi parts (float tf32 / half)
+    const void* lo = nullptr;  // remainders
+    const float* rs = nullptr; // f16: row scales [128]
+    const float* cs = nullptr; // f16: column scales [128]
+    bool f16 = false;
+};
 bool m2l_tc_supported(int p, int level);
 bool m2l_tc_shape_ok(const int box[6]);
 size_t m2l_tc_grid_floats(int level);
-int launch_m2l_tc(const float* ops_hi, const float* ops_lo, const int* il_slots, int p,
-                  const float* M_l, float* L_l, int level, int periodic, float* ghi, float* glo,
+// maxbits: one zeroed uint32 per launch (f16: the level's max |cs[k] M_k|, as float bits)
+int launch_m2l_tc(const TcOps& ops, const int* il_slots, int p, const float* M_l, float* L_l,
+                  int level, int periodic, float* ghi, float* glo, uint32_t* maxbits,
                   const int box[6], cudaStream_t st);
 
 // p2p.cu
@@ -107,6 +119,12 @@ struct KernelConsts {
     float r2_series;     // r^2 below which the Taylor series is used (rho^2 < 1/4)
     float t_scale;       // 1 / (2 sqrt(2) sigma): t = 1 / (1 + r t_scale) = 1/(1 + rho/2)
     float q_scale;       // 2 / (4 pi sqrt(pi) sqrt(2) sigma): rho term of (1 - g)/(4 pi)
+    // packed fast path (p2p.cu fq_closed2): e_z = zeta0 e^{-rho^2} = 2^(r^2 neg_l2e_inv2s2 +
+    // ez_off); (1 - g)/(4 pi) = -e_z Qn with Qn = qn_scale r + sum_k en[k] t^k (the erfcx
+    // polynomial expanded in powers of t and scaled by -1/zeta0)
+    float ez_off;        // log2(zeta0)
+    float qn_scale;      // -q_scale / zeta0
+    float en[8];
 };
 KernelConsts make_kernel_consts(float sigma);
 void launch_p2p(const float* sorted6, int64_t n, const int* leaf_start, int depth, float a,

@@ -247,14 +247,16 @@ def test_c4_full_size_sampled_targets():
 
 # ------------------------------------------------------------------ tensor-core M2L (tcgen05)
 
+@pytest.mark.parametrize("engine", ["tf32", "f16"])
 @pytest.mark.parametrize("n,depth,p,lam", [(64, 5, 10, 3), (48, 5, 6, 0), (128, 6, 8, 1)])
-def test_m2l_tensor_core_matches_simt(n, depth, p, lam, monkeypatch):
-    """Levels >= 2 run M2L on tcgen05 (3xTF32); the SIMT FP32 gather-GEMM (validated against
-    the fp64 FMM oracle above) computes the same translations.  The tensor core accumulates
-    with truncation (round toward zero), so even with the TMEM chain cut after every offset the
-    two differ by ~1e-5, not FP32 round-off."""
+def test_m2l_tensor_core_matches_simt(n, depth, p, lam, engine, monkeypatch):
+    """Levels >= 2 run M2L on tcgen05 (3xTF32, or the balanced 3xFP16 split); the SIMT FP32
+    gather-GEMM (validated against the fp64 FMM oracle above) computes the same translations.
+    The tensor core accumulates with truncation (round toward zero), so even with the TMEM chain
+    cut after every offset the two differ by ~1e-5, not FP32
+    round-off."""
     f = synthgen.isotropic(n, seed=21)
-    monkeypatch.setenv("VFMM_M2L", "tc")
+    monkeypatch.setenv("VFMM_M2L", engine)
     v1, s1, ev1 = run(f, p=p, depth=depth, image_levels=lam, mode=vf.MODE_FAR_ONLY)
     monkeypatch.setenv("VFMM_M2L", "simt")
     v2, s2, ev2 = run(f, p=p, depth=depth, image_levels=lam, mode=vf.MODE_FAR_ONLY)
