@@ -25,6 +25,22 @@ namespace vfmm {
 
 namespace {
 
+// packed FP32x2 helpers (Blackwell FFMA2)
+typedef unsigned long long f2x;
+__device__ __forceinline__ f2x pk2(float a, float b) {
+    f2x r;
+    asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(a), "f"(b));
+    return r;
+}
+__device__ __forceinline__ void upk2(f2x v, float& a, float& b) {
+    asm("mov.b64 {%0, %1}, %2;" : "=f"(a), "=f"(b) : "l"(v));
+}
+__device__ __forceinline__ f2x ffma2(f2x a, f2x b, f2x c) {
+    f2x r;
+    asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
+    return r;
+}
+
 __device__ __forceinline__ uint32_t spread3d(uint32_t v) {
     v &= 0x3ffu;
     v = (v | (v << 16)) & 0x030000FFu;
@@ -51,11 +67,15 @@ __constant__ float c_mhalf[17] = {0.000000000e+00f, -5.000000000e-01f, -2.500000
 // one block (64 threads) per leaf; thread j builds conj(R) of particle j in smem,
 // then threads reduce the 3 x nc outputs over particles.
 // ---------------------------------------------------------------------------
-__device__ void solid_R_packed(float x, float y, float z, int p, float* out, int stride,
-                               bool conj_) {
-    // packed real R_n^m for 0 <= m <= n <= p, written to out[k * stride]
+template <int PC>
+__device__ __forceinline__ void solid_R_packed(float x, float y, float z, int p_rt, float* out,
+                                               int stride, bool conj_) {
+    // packed real R_n^m for 0 <= m <= n <= p, written to out[k * stride]; PC > 0: p = PC
+    // known at compile time (recurrences fully unrolled)
+    const int p = PC > 0 ? PC : p_rt;
     const float r2 = x * x + y * y + z * z;
     float dre = 1.f, dim = 0.f;  // R_m^m
+#pragma unroll
     for (int m = 0; m <= p; ++m) {
         if (m > 0) {
             const float s = c_mhalf[m];
@@ -73,6 +93,7 @@ __device__ void solid_R_packed(float x, float y, float z, int p, float* out, int
             out[pk_re(m + 1, m) * stride] = p1re;
             if (m > 0) out[pk_im(m + 1, m) * stride] = conj_ ? -p1im : p1im;
         }
+#pragma unroll
         for (int n = m + 2; n <= p; ++n) {
             const float inv = c_rinv[n * 17 + m];
             const float a = (2.f * n - 1.f) * z;
@@ -88,10 +109,12 @@ __device__ void solid_R_packed(float x, float y, float z, int p, float* out, int
     }
 }
 
+template <int PC>
 __global__ void __launch_bounds__(64) p2m_kernel(const float* __restrict__ s6, int64_t n,
-                                                 const int* __restrict__ leaf_start, int p,
+                                                 const int* __restrict__ leaf_start, int p_rt,
                                                  float inv_a, float* __restrict__ M,
                                                  int64_t leaf_lo) {
+    const int p = PC > 0 ? PC : p_rt;
     // thread j: conj(R) of particle j -> Rs[k][j] (row stride 68: float4-aligned rows);
     // then thread k: M[c][k] for c = 0..2 from float4 loads of Rs[k][.] and gamma_c[.]
     extern __shared__ float4 p2m_sm4[];
@@ -111,8 +134,8 @@ __global__ void __launch_bounds__(64) p2m_kernel(const float* __restrict__ s6, i
             const int cnt = min(64, e - b);
             __syncthreads();
             if (threadIdx.x < cnt) {
-                solid_R_packed(s6[j] * inv_a, s6[n + j] * inv_a, s6[2 * n + j] * inv_a, p,
-                               Rs + threadIdx.x, RST, true);
+                solid_R_packed<PC>(s6[j] * inv_a, s6[n + j] * inv_a, s6[2 * n + j] * inv_a, p,
+                                   Rs + threadIdx.x, RST, true);
                 gs[threadIdx.x] = s6[3 * n + j];
                 gs[64 + threadIdx.x] = s6[4 * n + j];
                 gs[128 + threadIdx.x] = s6[5 * n + j];
@@ -168,7 +191,7 @@ constexpr size_t TRANSLATE_SMEM =
 
 // grid.x: column tiles; grid.y: row tiles (nc > 128).  256 threads: 16 x 16, each 8 rows x 6 cols.
 template <int KIND>
-__global__ void __launch_bounds__(256) translate_kernel(
+__global__ void __launch_bounds__(256, 2) translate_kernel(
     const float* __restrict__ mats, const int* __restrict__ slots, int p, int KP, int NR,
     const float* __restrict__ src, float* __restrict__ dst, int level, int periodic, int64_t plo,
     int64_t pcnt, int opsplit) {
@@ -391,20 +414,26 @@ __device__ void deriv_expansion(const float* in, int pin, int axis, float* out, 
     }
 }
 
-template <int SCHEME>
+// PC > 0: the order p is a compile-time constant (loops fully unrolled: immediate shared-memory
+// offsets and recurrence constants); PC = 0: runtime p
+template <int SCHEME, int PC>
 __global__ void __launch_bounds__(64) l2p_combine_kernel(
     const float* __restrict__ s6, const float* __restrict__ near6,
-    const uint32_t* __restrict__ perm, int64_t n, const int* __restrict__ leaf_start, int p,
+    const uint32_t* __restrict__ perm, int64_t n, const int* __restrict__ leaf_start, int p_rt,
     float inv_a, const float* __restrict__ Lleaf, int use_near, int use_far,
     float* __restrict__ vel, float* __restrict__ dgam, int64_t leaf_lo, int64_t gbase,
     int64_t nout) {
-    // smem: D [ng][28] (q: 9 gradients then 18 Hessian entries, pad); Ls [3][nc]; G; H
+    const int p = PC > 0 ? PC : p_rt;
+    // smem: D [ng][12]; Ls [3][nc]; G [9][ng]; H [18][nh].  The 12 columns of D are the
+    // combinations the output needs: u = curl phi (3) and J[a][k] = d_k u_a (9), each a
+    // difference of two derivative expansions of phi_c (so 12 accumulators per particle)
+    constexpr int DQ = 12;
     extern __shared__ float4 l2p_sm4[];
     float* sm = reinterpret_cast<float*>(l2p_sm4);
     const int nc = (p + 1) * (p + 1);
     const int ng = p * p, nh = (p - 1) * (p - 1);
     const float4* D4 = l2p_sm4;
-    float* Ls = sm + ng * 28;
+    float* Ls = sm + ng * DQ;
     float* G = Ls + 3 * nc;
     float* H = G + 9 * ng;
     const int64_t leaf = leaf_lo + blockIdx.x;
@@ -426,12 +455,25 @@ __global__ void __launch_bounds__(64) l2p_combine_kernel(
                                     threadIdx.x, 64);
         }
         __syncthreads();
-        // transpose into D[k][q]: q < 9 -> G[q][k]; 9 <= q < 27 -> H[q-9][k] (0 beyond nh)
-        for (int i = threadIdx.x; i < ng * 28; i += 64) {
-            const int k = i / 28, q = i - k * 28;
-            float v = 0.f;
-            if (q < 9) v = G[q * ng + k];
-            else if (q < 27 && k < nh) v = H[(q - 9) * nh + k];
+        // D[k][q]: q < 3: u_q = (curl phi)_q; q = 3 + 3a + kk: J[a][kk] = d_kk u_a (0 beyond nh)
+        auto gi_ = [&](int c, int ax, int k) { return G[(c * 3 + ax) * ng + k]; };
+        auto hi_ = [&](int c, int a1, int b1, int k) {
+            const int lo = a1 < b1 ? a1 : b1, hi = a1 < b1 ? b1 : a1;
+            const int q = lo == 0 ? hi : (lo == 1 ? 2 + hi : 5);
+            return k < nh ? H[(c * 6 + q) * nh + k] : 0.f;
+        };
+        for (int i = threadIdx.x; i < ng * DQ; i += 64) {
+            const int k = i / DQ, q = i - k * DQ;
+            float v;
+            if (q == 0) v = gi_(2, 1, k) - gi_(1, 2, k);
+            else if (q == 1) v = gi_(0, 2, k) - gi_(2, 0, k);
+            else if (q == 2) v = gi_(1, 0, k) - gi_(0, 1, k);
+            else {
+                const int a1 = (q - 3) / 3, kk = (q - 3) % 3;
+                if (a1 == 0) v = hi_(2, kk, 1, k) - hi_(1, kk, 2, k);
+                else if (a1 == 1) v = hi_(0, kk, 2, k) - hi_(2, kk, 0, k);
+                else v = hi_(1, kk, 0, k) - hi_(0, kk, 1, k);
+            }
             sm[i] = v;
         }
         __syncthreads();
@@ -448,14 +490,15 @@ __global__ void __launch_bounds__(64) l2p_combine_kernel(
         }
         if (use_far && act) {
             const float x = s6[j] * inv_a, y = s6[n + j] * inv_a, z = s6[2 * n + j] * inv_a;
-            float acc[28];
+            f2x acc2[DQ / 2];  // accumulators as packed pairs (q, q+1): FFMA2 with broadcast w
 #pragma unroll
-            for (int q = 0; q < 28; ++q) acc[q] = 0.f;
+            for (int q = 0; q < DQ / 2; ++q) acc2[q] = pk2(0.f, 0.f);
             // R_n^m(z/a) by recurrence (m outer, n inner, n <= p-1), accumulated on the fly:
             // value_q = sum_k D[k][q] w_k, w = R_re (m = 0); 2 R_re, -2 R_im (m > 0)
             const float r2 = x * x + y * y + z * z;
             float dre = 1.f, dim = 0.f;
-            const int pm = p - 1;
+            const int pm = (PC > 0 ? PC : p) - 1;
+#pragma unroll
             for (int m = 0; m <= pm; ++m) {
                 if (m > 0) {
                     const float sc = c_mhalf[m];
@@ -465,6 +508,7 @@ __global__ void __launch_bounds__(64) l2p_combine_kernel(
                     dim = nim;
                 }
                 float p2re = 0.f, p2im = 0.f, p1re = 0.f, p1im = 0.f;
+#pragma unroll
                 for (int nn = m; nn <= pm; ++nn) {
                     float cre, cim;
                     if (nn == m) {
@@ -483,54 +527,45 @@ __global__ void __launch_bounds__(64) l2p_combine_kernel(
                     p2im = p1im;
                     p1re = cre;
                     p1im = cim;
-                    const float4* Dr = D4 + pk_re(nn, m) * 7;
+                    const float4* Dr = D4 + pk_re(nn, m) * (DQ / 4);
                     if (m == 0) {
+                        const f2x w = pk2(cre, cre);
 #pragma unroll
-                        for (int q4 = 0; q4 < 7; ++q4) {
+                        for (int q4 = 0; q4 < DQ / 4; ++q4) {
                             const float4 d = Dr[q4];
-                            acc[4 * q4 + 0] = fmaf(d.x, cre, acc[4 * q4 + 0]);
-                            acc[4 * q4 + 1] = fmaf(d.y, cre, acc[4 * q4 + 1]);
-                            acc[4 * q4 + 2] = fmaf(d.z, cre, acc[4 * q4 + 2]);
-                            acc[4 * q4 + 3] = fmaf(d.w, cre, acc[4 * q4 + 3]);
+                            acc2[2 * q4 + 0] = ffma2(pk2(d.x, d.y), w, acc2[2 * q4 + 0]);
+                            acc2[2 * q4 + 1] = ffma2(pk2(d.z, d.w), w, acc2[2 * q4 + 1]);
                         }
                     } else {
-                        const float4* Di = D4 + pk_im(nn, m) * 7;
-                        const float wr = 2.f * cre, wi = -2.f * cim;
+                        const float4* Di = D4 + pk_im(nn, m) * (DQ / 4);
+                        const f2x wr = pk2(2.f * cre, 2.f * cre), wi = pk2(-2.f * cim, -2.f * cim);
 #pragma unroll
-                        for (int q4 = 0; q4 < 7; ++q4) {
+                        for (int q4 = 0; q4 < DQ / 4; ++q4) {
                             const float4 d = Dr[q4], f = Di[q4];
-                            acc[4 * q4 + 0] = fmaf(d.x, wr, fmaf(f.x, wi, acc[4 * q4 + 0]));
-                            acc[4 * q4 + 1] = fmaf(d.y, wr, fmaf(f.y, wi, acc[4 * q4 + 1]));
-                            acc[4 * q4 + 2] = fmaf(d.z, wr, fmaf(f.z, wi, acc[4 * q4 + 2]));
-                            acc[4 * q4 + 3] = fmaf(d.w, wr, fmaf(f.w, wi, acc[4 * q4 + 3]));
+                            acc2[2 * q4 + 0] =
+                                ffma2(pk2(d.x, d.y), wr, ffma2(pk2(f.x, f.y), wi, acc2[2 * q4 + 0]));
+                            acc2[2 * q4 + 1] =
+                                ffma2(pk2(d.z, d.w), wr, ffma2(pk2(f.z, f.w), wi, acc2[2 * q4 + 1]));
                         }
                     }
                 }
             }
-            // acc[c*3 + axis] = d_axis phi_c ; acc[9 + c*6 + q] = Hessian pair q of phi_c
+            float acc[DQ];
+#pragma unroll
+            for (int q = 0; q < DQ / 2; ++q) upk2(acc2[q], acc[2 * q], acc[2 * q + 1]);
+            // acc[0..2] = curl phi ; acc[3 + 3a + k] = d_k u_a (before scaling)
             const float sg = inv4pi * inv_a * inv_a;  // gradient scale
             const float sh = sg * inv_a;              // Hessian scale
-            u[0] = sg * (acc[2 * 3 + 1] - acc[1 * 3 + 2]);
-            u[1] = sg * (acc[0 * 3 + 2] - acc[2 * 3 + 0]);
-            u[2] = sg * (acc[1 * 3 + 0] - acc[0 * 3 + 1]);
-            auto h = [&](int c, int a, int b2) -> float {
-                const int lo = a < b2 ? a : b2, hi = a < b2 ? b2 : a;
-                const int q = lo == 0 ? hi : (lo == 1 ? 2 + hi : 5);
-                return acc[9 + c * 6 + q];
-            };
-            float J[3][3];  // J[a][k] = d_k u_a / sh
-#pragma unroll
-            for (int k = 0; k < 3; ++k) {
-                J[0][k] = h(2, k, 1) - h(1, k, 2);
-                J[1][k] = h(0, k, 2) - h(2, k, 0);
-                J[2][k] = h(1, k, 0) - h(0, k, 1);
-            }
+            u[0] = sg * acc[0];
+            u[1] = sg * acc[1];
+            u[2] = sg * acc[2];
 #pragma unroll
             for (int a2 = 0; a2 < 3; ++a2) {
                 if (SCHEME == 0)
-                    sd[a2] = sh * (J[a2][0] * gi[0] + J[a2][1] * gi[1] + J[a2][2] * gi[2]);
+                    sd[a2] = sh * (acc[3 + 3 * a2] * gi[0] + acc[4 + 3 * a2] * gi[1] +
+                                   acc[5 + 3 * a2] * gi[2]);
                 else
-                    sd[a2] = sh * (J[0][a2] * gi[0] + J[1][a2] * gi[1] + J[2][a2] * gi[2]);
+                    sd[a2] = sh * (acc[3 + a2] * gi[0] + acc[6 + a2] * gi[1] + acc[9 + a2] * gi[2]);
             }
         }
         if (act) {
@@ -569,12 +604,25 @@ void launch_p2m(const float* sorted6, int64_t n, const int* leaf_start, int p, f
     const size_t smem = sizeof(float) * (nc * 68 + 3 * 64);
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(p2m_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        const void* ks[] = {(const void*)p2m_kernel<0>, (const void*)p2m_kernel<4>,
+                            (const void*)p2m_kernel<6>, (const void*)p2m_kernel<8>,
+                            (const void*)p2m_kernel<10>};
+        for (const void* k : ks)
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
     if (leaf_cnt <= 0) return;
-    p2m_kernel<<<(unsigned)leaf_cnt, 64, smem, st>>>(sorted6, n, leaf_start, p, inv_a, M_leaf,
-                                                     leaf_lo);
+    auto go = [&](auto kern) {
+        kern<<<(unsigned)leaf_cnt, 64, smem, st>>>(sorted6, n, leaf_start, p, inv_a, M_leaf,
+                                                   leaf_lo);
+    };
+    switch (p) {  // compile-time orders for the common p
+        case 4: go(p2m_kernel<4>); break;
+        case 6: go(p2m_kernel<6>); break;
+        case 8: go(p2m_kernel<8>); break;
+        case 10: go(p2m_kernel<10>); break;
+        default: go(p2m_kernel<0>);
+    }
 }
 
 void launch_m2m(const float* ops_m2m, int p, int KP, int NR, const float* M_child, float* M_par,
@@ -625,24 +673,41 @@ void launch_l2p_combine(const float* sorted6, const float* near6, const uint32_t
                         int64_t leaf_lo, int64_t leaf_cnt, int64_t gbase, int64_t nout,
                         cudaStream_t st) {
     const int nc = (p + 1) * (p + 1), ng = p * p, nh = (p - 1) * (p - 1);
-    const size_t smem = sizeof(float) * (ng * 28 + 3 * nc + 9 * ng + 18 * (nh > 0 ? nh : 1));
+    const size_t smem = sizeof(float) * (ng * 12 + 3 * nc + 9 * ng + 18 * (nh > 0 ? nh : 1));
+    if (leaf_cnt <= 0) return;
+    const float inv_a = 1.f / a;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(l2p_combine_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             200 * 1024);
-        cudaFuncSetAttribute(l2p_combine_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             200 * 1024);
+        const void* ks[] = {(const void*)l2p_combine_kernel<0, 4>, (const void*)l2p_combine_kernel<1, 4>,
+                            (const void*)l2p_combine_kernel<0, 6>, (const void*)l2p_combine_kernel<1, 6>,
+                            (const void*)l2p_combine_kernel<0, 8>, (const void*)l2p_combine_kernel<1, 8>,
+                            (const void*)l2p_combine_kernel<0, 10>, (const void*)l2p_combine_kernel<1, 10>,
+                            (const void*)l2p_combine_kernel<0, 0>, (const void*)l2p_combine_kernel<1, 0>};
+        for (const void* k : ks)
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
         attr = true;
     }
-    if (leaf_cnt <= 0) return;
-    if (scheme == 0)
-        l2p_combine_kernel<0><<<(unsigned)leaf_cnt, 64, smem, st>>>(
-            sorted6, near6, perm, n, leaf_start, p, 1.f / a, L_leaf, use_near, use_far, vel, dgam,
-            leaf_lo, gbase, nout);
-    else
-        l2p_combine_kernel<1><<<(unsigned)leaf_cnt, 64, smem, st>>>(
-            sorted6, near6, perm, n, leaf_start, p, 1.f / a, L_leaf, use_near, use_far, vel, dgam,
-            leaf_lo, gbase, nout);
+    auto go = [&](auto kern) {
+        kern<<<(unsigned)leaf_cnt, 64, smem, st>>>(sorted6, near6, perm, n, leaf_start, p, inv_a,
+                                                   L_leaf, use_near, use_far, vel, dgam, leaf_lo,
+                                                   gbase, nout);
+    };
+    // compile-time orders for the common p, runtime-p kernel otherwise
+#define L2P_CASE(PV)                                                             \
+    case PV:                                                                     \
+        if (scheme == 0) go(l2p_combine_kernel<0, PV>);                         \
+        else go(l2p_combine_kernel<1, PV>);                                     \
+        return;
+    switch (p) {
+        L2P_CASE(4)
+        L2P_CASE(6)
+        L2P_CASE(8)
+        L2P_CASE(10)
+        default:
+            if (scheme == 0) go(l2p_combine_kernel<0, 0>);
+            else go(l2p_combine_kernel<1, 0>);
+    }
+#undef L2P_CASE
 }
 
 }  // namespace vfmm

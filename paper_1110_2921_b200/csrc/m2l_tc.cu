@@ -474,7 +474,9 @@ __global__ void m2l_stage_kernel(const float* __restrict__ M, int nP, int period
     }
 }
 
-// f16 staging, two passes over the same padded grid (blockDim = (128 k, 4 rows)):
+// f16 staging, two passes over the same padded grid.  One block per (pi', Z, Y) x-row of the
+// grid (blockDim = (128 k, 4)); the 4 thread rows walk its 3 (Xp) (X, comp) rows, so the
+// Morton bits of (Y, Z, pi') are computed once per block.
 // MAXPASS: max |cs[k] M_k| of the staged values -> atomicMax on the float bits (non-negative);
 // else:    grid[pi'][Z][Y][X][comp][128] = half split of M_k cs[k] s, s = 2^h16_scale_exp(max)
 template <bool MAXPASS>
@@ -485,32 +487,25 @@ __global__ void __launch_bounds__(512) m2l_stage16_kernel(const float* __restric
                                                           __half* __restrict__ ghi,
                                                           __half* __restrict__ glo) {
     const int Xp = nP + 4;
-    const int nrows = 8 * Xp * Xp * Xp * 3;
     const int k = threadIdx.x;
     const float ck = k < nc ? cs[k] : 0.f;
     const float s = MAXPASS ? 1.f : ldexpf(1.f, h16_scale_exp(*maxbits));
+    const int Y = blockIdx.x % Xp, Z = (blockIdx.x / Xp) % Xp, ps = blockIdx.x / (Xp * Xp);
+    int py = Y - 2, pz = Z - 2;
+    const bool yz_in = py >= 0 && py < nP && pz >= 0 && pz < nP;
+    py = (py + nP) & (nP - 1);
+    pz = (pz + nP) & (nP - 1);
+    const uint32_t cyz = (spread3t(2 * py + ((ps >> 1) & 1)) << 1) |
+                         (spread3t(2 * pz + ((ps >> 2) & 1)) << 2);
+    const bool kin = k < nc && (periodic || yz_in);
+    const int64_t row0 = (int64_t)blockIdx.x * Xp * 3;  // grid row of (X = 0, comp = 0)
     float mx = 0.f;
-    for (int row = blockIdx.x * blockDim.y + threadIdx.y; row < nrows;
-         row += gridDim.x * blockDim.y) {
-        int q = row;
-        const int comp = q % 3;
-        q /= 3;
-        const int X = q % Xp;
-        q /= Xp;
-        const int Y = q % Xp;
-        q /= Xp;
-        const int Z = q % Xp;
-        const int ps = q / Xp;
-        int px = X - 2, py = Y - 2, pz = Z - 2;
+    for (int rr = threadIdx.y; rr < 3 * Xp; rr += blockDim.y) {
+        const int X = rr / 3, comp = rr - 3 * X;
+        const int px = X - 2;
         float v = 0.f;
-        const bool inside = px >= 0 && px < nP && py >= 0 && py < nP && pz >= 0 && pz < nP;
-        if (k < nc && (periodic || inside)) {
-            px = (px + nP) & (nP - 1);
-            py = (py + nP) & (nP - 1);
-            pz = (pz + nP) & (nP - 1);
-            const uint32_t cell = spread3t(2 * px + (ps & 1)) |
-                                  (spread3t(2 * py + ((ps >> 1) & 1)) << 1) |
-                                  (spread3t(2 * pz + ((ps >> 2) & 1)) << 2);
+        if (kin && (periodic || (px >= 0 && px < nP))) {
+            const uint32_t cell = spread3t(2 * ((px + nP) & (nP - 1)) + (ps & 1)) | cyz;
             v = M[((int64_t)cell * 3 + comp) * nc + k];
         }
         if (MAXPASS) {
@@ -519,8 +514,8 @@ __global__ void __launch_bounds__(512) m2l_stage16_kernel(const float* __restric
             const float x = v * ck * s;
             const __half h = __float2half_rn(x);
             const __half l = __float2half_rn(x - __half2float(h));
-            ghi[(int64_t)row * 128 + k] = h;
-            glo[(int64_t)row * 128 + k] = l;
+            ghi[(row0 + rr) * 128 + k] = h;
+            glo[(row0 + rr) * 128 + k] = l;
         }
     }
     if (MAXPASS) {
@@ -583,9 +578,7 @@ int launch_m2l_tc(const TcOps& ops, const int* il_slots, int p, const float* M_l
     {
         const int64_t total = (int64_t)8 * Xp * Xp * Xp * 3 * 128;
         if (f16) {
-            const int64_t rows = total / 128;
-            int64_t blocks = (rows + 3) / 4;
-            if (blocks > 148 * 8) blocks = 148 * 8;
+            const int64_t blocks = (int64_t)8 * Xp * Xp;  // one per (pi', Z, Y) x-row
             const dim3 blk(128, 4);
             m2l_stage16_kernel<true><<<(unsigned)blocks, blk, 0, st>>>(
                 M_l, nP, periodic, nc, ops.cs, maxbits, nullptr, nullptr);
