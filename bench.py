@@ -287,17 +287,23 @@ def main():
     pairs = phases[0]["n_p2p_pairs"] or 27 * 64 * n_total
     p2p_tf = pairs * P2P_FLOP_PER_PAIR / t_p2p / 1e12
     m2l_tf = phases[0]["n_m2l"] * 6 * nc * nc / t_m2l / 1e12
-    tc_m2l = p <= 10 and depth >= 2  # levels >= 2 run M2L on tcgen05 (3xTF32)
+    engine = os.environ.get("VFMM_M2L", "f16")  # same selection as the library (capi.cu)
+    tc_m2l = p <= 10 and depth >= 2 and engine != "simt"  # levels >= 2 run M2L on tcgen05
     bf16 = float(peaks.get("bf16_tflops", 1630.5))
-    tf32_peak = bf16 * (1.1 / 2.25)  # guide's nominal dense tf32 / bf16 ratio x measured bf16
+    if engine == "tf32":
+        tc_peak, tc_note, tc_split = bf16 * (1.1 / 2.25), \
+            "measured bf16 burst x nominal tf32/bf16 (1.1/2.25 PF)", "3xTF32"
+    else:  # kind::f16 runs at the dense fp16/bf16 rate
+        tc_peak, tc_note, tc_split = bf16, "measured bf16 burst (fp16 dense = bf16 dense rate)", \
+            "scaled 3xFP16"
     if t_m2l >= t_p2p:
         if tc_m2l:
-            roof = {"kernel": "m2l (m2l_tc_kernel tcgen05 3xTF32 at levels >= 2, SIMT level 1)",
-                    "bound": "tensor", "achieved": m2l_tf, "peak": tf32_peak, "unit": "TFLOP/s",
-                    "frac": m2l_tf / tf32_peak, "traffic": None,
+            roof = {"kernel": f"m2l (m2l_tc_kernel tcgen05 {tc_split} at levels >= 2, SIMT level 1)",
+                    "bound": "tensor", "achieved": m2l_tf, "peak": tc_peak, "unit": "TFLOP/s",
+                    "frac": m2l_tf / tc_peak, "traffic": None,
                     "per_unit": f"6(p+1)^4 = {6 * nc * nc} useful flop per M2L translation; "
-                                "3xTF32 issues 3 tensor products per useful product",
-                    "peak_note": "measured bf16 burst x nominal tf32/bf16 (1.1/2.25 PF)"}
+                                f"{tc_split} issues 3 tensor products per useful product",
+                    "peak_note": tc_note}
         else:
             roof = {"kernel": "m2l (translate_kernel<M2L>, all levels)", "bound": "alu",
                     "achieved": m2l_tf, "peak": fp32_peak, "unit": "TFLOP/s",
@@ -338,6 +344,7 @@ def main():
         "p2p_interactions_per_s": pairs / t_p2p,
         "p2p_pairs_per_eval": pairs,
         "fp32_frac_p2p": p2p_tf / fp32_peak, "m2l_useful_tflops": m2l_tf,
+        "m2l_engine": engine if tc_m2l else "simt",
         "phase_ms": {k[3:]: round(v, 4) for k, v in avg.items() if k.startswith("ms_")},
         "roofline": roof, "cpu_baseline": cb, "e2e": e2e,
         "gpu_launches": int(phases[0]["n_kernel_launches"]) * args.steps,

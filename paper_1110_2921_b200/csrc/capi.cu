@@ -37,6 +37,7 @@ struct vfmm_ctx {
     cudaStream_t side = nullptr;                   // coarse M2L levels run here, joined by events
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int* d_slots = nullptr;  // [8][189]
+    int* d_groups = nullptr; // [8][72][4] offset groups (tensor-core M2L y-windows)
     // workspace
     int64_t cap_n = 0;
     int cap_depth = -1, cap_p = -1;
@@ -80,6 +81,7 @@ int m2l_env_mode() {
 
 TcOps tc_ops(const vfmm_ctx* c) {
     TcOps t;
+    t.groups = reinterpret_cast<const int4*>(c->d_groups);
     if (m2l_env_mode() == 2 && c->d_h16_hi) {
         t.hi = c->d_h16_hi;
         t.lo = c->d_h16_lo;
@@ -189,6 +191,11 @@ vfmm_status ensure_ops(vfmm_ctx* c) {
         CK(cudaMemcpy(c->d_slots, slots.data(), slots.size() * sizeof(int),
                       cudaMemcpyHostToDevice),
            "upload slots");
+        const std::vector<int> groups = m2l_groups();
+        CK(cudaMalloc((void**)&c->d_groups, groups.size() * sizeof(int)), "alloc groups");
+        CK(cudaMemcpy(c->d_groups, groups.data(), groups.size() * sizeof(int),
+                      cudaMemcpyHostToDevice),
+           "upload groups");
     }
     c->ops_p = c->prm.p;
     c->ops_levels = c->prm.image_levels;
@@ -755,6 +762,7 @@ void vfmm_destroy(vfmm_ctx* c) {
     dfree(c->d_m2l);
     dfree(c->d_per);
     dfree(c->d_slots);
+    dfree(c->d_groups);
     dfree(c->d_tc_hi);
     dfree(c->d_tc_lo);
     dfree(c->d_h16_hi);

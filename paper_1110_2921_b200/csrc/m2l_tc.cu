@@ -14,18 +14,21 @@
 // The M2L of level l is a batch of dense GEMMs, one per (target parity pi, offset o):
 //   D[r][(px,c)] += sum_k T_o[r][k] * Msrc[(px + dx, c)][k]
 // A = T_o (128 output coefficients r x 128 input coefficients k, zero padded, one per slot),
-// B = a "slab" of source multipoles: one x-row of XT <= 32 parent cells x 3 strength
-// components = N <= 96 rows, read from a parity-major, halo-padded copy of the level's
-// multipoles (m2l_stage_kernel) so every (target row, offset) maps to one TMA box.
-// A CTA owns T = 2 target rows (Py, Pz) of one parity; their slabs are stacked in one B
-// stage so a single MMA (N' = 2N <= 192) serves both rows: the operator is read from shared
-// memory once per K-step for both (2 accumulator tiles side by side in TMEM).
+// B = a "slab" of source multipoles: one x-row of XT <= 16 parent cells x 3 strength
+// components = N <= 48 rows, read from a parity-major, halo-padded copy of the level's
+// multipoles (stage kernels) so every (target row, offset) maps to one TMA box row.
+// A CTA owns T target rows (Py .. Py+T-1, Pz) of one parity; their slabs are stacked so a
+// single MMA (N' = T N <= 192) serves all T rows (T accumulator tiles side by side in TMEM).
+// y-windows: the 189 offsets of a parity fall into 72 groups (source parent dx, dz, source
+// parity) of <= 3 offsets dy = -1, 0, 1.  One TMA box of T + 2 consecutive y-slabs per group
+// and K chunk serves all of them -- the B operand of offset dy is the window shifted by
+// (dy + 1) N rows -- cutting the slab traffic to (T+2)/(2.6 T) of one load per offset.
 //
 // Accuracy: the tensor core accumulates with truncation, so a TMEM chain over all
 // 189 offsets x 16 K-steps x 3 products (~9000 accumulations) drifts by ~1e-4.  The chain is
-// therefore cut after every offset (TC_G = 1: <= 48 accumulations): the MMA warp alternates between
-// two TMEM buffers and the epilogue warps add each finished buffer into FP32 registers
-// (round-to-nearest), so the result keeps FP32 accuracy.
+// therefore cut after every group (<= 3 offsets x 4 K-steps x K chunks x 3 products): the MMA
+// warp alternates between two TMEM buffers and the epilogue warps add each finished buffer
+// into FP32 registers (round-to-nearest), so the result keeps ~FP32 accuracy.
 //
 // Warp roles (320 threads): warp 0 = TMA producer, warp 1 = TMEM alloc + MMA issuer,
 // warps 2-9 = epilogue (TMEM -> FP32 register sums -> L in Morton order).
@@ -44,14 +47,14 @@ namespace vfmm {
 
 namespace {
 
-constexpr int TC_G = 1;        // offsets per TMEM accumulation group (flushed to FP32 registers)
 // K chunks of 128 B: 4 x 32 tf32 or 2 x 64 halves (K = 128)
 template <bool F16> __host__ __device__ constexpr int tc_nkc() { return F16 ? 2 : 4; }
 template <bool F16> __host__ __device__ constexpr int tc_ke() { return F16 ? 64 : 32; }
 constexpr int TC_AST = 2;      // A (operator) pipeline stages
-constexpr int TC_BST = 3;      // B pipeline stages (each holds the slabs of all T rows)
+constexpr int TC_BST = 2;      // B pipeline stages (each holds one y-window of T + 2 slabs)
 constexpr int A_BYTES = 128 * 128;  // one K chunk of one operator half (hi or lo): 16 KB
-constexpr int B_BYTES = 192 * 128;  // one K chunk of the T stacked slabs (T N <= 192 rows), one half
+constexpr int B_WROWS = 288;        // max window rows (T + 2) N
+constexpr int B_BYTES = B_WROWS * 128;  // one K chunk of a y-window of slabs, one half: 36 KB
 constexpr int TC_EPI_WARPS = 8;  // 2 per TMEM lane quarter: warp pair splits the T tiles
 constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;
 constexpr size_t TC_SMEM = 1024 + (size_t)TC_AST * 2 * A_BYTES + (size_t)TC_BST * 2 * B_BYTES + 512;
@@ -182,6 +185,7 @@ struct TcParams {
     float* L;          // local expansions of this level, Morton [cell][3][nc]
     const float* rs;   // f16: row scales [128]
     const uint32_t* maxbits;  // f16: the level's max |cs[k] M_k| (float bits)
+    const int4* groups;  // [8][72] offset groups per target parity (see m2l_groups)
 };
 
 // f16 staging scale s = 2^(14 - e) for the level max m = f 2^e (f in [0.5, 1)): max |Mhat| < 2^14
@@ -241,7 +245,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     int gtx, gpy0, gpz;
     group_rows(P, g, &gtx, &gpy0, &gpz);
     constexpr uint32_t tmem_cols = 512;  // 2 buffers x 256 columns
-    const int ngroups = (189 + TC_G - 1) / TC_G;
 
     if (warp == 0 && lane == 0) {
         for (int i = 0; i < TC_AST; ++i) {
@@ -272,43 +275,47 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
 
     if (warp == 0) {
         // ===================== TMA producer =====================
+        // per offset group (dx, dz, source parity): one y-window of T + 2 slabs (rows
+        // gpy0 - 1 .. gpy0 + T) per K chunk serves the group's <= 3 offsets dy = -1, 0, 1;
+        // then the operator chunk of each valid offset (shared with the peer CTA)
         if (lane == 0) {
             int sa = 0, sb = 0;
             uint32_t pa = 0, pb = 0;
-            const uint32_t b_tx = 2u * (uint32_t)P.N * 128u;
-            for (int oi = 0; oi < 189; ++oi) {
-                const int slot = P.slots[pi * 189 + oi];
-                const int ox = slot / 49 - 3, oy = (slot / 7) % 7 - 3, oz = slot % 7 - 3;
-                const int sx = pix + ox, sy = piy + oy, sz = piz + oz;
-                const int dx = sx >> 1, dy = sy >> 1, dz = sz >> 1;  // floor division
-                const int pis = (sx & 1) | ((sy & 1) << 1) | ((sz & 1) << 2);
+            const uint32_t b_tx = 2u * (uint32_t)((P.T + 2) * P.N) * 128u;
+            for (int gi = 0; gi < 72; ++gi) {
+                const int4 G = P.groups[pi * 72 + gi];
+                const int mask = G.x & 7;
+                if (!mask) continue;
+                const int dx = ((G.x >> 4) & 3) - 1, dz = ((G.x >> 6) & 3) - 1, pis = (G.x >> 8) & 7;
+                const int c1 = 3 * (2 + P.bx0 + gtx * P.XT + dx);
+                const int c2 = 1 + gpy0, c3 = 2 + gpz + dz;
                 for (int kc = 0; kc < tc_nkc<F16>(); ++kc) {
-                    mbar_wait(&a_empty[sa], pa ^ 1);
-                    mbar_expect_tx(&a_full[sa], 2u * A_BYTES);  // hi from rank 0, lo from rank 1
-                    if (crank == 0)
-                        tma_load_3d_mc(Abuf + (sa * 2 + 0) * A_BYTES, &tmA_hi, &a_full[sa], kc * tc_ke<F16>(), 0,
-                                       slot, (uint16_t)3);
-                    else
-                        tma_load_3d_mc(Abuf + (sa * 2 + 1) * A_BYTES, &tmA_lo, &a_full[sa], kc * tc_ke<F16>(), 0,
-                                       slot, (uint16_t)3);
-                    if (++sa == TC_AST) {
-                        sa = 0;
-                        pa ^= 1;
-                    }
-                    // both rows' slabs stacked in one stage: rows [t N, (t+1) N) of the B operand
                     mbar_wait(&b_empty[sb], pb ^ 1);
-                    mbar_expect_tx(&b_full[sb], (uint32_t)P.T * b_tx);
-                    for (int t = 0; t < P.T; ++t) {
-                        const int c1 = 3 * (2 + P.bx0 + gtx * P.XT + dx);
-                        const int c2 = 2 + gpy0 + t + dy, c3 = 2 + gpz + dz;
-                        uint8_t* bh = Bbuf + (sb * 2 + 0) * B_BYTES + t * P.N * 128;
-                        uint8_t* bl = Bbuf + (sb * 2 + 1) * B_BYTES + t * P.N * 128;
-                        tma_load_5d(bh, &tmB_hi, &b_full[sb], kc * tc_ke<F16>(), c1, c2, c3, pis);
-                        tma_load_5d(bl, &tmB_lo, &b_full[sb], kc * tc_ke<F16>(), c1, c2, c3, pis);
-                    }
+                    mbar_expect_tx(&b_full[sb], b_tx);
+                    tma_load_5d(Bbuf + (sb * 2 + 0) * B_BYTES, &tmB_hi, &b_full[sb], kc * tc_ke<F16>(),
+                                c1, c2, c3, pis);
+                    tma_load_5d(Bbuf + (sb * 2 + 1) * B_BYTES, &tmB_lo, &b_full[sb], kc * tc_ke<F16>(),
+                                c1, c2, c3, pis);
                     if (++sb == TC_BST) {
                         sb = 0;
                         pb ^= 1;
+                    }
+#pragma unroll
+                    for (int d = 0; d < 3; ++d) {
+                        if (!((mask >> d) & 1)) continue;
+                        const int slot = d == 0 ? G.y : (d == 1 ? G.z : G.w);
+                        mbar_wait(&a_empty[sa], pa ^ 1);
+                        mbar_expect_tx(&a_full[sa], 2u * A_BYTES);  // hi from rank 0, lo from rank 1
+                        if (crank == 0)
+                            tma_load_3d_mc(Abuf + (sa * 2 + 0) * A_BYTES, &tmA_hi, &a_full[sa],
+                                           kc * tc_ke<F16>(), 0, slot, (uint16_t)3);
+                        else
+                            tma_load_3d_mc(Abuf + (sa * 2 + 1) * A_BYTES, &tmA_lo, &a_full[sa],
+                                           kc * tc_ke<F16>(), 0, slot, (uint16_t)3);
+                        if (++sa == TC_AST) {
+                            sa = 0;
+                            pa ^= 1;
+                        }
                     }
                 }
             }
@@ -316,60 +323,71 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     } else if (warp == 1) {
         // ===================== MMA issuer =====================
         // instruction descriptor: D f32, A/B tf32 (2) or f16 (0), both K-major, N, M = 128
-        // one MMA covers all T rows: N' = T N columns (tile t at columns [t N, (t+1) N))
+        // one MMA covers all T rows: N' = T N columns (tile t at columns [t N, (t+1) N)); the
+        // B operand of offset dy starts (dy + 1) N rows into the y-window.  One TMEM
+        // accumulation chain per group (<= 3 offsets x K x 3 products), then flushed to FP32
         const uint32_t ab_fmt = F16 ? 0u : 2u;
         const uint32_t idesc = (1u << 4) | (ab_fmt << 7) | (ab_fmt << 10) |
                                ((uint32_t)((P.T * P.N) >> 3) << 17) | ((uint32_t)(128 >> 4) << 24);
+        const uint64_t slab_step = (uint64_t)((P.N * 128) >> 4);  // descriptor units (16 B)
         int sa = 0, sb = 0;
         uint32_t pa = 0, pb = 0;
-        for (int grp = 0; grp < ngroups; ++grp) {
+        int grp = 0;
+        for (int gi = 0; gi < 72; ++gi) {
+            const int mask = P.groups[pi * 72 + gi].x & 7;
+            if (!mask) continue;
             const int buf = grp & 1;
             mbar_wait(&acc_empty[buf], ((grp >> 1) & 1) ^ 1);  // epilogue drained this buffer
             tc_fence_after();
-            const int o_end = min(189, (grp + 1) * TC_G);
-            for (int oi = grp * TC_G; oi < o_end; ++oi) {
-                for (int kc = 0; kc < tc_nkc<F16>(); ++kc) {
+            const uint32_t d = tmem + (uint32_t)(buf * 256);
+            bool first = true;
+            for (int kc = 0; kc < tc_nkc<F16>(); ++kc) {
+                mbar_wait(&b_full[sb], pb);
+                tc_fence_after();
+                const uint64_t bhi = sw128_desc(Bbuf + (sb * 2 + 0) * B_BYTES);
+                const uint64_t blo = sw128_desc(Bbuf + (sb * 2 + 1) * B_BYTES);
+#pragma unroll
+                for (int dd = 0; dd < 3; ++dd) {
+                    if (!((mask >> dd) & 1)) continue;
                     mbar_wait(&a_full[sa], pa);
                     tc_fence_after();
                     const uint64_t ahi = sw128_desc(Abuf + (sa * 2 + 0) * A_BYTES);
                     const uint64_t alo = sw128_desc(Abuf + (sa * 2 + 1) * A_BYTES);
-                    mbar_wait(&b_full[sb], pb);
-                    tc_fence_after();
-                    const uint64_t bhi = sw128_desc(Bbuf + (sb * 2 + 0) * B_BYTES);
-                    const uint64_t blo = sw128_desc(Bbuf + (sb * 2 + 1) * B_BYTES);
-                    const uint32_t d = tmem + (uint32_t)(buf * 256);
+                    const uint64_t bsh = (uint64_t)dd * slab_step;
                     if (lane == 0) {
 #pragma unroll
                         for (int ks = 0; ks < 4; ++ks) {  // K = 8 tf32 / 16 f16 = 32 B per MMA
                             const uint64_t adv = (uint64_t)(ks * 2);
-                            const uint32_t acc = (oi != grp * TC_G || kc != 0 || ks != 0) ? 1u : 0u;
+                            const uint32_t acc = (first && ks == 0) ? 0u : 1u;
                             if (F16) {
-                                mma_f16(d, ahi + adv, bhi + adv, idesc, acc);
-                                mma_f16(d, ahi + adv, blo + adv, idesc, 1u);
-                                mma_f16(d, alo + adv, bhi + adv, idesc, 1u);
+                                mma_f16(d, ahi + adv, bhi + bsh + adv, idesc, acc);
+                                mma_f16(d, ahi + adv, blo + bsh + adv, idesc, 1u);
+                                mma_f16(d, alo + adv, bhi + bsh + adv, idesc, 1u);
                             } else {
-                                mma_tf32(d, ahi + adv, bhi + adv, idesc, acc);
-                                mma_tf32(d, ahi + adv, blo + adv, idesc, 1u);
-                                mma_tf32(d, alo + adv, bhi + adv, idesc, 1u);
+                                mma_tf32(d, ahi + adv, bhi + bsh + adv, idesc, acc);
+                                mma_tf32(d, ahi + adv, blo + bsh + adv, idesc, 1u);
+                                mma_tf32(d, alo + adv, bhi + bsh + adv, idesc, 1u);
                             }
                         }
-                        mma_commit(&b_empty[sb]);
+                        mma_commit_mc(&a_empty[sa], (uint16_t)3);  // release in both CTAs
                     }
                     __syncwarp();
-                    if (++sb == TC_BST) {
-                        sb = 0;
-                        pb ^= 1;
-                    }
-                    if (lane == 0) mma_commit_mc(&a_empty[sa], (uint16_t)3);  // release in both CTAs
-                    __syncwarp();
+                    first = false;
                     if (++sa == TC_AST) {
                         sa = 0;
                         pa ^= 1;
                     }
                 }
+                if (lane == 0) mma_commit(&b_empty[sb]);
+                __syncwarp();
+                if (++sb == TC_BST) {
+                    sb = 0;
+                    pb ^= 1;
+                }
             }
             if (lane == 0) mma_commit(&acc_full[buf]);
             __syncwarp();
+            ++grp;
         }
     } else {
         // ===================== epilogue: TMEM groups -> FP32 register sums -> L =====================
@@ -382,6 +400,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         float acc[96];
 #pragma unroll
         for (int j = 0; j < 96; ++j) acc[j] = 0.f;
+        int ngroups = 0;
+        for (int gi = 0; gi < 72; ++gi) ngroups += (P.groups[pi * 72 + gi].x & 7) != 0;
         for (int grp = 0; grp < ngroups; ++grp) {
             const int buf = grp & 1;
             mbar_wait(&acc_full[buf], (grp >> 1) & 1);
@@ -542,14 +562,16 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 // rows per CTA for a box: the largest T in {8, 4, 2} with T N <= 192, T | bny and an even
 // number of CTAs (2-CTA clusters); 0 if none
+static int pick_XT(const int box[6]) { return box[3] < 16 ? box[3] : 16; }
 static int pick_T(const int box[6]) {
     const int bnx = box[3], bny = box[4], bnz = box[5];
-    const int XT = bnx < 32 ? bnx : 32;
+    const int XT = pick_XT(box);
     if (bnx % XT != 0) return 0;
     const int N = (3 * XT + 15) / 16 * 16;
     const int rows = bny * bnz * (bnx / XT);
     for (int T = 8; T >= 2; T /= 2)
-        if (T * N <= 192 && bny % T == 0 && (rows / T) % 2 == 0) return T;
+        if (T * N <= 192 && (T + 2) * N <= B_WROWS && bny % T == 0 && (rows / T) % 2 == 0)
+            return T;
     return 0;
 }
 
@@ -611,15 +633,17 @@ int launch_m2l_tc(const TcOps& ops, const int* il_slots, int p, const float* M_l
     }
     // owned box of target parents: origin box[0..2], extents box[3..5] (whole level: 0, nP)
     const int bnx = box[3], bny = box[4], bnz = box[5];
-    const int XT = bnx < 32 ? bnx : 32;
+    const int XT = pick_XT(box);
     const int NV = 3 * XT;
+    const int T = pick_T(box);
+    if (T == 0) return -4;
     const int N = (NV + 15) / 16 * 16;  // MMA N (multiple of 16 for M = 128)
     {
         cuuint64_t dims[5] = {128, (cuuint64_t)3 * Xp, (cuuint64_t)Xp, (cuuint64_t)Xp, 8};
         cuuint64_t strides[4] = {128 * esz, (cuuint64_t)3 * Xp * 128 * esz,
                                  (cuuint64_t)Xp * 3 * Xp * 128 * esz,
                                  (cuuint64_t)Xp * Xp * 3 * Xp * 128 * esz};
-        cuuint32_t bx[5] = {ke, (cuuint32_t)N, 1, 1, 1};
+        cuuint32_t bx[5] = {ke, (cuuint32_t)N, (cuuint32_t)(T + 2), 1, 1};  // y-window
         cuuint32_t es[5] = {1, 1, 1, 1, 1};
         if (enc(&mBh, dt, 5, (void*)ghi, dims, strides, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                 CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
@@ -655,8 +679,8 @@ int launch_m2l_tc(const TcOps& ops, const int* il_slots, int p, const float* M_l
     P.L = L_l;
     P.rs = ops.rs;
     P.maxbits = maxbits;
-    P.T = pick_T(box);
-    if (P.T == 0) return -4;
+    P.T = T;
+    P.groups = ops.groups;
     const unsigned grid = (unsigned)(8 * (P.rows / P.T));
     if (f16)
         m2l_tc_kernel<true><<<grid, TC_THREADS, TC_SMEM, st>>>(mAh, mAl, mBh, mBl, P);

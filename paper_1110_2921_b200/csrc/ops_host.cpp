@@ -278,6 +278,35 @@ void store_t(std::vector<float>& dst, int slot, const std::vector<double>& A, in
 
 }  // namespace
 
+std::vector<int> m2l_groups() {
+    std::vector<int> g((size_t)8 * 72 * 4, 0);
+    for (int pi = 0; pi < 8; ++pi) {
+        for (int i = 0; i < 72; ++i) {
+            int* e = &g[((size_t)pi * 72 + i) * 4];
+            const int dx = i / 24 - 1, dz = (i / 8) % 3 - 1, pis = i % 8;
+            e[0] = ((dx + 1) << 4) | ((dz + 1) << 6) | (pis << 8);
+            e[1] = e[2] = e[3] = -1;
+        }
+        const int bx = pi & 1, by = (pi >> 1) & 1, bz = (pi >> 2) & 1;
+        int cnt = 0;
+        for (int ox = -2 - bx; ox <= 3 - bx; ++ox)
+            for (int oy = -2 - by; oy <= 3 - by; ++oy)
+                for (int oz = -2 - bz; oz <= 3 - bz; ++oz) {
+                    if (std::abs(ox) <= 1 && std::abs(oy) <= 1 && std::abs(oz) <= 1) continue;
+                    const int sx = bx + ox, sy = by + oy, sz = bz + oz;  // source child coords
+                    const int dx = sx >> 1, dy = sy >> 1, dz = sz >> 1;   // floor division
+                    const int pis = (sx & 1) | ((sy & 1) << 1) | ((sz & 1) << 2);
+                    const int i = ((dx + 1) * 3 + (dz + 1)) * 8 + pis;
+                    int* e = &g[((size_t)pi * 72 + i) * 4];
+                    e[0] |= 1 << (dy + 1);
+                    e[1 + dy + 1] = m2l_slot(ox, oy, oz);
+                    ++cnt;
+                }
+        (void)cnt;  // 189 per parity (checked with the slot table in capi.cu)
+    }
+    return g;
+}
+
 void build_host_ops(int p, int image_levels, HostOps* out) {
     const int nc = (p + 1) * (p + 1);
     out->p = p;

@@ -99,8 +99,13 @@ struct TcOps {
     const void* lo = nullptr;  // remainders
     const float* rs = nullptr; // f16: row scales [128]
     const float* cs = nullptr; // f16: column scales [128]
+    const int4* groups = nullptr;  // [8][72] offset groups per target parity (m2l_groups)
     bool f16 = false;
 };
+// The 189 M2L offsets of target parity pi grouped by (source parent dx, dz, source parity):
+// entry [pi][((dx+1) 3 + (dz+1)) 8 + pis] = {mask (bit dy+1 set if offset (dx, dy, dz, pis) is
+// in the list) | (dx+1) << 4 | (dz+1) << 6 | pis << 8, slot(dy=-1), slot(0), slot(1)}
+std::vector<int> m2l_groups();
 bool m2l_tc_supported(int p, int level);
 bool m2l_tc_shape_ok(const int box[6]);
 size_t m2l_tc_grid_floats(int level);
