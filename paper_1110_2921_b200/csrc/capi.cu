@@ -38,6 +38,10 @@ struct vfmm_ctx {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int* d_slots = nullptr;  // [8][189]
     int* d_groups = nullptr; // [8][72][4] offset groups (tensor-core M2L y-windows)
+    float* m2m_scratch = nullptr;  // coarse-level M2M op-split partials (8 x 1024 x 3 nc)
+    size_t m2m_scratch_floats = 0;
+    int *d_l2p_rowptr = nullptr, *d_l2p_src = nullptr;  // L2P derivative map (CSR)
+    float* d_l2p_coef = nullptr;
     // workspace
     int64_t cap_n = 0;
     int cap_depth = -1, cap_p = -1;
@@ -77,6 +81,14 @@ int m2l_env_mode() {
     if (e && strcmp(e, "simt") == 0) return 0;
     if (e && strcmp(e, "tf32") == 0) return 1;
     return 2;
+}
+
+L2PMap l2p_map(const vfmm_ctx* c) {
+    L2PMap m;
+    m.rowptr = c->d_l2p_rowptr;
+    m.src = c->d_l2p_src;
+    m.coef = c->d_l2p_coef;
+    return m;
 }
 
 TcOps tc_ops(const vfmm_ctx* c) {
@@ -152,6 +164,23 @@ vfmm_status ensure_ops(vfmm_ctx* c) {
     CK(up(c->hops.l2l, &c->d_l2l), "upload l2l");
     CK(up(c->hops.m2l, &c->d_m2l), "upload m2l");
     CK(up(c->hops.per, &c->d_per), "upload periodic");
+    dfree(c->d_l2p_rowptr);
+    dfree(c->d_l2p_src);
+    dfree(c->d_l2p_coef);
+    dfree(c->m2m_scratch);
+    c->m2m_scratch_floats = (size_t)8 * 1024 * 3 * c->hops.nc;
+    CK(cudaMalloc((void**)&c->m2m_scratch, c->m2m_scratch_floats * sizeof(float)),
+       "alloc m2m scratch");
+    {
+        auto upi = [&](const std::vector<int>& h, int** d) -> cudaError_t {
+            cudaError_t e = cudaMalloc((void**)d, std::max<size_t>(h.size(), 1) * sizeof(int));
+            if (e != cudaSuccess || h.empty()) return e;
+            return cudaMemcpy(*d, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice);
+        };
+        CK(upi(c->hops.l2p_rowptr, &c->d_l2p_rowptr), "upload l2p map");
+        CK(upi(c->hops.l2p_src, &c->d_l2p_src), "upload l2p map");
+        CK(up(c->hops.l2p_coef, &c->d_l2p_coef), "upload l2p map");
+    }
     dfree(c->d_tc_hi);
     dfree(c->d_tc_lo);
     dfree(c->d_h16_hi);
@@ -249,6 +278,9 @@ DistShared make_shared(vfmm_ctx* c, int R) {
     D.m2l = c->d_m2l;
     D.per = c->d_per;
     D.tc = tc_ops(c);
+    D.l2p = l2p_map(c);
+    D.m2m_scratch = c->m2m_scratch;
+    D.m2m_scratch_floats = c->m2m_scratch_floats;
     D.slots = c->d_slots;
     D.KP = c->hops.KP;
     D.NR = c->hops.NR;
@@ -559,9 +591,8 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
     CK(cudaEventRecord(c->ev[4], st), "event");
     if (use_far) {
         for (int l = depth - 1; l >= 0; --l) {
-            launch_m2m(c->d_m2m, p, H.KP, H.NR, Mlev(l + 1), Mlev(l), l, 0, (int64_t)1 << (3 * l),
-                       st);
-            ++nl;
+            nl += launch_m2m(c->d_m2m, p, H.KP, H.NR, Mlev(l + 1), Mlev(l), l, 0,
+                             (int64_t)1 << (3 * l), c->m2m_scratch, c->m2m_scratch_floats, st);
             S.n_m2m += (int64_t)8 << (3 * l);
         }
         CK(cudaGetLastError(), "upward kernels");
@@ -641,7 +672,7 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
         CK(cudaGetLastError(), "p2p kernel");
     }
     CK(cudaEventRecord(c->ev[8], st), "event");
-    launch_l2p_combine(c->sorted6, c->near6, c->perm, n, c->leaf_start, p, a, Llev(depth),
+    launch_l2p_combine(l2p_map(c), c->sorted6, c->near6, c->perm, n, c->leaf_start, p, a, Llev(depth),
                        P.scheme, use_near, use_far, vel, dgamma, 0, (int64_t)1 << (3 * depth), 0, n,
                        st);
     ++nl;
@@ -763,6 +794,10 @@ void vfmm_destroy(vfmm_ctx* c) {
     dfree(c->d_per);
     dfree(c->d_slots);
     dfree(c->d_groups);
+    dfree(c->d_l2p_rowptr);
+    dfree(c->d_l2p_src);
+    dfree(c->d_l2p_coef);
+    dfree(c->m2m_scratch);
     dfree(c->d_tc_hi);
     dfree(c->d_tc_lo);
     dfree(c->d_h16_hi);

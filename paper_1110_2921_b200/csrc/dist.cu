@@ -476,7 +476,7 @@ vfmm_status dist_phase3(RankState& S, const DistShared& D, cudaStream_t st, std:
                owned_cnt(L, R), st);
     for (int l = L - 1; l >= 1; --l)
         launch_m2m(D.m2m, p, D.KP, D.NR, Mlev(l + 1), Mlev(l), l, owned_lo(l, R, r),
-                   owned_cnt(l, R), st);
+                   owned_cnt(l, R), D.m2m_scratch, D.m2m_scratch_floats, st);
     // ---- pack LET multipoles (levels 2..L) per peer ----
     std::vector<int> cells;
     S.m_send_off.assign(R, 0);
@@ -553,7 +553,8 @@ vfmm_status dist_phase4(RankState& S, const DistShared& D, cudaStream_t st, std:
             boff += (int64_t)cnt * cellsz;
         }
     // root multipole (every rank, from the all-gathered level 1)
-    launch_m2m(D.m2m, p, D.KP, D.NR, Mlev(1), Mlev(0), 0, 0, 1, st);
+    launch_m2m(D.m2m, p, D.KP, D.NR, Mlev(1), Mlev(0), 0, 0, 1, D.m2m_scratch,
+               D.m2m_scratch_floats, st);
     // M2L for owned targets (level 1: all 8 cells -- sources are global there)
     for (int l = 1; l <= L; ++l) {
         const int64_t plo = l == 1 ? 0 : owned_lo(l - 1, R, r);
@@ -611,7 +612,7 @@ vfmm_status dist_phase4(RankState& S, const DistShared& D, cudaStream_t st, std:
         launch_p2p(S.sorted6, S.n_total, S.gstart, L, a, periodic, P.scheme, kc, S.near6, S.d_pairs,
                    owned_lo(L - 1, R, r), owned_cnt(L - 1, R), st);
     if (S.n_local > 0)
-        launch_l2p_combine(S.sorted6, S.near6, S.perm, S.n_total, S.gstart, p, a, Llev(L), P.scheme,
+        launch_l2p_combine(D.l2p, S.sorted6, S.near6, S.perm, S.n_total, S.gstart, p, a, Llev(L), P.scheme,
                            use_near, use_far, S.vel, S.dg, owned_lo(L, R, r), owned_cnt(L, R),
                            S.gbase, S.n_local, st);
     DCK(cudaGetLastError(), "phase4 kernels");

@@ -77,6 +77,9 @@ struct DistShared {
     int depth = 0, R = 1;
     const float *m2m = nullptr, *l2l = nullptr, *m2l = nullptr, *per = nullptr;
     TcOps tc;  // tensor-core M2L operators (3xTF32 or 3xFP16)
+    L2PMap l2p;  // L2P derivative map
+    float* m2m_scratch = nullptr;  // coarse-level M2M op-split partials (used on the stream of
+    size_t m2m_scratch_floats = 0; // the phase; logical ranks run their phases in sequence)
     const int* slots = nullptr;
     int KP = 0, NR = 0;
     bool allow_tc = true;

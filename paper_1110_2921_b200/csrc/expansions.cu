@@ -194,7 +194,7 @@ template <int KIND>
 __global__ void __launch_bounds__(256, 2) translate_kernel(
     const float* __restrict__ mats, const int* __restrict__ slots, int p, int KP, int NR,
     const float* __restrict__ src, float* __restrict__ dst, int level, int periodic, int64_t plo,
-    int64_t pcnt, int opsplit) {
+    int64_t pcnt, int opsplit, float* __restrict__ zpart = nullptr, int64_t zstride = 0) {
     extern __shared__ float4 dsm4[];
     float (*As)[KC][TROWS] = reinterpret_cast<float (*)[KC][TROWS]>(dsm4);
     float (*Bs)[KC][BSTR] = reinterpret_cast<float (*)[KC][BSTR]>(
@@ -344,12 +344,15 @@ __global__ void __launch_bounds__(256, 2) translate_kernel(
     for (int col = warp; col < TCOLS; col += 8) {
         const int cell = col / 3, comp = col - cell * 3;
         if (cell >= ncell_tile) continue;
-        float* out = dst + (target_cell(cell) * 3 + comp) * nc;
+        // zpart: the op split writes per-slice partials (summed in a fixed order afterwards)
+        float* out = zpart ? zpart + blockIdx.z * zstride + ((target_cell(cell) - plo) * 3 + comp) * nc
+                           : dst + (target_cell(cell) * 3 + comp) * nc;
         for (int rr = lane; rr < TROWS; rr += 32) {
             const int r = row0 + rr;
             if (r >= nc) continue;
             const float v = Cs[col * 129 + rr];
-            if (opsplit > 1) atomicAdd(out + r, v);
+            if (zpart) out[r] = v;
+            else if (opsplit > 1) atomicAdd(out + r, v);
             else if (KIND == OP_L2L) out[r] += v;  // L2L accumulates onto M2L
             else out[r] = v;
         }
@@ -376,44 +379,6 @@ __global__ void periodic_kernel(const float* __restrict__ P, int KP, int NR, int
 // Derivative expansions (DESIGN.md): d_z D[n,m] = L[n+1,m],
 //   d_x D[n,m] = (-L[n+1,m+1] + L[n+1,m-1])/2,  d_y D[n,m] = -i (L[n+1,m+1] + L[n+1,m-1])/2
 // ---------------------------------------------------------------------------
-struct cf {
-    float re, im;
-};
-__device__ __forceinline__ cf getc(const float* L, int n, int m) {
-    // complex coefficient (n, m) of a packed real expansion, any |m| <= n; 0 outside
-    if (m > n || -m > n || n < 0) return {0.f, 0.f};
-    if (m == 0) return {L[pk_re(n, 0)], 0.f};
-    const int am = m < 0 ? -m : m;
-    cf v{L[pk_re(n, am)], L[pk_im(n, am)]};
-    if (m < 0) {  // (-1)^m conj
-        v.im = -v.im;
-        if (am & 1) {
-            v.re = -v.re;
-            v.im = -v.im;
-        }
-    }
-    return v;
-}
-// derivative of expansion `in` (degree <= pin) along axis -> `out` (degree pin-1), packed
-__device__ void deriv_expansion(const float* in, int pin, int axis, float* out, int tid, int nthr) {
-    const int ncout = pin * pin;
-    for (int k = tid; k < ncout; k += nthr) {
-        const int n = (int)sqrtf((float)k + 0.5f);
-        const int j = k - n * n;
-        const int m = (j + 1) >> 1;
-        const bool isim = j > 0 && (j & 1) == 0;
-        cf v;
-        if (axis == 2) {
-            v = getc(in, n + 1, m);
-        } else {
-            const cf up = getc(in, n + 1, m + 1), dn = getc(in, n + 1, m - 1);
-            if (axis == 0) v = {0.5f * (dn.re - up.re), 0.5f * (dn.im - up.im)};
-            else v = {0.5f * (up.im + dn.im), -0.5f * (up.re + dn.re)};  // -i/2 (up + dn)
-        }
-        out[k] = isim ? v.im : v.re;
-    }
-}
-
 // PC > 0: the order p is a compile-time constant (loops fully unrolled: immediate shared-memory
 // offsets and recurrence constants); PC = 0: runtime p
 template <int SCHEME, int PC>
@@ -422,20 +387,22 @@ __global__ void __launch_bounds__(64) l2p_combine_kernel(
     const uint32_t* __restrict__ perm, int64_t n, const int* __restrict__ leaf_start, int p_rt,
     float inv_a, const float* __restrict__ Lleaf, int use_near, int use_far,
     float* __restrict__ vel, float* __restrict__ dgam, int64_t leaf_lo, int64_t gbase,
-    int64_t nout) {
+    int64_t nout, const int* __restrict__ map_rowptr, const int* __restrict__ map_src,
+    const float* __restrict__ map_coef) {
     const int p = PC > 0 ? PC : p_rt;
-    // smem: D [ng][12]; Ls [3][nc]; G [9][ng]; H [18][nh].  The 12 columns of D are the
-    // combinations the output needs: u = curl phi (3) and J[a][k] = d_k u_a (9), each a
-    // difference of two derivative expansions of phi_c (so 12 accumulators per particle)
+    // smem: D [ng][12]; Ls [3][nc].  The 12 columns of D are the combinations the output
+    // needs: u = curl phi (3) and J[a][k] = d_k u_a (9), each a difference of two derivative
+    // expansions of phi_c (so 12 accumulators per particle).  D is a fixed sparse linear map
+    // of the leaf's L (host-built CSR, ops_host.cpp build_l2p_map: the derivative rules of
+    // derivative rules -- complex (n, m) -> (n+1, m +- 1) stencils -- replayed symbolically),
+    // evaluated here per leaf.
     constexpr int DQ = 12;
     extern __shared__ float4 l2p_sm4[];
     float* sm = reinterpret_cast<float*>(l2p_sm4);
     const int nc = (p + 1) * (p + 1);
-    const int ng = p * p, nh = (p - 1) * (p - 1);
+    const int ng = p * p;
     const float4* D4 = l2p_sm4;
     float* Ls = sm + ng * DQ;
-    float* G = Ls + 3 * nc;
-    float* H = G + 9 * ng;
     const int64_t leaf = leaf_lo + blockIdx.x;
     const int s = leaf_start[leaf], e = leaf_start[leaf + 1];
     if (e == s) return;
@@ -443,37 +410,11 @@ __global__ void __launch_bounds__(64) l2p_combine_kernel(
     if (use_far) {
         for (int i = threadIdx.x; i < 3 * nc; i += 64) Ls[i] = Lleaf[leaf * 3 * nc + i];
         __syncthreads();
-        for (int c = 0; c < 3; ++c)
-            for (int ax = 0; ax < 3; ++ax)
-                deriv_expansion(Ls + c * nc, p, ax, G + (c * 3 + ax) * ng, threadIdx.x, 64);
-        __syncthreads();
-        if (p >= 2) {
-            const int pa[6] = {0, 0, 0, 1, 1, 2}, pb[6] = {0, 1, 2, 1, 2, 2};
-            for (int c = 0; c < 3; ++c)
-                for (int q = 0; q < 6; ++q)
-                    deriv_expansion(G + (c * 3 + pb[q]) * ng, p - 1, pa[q], H + (c * 6 + q) * nh,
-                                    threadIdx.x, 64);
-        }
-        __syncthreads();
-        // D[k][q]: q < 3: u_q = (curl phi)_q; q = 3 + 3a + kk: J[a][kk] = d_kk u_a (0 beyond nh)
-        auto gi_ = [&](int c, int ax, int k) { return G[(c * 3 + ax) * ng + k]; };
-        auto hi_ = [&](int c, int a1, int b1, int k) {
-            const int lo = a1 < b1 ? a1 : b1, hi = a1 < b1 ? b1 : a1;
-            const int q = lo == 0 ? hi : (lo == 1 ? 2 + hi : 5);
-            return k < nh ? H[(c * 6 + q) * nh + k] : 0.f;
-        };
         for (int i = threadIdx.x; i < ng * DQ; i += 64) {
-            const int k = i / DQ, q = i - k * DQ;
-            float v;
-            if (q == 0) v = gi_(2, 1, k) - gi_(1, 2, k);
-            else if (q == 1) v = gi_(0, 2, k) - gi_(2, 0, k);
-            else if (q == 2) v = gi_(1, 0, k) - gi_(0, 1, k);
-            else {
-                const int a1 = (q - 3) / 3, kk = (q - 3) % 3;
-                if (a1 == 0) v = hi_(2, kk, 1, k) - hi_(1, kk, 2, k);
-                else if (a1 == 1) v = hi_(0, kk, 2, k) - hi_(2, kk, 0, k);
-                else v = hi_(1, kk, 0, k) - hi_(0, kk, 1, k);
-            }
+            float v = 0.f;
+            const int t1 = __ldg(map_rowptr + i + 1);
+            for (int t = __ldg(map_rowptr + i); t < t1; ++t)
+                v = fmaf(__ldg(map_coef + t), Ls[__ldg(map_src + t)], v);
             sm[i] = v;
         }
         __syncthreads();
@@ -584,6 +525,17 @@ __global__ void __launch_bounds__(64) l2p_combine_kernel(
     }
 }
 
+// out[i] = sum_{z < nz} part[z * stride + i], in z order (deterministic op-split reduction)
+__global__ void zsum_kernel(const float* __restrict__ part, int64_t stride, int nz,
+                            float* __restrict__ out, int64_t count) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        float v = 0.f;
+        for (int z = 0; z < nz; ++z) v += part[z * stride + i];
+        out[i] = v;
+    }
+}
+
 void translate_attrs() {
     static bool done = false;
     if (done) return;
@@ -625,13 +577,30 @@ void launch_p2m(const float* sorted6, int64_t n, const int* leaf_start, int p, f
     }
 }
 
-void launch_m2m(const float* ops_m2m, int p, int KP, int NR, const float* M_child, float* M_par,
-                int level_par, int64_t plo, int64_t pcnt, cudaStream_t st) {
-    if (pcnt <= 0) return;
-    dim3 grid((unsigned)((pcnt + TCELLS - 1) / TCELLS), NR / TROWS);
+int launch_m2m(const float* ops_m2m, int p, int KP, int NR, const float* M_child, float* M_par,
+               int level_par, int64_t plo, int64_t pcnt, float* scratch, size_t scratch_floats,
+               cudaStream_t st) {
+    if (pcnt <= 0) return 0;
+    const int nc = (p + 1) * (p + 1);
+    const int64_t tiles = (pcnt + TCELLS - 1) / TCELLS;
+    const int64_t zstride = pcnt * 3 * nc;
     translate_attrs();
+    if (tiles < 32 && scratch && (size_t)(8 * zstride) <= scratch_floats) {
+        // coarse levels: one block per child octant (8 x the parallelism of the serial
+        // 8-child chain), partials summed in child order by zsum_kernel (deterministic)
+        dim3 grid((unsigned)tiles, NR / TROWS, 8);
+        translate_kernel<OP_M2M><<<grid, 256, TRANSLATE_SMEM, st>>>(
+            ops_m2m, nullptr, p, KP, NR, M_child, M_par, level_par, 0, plo, pcnt, 8, scratch,
+            zstride);
+        const int64_t blocks = std::min<int64_t>((zstride + 255) / 256, 148 * 8);
+        zsum_kernel<<<(unsigned)blocks, 256, 0, st>>>(scratch, zstride, 8, M_par + plo * 3 * nc,
+                                                      zstride);
+        return 2;
+    }
+    dim3 grid((unsigned)tiles, NR / TROWS);
     translate_kernel<OP_M2M><<<grid, 256, TRANSLATE_SMEM, st>>>(ops_m2m, nullptr, p, KP, NR, M_child,
                                                                 M_par, level_par, 0, plo, pcnt, 1);
+    return 1;
 }
 
 void launch_l2l(const float* ops_l2l, int p, int KP, int NR, const float* L_par, float* L_child,
@@ -667,13 +636,13 @@ void launch_periodic(const float* ops_per, int p, int KP, int NR, const float* M
     periodic_kernel<<<1, 256, 0, st>>>(ops_per, KP, NR, (p + 1) * (p + 1), M0, L0);
 }
 
-void launch_l2p_combine(const float* sorted6, const float* near6, const uint32_t* perm,
+void launch_l2p_combine(const L2PMap& map, const float* sorted6, const float* near6, const uint32_t* perm,
                         int64_t n, const int* leaf_start, int p, float a, const float* L_leaf,
                         int scheme, int use_near, int use_far, float* vel, float* dgam,
                         int64_t leaf_lo, int64_t leaf_cnt, int64_t gbase, int64_t nout,
                         cudaStream_t st) {
-    const int nc = (p + 1) * (p + 1), ng = p * p, nh = (p - 1) * (p - 1);
-    const size_t smem = sizeof(float) * (ng * 12 + 3 * nc + 9 * ng + 18 * (nh > 0 ? nh : 1));
+    const int nc = (p + 1) * (p + 1), ng = p * p;
+    const size_t smem = sizeof(float) * (ng * 12 + 3 * nc);
     if (leaf_cnt <= 0) return;
     const float inv_a = 1.f / a;
     static bool attr = false;
@@ -690,7 +659,7 @@ void launch_l2p_combine(const float* sorted6, const float* near6, const uint32_t
     auto go = [&](auto kern) {
         kern<<<(unsigned)leaf_cnt, 64, smem, st>>>(sorted6, near6, perm, n, leaf_start, p, inv_a,
                                                    L_leaf, use_near, use_far, vel, dgam, leaf_lo,
-                                                   gbase, nout);
+                                                   gbase, nout, map.rowptr, map.src, map.coef);
     };
     // compile-time orders for the common p, runtime-p kernel otherwise
 #define L2P_CASE(PV)                                                             \

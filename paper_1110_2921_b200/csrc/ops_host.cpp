@@ -21,6 +21,8 @@
 #include <cmath>
 #include <cstring>
 #include <complex>
+#include <map>
+#include <utility>
 #include <vector>
 
 #include "vfmm_internal.h"
@@ -278,6 +280,100 @@ void store_t(std::vector<float>& dst, int slot, const std::vector<double>& A, in
 
 }  // namespace
 
+// ---- L2P: the 12 derivative combinations of a leaf's local expansion as a sparse map ----
+// Symbolic replay of the device's derivative rules (expansions.cu deriv_expansion / getc):
+// every entry of an expansion is a sparse vector over the 3 nc packed inputs of L.
+namespace {
+using SV = std::vector<std::pair<int, double>>;
+SV sv_axpy(const SV& a, double ca, const SV& b, double cb) {
+    std::map<int, double> m;
+    for (const auto& t : a) m[t.first] += ca * t.second;
+    for (const auto& t : b) m[t.first] += cb * t.second;
+    SV r;
+    for (const auto& t : m)
+        if (t.second != 0.0) r.emplace_back(t.first, t.second);
+    return r;
+}
+struct CSV {
+    SV re, im;
+};
+CSV getc_sym(const std::vector<SV>& E, int n, int m) {
+    if (m > n || -m > n || n < 0) return {};
+    if (m == 0) return {E[pk_re(n, 0)], {}};
+    const int am = m < 0 ? -m : m;
+    CSV v{E[pk_re(n, am)], E[pk_im(n, am)]};
+    if (m < 0) {  // (-1)^m conj
+        v.im = sv_axpy(v.im, -1.0, {}, 0.0);
+        if (am & 1) {
+            v.re = sv_axpy(v.re, -1.0, {}, 0.0);
+            v.im = sv_axpy(v.im, -1.0, {}, 0.0);
+        }
+    }
+    return v;
+}
+std::vector<SV> deriv_sym(const std::vector<SV>& E, int pin, int axis) {
+    std::vector<SV> out((size_t)pin * pin);
+    for (int k = 0; k < pin * pin; ++k) {
+        int n = 0;
+        while ((n + 1) * (n + 1) <= k) ++n;
+        const int j = k - n * n, m = (j + 1) >> 1;
+        const bool isim = j > 0 && (j & 1) == 0;
+        CSV v;
+        if (axis == 2) {
+            v = getc_sym(E, n + 1, m);
+        } else {
+            const CSV up = getc_sym(E, n + 1, m + 1), dn = getc_sym(E, n + 1, m - 1);
+            if (axis == 0) v = {sv_axpy(dn.re, 0.5, up.re, -0.5), sv_axpy(dn.im, 0.5, up.im, -0.5)};
+            else v = {sv_axpy(up.im, 0.5, dn.im, 0.5), sv_axpy(up.re, -0.5, dn.re, -0.5)};
+        }
+        out[k] = isim ? v.im : v.re;
+    }
+    return out;
+}
+}  // namespace
+
+void build_l2p_map(int p, HostOps* out) {
+    const int nc = (p + 1) * (p + 1), ng = p * p, nh = (p - 1) * (p - 1);
+    std::vector<SV> Lc[3];
+    for (int c = 0; c < 3; ++c) {
+        Lc[c].resize(nc);
+        for (int i = 0; i < nc; ++i) Lc[c][i] = {{c * nc + i, 1.0}};
+    }
+    std::vector<SV> G[3][3], H[3][6];
+    const int pa[6] = {0, 0, 0, 1, 1, 2}, pb[6] = {0, 1, 2, 1, 2, 2};
+    for (int c = 0; c < 3; ++c) {
+        for (int ax = 0; ax < 3; ++ax) G[c][ax] = deriv_sym(Lc[c], p, ax);
+        if (p >= 2)
+            for (int q = 0; q < 6; ++q) H[c][q] = deriv_sym(G[c][pb[q]], p - 1, pa[q]);
+    }
+    auto h = [&](int c, int a1, int b1, int k) -> SV {
+        const int lo = a1 < b1 ? a1 : b1, hi = a1 < b1 ? b1 : a1;
+        const int q = lo == 0 ? hi : (lo == 1 ? 2 + hi : 5);
+        return k < nh ? H[c][q][k] : SV{};
+    };
+    out->l2p_rowptr.assign(1, 0);
+    out->l2p_src.clear();
+    out->l2p_coef.clear();
+    for (int k = 0; k < ng; ++k)
+        for (int q = 0; q < 12; ++q) {
+            SV v;
+            if (q == 0) v = sv_axpy(G[2][1][k], 1.0, G[1][2][k], -1.0);
+            else if (q == 1) v = sv_axpy(G[0][2][k], 1.0, G[2][0][k], -1.0);
+            else if (q == 2) v = sv_axpy(G[1][0][k], 1.0, G[0][1][k], -1.0);
+            else {
+                const int a1 = (q - 3) / 3, kk = (q - 3) % 3;
+                if (a1 == 0) v = sv_axpy(h(2, kk, 1, k), 1.0, h(1, kk, 2, k), -1.0);
+                else if (a1 == 1) v = sv_axpy(h(0, kk, 2, k), 1.0, h(2, kk, 0, k), -1.0);
+                else v = sv_axpy(h(1, kk, 0, k), 1.0, h(0, kk, 1, k), -1.0);
+            }
+            for (const auto& t : v) {
+                out->l2p_src.push_back(t.first);
+                out->l2p_coef.push_back((float)t.second);
+            }
+            out->l2p_rowptr.push_back((int)out->l2p_src.size());
+        }
+}
+
 std::vector<int> m2l_groups() {
     std::vector<int> g((size_t)8 * 72 * 4, 0);
     for (int pi = 0; pi < 8; ++pi) {
@@ -341,6 +437,7 @@ void build_host_ops(int p, int image_levels, HostOps* out) {
                 }
             }
     if (tc) store_h16(tc_ops, nc, out);
+    build_l2p_map(p, out);
     out->per_d = build_periodic(p, image_levels);
     store_t(out->per, 0, out->per_d, nc, out->KP, out->NR);
 }

@@ -9,7 +9,7 @@
 //              sdot_i = A_i x gamma_i + B_i                          Eq. (8)
 //   transpose: B_i += q (gamma_i . (gamma_j x d)) d; sdot_i = gamma_i x A_i + B_i
 // rho^2 < 1/4: Taylor series in rho^2 (exact r -> 0 limits, no cancellation);
-// otherwise 1 - g = e^{-rho^2} (erfcx(rho) + 2 rho/sqrt(pi)) with erfcx from a degree-7
+// otherwise 1 - g = e^{-rho^2} (erfcx(rho) + 2 rho/sqrt(pi)) with erfcx from a degree-5
 // polynomial in t = 1/(1 + rho/2) (scripts/fit_cutoff_poly.py): 3 MUFU (rsqrt, ex2, rcp).
 #include <cuda_runtime.h>
 
@@ -18,6 +18,12 @@
 #include "vfmm_internal.h"
 
 namespace vfmm {
+
+// erfcx(rho) / (4 pi) ~= sum_k ERFCX_Ck t^k, t = 1/(1 + rho/2), degree 5
+// (scripts/fit_cutoff_poly.py: relative error of g <= 1.6e-8 over rho in [0.5, 10])
+constexpr float ERFCX_C0 = -1.304099035e-04f, ERFCX_C1 = 2.284340506e-02f,
+                ERFCX_C2 = 2.471552502e-02f, ERFCX_C3 = 5.650036563e-03f,
+                ERFCX_C4 = 4.221915334e-02f, ERFCX_C5 = -1.572556573e-02f;
 
 KernelConsts make_kernel_consts(float sigma) {
     const double s = (double)sigma;
@@ -31,23 +37,12 @@ KernelConsts make_kernel_consts(float sigma) {
     k.r2_series = (float)(0.5 * s * s);
     k.t_scale = (float)(1.0 / (2.0 * std::sqrt(2.0) * s));
     k.q_scale = (float)(2.0 / (4.0 * M_PI * std::sqrt(M_PI)) / (std::sqrt(2.0) * s));
-    // packed path: the degree-7 erfcx/(4 pi) polynomial in (t - 1/2) (coefficients below, as
-    // in fq_closed) re-expanded in powers of t, scaled by -1/zeta0 (folds the zeta0 factor
-    // of the exponential into the ex2 argument and removes the shift and a negation)
-    static const double cp[8] = {2.032374185e-02, 6.798874982e-02,  7.692235843e-02,
-                                 5.027046960e-02, 4.873839158e-03,  -1.861016238e-02,
-                                 -1.664231425e-03, 6.204596458e-03};  // ascending in t - 1/2
-    double ce[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-    for (int j = 0; j < 8; ++j) {  // (t - 1/2)^j = sum_i C(j, i) t^i (-1/2)^(j - i)
-        double binom = 1.0;
-        for (int i = 0; i <= j; ++i) {
-            ce[i] += cp[j] * binom * std::pow(-0.5, j - i);
-            binom = binom * (j - i) / (i + 1);
-        }
-    }
+    // packed path: the erfcx/(4 pi) polynomial (ERFCX_C0..5, ascending in t) scaled by -1/zeta0
+    // (folds the zeta0 factor of the exponential into the ex2 argument and a negation)
     k.ez_off = (float)std::log2(z0);
     k.qn_scale = (float)(-(2.0 / (4.0 * M_PI * std::sqrt(M_PI)) / (std::sqrt(2.0) * s)) / z0);
-    for (int i = 0; i < 8; ++i) k.en[i] = (float)(-ce[i] / z0);
+    const float c[6] = {ERFCX_C0, ERFCX_C1, ERFCX_C2, ERFCX_C3, ERFCX_C4, ERFCX_C5};
+    for (int i = 0; i < 6; ++i) k.en[i] = (float)(-(double)c[i] / z0);
     return k;
 }
 
@@ -130,15 +125,13 @@ __device__ __forceinline__ void fq_closed(float r2, const KernelConsts& kc, floa
     const float rinv = rsqrt_approx(r2);
     const float e = ex2_approx(r2 * kc.neg_l2e_inv2s2);
     const float r = r2 * rinv;
-    const float t = rcp_approx(fmaf(kc.t_scale, r, 1.f)) - 0.5f;
-    float E = 6.204596458e-03f;  // erfcx(rho)/(4 pi), polynomial in t - 1/2
-    E = fmaf(E, t, -1.664231425e-03f);
-    E = fmaf(E, t, -1.861016238e-02f);
-    E = fmaf(E, t, 4.873839158e-03f);
-    E = fmaf(E, t, 5.027046960e-02f);
-    E = fmaf(E, t, 7.692235843e-02f);
-    E = fmaf(E, t, 6.798874982e-02f);
-    E = fmaf(E, t, 2.032374185e-02f);
+    const float t = rcp_approx(fmaf(kc.t_scale, r, 1.f));
+    float E = ERFCX_C5;  // erfcx(rho)/(4 pi), polynomial in t
+    E = fmaf(E, t, ERFCX_C4);
+    E = fmaf(E, t, ERFCX_C3);
+    E = fmaf(E, t, ERFCX_C2);
+    E = fmaf(E, t, ERFCX_C1);
+    E = fmaf(E, t, ERFCX_C0);
     const float Q = fmaf(kc.q_scale, r, E);
     const float g4pi = fmaf(-e, Q, 0.0795774715459476679f);  // g / (4 pi)
     const float rinv2 = rinv * rinv;
@@ -159,9 +152,7 @@ __device__ __forceinline__ void fq_closed2(f2 r2, const KernelConsts& kc, f2& f,
     float da, db;
     upk(fma2(r, bc(kc.t_scale), bc(1.f)), da, db);
     const f2 t = pk(rcp_approx(da), rcp_approx(db));
-    f2 E = fma2(bc(kc.en[7]), t, bc(kc.en[6]));
-    E = fma2(E, t, bc(kc.en[5]));
-    E = fma2(E, t, bc(kc.en[4]));
+    f2 E = fma2(bc(kc.en[5]), t, bc(kc.en[4]));
     E = fma2(E, t, bc(kc.en[3]));
     E = fma2(E, t, bc(kc.en[2]));
     E = fma2(E, t, bc(kc.en[1]));

@@ -41,6 +41,10 @@ struct HostOps {
     // |Ahat| <= 1), IEEE half bit patterns, same layout
     std::vector<uint16_t> m2l_h16_hi, m2l_h16_lo;
     std::vector<float> h16_rs, h16_cs;  // [128] row / column scales
+    // L2P: D[k][q] = sum_t coef[t] L[src[t]] for t in [rowptr[k 12 + q], rowptr[k 12 + q + 1]),
+    // src indexing the 3 nc packed coefficients of a leaf (q: curl psi 3, grad u 9; k < p^2)
+    std::vector<int> l2p_rowptr, l2p_src;
+    std::vector<float> l2p_coef;
 };
 
 // Build all operator tables for order p and image_levels (periodic operator is zero for
@@ -78,8 +82,11 @@ void launch_gather(const float* pos, const float* gamma, const uint32_t* perm,
 // expansions.cu  (ranges: the owned part of the tree; whole tree for one rank)
 void launch_p2m(const float* sorted6, int64_t n, const int* leaf_start, int p, float inv_a,
                 float* M_leaf, int64_t leaf_lo, int64_t leaf_cnt, cudaStream_t st);
-void launch_m2m(const float* ops_m2m, int p, int KP, int NR, const float* M_child, float* M_par,
-                int level_par, int64_t plo, int64_t pcnt, cudaStream_t st);
+// returns the number of kernels launched; scratch (>= 8 x 3 nc x 512 floats) enables the
+// deterministic op split at coarse levels (< 32 tiles)
+int launch_m2m(const float* ops_m2m, int p, int KP, int NR, const float* M_child, float* M_par,
+               int level_par, int64_t plo, int64_t pcnt, float* scratch, size_t scratch_floats,
+               cudaStream_t st);
 void launch_l2l(const float* ops_l2l, int p, int KP, int NR, const float* L_par, float* L_child,
                 int level_child, int64_t plo, int64_t pcnt, cudaStream_t st);
 void launch_m2l(const float* ops_m2l, const int* il_slots, int p, int KP, int NR,
@@ -87,7 +94,12 @@ void launch_m2l(const float* ops_m2l, const int* il_slots, int p, int KP, int NR
                 cudaStream_t st);
 void launch_periodic(const float* ops_per, int p, int KP, int NR, const float* M0, float* L0,
                      cudaStream_t st);
-void launch_l2p_combine(const float* sorted6, const float* near6, const uint32_t* perm,
+struct L2PMap {
+    const int* rowptr = nullptr;
+    const int* src = nullptr;
+    const float* coef = nullptr;
+};
+void launch_l2p_combine(const L2PMap& map, const float* sorted6, const float* near6, const uint32_t* perm,
                         int64_t n, const int* leaf_start, int p, float a, const float* L_leaf,
                         int scheme, int use_near, int use_far, float* vel, float* dgam,
                         int64_t leaf_lo, int64_t leaf_cnt, int64_t gbase, int64_t nout,
@@ -129,7 +141,7 @@ struct KernelConsts {
     // polynomial expanded in powers of t and scaled by -1/zeta0)
     float ez_off;        // log2(zeta0)
     float qn_scale;      // -q_scale / zeta0
-    float en[8];
+    float en[6];
 };
 KernelConsts make_kernel_consts(float sigma);
 void launch_p2p(const float* sorted6, int64_t n, const int* leaf_start, int depth, float a,
