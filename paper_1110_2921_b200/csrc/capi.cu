@@ -466,7 +466,13 @@ vfmm_status vfmm_create(vfmm_ctx** out, const vfmm_params* prm, int device) {
         if (e2 == cudaSuccess) e2 = cudaMalloc((void**)&c->d_pairs, sizeof(unsigned long long));
         if (e2 == cudaSuccess) e2 = cudaMemset(c->d_err, 0, sizeof(int));
         if (e2 == cudaSuccess) e2 = cudaStreamCreateWithFlags(&c->own_stream, cudaStreamNonBlocking);
-        if (e2 == cudaSuccess) e2 = cudaStreamCreateWithFlags(&c->side, cudaStreamNonBlocking);
+        // the side stream (coarse M2L levels, latency-bound chains of few CTAs) gets the
+        // highest priority, so its CTAs take SMs as soon as level-L CTAs retire and the coarse
+        // levels run under the level-L kernel instead of after it
+        int prio_least = 0, prio_greatest = 0;
+        if (e2 == cudaSuccess) e2 = cudaDeviceGetStreamPriorityRange(&prio_least, &prio_greatest);
+        if (e2 == cudaSuccess)
+            e2 = cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_greatest);
         if (e2 == cudaSuccess) e2 = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
         if (e2 == cudaSuccess) e2 = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
         for (int i = 0; i < vfmm_ctx::NEV && e2 == cudaSuccess; ++i) e2 = cudaEventCreate(&c->ev[i]);

@@ -14,6 +14,8 @@
 #include <cuda_runtime.h>
 
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
 
 #include "vfmm_internal.h"
 
@@ -96,6 +98,13 @@ __device__ __forceinline__ f2 fma2(f2 a, f2 b, f2 c) {
 }
 struct Acc2 {
     f2 u0, u1, u2, a0, a1, a2, b0, b1, b2;
+};
+// classical scheme with source cross products s_j = gamma_j x x_j staged per source: with
+// d = x_i - x_j, sum f (gamma_j x d) = A x x_i - V and sum w (gamma_j x d) = Wg x x_i - Ws,
+// so no per-pair cross product is formed (A = sum f gamma_j, V = sum f s_j, Wg = sum w gamma_j,
+// Ws = sum w s_j, w = q (gamma_i . d))
+struct Acc2S {
+    f2 a0, a1, a2, v0, v1, v2, wg0, wg1, wg2, ws0, ws1, ws2;
 };
 
 // f, q by the Taylor series (rho^2 < 1/4, incl. r = 0)
@@ -197,6 +206,24 @@ __device__ __forceinline__ void accumulate2(f2 dx, f2 dy, f2 dz, f2 f, f2 q, flo
     }
 }
 
+__device__ __forceinline__ void accumulate2s(f2 dx, f2 dy, f2 dz, f2 f, f2 q, float gjx,
+                                             float gjy, float gjz, float sjx, float sjy,
+                                             float sjz, f2 gix, f2 giy, f2 giz, Acc2S& acc) {
+    acc.a0 = fma2(f, bc(gjx), acc.a0);
+    acc.a1 = fma2(f, bc(gjy), acc.a1);
+    acc.a2 = fma2(f, bc(gjz), acc.a2);
+    acc.v0 = fma2(f, bc(sjx), acc.v0);
+    acc.v1 = fma2(f, bc(sjy), acc.v1);
+    acc.v2 = fma2(f, bc(sjz), acc.v2);
+    const f2 w = mul2(q, fma2(gix, dx, fma2(giy, dy, mul2(giz, dz))));
+    acc.wg0 = fma2(w, bc(gjx), acc.wg0);
+    acc.wg1 = fma2(w, bc(gjy), acc.wg1);
+    acc.wg2 = fma2(w, bc(gjz), acc.wg2);
+    acc.ws0 = fma2(w, bc(sjx), acc.ws0);
+    acc.ws1 = fma2(w, bc(sjy), acc.ws1);
+    acc.ws2 = fma2(w, bc(sjz), acc.ws2);
+}
+
 template <int SCHEME>
 __device__ __forceinline__ void accumulate(float dx, float dy, float dz, float f, float q,
                                            float gjx, float gjy, float gjz, float gix, float giy,
@@ -275,17 +302,26 @@ __device__ __forceinline__ uint32_t compact3p(uint32_t v) {
 // offsets (reading R8).  If the 64 source leaves exceed the shared-memory capacity they are
 // staged in passes of consecutive region leaves.
 constexpr int P2P_THREADS = 256;
-constexpr int P2P_CAP = 4352;  // sources per pass (104 KB) -> 2 blocks / SM
+// sources per pass at 2 blocks / SM: 24 B per source (x y z gx | gy gz) or, with the staged
+// cross products, 36 B (x y z gx | gy gz sx sy | sz)
+template <bool SJ> constexpr int p2p_cap() { return SJ ? 3072 : 4352; }
 constexpr int P2P_PAD = 4;     // slack after each staged array for the prefetch reads
 
-template <int SCHEME>
+// SJ (classical scheme only): accumulate with the staged source cross products s_j (Acc2S:
+// 38 instead of 41 FP32 instructions per pair, rounding ~1.4x larger since the sums carry
+// |x_j| instead of |d|); otherwise the per-pair cross product gamma_j x d
+template <int SCHEME, bool SJ>
 __global__ void __launch_bounds__(P2P_THREADS, 2) p2p_kernel(
     const float* __restrict__ s6, int64_t n, const int* __restrict__ leaf_start, int depth,
     float a, int periodic, KernelConsts kc, float* __restrict__ near6,
     unsigned long long* __restrict__ npairs, int64_t plo) {
     extern __shared__ float4 p2p_sm[];
-    float4* S4 = p2p_sm;                                        // x, y, z, gx
-    float2* S2 = reinterpret_cast<float2*>(S4 + P2P_CAP + P2P_PAD);  // gy, gz
+    constexpr int P2P_CAP = p2p_cap<SJ>();
+    float4* S4 = p2p_sm;                         // x, y, z, gx
+    // SJ: gy, gz, sx, sy (s_j = gamma_j x x_j) and sz; else gy, gz
+    float4* S4b = S4 + P2P_CAP + P2P_PAD;
+    float* S1 = reinterpret_cast<float*>(S4b + P2P_CAP + P2P_PAD);
+    float2* S2 = reinterpret_cast<float2*>(S4 + P2P_CAP + P2P_PAD);
     __shared__ int rstart[65], rcnt[64], rsrc[64];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const uint32_t parent = (uint32_t)(plo + blockIdx.x);
@@ -357,6 +393,7 @@ __global__ void __launch_bounds__(P2P_THREADS, 2) p2p_kernel(
         const f2 GX = pk(g0x, g1x), GY = pk(g0y, g1y), GZ = pk(g0z, g1z);
         const f2 z2 = pk(0.f, 0.f);
         Acc2 C = {z2, z2, z2, z2, z2, z2, z2, z2, z2};
+        Acc2S CS = {z2, z2, z2, z2, z2, z2, z2, z2, z2, z2, z2, z2};
         const f2 thr = bc(kc.r2_series);
         (void)thr;
         // windows [w0, w1) of the concatenated region sources, P2P_CAP at a time
@@ -371,9 +408,15 @@ __global__ void __launch_bounds__(P2P_THREADS, 2) p2p_kernel(
                             oz = ((rl >> 4) - 1.5f) * a;
                 for (int k = lane; k < hi - lo; k += 32) {
                     const int j = src + k;
-                    S4[lo - w0 + k] = make_float4(s6[j] + ox, s6[n + j] + oy, s6[2 * n + j] + oz,
-                                                  s6[3 * n + j]);
-                    S2[lo - w0 + k] = make_float2(s6[4 * n + j], s6[5 * n + j]);
+                    const float x = s6[j] + ox, y = s6[n + j] + oy, z = s6[2 * n + j] + oz;
+                    const float gx = s6[3 * n + j], gy = s6[4 * n + j], gz = s6[5 * n + j];
+                    S4[lo - w0 + k] = make_float4(x, y, z, gx);
+                    if (SJ) {
+                        S4b[lo - w0 + k] = make_float4(gy, gz, gy * z - gz * y, gz * x - gx * z);
+                        S1[lo - w0 + k] = gx * y - gy * x;
+                    } else {
+                        S2[lo - w0 + k] = make_float2(gy, gz);
+                    }
                 }
             }
             __syncthreads();
@@ -384,18 +427,25 @@ __global__ void __launch_bounds__(P2P_THREADS, 2) p2p_kernel(
                 // two sources per iteration; each source x two targets = one packed pair.
                 // The next two sources are prefetched from shared memory one iteration ahead
                 // (the buffers are padded, so reads past je stay inside them and are unused)
+                // (SJ: the 4-wide second record; else the 2-wide one, zero-extended)
+                auto rec2 = [&](int jj) {
+                    if (SJ) return S4b[jj];
+                    const float2 t = S2[jj];
+                    return make_float4(t.x, t.y, 0.f, 0.f);
+                };
                 float4 na = S4[js], nbb = S4[js + 1];
-                float2 nqa = S2[js], nqb = S2[js + 1];
+                float4 nqa = rec2(js), nqb = rec2(js + 1);
                 for (int j = js; j < je; j += 2) {
                     const bool two = j + 1 < je;
                     const float4 pa = na;
-                    const float2 qa = nqa;
+                    const float4 qa = nqa;
                     const float4 pb = two ? nbb : pa;
-                    const float2 qb = two ? nqb : make_float2(0.f, 0.f);
+                    const float4 qb = two ? nqb : make_float4(0.f, 0.f, 0.f, 0.f);
+                    const float sza = SJ ? S1[j] : 0.f, szb = SJ && two ? S1[j + 1] : 0.f;
                     na = S4[j + 2];
                     nbb = S4[j + 3];
-                    nqa = S2[j + 2];
-                    nqb = S2[j + 3];
+                    nqa = rec2(j + 2);
+                    nqb = rec2(j + 3);
                     const float gbx = two ? pb.w : 0.f;  // a missing 2nd source has zero strength
                     const f2 dxa = sub2(X, bc(pa.x)), dya = sub2(Y, bc(pa.y)), dza = sub2(Z, bc(pa.z));
                     const f2 dxb = sub2(X, bc(pb.x)), dyb = sub2(Y, bc(pb.y)), dzb = sub2(Z, bc(pb.z));
@@ -422,10 +472,28 @@ __global__ void __launch_bounds__(P2P_THREADS, 2) p2p_kernel(
                         fq_closed2(r2a, kc, fa, qa2);
                         fq_closed2(r2b, kc, fb, qb2);
                     }
-                    accumulate2<SCHEME>(dxa, dya, dza, fa, qa2, pa.w, qa.x, qa.y, GX, GY, GZ, C);
-                    accumulate2<SCHEME>(dxb, dyb, dzb, fb, qb2, gbx, qb.x, qb.y, GX, GY, GZ, C);
+                    if (SJ) {
+                        accumulate2s(dxa, dya, dza, fa, qa2, pa.w, qa.x, qa.y, qa.z, qa.w, sza, GX,
+                                     GY, GZ, CS);
+                        accumulate2s(dxb, dyb, dzb, fb, qb2, gbx, qb.x, qb.y, qb.z, qb.w, szb, GX,
+                                     GY, GZ, CS);
+                    } else {
+                        accumulate2<SCHEME>(dxa, dya, dza, fa, qa2, pa.w, qa.x, qa.y, GX, GY, GZ, C);
+                        accumulate2<SCHEME>(dxb, dyb, dzb, fb, qb2, gbx, qb.x, qb.y, GX, GY, GZ, C);
+                    }
                 }
             }
+        }
+        if (SJ) {  // u = A x x_i - V, B = Wg x x_i - Ws
+            C.a0 = CS.a0;
+            C.a1 = CS.a1;
+            C.a2 = CS.a2;
+            C.u0 = sub2(sub2(mul2(CS.a1, Z), mul2(CS.a2, Y)), CS.v0);
+            C.u1 = sub2(sub2(mul2(CS.a2, X), mul2(CS.a0, Z)), CS.v1);
+            C.u2 = sub2(sub2(mul2(CS.a0, Y), mul2(CS.a1, X)), CS.v2);
+            C.b0 = sub2(sub2(mul2(CS.wg1, Z), mul2(CS.wg2, Y)), CS.ws0);
+            C.b1 = sub2(sub2(mul2(CS.wg2, X), mul2(CS.wg0, Z)), CS.ws1);
+            C.b2 = sub2(sub2(mul2(CS.wg0, Y), mul2(CS.wg1, X)), CS.ws2);
         }
         Acc c0, c1;
         upk(C.u0, c0.u0, c1.u0);
@@ -526,20 +594,32 @@ __global__ void __launch_bounds__(128) direct_kernel(const float* __restrict__ p
 void launch_p2p(const float* sorted6, int64_t n, const int* leaf_start, int depth, float a,
                 int periodic, int scheme, KernelConsts kc, float* near6,
                 unsigned long long* npairs, int64_t plo, int64_t pcnt, cudaStream_t st) {
-    const size_t smem = (size_t)(P2P_CAP + P2P_PAD) * (sizeof(float4) + sizeof(float2));
+    const size_t smem_sj = (size_t)(p2p_cap<true>() + P2P_PAD) * (2 * sizeof(float4) + sizeof(float));
+    const size_t smem_x = (size_t)(p2p_cap<false>() + P2P_PAD) * (sizeof(float4) + sizeof(float2));
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(p2p_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        cudaFuncSetAttribute(p2p_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(p2p_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem_sj);
+        cudaFuncSetAttribute(p2p_kernel<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem_x);
+        cudaFuncSetAttribute(p2p_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem_x);
         attr = true;
     }
     if (pcnt <= 0) return;
-    if (scheme == 0)
-        p2p_kernel<0><<<(unsigned)pcnt, P2P_THREADS, smem, st>>>(sorted6, n, leaf_start, depth, a,
-                                                                periodic, kc, near6, npairs, plo);
+    // VFMM_P2P=cross: per-pair cross products in the classical scheme (smaller rounding);
+    // default: staged source cross products (fewer instructions)
+    const char* env = getenv("VFMM_P2P");
+    const bool sj = !(env && strcmp(env, "cross") == 0);
+    if (scheme == 0 && sj)
+        p2p_kernel<0, true><<<(unsigned)pcnt, P2P_THREADS, smem_sj, st>>>(
+            sorted6, n, leaf_start, depth, a, periodic, kc, near6, npairs, plo);
+    else if (scheme == 0)
+        p2p_kernel<0, false><<<(unsigned)pcnt, P2P_THREADS, smem_x, st>>>(
+            sorted6, n, leaf_start, depth, a, periodic, kc, near6, npairs, plo);
     else
-        p2p_kernel<1><<<(unsigned)pcnt, P2P_THREADS, smem, st>>>(sorted6, n, leaf_start, depth, a,
-                                                                periodic, kc, near6, npairs, plo);
+        p2p_kernel<1, false><<<(unsigned)pcnt, P2P_THREADS, smem_x, st>>>(
+            sorted6, n, leaf_start, depth, a, periodic, kc, near6, npairs, plo);
 }
 
 void launch_direct(const float* pos, const float* gamma, int64_t n, float len, int image_levels,
