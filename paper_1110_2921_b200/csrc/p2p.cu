@@ -161,6 +161,7 @@ __device__ __forceinline__ void fq_closed2(f2 r2, const KernelConsts& kc, f2& f,
     float da, db;
     upk(fma2(r, bc(kc.t_scale), bc(1.f)), da, db);
     const f2 t = pk(rcp_approx(da), rcp_approx(db));
+    // Horner (Estrin's depth-3 form measured 4% slower for its extra instruction)
     f2 E = fma2(bc(kc.en[5]), t, bc(kc.en[4]));
     E = fma2(E, t, bc(kc.en[3]));
     E = fma2(E, t, bc(kc.en[2]));
@@ -396,7 +397,9 @@ __global__ void __launch_bounds__(P2P_THREADS, 2) p2p_kernel(
         Acc2S CS = {z2, z2, z2, z2, z2, z2, z2, z2, z2, z2, z2, z2};
         const f2 thr = bc(kc.r2_series);
         (void)thr;
-        // windows [w0, w1) of the concatenated region sources, P2P_CAP at a time
+        // windows [w0, w1) of the concatenated region sources, P2P_CAP at a time (a warp idle
+        // at a window barrier leaves the pipes to the SM's other block; balanced two-phase
+        // staging by source layers measured 1.5% slower for its 25% extra staging)
         for (int w0 = 0; w0 < total; w0 += P2P_CAP) {
             const int w1 = min(w0 + P2P_CAP, total);
             __syncthreads();
@@ -424,6 +427,7 @@ __global__ void __launch_bounds__(P2P_THREADS, 2) p2p_kernel(
                 const int rx = bx + nb % 3, ry = by + (nb / 3) % 3, rz = bz + nb / 9;
                 const int rl = rx + 4 * ry + 16 * rz;
                 const int js = max(rstart[rl], w0) - w0, je = min(rstart[rl + 1], w1) - w0;
+                if (js >= je) continue;  // leaf not in this window (keeps the prefetch in bounds)
                 // two sources per iteration; each source x two targets = one packed pair.
                 // The next two sources are prefetched from shared memory one iteration ahead
                 // (the buffers are padded, so reads past je stay inside them and are unused)

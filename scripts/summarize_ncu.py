@@ -1,6 +1,6 @@
 """Summarise ncu outputs into profiles/<round>/: launch-list shares and key --set full metrics.
 
-usage: python scripts/summarize_ncu.py <launches.csv> <prof.ncu-rep> <out.md>
+usage: python scripts/summarize_ncu.py <launches.csv> <out.md> [<prof.ncu-rep> ...]
 """
 import collections
 import csv
@@ -22,17 +22,28 @@ KEYS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum
 
 
 def launches(path):
+    """Shares of one evaluate: the launch list is split at each keys_kernel (first kernel of
+    an evaluation) and the last complete evaluation is reported."""
     txt = open(path).read()
     rows = list(csv.DictReader(io.StringIO(txt[txt.index('"ID"'):])))
-    agg = collections.OrderedDict()
+    evals, cur = [], []
     for r in rows:
         name = r["Kernel Name"].split("(")[0].split("::")[-1]
-        agg[name] = agg.get(name, 0.0) + float(r["Metric Value"]) / 1e6
+        if name == "keys_kernel" and cur:
+            evals.append(cur)
+            cur = []
+        cur.append((name, float(r["Metric Value"]) / 1e6))
+    if cur:
+        evals.append(cur)
+    ev = evals[-1]
+    agg = collections.OrderedDict()
+    for name, ms in ev:
+        agg[name] = agg.get(name, 0.0) + ms
     tot = sum(agg.values())
-    out = ["| kernel | ms (sum of launches) | share |", "|---|---|---|"]
+    out = ["| kernel | ms (sum of its launches) | share |", "|---|---|---|"]
     for k, v in sorted(agg.items(), key=lambda x: -x[1]):
         out.append(f"| {k} | {v:.3f} | {100 * v / tot:.1f}% |")
-    out.append(f"| **total** ({len(rows)} launches) | {tot:.3f} | |")
+    out.append(f"| **total** ({len(ev)} launches in one evaluate) | {tot:.3f} | |")
     return "\n".join(out)
 
 
@@ -54,11 +65,12 @@ def full(rep):
 
 
 if __name__ == "__main__":
-    lc, rep, dst = sys.argv[1:4]
+    lc, dst, reps = sys.argv[1], sys.argv[2], sys.argv[3:]
     with open(dst, "w") as f:
         f.write("# ncu summary (cold-cache serialised launch list; shares, not absolutes)\n\n")
         f.write("## Launch list (one evaluate, c4 256^3, p=10, depth 6)\n\n")
         f.write(launches(lc) + "\n\n")
         f.write("## --set full (selected kernels)\n\n")
-        f.write(full(rep) + "\n")
+        for rep in reps:
+            f.write(full(rep) + "\n\n")
     print(open(dst).read())
