@@ -38,7 +38,8 @@ struct vfmm_ctx {
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     int* d_slots = nullptr;  // [8][189]
     int* d_groups = nullptr; // [8][72][4] offset groups (tensor-core M2L y-windows)
-    float* m2m_scratch = nullptr;  // coarse-level M2M op-split partials (8 x 1024 x 3 nc)
+    float* m2m_scratch = nullptr;  // coarse-level op-split partials (M2M, SIMT M2L): main stream
+    float* side_scratch = nullptr; // the same for the side stream's SIMT M2L levels
     size_t m2m_scratch_floats = 0;
     int *d_l2p_rowptr = nullptr, *d_l2p_src = nullptr;  // L2P derivative map (CSR)
     float* d_l2p_coef = nullptr;
@@ -168,9 +169,23 @@ vfmm_status ensure_ops(vfmm_ctx* c) {
     dfree(c->d_l2p_src);
     dfree(c->d_l2p_coef);
     dfree(c->m2m_scratch);
-    c->m2m_scratch_floats = (size_t)8 * 1024 * 3 * c->hops.nc;
+    dfree(c->side_scratch);
+    dfree(c->side_scratch);
+    {
+        // largest op-split partial set: M2M of <= 1024 coarse parents x 8 children, or a SIMT
+        // M2L level with < 296 tiles (opsplit slices x 8 children x parents), launch_m2l
+        size_t need = (size_t)8 * 1024;
+        for (int64_t pc = 1; pc <= 4096; pc *= 8) {
+            const int64_t tiles = 8 * ((pc + 31) / 32) * (c->hops.NR / 128);
+            const int64_t os = tiles >= 296 ? 1 : std::min<int64_t>(27, (296 + tiles - 1) / tiles);
+            if (os > 1) need = std::max(need, (size_t)(os * 8 * pc));
+        }
+        c->m2m_scratch_floats = need * 3 * c->hops.nc;
+    }
     CK(cudaMalloc((void**)&c->m2m_scratch, c->m2m_scratch_floats * sizeof(float)),
-       "alloc m2m scratch");
+       "alloc op-split scratch");
+    CK(cudaMalloc((void**)&c->side_scratch, c->m2m_scratch_floats * sizeof(float)),
+       "alloc op-split scratch");
     {
         auto upi = [&](const std::vector<int>& h, int** d) -> cudaError_t {
             cudaError_t e = cudaMalloc((void**)d, std::max<size_t>(h.size(), 1) * sizeof(int));
@@ -640,9 +655,10 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
                 }
                 nl += tco.f16 ? 3 : 2;
             } else {
-                launch_m2l(c->d_m2l, c->d_slots, p, H.KP, H.NR, Mlev(l), Llev(l), l,
-                           P.image_levels > 0, 0, (int64_t)1 << (3 * (l - 1)), sl);
-                ++nl;
+                nl += launch_m2l(c->d_m2l, c->d_slots, p, H.KP, H.NR, Mlev(l), Llev(l), l,
+                                 P.image_levels > 0, 0, (int64_t)1 << (3 * (l - 1)),
+                                 l == depth ? c->m2m_scratch : c->side_scratch,
+                                 c->m2m_scratch_floats, sl);
             }
             S.n_m2l += (int64_t)189 << (3 * l);
         }
@@ -804,6 +820,7 @@ void vfmm_destroy(vfmm_ctx* c) {
     dfree(c->d_l2p_src);
     dfree(c->d_l2p_coef);
     dfree(c->m2m_scratch);
+    dfree(c->side_scratch);
     dfree(c->d_tc_hi);
     dfree(c->d_tc_lo);
     dfree(c->d_h16_hi);

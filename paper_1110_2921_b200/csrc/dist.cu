@@ -593,7 +593,8 @@ vfmm_status dist_phase4(RankState& S, const DistShared& D, cudaStream_t st, std:
                 return VFMM_ECUDA;
             }
         } else {
-            launch_m2l(D.m2l, D.slots, p, D.KP, D.NR, Mlev(l), Llev(l), l, periodic, plo, pcnt, st);
+            launch_m2l(D.m2l, D.slots, p, D.KP, D.NR, Mlev(l), Llev(l), l, periodic, plo, pcnt,
+                       D.m2m_scratch, D.m2m_scratch_floats, st);
         }
     }
     if (P.image_levels >= 2) launch_periodic(D.per, p, D.KP, D.NR, Mlev(0), Llev(0), st);

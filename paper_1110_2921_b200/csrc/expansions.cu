@@ -345,7 +345,8 @@ __global__ void __launch_bounds__(256, 2) translate_kernel(
         const int cell = col / 3, comp = col - cell * 3;
         if (cell >= ncell_tile) continue;
         // zpart: the op split writes per-slice partials (summed in a fixed order afterwards)
-        float* out = zpart ? zpart + blockIdx.z * zstride + ((target_cell(cell) - plo) * 3 + comp) * nc
+        const int64_t tbase = KIND == OP_M2M ? plo : plo * 8;  // first target cell of the range
+        float* out = zpart ? zpart + blockIdx.z * zstride + ((target_cell(cell) - tbase) * 3 + comp) * nc
                            : dst + (target_cell(cell) * 3 + comp) * nc;
         for (int rr = lane; rr < TROWS; rr += 32) {
             const int r = row0 + rr;
@@ -612,23 +613,30 @@ void launch_l2l(const float* ops_l2l, int p, int KP, int NR, const float* L_par,
                                                                 L_child, level_child, 0, plo, pcnt, 1);
 }
 
-void launch_m2l(const float* ops_m2l, const int* il_slots, int p, int KP, int NR,
-                const float* M_l, float* L_l, int level, int periodic, int64_t plo, int64_t pcnt,
-                cudaStream_t st) {
-    if (pcnt <= 0) return;
-    // few target tiles (coarse levels): split the 189 offsets over grid.z and accumulate
-    // atomically into the zeroed output, so the level does not run on a handful of SMs
+int launch_m2l(const float* ops_m2l, const int* il_slots, int p, int KP, int NR,
+               const float* M_l, float* L_l, int level, int periodic, int64_t plo, int64_t pcnt,
+               float* scratch, size_t scratch_floats, cudaStream_t st) {
+    if (pcnt <= 0) return 0;
+    // few target tiles (coarse levels): split the 189 offsets over grid.z so the level does not
+    // run on a handful of SMs; the slices write partial sums that zsum_kernel adds in slice
+    // order (deterministic), or -- without room in the scratch -- accumulate atomically
+    const int nc = (p + 1) * (p + 1);
     const int64_t tiles = 8 * ((pcnt + TCELLS - 1) / TCELLS) * (NR / TROWS);
     const int opsplit = tiles >= 296 ? 1 : (int)std::min<int64_t>(27, (296 + tiles - 1) / tiles);
-    if (opsplit > 1) {
-        const int nc = (p + 1) * (p + 1);
+    const int64_t zstride = pcnt * 8 * 3 * nc;
+    const bool zs = opsplit > 1 && scratch && (size_t)(opsplit * zstride) <= scratch_floats;
+    if (opsplit > 1 && !zs)
         cudaMemsetAsync(L_l + plo * 8 * 3 * nc, 0, (size_t)pcnt * 8 * 3 * nc * sizeof(float), st);
-    }
     dim3 grid((unsigned)(8 * ((pcnt + TCELLS - 1) / TCELLS)), NR / TROWS, opsplit);
     translate_attrs();
-    translate_kernel<OP_M2L><<<grid, 256, TRANSLATE_SMEM, st>>>(ops_m2l, il_slots, p, KP, NR, M_l,
-                                                                L_l, level, periodic, plo, pcnt,
-                                                                opsplit);
+    translate_kernel<OP_M2L><<<grid, 256, TRANSLATE_SMEM, st>>>(
+        ops_m2l, il_slots, p, KP, NR, M_l, L_l, level, periodic, plo, pcnt, opsplit,
+        zs ? scratch : nullptr, zstride);
+    if (!zs) return 1;
+    const int64_t blocks = std::min<int64_t>((zstride + 255) / 256, 148 * 8);
+    zsum_kernel<<<(unsigned)blocks, 256, 0, st>>>(scratch, zstride, opsplit,
+                                                  L_l + plo * 8 * 3 * nc, zstride);
+    return 2;
 }
 
 void launch_periodic(const float* ops_per, int p, int KP, int NR, const float* M0, float* L0,

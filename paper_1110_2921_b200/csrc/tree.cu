@@ -57,25 +57,27 @@ __global__ void keys_kernel(const float* __restrict__ pos, int64_t n, float lo, 
 }
 
 // ---- LSD radix sort: 8-bit digits, tiles of 4096 keys (8 warps x 16 chunks x 32) ----
-constexpr int RB = 8;
-constexpr int RBINS = 1 << RB;
+// digit width per pass <= RB (9 bits): the key bits are split into equal-width passes
+// (18-bit keys at depth 6: 2 passes of 9 bits instead of 3 of 8)
+constexpr int RB = 9;
+constexpr int RBINS = 1 << RB;  // bins of the widest digit
 constexpr int RWARPS = 8;
 constexpr int RCHUNK = 16;
 constexpr int RTILE = RWARPS * RCHUNK * 32;  // 4096
 
 __global__ void __launch_bounds__(256) radix_count(const uint32_t* __restrict__ keys, int64_t n,
-                                                   int shift, uint32_t* __restrict__ counts,
-                                                   int nblocks) {
+                                                   int shift, int nbins,
+                                                   uint32_t* __restrict__ counts, int nblocks) {
     __shared__ uint32_t h[RBINS];
-    h[threadIdx.x] = 0;
+    for (int d = threadIdx.x; d < nbins; d += 256) h[d] = 0;
     __syncthreads();
     const int64_t base = (int64_t)blockIdx.x * RTILE;
     for (int i = threadIdx.x; i < RTILE; i += 256) {
         const int64_t k = base + i;
-        if (k < n) atomicAdd(&h[(keys[k] >> shift) & (RBINS - 1)], 1u);
+        if (k < n) atomicAdd(&h[(keys[k] >> shift) & (nbins - 1)], 1u);
     }
     __syncthreads();
-    counts[(int64_t)threadIdx.x * nblocks + blockIdx.x] = h[threadIdx.x];
+    for (int d = threadIdx.x; d < nbins; d += 256) counts[(int64_t)d * nblocks + blockIdx.x] = h[d];
 }
 
 // one block per digit: exclusive scan of its row over blocks; row total -> totals[d]
@@ -112,26 +114,26 @@ __global__ void __launch_bounds__(256) radix_scan_rows(uint32_t* __restrict__ co
     if (threadIdx.x == 0) totals[blockIdx.x] = carry;
 }
 
-__global__ void __launch_bounds__(256) radix_scan_totals(uint32_t* __restrict__ totals) {
+__global__ void __launch_bounds__(256) radix_scan_totals(uint32_t* __restrict__ totals, int nbins) {
     __shared__ uint32_t s[RBINS];
-    s[threadIdx.x] = totals[threadIdx.x];
+    for (int d = threadIdx.x; d < nbins; d += blockDim.x) s[d] = totals[d];
     __syncthreads();
     if (threadIdx.x == 0) {
         uint32_t run = 0;
-        for (int d = 0; d < RBINS; ++d) {
+        for (int d = 0; d < nbins; ++d) {
             const uint32_t t = s[d];
             s[d] = run;
             run += t;
         }
     }
     __syncthreads();
-    totals[threadIdx.x] = s[threadIdx.x];
+    for (int d = threadIdx.x; d < nbins; d += blockDim.x) totals[d] = s[d];
 }
 
 __global__ void __launch_bounds__(256) radix_scatter(
     const uint32_t* __restrict__ kin, const uint32_t* __restrict__ vin, int64_t n, int shift,
-    const uint32_t* __restrict__ counts, const uint32_t* __restrict__ digit_base, int nblocks,
-    uint32_t* __restrict__ kout, uint32_t* __restrict__ vout) {
+    int nbins, const uint32_t* __restrict__ counts, const uint32_t* __restrict__ digit_base,
+    int nblocks, uint32_t* __restrict__ kout, uint32_t* __restrict__ vout) {
     __shared__ uint32_t wh[RWARPS][RBINS];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     for (int i = threadIdx.x; i < RWARPS * RBINS; i += 256) (&wh[0][0])[i] = 0;
@@ -145,7 +147,7 @@ __global__ void __launch_bounds__(256) radix_scatter(
         const bool ok = k < n;
         key[c] = ok ? kin[k] : 0u;
         val[c] = ok ? vin[k] : 0u;
-        const uint32_t d = ok ? ((key[c] >> shift) & (RBINS - 1)) : (uint32_t)RBINS;  // RBINS: none
+        const uint32_t d = ok ? ((key[c] >> shift) & (nbins - 1)) : (uint32_t)RBINS;  // RBINS: none
         const uint32_t peers = __match_any_sync(0xffffffffu, d);
         const uint32_t rank = __popc(peers & lt);
         const uint32_t before = (d < RBINS) ? wh[w][d] : 0u;
@@ -155,8 +157,7 @@ __global__ void __launch_bounds__(256) radix_scatter(
         __syncwarp();
     }
     __syncthreads();
-    {  // exclusive prefix over warps for each digit; add the global base
-        const int d = threadIdx.x;
+    for (int d = threadIdx.x; d < nbins; d += 256) {  // exclusive prefix over warps per digit
         uint32_t run = digit_base[d] + counts[(int64_t)d * nblocks + blockIdx.x];
         for (int i = 0; i < RWARPS; ++i) {
             const uint32_t t = wh[i][d];
@@ -169,7 +170,7 @@ __global__ void __launch_bounds__(256) radix_scatter(
     for (int c = 0; c < RCHUNK; ++c) {
         const int64_t k = base + c * 32 + lane;
         if (k < n) {
-            const uint32_t d = (key[c] >> shift) & (RBINS - 1);
+            const uint32_t d = (key[c] >> shift) & (nbins - 1);
             const uint32_t o = wh[w][d] + lpos[c];
             kout[o] = key[c];
             vout[o] = val[c];
@@ -236,11 +237,14 @@ void launch_radix_sort(uint32_t* keys, uint32_t* vals, uint32_t* keys_alt, uint3
     uint32_t* counts = (uint32_t*)temp;
     uint32_t* totals = counts + (size_t)nb * RBINS;
     uint32_t *ki = keys, *vi = vals, *ko = keys_alt, *vo = vals_alt;
-    for (int shift = 0; shift < key_bits; shift += RB) {
-        radix_count<<<nb, 256, 0, st>>>(ki, n, shift, counts, nb);
-        radix_scan_rows<<<RBINS, 256, 0, st>>>(counts, nb, totals);
-        radix_scan_totals<<<1, RBINS, 0, st>>>(totals);
-        radix_scatter<<<nb, 256, 0, st>>>(ki, vi, n, shift, counts, totals, nb, ko, vo);
+    const int passes = key_bits <= 0 ? 1 : (key_bits + RB - 1) / RB;
+    const int width = key_bits <= 0 ? 1 : (key_bits + passes - 1) / passes;  // <= RB
+    for (int shift = 0, pass = 0; pass < passes; shift += width, ++pass) {
+        const int nbins = 1 << width;
+        radix_count<<<nb, 256, 0, st>>>(ki, n, shift, nbins, counts, nb);
+        radix_scan_rows<<<nbins, 256, 0, st>>>(counts, nb, totals);
+        radix_scan_totals<<<1, 256, 0, st>>>(totals, nbins);
+        radix_scatter<<<nb, 256, 0, st>>>(ki, vi, n, shift, nbins, counts, totals, nb, ko, vo);
         *n_launch += 4;
         uint32_t* t = ki;
         ki = ko;

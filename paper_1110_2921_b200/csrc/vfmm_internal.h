@@ -89,9 +89,11 @@ int launch_m2m(const float* ops_m2m, int p, int KP, int NR, const float* M_child
                cudaStream_t st);
 void launch_l2l(const float* ops_l2l, int p, int KP, int NR, const float* L_par, float* L_child,
                 int level_child, int64_t plo, int64_t pcnt, cudaStream_t st);
-void launch_m2l(const float* ops_m2l, const int* il_slots, int p, int KP, int NR,
-                const float* M_l, float* L_l, int level, int periodic, int64_t plo, int64_t pcnt,
-                cudaStream_t st);
+// returns the number of kernels launched; the scratch (if large enough) makes the coarse
+// levels' op split deterministic (partials + zsum) instead of atomic
+int launch_m2l(const float* ops_m2l, const int* il_slots, int p, int KP, int NR,
+               const float* M_l, float* L_l, int level, int periodic, int64_t plo, int64_t pcnt,
+               float* scratch, size_t scratch_floats, cudaStream_t st);
 void launch_periodic(const float* ops_per, int p, int KP, int NR, const float* M0, float* L0,
                      cudaStream_t st);
 struct L2PMap {

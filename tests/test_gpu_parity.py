@@ -143,6 +143,8 @@ def _fmm_oracle(f, depth, p, lam, scheme=0):
     ("iso16", 2, 6, 2, 1),
     ("iso16", 3, 3, 0, 0),
     ("c1j", 2, 5, 1, 0),
+    ("iso16", 2, 10, 2, 0),  # compile-time p = 10 kernels, tcgen05 f16 M2L
+    ("c1", 2, 12, 1, 0),     # (p+1)^2 = 169 > 128: SIMT M2L, runtime-p P2M / L2P kernels
 ])
 def test_fmm_vs_fmm_oracle(name, depth, p, lam, scheme):
     f = {"c1": lambda: synthgen.make("c1"), "iso16": lambda: synthgen.isotropic(16, seed=9),
@@ -181,6 +183,32 @@ def _pack(C, p, scale_n):
 
 
 # ------------------------------------------------------------------ FMM vs direct sum
+
+def test_auto_depth_matches_explicit():
+    """depth = 0 picks the depth from N (~64 particles per leaf): same result as asking for it."""
+    f = synthgen.isotropic(32, seed=4)
+    v0, s0, ev0 = run(f, p=6, depth=0, image_levels=1)
+    st = ev0.stats()
+    L = st["depth_used"]
+    assert L == 3  # 32^3 / 64 = 8^3 leaves
+    v1, s1, ev1 = run(f, p=6, depth=L, image_levels=1)
+    assert np.array_equal(v0, v1) and np.array_equal(s0, s1)
+    ev0.close()
+    ev1.close()
+
+
+@pytest.mark.parametrize("engine", ["f16", "simt"])
+def test_evaluation_is_deterministic(engine, monkeypatch):
+    """No atomics on the value path (op splits reduce partials in a fixed order): two
+    evaluations of the same input are bitwise identical."""
+    monkeypatch.setenv("VFMM_M2L", engine)
+    f = synthgen.isotropic(16, seed=3)
+    v0, s0, ev = run(f, p=6, depth=3, image_levels=2)
+    v1, s1, ev1 = run(f, p=6, depth=3, image_levels=2)
+    assert np.array_equal(v0, v1) and np.array_equal(s0, s1)
+    ev.close()
+    ev1.close()
+
 
 def test_c1_fmm_vs_direct_oracle():
     f = synthgen.make("c1")
@@ -237,10 +265,12 @@ def test_zero_strengths_give_zero():
 # ------------------------------------------------------------------ full size (bench config)
 
 @pytest.mark.slow
-def test_c4_full_size_sampled_targets():
-    """256^3 (the bench workload, p = 10, depth 6): lambda = 1 so the oracle finishes in
-    seconds per target; the lambda = 3 far-image operator is covered at c1/c2 sizes."""
-    f = synthgen.make("c4")
+@pytest.mark.parametrize("cfg", ["c4", "c5"])
+def test_c4_full_size_sampled_targets(cfg):
+    """256^3 (the bench workload c4, and the intermittent Re_lambda = 100 field c5; p = 10,
+    depth 6): lambda = 1 so the oracle finishes in seconds per target; the lambda = 3
+    far-image operator is covered at c1/c2 sizes."""
+    f = synthgen.make(cfg)
     v, s, ev = run(f, p=10, depth=6, image_levels=1)
     tg = synthgen.sample_targets(f.pos.shape[1], 8, n_lattice=f.n)
     vo, so = oracle.direct(f.pos, f.gamma, f.sigma, f.box_lo, f.box_len, 1, 0, targets=tg)
