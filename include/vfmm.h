@@ -130,7 +130,8 @@ vfmm_status vfmm_evaluate(vfmm_ctx* ctx, int64_t n, const float* pos, const floa
 vfmm_status vfmm_nccl_get_unique_id(void* out128);
 
 /* Collective: create a context for rank `rank` of `nranks` on `device`, initialising an NCCL
-   communicator from `nccl_id128` (host, 128 bytes).  prm->depth must be >= 2. */
+   communicator from `nccl_id128` (host, 128 bytes).  prm->depth must be >= 2.  Such a context
+   always runs the distributed phases, also for nranks = 1 (a one-rank communicator). */
 vfmm_status vfmm_create_nccl(vfmm_ctx** ctx, const vfmm_params* prm, int device,
                              const void* nccl_id128, int nranks, int rank);
 

@@ -172,9 +172,9 @@ def nccl_unique_id() -> bytes:
 class Evaluator:
     """One vfmm context on one CUDA device (not thread-safe).
 
-    Distributed (one process per GPU): pass nranks > 1, rank and the 128-byte NCCL unique id
+    Distributed (one process per GPU): pass nranks, rank and the 128-byte NCCL unique id
     (rank 0's nccl_unique_id(), broadcast by the caller, e.g. torch.distributed) -- see
-    init_distributed()."""
+    init_distributed().  An NCCL context runs the distributed phases even with nranks = 1."""
 
     def __init__(self, device: int | None = None, nranks: int = 1, rank: int = 0,
                  nccl_id: bytes | None = None, **kw):
@@ -186,7 +186,7 @@ class Evaluator:
         self._ctx = ctypes.c_void_p()
         prm = self.params.to_c()
         self.nranks, self.rank = nranks, rank
-        if nranks > 1:
+        if nranks > 1 or nccl_id is not None:  # NCCL context (also 1 rank: distributed path)
             idb = ctypes.create_string_buffer(nccl_id, 128)
             _check(self._L, None, self._L.vfmm_create_nccl(
                 ctypes.byref(self._ctx), ctypes.byref(prm), self.device, idb, nranks, rank))

@@ -65,8 +65,10 @@ struct vfmm_ctx {
     int last_depth = 0;
     bool have_tree = false, have_exp = false;
     vfmm_stats stats{};
-    // distributed state (R > 1: NCCL; logical mode: one RankState per logical rank)
+    // distributed state (dist: NCCL context, this process = rank `rank` of R; logical mode:
+    // one RankState per logical rank)
     int R = 1, rank = 0;
+    bool dist = false;
     void* comm = nullptr;
     std::vector<vfmm::RankState*> ranks;
     static constexpr int NEV = 10;
@@ -372,7 +374,10 @@ vfmm_status vfmm_create_nccl(vfmm_ctx** out, const vfmm_params* prm, int device,
     vfmm_ctx* c = *out;
     c->R = nranks;
     c->rank = rank;
-    if (nranks > 1) {
+    // every NCCL context runs the distributed phases, also with one rank (a 1-rank
+    // communicator: the all-gathers degenerate to copies), so the NCCL plumbing is exercised
+    c->dist = true;
+    {
         s = nccl_init(&c->comm, nranks, rank, nccl_id128);
         if (s != VFMM_OK) {
             c->err = "ncclCommInitRank failed";
@@ -529,7 +534,7 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
     CK(cudaSetDevice(c->device), "set device");
     (void)cudaGetLastError();  // drop stale non-sticky errors of unrelated earlier calls
     cudaStream_t st = (cudaStream_t)stream;
-    if (c->R > 1) {  // distributed evaluation over NCCL (this process = one rank)
+    if (c->dist) {  // distributed evaluation over NCCL (this process = one rank)
         ensure_rank_states(c, c->R, c->rank, 1);
         DistShared D = make_shared(c, c->R);
         RankState& R0 = *c->ranks[0];
@@ -732,7 +737,7 @@ vfmm_status vfmm_sync_status(vfmm_ctx* c) {
     if (!c) return VFMM_EINVAL;
     CK(cudaSetDevice(c->device), "set device");
     CK(cudaStreamSynchronize(c->last_stream), "sync");
-    if (c->R > 1 && !c->ranks.empty()) {
+    if (c->dist && !c->ranks.empty()) {
         vfmm_status s = dist_sticky(c, c->ranks[0]);
         if (s != VFMM_OK) return s;
     }

@@ -23,7 +23,7 @@ def _split(f, depth, R):
 
 
 @pytest.mark.parametrize("R,n,depth,p,lam,jit", [
-    (2, 32, 3, 6, 3, False), (4, 32, 3, 6, 1, True), (8, 32, 3, 4, 0, False),
+    (1, 32, 3, 6, 3, False), (2, 32, 3, 6, 3, False), (4, 32, 3, 6, 1, True), (8, 32, 3, 4, 0, False),
     (8, 64, 4, 6, 3, False), (2, 64, 5, 8, 3, False), (4, 48, 5, 6, 2, True)])
 def test_logical_ranks_equal_single_rank(R, n, depth, p, lam, jit):
     f = synthgen.isotropic(n, seed=31)
@@ -55,6 +55,33 @@ def test_logical_ranks_equal_single_rank(R, n, depth, p, lam, jit):
     assert (st["bytes_sent"] > 0) == (R > 1)
     ev1.close()
     evR.close()
+
+
+def test_nccl_one_rank_context_equals_single_rank():
+    """A one-rank NCCL communicator drives the distributed phases with the real NCCL calls
+    (unique id, CommInitRank, the all-gathers of per-leaf counts and level-1 multipoles): the
+    result equals the single-context evaluation."""
+    try:
+        uid = vf.nccl_unique_id()
+    except Exception as e:  # pragma: no cover
+        pytest.skip(f"NCCL unavailable: {e}")
+    f = synthgen.isotropic(32, seed=5)
+    kw = dict(p=6, depth=3, image_levels=3, sigma=f.sigma, box_lo=f.box_lo, box_len=f.box_len)
+    pos = torch.from_numpy(f.pos).to(DEV)
+    gam = torch.from_numpy(f.gamma).to(DEV)
+    ev1 = vf.Evaluator(**kw)
+    v1, s1 = ev1.evaluate(pos, gam)
+    ev1.sync_status()
+    evn = vf.Evaluator(nranks=1, rank=0, nccl_id=uid, **kw)
+    vn, sn = evn.evaluate(pos, gam)
+    evn.sync_status()
+    torch.cuda.synchronize()
+    v1, s1, vn, sn = (t.cpu().numpy() for t in (v1, s1, vn, sn))
+    ru = np.linalg.norm(vn - v1) / np.linalg.norm(v1)
+    rs = np.linalg.norm(sn - s1) / np.linalg.norm(s1)
+    assert ru < 1e-6 and rs < 1e-6, (ru, rs)
+    ev1.close()
+    evn.close()
 
 
 def test_particles_outside_rank_range_are_flagged():
