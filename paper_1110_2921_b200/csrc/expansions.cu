@@ -266,11 +266,11 @@ __global__ void __launch_bounds__(256, 2) translate_kernel(
     }
     __syncthreads();
 
-    float acc[8][6];
+    f2x acc2[8][3];  // acc[i][2h], acc[i][2h+1] as packed pairs (FFMA2, broadcast a[i])
 #pragma unroll
     for (int i = 0; i < 8; ++i)
 #pragma unroll
-        for (int j = 0; j < 6; ++j) acc[i][j] = 0.f;
+        for (int h = 0; h < 3; ++h) acc2[i][h] = pk2(0.f, 0.f);
 
     const int nkc = KP / KC;
     const int niter = (op1 - op0) * nkc;
@@ -322,13 +322,16 @@ __global__ void __launch_bounds__(256, 2) translate_kernel(
             const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 8]);
             const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][kk][ty * 8 + 4]);
             const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
-            float b[6];
+            f2x b2[3];
 #pragma unroll
-            for (int j = 0; j < 6; ++j) b[j] = Bs[buf][kk][tx * 6 + j];
+            for (int h = 0; h < 3; ++h) {
+                const float2 bb = *reinterpret_cast<const float2*>(&Bs[buf][kk][tx * 6 + 2 * h]);
+                b2[h] = pk2(bb.x, bb.y);
+            }
 #pragma unroll
             for (int i = 0; i < 8; ++i)
 #pragma unroll
-                for (int j = 0; j < 6; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+                for (int h = 0; h < 3; ++h) acc2[i][h] = ffma2(pk2(a[i], a[i]), b2[h], acc2[i][h]);
         }
         if (it + 1 < niter) store_smem(buf ^ 1);
         __syncthreads();
@@ -338,7 +341,11 @@ __global__ void __launch_bounds__(256, 2) translate_kernel(
 #pragma unroll
     for (int j = 0; j < 6; ++j)
 #pragma unroll
-        for (int i = 0; i < 8; ++i) Cs[(tx * 6 + j) * 129 + ty * 8 + i] = acc[i][j];
+        for (int i = 0; i < 8; ++i) {
+            float lo, hi;
+            upk2(acc2[i][j >> 1], lo, hi);
+            Cs[(tx * 6 + j) * 129 + ty * 8 + i] = (j & 1) ? hi : lo;
+        }
     __syncthreads();
     const int lane = tid & 31, warp = tid >> 5;
     for (int col = warp; col < TCOLS; col += 8) {
