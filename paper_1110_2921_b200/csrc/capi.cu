@@ -41,8 +41,7 @@ struct vfmm_ctx {
     float* m2m_scratch = nullptr;  // coarse-level op-split partials (M2M, SIMT M2L): main stream
     float* side_scratch = nullptr; // the same for the side stream's SIMT M2L levels
     size_t m2m_scratch_floats = 0;
-    int *d_l2p_rowptr = nullptr, *d_l2p_src = nullptr;  // L2P derivative map (CSR)
-    float* d_l2p_coef = nullptr;
+    int *d_l2p_rowptr = nullptr, *d_l2p_pairs = nullptr;  // L2P derivative map (CSR)
     // workspace
     int64_t cap_n = 0;
     int cap_depth = -1, cap_p = -1;
@@ -89,8 +88,7 @@ int m2l_env_mode() {
 L2PMap l2p_map(const vfmm_ctx* c) {
     L2PMap m;
     m.rowptr = c->d_l2p_rowptr;
-    m.src = c->d_l2p_src;
-    m.coef = c->d_l2p_coef;
+    m.pairs = reinterpret_cast<const int4*>(c->d_l2p_pairs);
     return m;
 }
 
@@ -168,10 +166,8 @@ vfmm_status ensure_ops(vfmm_ctx* c) {
     CK(up(c->hops.m2l, &c->d_m2l), "upload m2l");
     CK(up(c->hops.per, &c->d_per), "upload periodic");
     dfree(c->d_l2p_rowptr);
-    dfree(c->d_l2p_src);
-    dfree(c->d_l2p_coef);
+    dfree(c->d_l2p_pairs);
     dfree(c->m2m_scratch);
-    dfree(c->side_scratch);
     dfree(c->side_scratch);
     {
         // largest op-split partial set: M2M of <= 1024 coarse parents x 8 children, or a SIMT
@@ -195,8 +191,12 @@ vfmm_status ensure_ops(vfmm_ctx* c) {
             return cudaMemcpy(*d, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice);
         };
         CK(upi(c->hops.l2p_rowptr, &c->d_l2p_rowptr), "upload l2p map");
-        CK(upi(c->hops.l2p_src, &c->d_l2p_src), "upload l2p map");
-        CK(up(c->hops.l2p_coef, &c->d_l2p_coef), "upload l2p map");
+        std::vector<int> pairs(2 * c->hops.l2p_src.size());
+        for (size_t t = 0; t < c->hops.l2p_src.size(); ++t) {
+            pairs[2 * t] = c->hops.l2p_src[t];
+            memcpy(&pairs[2 * t + 1], &c->hops.l2p_coef[t], sizeof(float));
+        }
+        CK(upi(pairs, &c->d_l2p_pairs), "upload l2p map");
     }
     dfree(c->d_tc_hi);
     dfree(c->d_tc_lo);
@@ -822,8 +822,7 @@ void vfmm_destroy(vfmm_ctx* c) {
     dfree(c->d_slots);
     dfree(c->d_groups);
     dfree(c->d_l2p_rowptr);
-    dfree(c->d_l2p_src);
-    dfree(c->d_l2p_coef);
+    dfree(c->d_l2p_pairs);
     dfree(c->m2m_scratch);
     dfree(c->side_scratch);
     dfree(c->d_tc_hi);

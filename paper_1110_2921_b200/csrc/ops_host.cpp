@@ -370,6 +370,10 @@ void build_l2p_map(int p, HostOps* out) {
                 out->l2p_src.push_back(t.first);
                 out->l2p_coef.push_back((float)t.second);
             }
+            if (out->l2p_src.size() & 1) {  // even row lengths: two terms per 16-byte load
+                out->l2p_src.push_back(0);
+                out->l2p_coef.push_back(0.f);
+            }
             out->l2p_rowptr.push_back((int)out->l2p_src.size());
         }
 }
