@@ -346,11 +346,11 @@ __global__ void __launch_bounds__(P2P_THREADS, 2) p2p_kernel(
         rsrc[tid] = st;
     }
     __syncthreads();
-    if (tid == 0) {
+    if (tid == 0) {  // staged offsets: every leaf padded to an even count (see staging)
         int run = 0;
         for (int i = 0; i < 64; ++i) {
             rstart[i] = run;
-            run += rcnt[i];
+            run += (rcnt[i] + 1) & ~1;
         }
         rstart[64] = run;
     }
@@ -410,9 +410,14 @@ __global__ void __launch_bounds__(P2P_THREADS, 2) p2p_kernel(
                 const float ox = ((rl & 3) - 1.5f) * a, oy = (((rl >> 2) & 3) - 1.5f) * a,
                             oz = ((rl >> 4) - 1.5f) * a;
                 for (int k = lane; k < hi - lo; k += 32) {
+                    // an odd leaf ends with a padding source: far away, zero strength (exact 0
+                    // contribution), so the pair loop runs over whole pairs of sources
                     const int j = src + k;
-                    const float x = s6[j] + ox, y = s6[n + j] + oy, z = s6[2 * n + j] + oz;
-                    const float gx = s6[3 * n + j], gy = s6[4 * n + j], gz = s6[5 * n + j];
+                    const bool real = lo - rstart[rl] + k < rcnt[rl];
+                    const float x = real ? s6[j] + ox : 1e4f, y = real ? s6[n + j] + oy : 1e4f,
+                                z = real ? s6[2 * n + j] + oz : 1e4f;
+                    const float gx = real ? s6[3 * n + j] : 0.f, gy = real ? s6[4 * n + j] : 0.f,
+                                gz = real ? s6[5 * n + j] : 0.f;
                     S4[lo - w0 + k] = make_float4(x, y, z, gx);
                     if (SJ) {
                         S4b[lo - w0 + k] = make_float4(gy, gz, gy * z - gz * y, gz * x - gx * z);
@@ -439,18 +444,19 @@ __global__ void __launch_bounds__(P2P_THREADS, 2) p2p_kernel(
                 };
                 float4 na = S4[js], nbb = S4[js + 1];
                 float4 nqa = rec2(js), nqb = rec2(js + 1);
-                for (int j = js; j < je; j += 2) {
-                    const bool two = j + 1 < je;
+                // unrolled by 2 (c4 P2P: 43.5 ms; 49.6 without unrolling, 43.4 unrolled by 4)
+#pragma unroll 2
+                for (int j = js; j < je; j += 2) {  // js, je even (padded leaves, even CAP)
                     const float4 pa = na;
                     const float4 qa = nqa;
-                    const float4 pb = two ? nbb : pa;
-                    const float4 qb = two ? nqb : make_float4(0.f, 0.f, 0.f, 0.f);
-                    const float sza = SJ ? S1[j] : 0.f, szb = SJ && two ? S1[j + 1] : 0.f;
+                    const float4 pb = nbb;
+                    const float4 qb = nqb;
+                    const float sza = SJ ? S1[j] : 0.f, szb = SJ ? S1[j + 1] : 0.f;
                     na = S4[j + 2];
                     nbb = S4[j + 3];
                     nqa = rec2(j + 2);
                     nqb = rec2(j + 3);
-                    const float gbx = two ? pb.w : 0.f;  // a missing 2nd source has zero strength
+                    const float gbx = pb.w;
                     const f2 dxa = sub2(X, bc(pa.x)), dya = sub2(Y, bc(pa.y)), dza = sub2(Z, bc(pa.z));
                     const f2 dxb = sub2(X, bc(pb.x)), dyb = sub2(Y, bc(pb.y)), dzb = sub2(Z, bc(pb.z));
                     const f2 r2a = fma2(dxa, dxa, fma2(dya, dya, mul2(dza, dza)));
