@@ -109,8 +109,8 @@ def test_direct_mode_vs_oracle(lam, scheme):
 @pytest.mark.parametrize("scheme,p2p", [(0, "sj"), (0, "cross"), (1, "cross")])
 def test_near_only_depth1_free_space_equals_direct(scheme, p2p, monkeypatch):
     """Depth 1, free space: all octants are neighbours, so P2P alone is the whole sum.
-    Classical scheme in both P2P accumulations (VFMM_P2P=cross: per-pair gamma_j x d;
-    default: staged gamma_j x x_j, looser FP32 rounding bound)."""
+    Classical scheme in both P2P accumulations (default / VFMM_P2P=cross: per-pair gamma_j x d;
+    VFMM_P2P=sj: staged gamma_j x x_j, looser FP32 rounding bound)."""
     monkeypatch.setenv("VFMM_P2P", p2p)
     f = synthgen.jitter(synthgen.taylor_green(12), seed=5)
     v, s, ev = run(f, p=2, depth=1, image_levels=0, scheme=scheme, mode=vf.MODE_NEAR_ONLY)
