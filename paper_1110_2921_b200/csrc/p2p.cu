@@ -461,13 +461,31 @@ __global__ void __launch_bounds__(P2P_THREADS, 2) p2p_kernel(
                     const float th = kc.r2_series;
                     const bool close = (a0 && (ra0 < th || rb0 < th)) || (a1 && (ra1 < th || rb1 < th));
                     f2 fa, qa2, fb, qb2;
-                    if (SJ) {  // closed form for all pairs outside the branch (schedules with the
-                               // neighbouring iteration: 42.2 vs 43.5 ms); the rare path overwrites
+                    if (SJ) {
+                        // closed form for all pairs, outside the branch (schedules with the
+                        // other unrolled iteration); the rare close pairs (self pairs, rho^2 <
+                        // 1/4) then get the Taylor series in place (41.9 ms; 42.7 with the
+                        // cross variant's form below)
                         fq_closed2(r2a, kc, fa, qa2);
                         fq_closed2(r2b, kc, fb, qb2);
-                    }
-                    if (__any_sync(0xffffffffu, close)) {
-                        // rare path (self pairs, close particles): per pair, series or closed form
+                        if (__any_sync(0xffffffffu, close)) {
+                            float f0, q0, f1, q1;
+                            upk(fa, f0, f1);
+                            upk(qa2, q0, q1);
+                            if (ra0 < th) fq_series(ra0, kc, f0, q0);
+                            if (ra1 < th) fq_series(ra1, kc, f1, q1);
+                            fa = pk(f0, f1);
+                            qa2 = pk(q0, q1);
+                            upk(fb, f0, f1);
+                            upk(qb2, q0, q1);
+                            if (rb0 < th) fq_series(rb0, kc, f0, q0);
+                            if (rb1 < th) fq_series(rb1, kc, f1, q1);
+                            fb = pk(f0, f1);
+                            qb2 = pk(q0, q1);
+                        }
+                    } else if (__any_sync(0xffffffffu, close)) {
+                        // rare path (self pairs, close particles): per pair, series or closed
+                        // form (this branch form schedules best for the cross variant: 43.1 ms)
                         float f0, q0, f1, q1;
                         if (ra0 < th) fq_series(ra0, kc, f0, q0); else fq_closed(ra0, kc, f0, q0);
                         if (ra1 < th) fq_series(ra1, kc, f1, q1); else fq_closed(ra1, kc, f1, q1);
@@ -477,7 +495,7 @@ __global__ void __launch_bounds__(P2P_THREADS, 2) p2p_kernel(
                         if (rb1 < th) fq_series(rb1, kc, f1, q1); else fq_closed(rb1, kc, f1, q1);
                         fb = pk(f0, f1);
                         qb2 = pk(q0, q1);
-                    } else if (!SJ) {  // (the cross variant schedules better this way: 43.5 vs 44.6)
+                    } else {
                         fq_closed2(r2a, kc, fa, qa2);
                         fq_closed2(r2b, kc, fb, qb2);
                     }
@@ -617,7 +635,7 @@ void launch_p2p(const float* sorted6, int64_t n, const int* leaf_start, int dept
     }
     if (pcnt <= 0) return;
     // default: per-pair cross products gamma_j x d (FP32-faithful rounding); VFMM_P2P=sj: the
-    // classical scheme with staged source cross products (3% faster at c4, 2-4x the rounding)
+    // classical scheme with staged source cross products (~3% faster at c4, 2-4x the rounding)
     const char* env = getenv("VFMM_P2P");
     const bool sj = env && strcmp(env, "sj") == 0;
     if (scheme == 0 && sj)
