@@ -3,6 +3,7 @@
 //   per level -> P2P -> L2P + combine + un-permute
 // (section 3.1; the step list is DESIGN.md "Hot path").  Every step is a kernel
 // on the caller's stream; the host only validates parameters and enqueues.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <cmath>
@@ -88,7 +89,7 @@ int m2l_env_mode() {
 L2PMap l2p_map(const vfmm_ctx* c) {
     L2PMap m;
     m.rowptr = c->d_l2p_rowptr;
-    m.pairs = reinterpret_cast<const int4*>(c->d_l2p_pairs);
+    m.terms = reinterpret_cast<const uint4*>(c->d_l2p_pairs);
     return m;
 }
 
@@ -191,12 +192,19 @@ vfmm_status ensure_ops(vfmm_ctx* c) {
             return cudaMemcpy(*d, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice);
         };
         CK(upi(c->hops.l2p_rowptr, &c->d_l2p_rowptr), "upload l2p map");
-        std::vector<int> pairs(2 * c->hops.l2p_src.size());
+        std::vector<int> terms(c->hops.l2p_src.size());
         for (size_t t = 0; t < c->hops.l2p_src.size(); ++t) {
-            pairs[2 * t] = c->hops.l2p_src[t];
-            memcpy(&pairs[2 * t + 1], &c->hops.l2p_coef[t], sizeof(float));
+            const float cf = c->hops.l2p_coef[t];
+            const __half h = __float2half_rn(cf);
+            if (__half2float(h) != cf || c->hops.l2p_src[t] > 0xffff) {
+                c->err = "L2P derivative map coefficient not exact in half";
+                return VFMM_ESTATE;
+            }
+            uint16_t hb;
+            memcpy(&hb, &h, 2);
+            terms[t] = (int)((uint32_t)c->hops.l2p_src[t] | ((uint32_t)hb << 16));
         }
-        CK(upi(pairs, &c->d_l2p_pairs), "upload l2p map");
+        CK(upi(terms, &c->d_l2p_pairs), "upload l2p map");
     }
     dfree(c->d_tc_hi);
     dfree(c->d_tc_lo);

@@ -15,6 +15,7 @@
 // 32 target cells x 3 strength components per block; every target in a block shares the
 // same operator sequence (same parity for M2L / L2L), B_op gathers the source cell of each
 // target for operator op.
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -397,7 +398,7 @@ __global__ void __launch_bounds__(64) l2p_combine_kernel(
     const uint32_t* __restrict__ perm, int64_t n, const int* __restrict__ leaf_start, int p_rt,
     float inv_a, const float* __restrict__ Lleaf, int use_near, int use_far,
     float* __restrict__ vel, float* __restrict__ dgam, int64_t leaf_lo, int64_t gbase,
-    int64_t nout, const int* __restrict__ map_rowptr, const int4* __restrict__ map_pairs) {
+    int64_t nout, const int* __restrict__ map_rowptr, const uint4* __restrict__ map_terms) {
     const int p = PC > 0 ? PC : p_rt;
     // smem: D [ng][12]; Ls [3][nc].  The 12 columns of D are the combinations the output
     // needs: u = curl phi (3) and J[a][k] = d_k u_a (9), each a difference of two derivative
@@ -419,18 +420,28 @@ __global__ void __launch_bounds__(64) l2p_combine_kernel(
     if (use_far) {
         for (int i = threadIdx.x; i < 3 * nc; i += 64) Ls[i] = Lleaf[leaf * 3 * nc + i];
         __syncthreads();
-        for (int i = threadIdx.x; i < ng * DQ; i += 64) {
-            float v = 0.f;
-            const int t1 = __ldg(map_rowptr + i + 1) >> 1;  // rows have even lengths
-            float v1 = 0.f;  // second accumulator (two independent chains)
-            for (int t = __ldg(map_rowptr + i) >> 1; t < t1; ++t) {
-                const int4 pp = __ldg(map_pairs + t);
-                v = fmaf(__int_as_float(pp.y), Ls[pp.x], v);
-                v1 = fmaf(__int_as_float(pp.w), Ls[pp.z], v1);
+        // stage 1: curl columns (q < 3) from L; stage 2: the velocity-gradient columns from the
+        // stage-1 rows (the map's src then indexes D itself)
+        auto row = [&](int e, const float* src_base) {
+            // rows are multiples of 4 terms; a term is (src | half(coef) << 16)
+            const int t1 = __ldg(map_rowptr + e + 1) >> 2;
+            float v = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f;  // four independent chains
+            auto term = [&](uint32_t u, float& acc) {
+                const float cf = __half2float(__ushort_as_half((unsigned short)(u >> 16)));
+                acc = fmaf(cf, src_base[u & 0xffffu], acc);
+            };
+            for (int t = __ldg(map_rowptr + e) >> 2; t < t1; ++t) {
+                const uint4 q = __ldg(map_terms + t);
+                term(q.x, v);
+                term(q.y, v1);
+                term(q.z, v2);
+                term(q.w, v3);
             }
-            v += v1;
-            sm[i] = v;
-        }
+            sm[e] = (v + v1) + (v2 + v3);
+        };
+        for (int i = threadIdx.x; i < ng * 3; i += 64) row((i / 3) * DQ + i % 3, Ls);
+        __syncthreads();
+        for (int i = threadIdx.x; i < ng * 9; i += 64) row((i / 9) * DQ + 3 + i % 9, sm);
         __syncthreads();
     }
     for (int b = s; b < e; b += 64) {
@@ -673,14 +684,15 @@ void launch_l2p_combine(const L2PMap& map, const float* sorted6, const float* ne
                             (const void*)l2p_combine_kernel<0, 8>, (const void*)l2p_combine_kernel<1, 8>,
                             (const void*)l2p_combine_kernel<0, 10>, (const void*)l2p_combine_kernel<1, 10>,
                             (const void*)l2p_combine_kernel<0, 0>, (const void*)l2p_combine_kernel<1, 0>};
-        for (const void* k : ks)
+        for (const void* k : ks) {
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        }
         attr = true;
     }
     auto go = [&](auto kern) {
         kern<<<(unsigned)leaf_cnt, 64, smem, st>>>(sorted6, near6, perm, n, leaf_start, p, inv_a,
                                                    L_leaf, use_near, use_far, vel, dgam, leaf_lo,
-                                                   gbase, nout, map.rowptr, map.pairs);
+                                                   gbase, nout, map.rowptr, map.terms);
     };
     // compile-time orders for the common p, runtime-p kernel otherwise
 #define L2P_CASE(PV)                                                             \

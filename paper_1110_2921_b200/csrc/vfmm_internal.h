@@ -43,7 +43,8 @@ struct HostOps {
     std::vector<float> h16_rs, h16_cs;  // [128] row / column scales
     // L2P: D[k][q] = sum_t coef[t] L[src[t]] for t in [rowptr[k 12 + q], rowptr[k 12 + q + 1]),
     // src indexing the 3 nc packed coefficients of a leaf (q: curl psi 3, grad u 9; k < p^2);
-    // rows padded to even lengths with zero terms (uploaded interleaved, two terms per int4)
+    // rows padded to multiples of 4 terms with zeros (uploaded as 32-bit terms: src in the low
+    // 16 bits, the coefficient -- sums of +-2^-k, exact in half -- in the high 16 bits)
     std::vector<int> l2p_rowptr, l2p_src;
     std::vector<float> l2p_coef;
 };
@@ -98,8 +99,8 @@ int launch_m2l(const float* ops_m2l, const int* il_slots, int p, int KP, int NR,
 void launch_periodic(const float* ops_per, int p, int KP, int NR, const float* M0, float* L0,
                      cudaStream_t st);
 struct L2PMap {
-    const int* rowptr = nullptr;  // [12 p^2 + 1], even offsets
-    const int4* pairs = nullptr;  // two terms per entry: {src0, bits(coef0), src1, bits(coef1)}
+    const int* rowptr = nullptr;   // [12 p^2 + 1], multiples of 4
+    const uint4* terms = nullptr;  // four terms per entry, each (src | half(coef) << 16)
 };
 void launch_l2p_combine(const L2PMap& map, const float* sorted6, const float* near6, const uint32_t* perm,
                         int64_t n, const int* leaf_start, int p, float a, const float* L_leaf,
