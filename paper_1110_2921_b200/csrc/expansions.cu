@@ -70,9 +70,10 @@ __constant__ float c_mhalf[17] = {0.000000000e+00f, -5.000000000e-01f, -2.500000
 // ---------------------------------------------------------------------------
 template <int PC>
 __device__ __forceinline__ void solid_R_packed(float x, float y, float z, int p_rt, float* out,
-                                               int stride, bool conj_) {
+                                               int stride, bool conj_, int mpar = -1) {
     // packed real R_n^m for 0 <= m <= n <= p, written to out[k * stride]; PC > 0: p = PC
-    // known at compile time (recurrences fully unrolled)
+    // known at compile time (recurrences fully unrolled).  mpar >= 0: only the orders m with
+    // m % 2 == mpar are written (the diagonal R_m^m chain is still walked for every m)
     const int p = PC > 0 ? PC : p_rt;
     const float r2 = x * x + y * y + z * z;
     float dre = 1.f, dim = 0.f;  // R_m^m
@@ -85,6 +86,7 @@ __device__ __forceinline__ void solid_R_packed(float x, float y, float z, int p_
             dre = nre;
             dim = nim;
         }
+        if (mpar >= 0 && (m & 1) != mpar) continue;
         float p2re = dre, p2im = dim, p1re = 0.f, p1im = 0.f;
         out[pk_re(m, m) * stride] = dre;
         if (m > 0) out[pk_im(m, m) * stride] = conj_ ? -dim : dim;
@@ -116,33 +118,38 @@ __global__ void __launch_bounds__(64) p2m_kernel(const float* __restrict__ s6, i
                                                  float inv_a, float* __restrict__ M,
                                                  int64_t leaf_lo) {
     const int p = PC > 0 ? PC : p_rt;
-    // thread j: conj(R) of particle j -> Rs[k][j] (row stride 68: float4-aligned rows);
-    // then thread k: M[c][k] for c = 0..2 from float4 loads of Rs[k][.] and gamma_c[.]
+    // chunks of 32 particles: particle j's conj(R) -> Rs[k][j] (row stride 36: float4-aligned
+    // rows), warp 0 writing the even orders m and warp 1 the odd ones (half the shared memory
+    // of one particle per thread: twice the resident blocks); then thread k: M[c][k] for
+    // c = 0..2 from float4 loads of Rs[k][.] and gamma_c[.]
     extern __shared__ float4 p2m_sm4[];
     float* sm = reinterpret_cast<float*>(p2m_sm4);
     const int nc = (p + 1) * (p + 1);
-    constexpr int RST = 68;
-    float* gs = sm;               // [3][64]
-    float* Rs = sm + 3 * 64;      // [nc][68]
+    constexpr int RST = 36, CH = 32;
+    float* gs = sm;               // [3][32]
+    float* Rs = sm + 3 * CH;      // [nc][36]
     const int64_t leaf = leaf_lo + blockIdx.x;
     const int s = leaf_start[leaf], e = leaf_start[leaf + 1];
+    const int lane = threadIdx.x & 31, wsel = threadIdx.x >> 5;
     float acc[2][3];              // k = tid, tid + 64 (nc <= 128 here; larger p loops below)
     for (int k0 = 0; k0 < nc; k0 += 128) {
 #pragma unroll
         for (int w = 0; w < 2; ++w) acc[w][0] = acc[w][1] = acc[w][2] = 0.f;
-        for (int b = s; b < e; b += 64) {
-            const int j = b + threadIdx.x;
-            const int cnt = min(64, e - b);
+        for (int b = s; b < e; b += CH) {
+            const int j = b + lane;
+            const int cnt = min(CH, e - b);
             __syncthreads();
-            if (threadIdx.x < cnt) {
+            if (lane < cnt) {
                 solid_R_packed<PC>(s6[j] * inv_a, s6[n + j] * inv_a, s6[2 * n + j] * inv_a, p,
-                                   Rs + threadIdx.x, RST, true);
-                gs[threadIdx.x] = s6[3 * n + j];
-                gs[64 + threadIdx.x] = s6[4 * n + j];
-                gs[128 + threadIdx.x] = s6[5 * n + j];
-            } else {  // zero pad so the float4 loop can run over whole quads
-                for (int k = 0; k < nc; ++k) Rs[k * RST + threadIdx.x] = 0.f;
-                gs[threadIdx.x] = gs[64 + threadIdx.x] = gs[128 + threadIdx.x] = 0.f;
+                                   Rs + lane, RST, true, wsel);
+                if (wsel == 0) {
+                    gs[lane] = s6[3 * n + j];
+                    gs[CH + lane] = s6[4 * n + j];
+                    gs[2 * CH + lane] = s6[5 * n + j];
+                }
+            } else if (wsel == 0) {  // zero pad so the float4 loop can run over whole quads
+                for (int k = 0; k < nc; ++k) Rs[k * RST + lane] = 0.f;
+                gs[lane] = gs[CH + lane] = gs[2 * CH + lane] = 0.f;
             }
             __syncthreads();
             const int nq = (cnt + 3) >> 2;
@@ -152,10 +159,9 @@ __global__ void __launch_bounds__(64) p2m_kernel(const float* __restrict__ s6, i
                 if (k >= nc) continue;
                 const float4* R4 = reinterpret_cast<const float4*>(Rs + k * RST);
                 const float4* G0 = reinterpret_cast<const float4*>(gs);
-                const float4* G1 = reinterpret_cast<const float4*>(gs + 64);
-                const float4* G2 = reinterpret_cast<const float4*>(gs + 128);
-                // (a packed FFMA2 form saved 0.03 ms but reorders the sums that cancel in the
-                // root multipole; kept in particle order)
+                const float4* G1 = reinterpret_cast<const float4*>(gs + CH);
+                const float4* G2 = reinterpret_cast<const float4*>(gs + 2 * CH);
+                // (kept in particle order: the sums cancel in the root multipole)
                 for (int q = 0; q < nq; ++q) {
                     const float4 r = R4[q], a = G0[q], bb = G1[q], c = G2[q];
                     acc[w][0] = fmaf(a.x, r.x, fmaf(a.y, r.y, fmaf(a.z, r.z, fmaf(a.w, r.w, acc[w][0]))));
@@ -578,7 +584,7 @@ void translate_attrs() {
 void launch_p2m(const float* sorted6, int64_t n, const int* leaf_start, int p, float inv_a,
                 float* M_leaf, int64_t leaf_lo, int64_t leaf_cnt, cudaStream_t st) {
     const int nc = (p + 1) * (p + 1);
-    const size_t smem = sizeof(float) * (nc * 68 + 3 * 64);
+    const size_t smem = sizeof(float) * (nc * 36 + 3 * 32);
     static bool attr = false;
     if (!attr) {
         const void* ks[] = {(const void*)p2m_kernel<0>, (const void*)p2m_kernel<4>,
