@@ -145,6 +145,7 @@ def _fmm_oracle(f, depth, p, lam, scheme=0):
     ("c1j", 2, 5, 1, 0),
     ("iso16", 2, 10, 2, 0),  # compile-time p = 10 kernels, tcgen05 f16 M2L
     ("c1", 2, 12, 1, 0),     # (p+1)^2 = 169 > 128: SIMT M2L, runtime-p P2M / L2P kernels
+    ("c1", 2, 16, 1, 0),     # VFMM_PMAX: (p+1)^2 = 289, three 128-row output tiles
 ])
 def test_fmm_vs_fmm_oracle(name, depth, p, lam, scheme):
     f = {"c1": lambda: synthgen.make("c1"), "iso16": lambda: synthgen.isotropic(16, seed=9),
@@ -166,8 +167,12 @@ def test_fmm_vs_fmm_oracle(name, depth, p, lam, scheme):
                 want = want[..., 1:]
             if np.abs(want).max() == 0:
                 continue
-            # FP32 sums over up to 8^L particles with cancellation (root multipole ~ 0)
-            assert rel(got, want) < 5e-5, (kind, l, rel(got, want))
+            # FP32 sums over up to 8^L particles with cancellation (root multipole ~ 0); at
+            # p = 16 the scaled M2L operators span ~(2p)! in magnitude and the high-order local
+            # coefficients of the coarse levels keep ~1e-4, while u and dgamma
+            # above still meet FMM_VS_FMM_ORACLE
+            tol = 5e-5 if p <= 12 else 5e-4
+            assert rel(got, want) < tol, (kind, l, rel(got, want))
     ev.close()
 
 
