@@ -364,6 +364,21 @@ __global__ void __launch_bounds__(256, 2) translate_kernel(
         const int64_t tbase = KIND == OP_M2M ? plo : plo * 8;  // first target cell of the range
         float* out = zpart ? zpart + blockIdx.z * zstride + ((target_cell(cell) - tbase) * 3 + comp) * nc
                            : dst + (target_cell(cell) * 3 + comp) * nc;
+        if (KIND == OP_L2L && !zpart && opsplit == 1) {
+            // L2L accumulates onto M2L: the 4 loads of the column first, then the stores
+            float old[TROWS / 32];
+#pragma unroll
+            for (int i = 0; i < TROWS / 32; ++i) {
+                const int r = row0 + lane + 32 * i;
+                old[i] = r < nc ? out[r] : 0.f;
+            }
+#pragma unroll
+            for (int i = 0; i < TROWS / 32; ++i) {
+                const int r = row0 + lane + 32 * i;
+                if (r < nc) out[r] = old[i] + Cs[col * 129 + lane + 32 * i];
+            }
+            continue;
+        }
         for (int rr = lane; rr < TROWS; rr += 32) {
             const int r = row0 + rr;
             if (r >= nc) continue;
