@@ -420,6 +420,7 @@ __global__ void __launch_bounds__(64) l2p_combine_kernel(
     float inv_a, const float* __restrict__ Lleaf, int use_near, int use_far,
     float* __restrict__ vel, float* __restrict__ dgam, int64_t leaf_lo, int64_t gbase,
     int64_t nout, const int* __restrict__ map_rowptr, const uint4* __restrict__ map_terms) {
+    (void)map_rowptr;  // fixed 4-term records (kept in the signature for the map's layout)
     const int p = PC > 0 ? PC : p_rt;
     // smem: D [ng][12]; Ls [3][nc].  The 12 columns of D are the combinations the output
     // needs: u = curl phi (3) and J[a][k] = d_k u_a (9), each a difference of two derivative
@@ -444,21 +445,14 @@ __global__ void __launch_bounds__(64) l2p_combine_kernel(
         // stage 1: curl columns (q < 3) from L; stage 2: the velocity-gradient columns from the
         // stage-1 rows (the map's src then indexes D itself)
         auto row = [&](int e, const float* src_base) {
-            // rows are multiples of 4 terms; a term is (src | half(coef) << 16)
-            const int t1 = __ldg(map_rowptr + e + 1) >> 2;
-            float v = 0.f, v1 = 0.f, v2 = 0.f, v3 = 0.f;  // four independent chains
-            auto term = [&](uint32_t u, float& acc) {
-                const float cf = __half2float(__ushort_as_half((unsigned short)(u >> 16)));
-                acc = fmaf(cf, src_base[u & 0xffffu], acc);
+            // one 16-byte record of 4 terms per row (record e; map_rowptr[e] = 4 e), a term is
+            // (src | half(coef) << 16): no row pointers on the dependent-load path
+            const uint4 q = __ldg(map_terms + e);
+            auto term = [&](uint32_t u) {
+                return __half2float(__ushort_as_half((unsigned short)(u >> 16))) *
+                       src_base[u & 0xffffu];
             };
-            for (int t = __ldg(map_rowptr + e) >> 2; t < t1; ++t) {
-                const uint4 q = __ldg(map_terms + t);
-                term(q.x, v);
-                term(q.y, v1);
-                term(q.z, v2);
-                term(q.w, v3);
-            }
-            sm[e] = (v + v1) + (v2 + v3);
+            sm[e] = (term(q.x) + term(q.y)) + (term(q.z) + term(q.w));
         };
         for (int i = threadIdx.x; i < ng * 3; i += 64) row((i / 3) * DQ + i % 3, Ls);
         __syncthreads();

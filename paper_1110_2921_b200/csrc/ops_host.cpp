@@ -22,6 +22,7 @@
 #include <cstring>
 #include <complex>
 #include <map>
+#include <stdexcept>
 #include <utility>
 #include <vector>
 
@@ -367,7 +368,10 @@ void build_l2p_map(int p, HostOps* out) {
                 out->l2p_src.push_back(t.first);
                 out->l2p_coef.push_back((float)t.second);
             }
-            while (out->l2p_src.size() & 3) {  // rows of 4k terms: four per 16-byte load
+            // every row has <= 4 terms (curl: two first-derivative entries of <= 2 terms each;
+            // grad u: one first-derivative entry): one 16-byte record per row
+            if (v.size() > 4) throw std::runtime_error("L2P map row with more than 4 terms");
+            for (size_t t = v.size(); t < 4; ++t) {  // exactly 4 slots: record e at 4 e
                 out->l2p_src.push_back(0);
                 out->l2p_coef.push_back(0.f);
             }
