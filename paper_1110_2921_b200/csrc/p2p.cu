@@ -306,7 +306,7 @@ constexpr int P2P_THREADS = 256;
 // sources per pass at 2 blocks / SM: 24 B per source (x y z gx | gy gz) or, with the staged
 // cross products, 36 B (x y z gx | gy gz sx sy | sz)
 template <bool SJ> constexpr int p2p_cap() { return SJ ? 3072 : 4352; }
-constexpr int P2P_PAD = 4;     // slack after each staged array for the prefetch reads
+constexpr int P2P_PAD = 4;     // slack after each staged array (keeps the arrays 16-byte aligned)
 
 // SJ (classical scheme only): accumulate with the staged source cross products s_j (Acc2S:
 // 38 instead of 41 FP32 instructions per pair, rounding ~1.4x larger since the sums carry
@@ -432,7 +432,7 @@ __global__ void __launch_bounds__(P2P_THREADS, 2) p2p_kernel(
                 const int rx = bx + nb % 3, ry = by + (nb / 3) % 3, rz = bz + nb / 9;
                 const int rl = rx + 4 * ry + 16 * rz;
                 const int js = max(rstart[rl], w0) - w0, je = min(rstart[rl + 1], w1) - w0;
-                if (js >= je) continue;  // leaf not in this window (keeps the prefetch in bounds)
+                if (js >= je) continue;  // leaf not in this window
                 // two sources per iteration; each source x two targets = one packed pair
                 // (SJ: the 4-wide second record; else the 2-wide one, zero-extended).  Loads
                 // are left to the compiler's schedule (an explicit one-iteration prefetch
