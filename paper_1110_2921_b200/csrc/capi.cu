@@ -37,6 +37,8 @@ struct vfmm_ctx {
     size_t g2_cap = 0;
     cudaStream_t side = nullptr;                   // coarse M2L levels run here, joined by events
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+    cudaEvent_t ev_gamma = nullptr;  // evaluate_host: strengths copied on the side stream
+    bool gamma_pending = false;      // the next evaluate waits for ev_gamma before the gather
     int* d_slots = nullptr;  // [8][189]
     int* d_groups = nullptr; // [8][72][4] offset groups (tensor-core M2L y-windows)
     float* m2m_scratch = nullptr;  // coarse-level op-split partials (M2M, SIMT M2L): main stream
@@ -503,6 +505,7 @@ vfmm_status vfmm_create(vfmm_ctx** out, const vfmm_params* prm, int device) {
             e2 = cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_greatest);
         if (e2 == cudaSuccess) e2 = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
         if (e2 == cudaSuccess) e2 = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
+        if (e2 == cudaSuccess) e2 = cudaEventCreateWithFlags(&c->ev_gamma, cudaEventDisableTiming);
         for (int i = 0; i < vfmm_ctx::NEV && e2 == cudaSuccess; ++i) e2 = cudaEventCreate(&c->ev[i]);
         if (e2 != cudaSuccess) s = cuda_fail(c, e2, "create");
     }
@@ -578,6 +581,10 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
     const KernelConsts kc = make_kernel_consts(P.sigma);
     CK(cudaEventRecord(c->ev[0], st), "event");
     if (P.mode == VFMM_MODE_DIRECT) {
+        if (c->gamma_pending) {
+            CK(cudaStreamWaitEvent(st, c->ev_gamma, 0), "wait h2d");
+            c->gamma_pending = false;
+        }
         launch_direct(pos, gamma, n, P.box_len, P.image_levels, P.scheme, kc, vel, dgamma, st);
         CK(cudaGetLastError(), "direct kernel");
         for (int i = 1; i < vfmm_ctx::NEV; ++i) CK(cudaEventRecord(c->ev[i], st), "event");
@@ -605,6 +612,10 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
                       st, &c->keys_sorted, &c->perm, &nl);
     CK(cudaEventRecord(c->ev[2], st), "event");
     launch_leaf_ranges(c->keys_sorted, n, depth, c->leaf_start, st);
+    if (c->gamma_pending) {  // evaluate_host: the strengths arrive on the side stream
+        CK(cudaStreamWaitEvent(st, c->ev_gamma, 0), "wait h2d");
+        c->gamma_pending = false;
+    }
     launch_gather(pos, gamma, c->perm, c->keys_sorted, n, g, c->sorted6, n, 0, st);
     nl += 2;
     CK(cudaGetLastError(), "tree kernels");
@@ -733,8 +744,20 @@ vfmm_status vfmm_evaluate_host(vfmm_ctx* c, int64_t n, const float* pos_h, const
     float* ds = dv + 3 * n;
     cudaStream_t st = c->own_stream;
     CK(cudaMemcpyAsync(dp, pos_h, 3 * n * sizeof(float), cudaMemcpyHostToDevice, st), "h2d");
-    CK(cudaMemcpyAsync(dg, gamma_h, 3 * n * sizeof(float), cudaMemcpyHostToDevice, st), "h2d");
+    // the strengths are first needed by the gather (after keys, sort and leaf ranges): copy
+    // them on the side stream so the copy overlaps the tree build (single-context path)
+    const bool overlap = !c->dist;
+    if (overlap) {
+        CK(cudaStreamWaitEvent(c->side, c->ev_join, 0), "order");  // previous evaluation done
+        CK(cudaMemcpyAsync(dg, gamma_h, 3 * n * sizeof(float), cudaMemcpyHostToDevice, c->side),
+           "h2d");
+        CK(cudaEventRecord(c->ev_gamma, c->side), "event");
+        c->gamma_pending = true;
+    } else {
+        CK(cudaMemcpyAsync(dg, gamma_h, 3 * n * sizeof(float), cudaMemcpyHostToDevice, st), "h2d");
+    }
     vfmm_status s = vfmm_evaluate(c, n, dp, dg, dv, ds, st);
+    c->gamma_pending = false;
     if (s != VFMM_OK) return s;
     CK(cudaMemcpyAsync(vel_h, dv, 3 * n * sizeof(float), cudaMemcpyDeviceToHost, st), "d2h");
     CK(cudaMemcpyAsync(dgamma_h, ds, 3 * n * sizeof(float), cudaMemcpyDeviceToHost, st), "d2h");
@@ -861,6 +884,7 @@ void vfmm_destroy(vfmm_ctx* c) {
     if (c->side) cudaStreamDestroy(c->side);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
+    if (c->ev_gamma) cudaEventDestroy(c->ev_gamma);
     dfree(c->g2_hi);
     dfree(c->g2_lo);
     for (auto* s : c->ranks) delete s;

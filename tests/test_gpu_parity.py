@@ -215,6 +215,19 @@ def test_evaluation_is_deterministic(engine, monkeypatch):
     ev1.close()
 
 
+@pytest.mark.parametrize("mode", ["fmm", "direct"])
+def test_host_buffers_match_device_buffers(mode):
+    """vfmm_evaluate_host (pageable host in/out; the strengths' copy overlaps the tree build on
+    a second stream) gives bitwise the device-buffer result, repeatedly."""
+    f = synthgen.isotropic(16, seed=8)
+    m = vf.MODE_FMM if mode == "fmm" else vf.MODE_DIRECT
+    v0, s0, ev = run(f, p=6, depth=2, image_levels=2, mode=m)
+    for _ in range(2):
+        vh, sh = ev.evaluate_host(f.pos, f.gamma)
+        assert np.array_equal(vh.astype(np.float64), v0) and np.array_equal(sh.astype(np.float64), s0)
+    ev.close()
+
+
 def test_c1_fmm_vs_direct_oracle():
     f = synthgen.make("c1")
     v, s, ev = run(f, p=4, depth=2, image_levels=3)
