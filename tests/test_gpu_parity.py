@@ -228,6 +228,40 @@ def test_host_buffers_match_device_buffers(mode):
     ev.close()
 
 
+def test_c_example_matches_python_binding():
+    """examples/vfmm_c_example.c drives the C ABI from plain C (vfmm_evaluate_host); its output
+    matches the Python binding on the same lattice field (inputs rebuilt in float32)."""
+    import os
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "examples", "vfmm_c_example")
+    lib = os.path.join(root, "paper_1110_2921_b200", "lib")
+    if not os.path.exists(exe):
+        subprocess.check_call(["gcc", "-O2", "-I", os.path.join(root, "include"), exe + ".c",
+                               "-L", lib, "-lvfmm", f"-Wl,-rpath,{lib}", "-lm", "-o", exe])
+    out = subprocess.run([exe, "16"], capture_output=True, text=True, check=True).stdout.split("\n")
+    n, p, depth = (int(t) for t in out[0].split()[:3])
+    assert (n, p, depth) == (16, 6, 2)
+    c_rows = np.array([[float(t) for t in out[k].split()] for k in (1, 2)])
+    lo, ln = np.float32(synthgen.BOX_LO), np.float32(synthgen.BOX_LEN)
+    h = ln / np.float32(n)
+    i = np.arange(n ** 3)
+    x = lo + h * ((i % n).astype(np.float32) + np.float32(0.5))
+    y = lo + h * (((i // n) % n).astype(np.float32) + np.float32(0.5))
+    z = lo + h * ((i // (n * n)).astype(np.float32) + np.float32(0.5))
+    v3 = h * h * h
+    g = np.stack([-np.cos(x) * np.sin(y) * np.sin(z) * v3, -np.sin(x) * np.cos(y) * np.sin(z) * v3,
+                  np.float32(2) * np.sin(x) * np.sin(y) * np.cos(z) * v3]).astype(np.float32)
+    pos = np.stack([x, y, z]).astype(np.float32)
+    ev = vf.Evaluator(p=6, depth=2, image_levels=3, sigma=float(h), box_lo=float(lo),
+                      box_len=float(ln))
+    v, s = ev.evaluate_host(pos, g)
+    py_rows = np.array([np.concatenate([v[:, k], s[:, k]]) for k in (0, n ** 3 - 1)])
+    assert np.allclose(c_rows, py_rows, rtol=1e-4, atol=1e-6 * np.abs(py_rows).max()), (c_rows, py_rows)
+    ev.close()
+
+
 def test_c1_fmm_vs_direct_oracle():
     f = synthgen.make("c1")
     v, s, ev = run(f, p=4, depth=2, image_levels=3)
