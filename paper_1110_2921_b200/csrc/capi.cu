@@ -173,9 +173,9 @@ vfmm_status ensure_ops(vfmm_ctx* c) {
     dfree(c->m2m_scratch);
     dfree(c->side_scratch);
     {
-        // largest op-split partial set: M2M of <= 1024 coarse parents x 8 children, or a SIMT
-        // M2L level with < 296 tiles (opsplit slices x 8 children x parents), launch_m2l
-        size_t need = (size_t)8 * 1024;
+        // largest op-split partial set: M2M of < 296 x 32 parents (< 2 tiles per SM) x 8
+        // children, or a SIMT M2L level with < 296 tiles (slices x 8 children x parents)
+        size_t need = (size_t)8 * 4096;
         for (int64_t pc = 1; pc <= 4096; pc *= 8) {
             const int64_t tiles = 8 * ((pc + 31) / 32) * (c->hops.NR / 128);
             const int64_t os = tiles >= 296 ? 1 : std::min<int64_t>(27, (296 + tiles - 1) / tiles);

@@ -625,7 +625,7 @@ int launch_m2m(const float* ops_m2m, int p, int KP, int NR, const float* M_child
     const int64_t tiles = (pcnt + TCELLS - 1) / TCELLS;
     const int64_t zstride = pcnt * 3 * nc;
     translate_attrs();
-    if (tiles < 32 && scratch && (size_t)(8 * zstride) <= scratch_floats) {
+    if (tiles < 296 && scratch && (size_t)(8 * zstride) <= scratch_floats) {
         // coarse levels: one block per child octant (8 x the parallelism of the serial
         // 8-child chain), partials summed in child order by zsum_kernel (deterministic)
         dim3 grid((unsigned)tiles, NR / TROWS, 8);

@@ -84,8 +84,8 @@ void launch_gather(const float* pos, const float* gamma, const uint32_t* perm,
 // expansions.cu  (ranges: the owned part of the tree; whole tree for one rank)
 void launch_p2m(const float* sorted6, int64_t n, const int* leaf_start, int p, float inv_a,
                 float* M_leaf, int64_t leaf_lo, int64_t leaf_cnt, cudaStream_t st);
-// returns the number of kernels launched; scratch (>= 8 x 3 nc x 512 floats) enables the
-// deterministic op split at coarse levels (< 32 tiles)
+// returns the number of kernels launched; scratch (>= 8 x 3 nc x parents floats) enables the
+// deterministic op split at coarse levels (< 296 tiles of 32 parents)
 int launch_m2m(const float* ops_m2m, int p, int KP, int NR, const float* M_child, float* M_par,
                int level_par, int64_t plo, int64_t pcnt, float* scratch, size_t scratch_floats,
                cudaStream_t st);
