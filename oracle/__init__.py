@@ -22,48 +22,54 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-_LIB = None
 
 
-def lib_path() -> str:
-    return os.path.join(_HERE, "liboracle.so")
+def lib_path(native: bool = False) -> str:
+    return os.path.join(_HERE, "liboracle_native.so" if native else "liboracle.so")
 
 
-def build(force: bool = False) -> str:
-    """Compile liboracle.so with gcc (-O2 -fopenmp -ffp-contract=off, no fast-math)."""
+def build(force: bool = False, native: bool = False) -> str:
+    """Compile liboracle.so with gcc (-O3 -fopenmp -ffp-contract=off, no fast-math;
+    -fno-math-errno only drops errno writes, results are unchanged).  native=True builds a
+    -march=native copy (liboracle_native.so) for long runs on this host only (same source,
+    same IEEE operations: see test_batched_oracle_is_bitwise_the_plain_one)."""
     import subprocess
 
-    out = lib_path()
+    out = lib_path(native)
     src = os.path.join(_HERE, "oracle.c")
     if force or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(src):
         subprocess.check_call([
-            "gcc", "-O2", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-fPIC",
-            "-shared", "-o", out, src, "-lm",
+            "gcc", "-O3", "-fopenmp", "-ffp-contract=off", "-fno-fast-math", "-fno-math-errno",
+            "-fPIC", "-shared", *(["-march=native", "-mprefer-vector-width=512"] if native else []), "-o", out, src, "-lm",
         ])
     return out
 
 
-def _lib():
-    global _LIB
-    if _LIB is None:
-        path = build()
+_LIBS = {}
+
+
+def _lib(native: bool = False):
+    if native not in _LIBS:
+        path = build(native=native)
         L = ctypes.CDLL(path)
         dp = ctypes.POINTER(ctypes.c_double)
         L.vfmm_oracle_kernels.argtypes = [ctypes.c_double, ctypes.c_double, dp, dp, dp, dp]
         L.vfmm_oracle_kernels.restype = None
-        L.vfmm_oracle_eval.argtypes = [
-            ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double, ctypes.c_double,
-            ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int64, ctypes.c_void_p,
-            ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_int,
-        ]
-        L.vfmm_oracle_eval.restype = ctypes.c_int
+        for fn in (L.vfmm_oracle_eval, L.vfmm_oracle_eval_batched):
+            fn.argtypes = [
+                ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double,
+                ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int64,
+                ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
+                ctypes.c_void_p, ctypes.c_int,
+            ]
+            fn.restype = ctypes.c_int
         L.vfmm_oracle_morton.argtypes = [
             ctypes.c_int64, ctypes.c_void_p, ctypes.c_int, ctypes.c_float, ctypes.c_float,
             ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
         ]
         L.vfmm_oracle_morton.restype = ctypes.c_int
-        _LIB = L
-    return _LIB
+        _LIBS[native] = L
+    return _LIBS[native]
 
 
 def kernels(r: float, sigma: float):
@@ -79,12 +85,14 @@ def _c(a, dtype):
 
 
 def direct(pos, gamma, sigma, box_lo, box_len, image_levels=3, scheme=0, targets=None,
-           probe_pos=None, probe_gamma=None, nthreads=0):
+           probe_pos=None, probe_gamma=None, nthreads=0, batched=False, native=False):
     """Direct periodic-image sum (oracle O1).
 
     pos, gamma: (3, N) arrays (SoA); values are widened exactly to float64.
     targets: optional int index array into the sources; probe_pos/probe_gamma: (3, T)
     explicit probes (targets != sources).  Returns (vel, dgamma), each (3, T) float64.
+    batched=True runs vfmm_oracle_eval_batched (bitwise the same result, one pass over the
+    sources per image serves 16 targets: for long sampled-target runs).
     """
     pos = _c(pos, np.float64)
     gamma = _c(gamma, np.float64)
@@ -100,7 +108,8 @@ def direct(pos, gamma, sigma, box_lo, box_len, image_levels=3, scheme=0, targets
         tp = tg = None
     vel = np.zeros((3, nt), np.float64)
     dg = np.zeros((3, nt), np.float64)
-    rc = _lib().vfmm_oracle_eval(
+    L = _lib(native)
+    rc = (L.vfmm_oracle_eval_batched if batched else L.vfmm_oracle_eval)(
         n, pos.ctypes.data, gamma.ctypes.data, float(sigma), float(box_lo), float(box_len),
         int(image_levels), int(scheme), nt, None if tidx is None else tidx.ctypes.data,
         None if tp is None else tp.ctypes.data, None if tg is None else tg.ctypes.data,

@@ -45,10 +45,11 @@
 
 /* ---- scalar kernels ------------------------------------------------------ */
 
-/* Returns zeta, g, f, q at distance r (r >= 0) for core radius sigma > 0. */
-void vfmm_oracle_kernels(double r, double sigma, double* zeta, double* g, double* f, double* q)
+/* zeta, g, f, q at distance r (r >= 0) for core radius sigma > 0, given
+   zeta0 = (2 pi sigma^2)^(-3/2) (hoisted out of the pair loops: the same double value). */
+static inline void or_kernels(double r, double sigma, double zeta0, double* zeta, double* g,
+                              double* f, double* q)
 {
-    const double zeta0 = pow(2.0 * OR_PI * sigma * sigma, -1.5);
     const double rho2 = r * r / (2.0 * sigma * sigma);
     const double rho = sqrt(rho2);
     if (r == 0.0) {
@@ -91,7 +92,42 @@ void vfmm_oracle_kernels(double r, double sigma, double* zeta, double* g, double
     *q = (*zeta - 3.0 * (*f)) / (r * r);
 }
 
+static double or_zeta0(double sigma) { return pow(2.0 * OR_PI * sigma * sigma, -1.5); }
+
+/* Returns zeta, g, f, q at distance r (r >= 0) for core radius sigma > 0. */
+void vfmm_oracle_kernels(double r, double sigma, double* zeta, double* g, double* f, double* q)
+{
+    or_kernels(r, sigma, or_zeta0(sigma), zeta, g, f, q);
+}
+
 /* ---- direct sum ----------------------------------------------------------- */
+/* One source-target pair's contribution (PAPER.md:81 Eq. 5, :100 Eq. 8):
+   c = gamma_j x d;  u += f c;
+   classical (scheme 0): s += f (gamma_j x gamma_i) + q (gamma_i . d) c
+   transpose (scheme 1): s += f (gamma_i x gamma_j) + q (gamma_i . c) d */
+static inline void or_pair(int scheme, double f, double q, double d0, double d1, double d2,
+                           double gj0, double gj1, double gj2, const double gi[3], double u[3],
+                           double s[3])
+{
+    const double c0 = gj1 * d2 - gj2 * d1;
+    const double c1 = gj2 * d0 - gj0 * d2;
+    const double c2 = gj0 * d1 - gj1 * d0;
+    u[0] += f * c0;
+    u[1] += f * c1;
+    u[2] += f * c2;
+    if (scheme == 0) {
+        const double gd = gi[0] * d0 + gi[1] * d1 + gi[2] * d2;
+        s[0] += f * (gj1 * gi[2] - gj2 * gi[1]) + q * gd * c0;
+        s[1] += f * (gj2 * gi[0] - gj0 * gi[2]) + q * gd * c1;
+        s[2] += f * (gj0 * gi[1] - gj1 * gi[0]) + q * gd * c2;
+    } else {
+        const double gc = gi[0] * c0 + gi[1] * c1 + gi[2] * c2;
+        s[0] += f * (gi[1] * gj2 - gi[2] * gj1) + q * gc * d0;
+        s[1] += f * (gi[2] * gj0 - gi[0] * gj2) + q * gc * d1;
+        s[2] += f * (gi[0] * gj1 - gi[1] * gj0) + q * gc * d2;
+    }
+}
+
 
 /*
  * n_src sources (SoA 3 x n_src doubles: x[0..n), y[..], z[..]).
@@ -116,6 +152,7 @@ int vfmm_oracle_eval(int64_t n_src, const double* src_pos, const double* src_gam
     const int side = 2 * m + 1;
     const int64_t n_img = (int64_t)side * side * side;
     const int periodic = image_levels > 0;
+    const double zeta0 = or_zeta0(sigma);
 
 #ifdef _OPENMP
     if (nthreads > 0) omp_set_num_threads(nthreads);
@@ -149,28 +186,9 @@ int vfmm_oracle_eval(int64_t n_src, const double* src_pos, const double* src_gam
                 const double d2 = xi[2] - src_pos[j + 2 * n_src] - sz;
                 const double r = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
                 double zeta, g, f, q;
-                vfmm_oracle_kernels(r, sigma, &zeta, &g, &f, &q);
-                const double gj0 = src_gam[j], gj1 = src_gam[j + n_src], gj2 = src_gam[j + 2 * n_src];
-                /* c = gamma_j x d */
-                const double c0 = gj1 * d2 - gj2 * d1;
-                const double c1 = gj2 * d0 - gj0 * d2;
-                const double c2 = gj0 * d1 - gj1 * d0;
-                u[0] += f * c0;
-                u[1] += f * c1;
-                u[2] += f * c2;
-                if (scheme == 0) {
-                    /* f (gamma_j x gamma_i) + q (gamma_i . d) (gamma_j x d) */
-                    const double gd = gi[0] * d0 + gi[1] * d1 + gi[2] * d2;
-                    s[0] += f * (gj1 * gi[2] - gj2 * gi[1]) + q * gd * c0;
-                    s[1] += f * (gj2 * gi[0] - gj0 * gi[2]) + q * gd * c1;
-                    s[2] += f * (gj0 * gi[1] - gj1 * gi[0]) + q * gd * c2;
-                } else {
-                    /* f (gamma_i x gamma_j) + q (gamma_i . (gamma_j x d)) d */
-                    const double gc = gi[0] * c0 + gi[1] * c1 + gi[2] * c2;
-                    s[0] += f * (gi[1] * gj2 - gi[2] * gj1) + q * gc * d0;
-                    s[1] += f * (gi[2] * gj0 - gi[0] * gj2) + q * gc * d1;
-                    s[2] += f * (gi[0] * gj1 - gi[1] * gj0) + q * gc * d2;
-                }
+                or_kernels(r, sigma, zeta0, &zeta, &g, &f, &q);
+                or_pair(scheme, f, q, d0, d1, d2, src_gam[j], src_gam[j + n_src],
+                        src_gam[j + 2 * n_src], gi, u, s);
             }
             for (int k = 0; k < 3; ++k) {
                 U[k] += u[k];
@@ -182,6 +200,114 @@ int vfmm_oracle_eval(int64_t n_src, const double* src_pos, const double* src_gam
             dgam[t + k * n_tgt] = S[k];
         }
     }
+    return 0;
+}
+
+/*
+ * Same sum, same result bit for bit, loops reordered for large sampled-target runs
+ * (tests/golden reference values at 27^3 images): targets go in batches of OR_TB; for each
+ * image (in parallel) one pass over the sources serves the whole batch, each target keeping
+ * its own per-image partial sums in the same j order as vfmm_oracle_eval; the per-image
+ * partials are then added in the same lexicographic image order.  Only the loop nest differs,
+ * so every floating-point operation and its order per target is vfmm_oracle_eval's
+ * (tests/test_oracle_pins.py::test_batched_oracle_is_bitwise_the_plain_one).
+ * Same arguments and return value as vfmm_oracle_eval; -2 if the partials cannot be allocated.
+ */
+#define OR_TB 16
+int vfmm_oracle_eval_batched(int64_t n_src, const double* src_pos, const double* src_gam,
+                             double sigma, double box_lo, double box_len, int image_levels,
+                             int scheme, int64_t n_tgt, const int64_t* tgt_idx,
+                             const double* tgt_pos, const double* tgt_gam, double* vel,
+                             double* dgam, int nthreads)
+{
+    (void)box_lo;
+    if (n_src < 1 || !(sigma > 0.0) || !(box_len > 0.0) || image_levels < 0 ||
+        image_levels > 6 || (scheme != 0 && scheme != 1) || n_tgt < 0)
+        return -1;
+    if (tgt_idx == NULL && (tgt_pos == NULL || tgt_gam == NULL)) return -1;
+    int m = 0;
+    for (int l = 0; l < image_levels; ++l) m = 3 * m + 1;
+    if (image_levels == 0) m = 0;
+    const int side = 2 * m + 1;
+    const int periodic = image_levels > 0;
+    const int64_t n_img = periodic ? (int64_t)side * side * side : 1;
+    const double zeta0 = or_zeta0(sigma);
+    const double far_r = 12.0 * sigma;
+    double* part = (double*)malloc(sizeof(double) * 6 * OR_TB * (size_t)n_img);
+    if (!part) return -2;
+#ifdef _OPENMP
+    if (nthreads > 0) omp_set_num_threads(nthreads);
+#else
+    (void)nthreads;
+#endif
+    for (int64_t t0 = 0; t0 < n_tgt; t0 += OR_TB) {
+        const int nb = (int)((n_tgt - t0) < OR_TB ? (n_tgt - t0) : OR_TB);
+        double xi[3][OR_TB], gi[3][OR_TB];
+        for (int b = 0; b < OR_TB; ++b) { /* unused lanes repeat the batch's first target */
+            const int64_t t = t0 + (b < nb ? b : 0);
+            for (int k = 0; k < 3; ++k) {
+                xi[k][b] = tgt_idx ? src_pos[tgt_idx[t] + k * n_src] : tgt_pos[t + k * n_tgt];
+                gi[k][b] = tgt_idx ? src_gam[tgt_idx[t] + k * n_src] : tgt_gam[t + k * n_tgt];
+            }
+        }
+#pragma omp parallel for schedule(dynamic, 1)
+        for (int64_t im = 0; im < n_img; ++im) {
+            const int nx = periodic ? (int)(im / ((int64_t)side * side)) - m : 0;
+            const int ny = periodic ? (int)((im / side) % side) - m : 0;
+            const int nz = periodic ? (int)(im % side) - m : 0;
+            const double sx = nx * box_len, sy = ny * box_len, sz = nz * box_len;
+            double u[OR_TB][3], s[OR_TB][3];
+            memset(u, 0, sizeof u);
+            memset(s, 0, sizeof s);
+            for (int64_t j = 0; j < n_src; ++j) {
+                const double xj0 = src_pos[j], xj1 = src_pos[j + n_src], xj2 = src_pos[j + 2 * n_src];
+                const double gj0 = src_gam[j], gj1 = src_gam[j + n_src], gj2 = src_gam[j + 2 * n_src];
+                double d0[OR_TB], d1[OR_TB], d2[OR_TB], r[OR_TB];
+                int n_far = 0;
+                for (int b = 0; b < OR_TB; ++b) {
+                    d0[b] = xi[0][b] - xj0 - sx;
+                    d1[b] = xi[1][b] - xj1 - sy;
+                    d2[b] = xi[2][b] - xj2 - sz;
+                    r[b] = sqrt(d0[b] * d0[b] + d1[b] * d1[b] + d2[b] * d2[b]);
+                    n_far += r[b] >= far_r;
+                }
+                if (n_far == OR_TB) { /* or_kernels' r >= 12 sigma branch, for every lane */
+                    for (int b = 0; b < OR_TB; ++b) {
+                        const double f = 1.0 / (4.0 * OR_PI * r[b] * r[b] * r[b]);
+                        const double q = -3.0 * f / (r[b] * r[b]);
+                        const double g3[3] = {gi[0][b], gi[1][b], gi[2][b]};
+                        or_pair(scheme, f, q, d0[b], d1[b], d2[b], gj0, gj1, gj2, g3, u[b], s[b]);
+                    }
+                } else {
+                    for (int b = 0; b < OR_TB; ++b) {
+                        double zeta, g, f, q;
+                        or_kernels(r[b], sigma, zeta0, &zeta, &g, &f, &q);
+                        const double g3[3] = {gi[0][b], gi[1][b], gi[2][b]};
+                        or_pair(scheme, f, q, d0[b], d1[b], d2[b], gj0, gj1, gj2, g3, u[b], s[b]);
+                    }
+                }
+            }
+            double* P = part + (size_t)im * 6 * OR_TB;
+            for (int b = 0; b < OR_TB; ++b)
+                for (int k = 0; k < 3; ++k) {
+                    P[b * 6 + k] = u[b][k];
+                    P[b * 6 + 3 + k] = s[b][k];
+                }
+        }
+        for (int b = 0; b < nb; ++b) {
+            double U[3] = {0, 0, 0}, S[3] = {0, 0, 0};
+            for (int64_t im = 0; im < n_img; ++im) /* lexicographic image order */
+                for (int k = 0; k < 3; ++k) {
+                    U[k] += part[(size_t)im * 6 * OR_TB + b * 6 + k];
+                    S[k] += part[(size_t)im * 6 * OR_TB + b * 6 + 3 + k];
+                }
+            for (int k = 0; k < 3; ++k) {
+                vel[t0 + b + k * n_tgt] = U[k];
+                dgam[t0 + b + k * n_tgt] = S[k];
+            }
+        }
+    }
+    free(part);
     return 0;
 }
 
