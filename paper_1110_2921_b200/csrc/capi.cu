@@ -43,7 +43,7 @@ struct vfmm_ctx {
     int* d_groups = nullptr; // [8][72][4] offset groups (tensor-core M2L y-windows)
     float* m2m_scratch = nullptr;  // coarse-level op-split partials (M2M, SIMT M2L): main stream
     float* side_scratch = nullptr; // the same for the side stream's SIMT M2L levels
-    size_t m2m_scratch_floats = 0;
+    size_t m2m_scratch_floats = 0, side_scratch_floats = 0;
     int *d_l2p_rowptr = nullptr, *d_l2p_pairs = nullptr;  // L2P derivative map (CSR)
     // workspace
     int64_t cap_n = 0;
@@ -62,6 +62,7 @@ struct vfmm_ctx {
     cudaStream_t own_stream = nullptr;
     // last evaluate
     cudaStream_t last_stream = nullptr;
+    bool have_last = false;  // ev[NEV-1] marks the end of an earlier evaluate
     uint32_t *keys_sorted = nullptr, *perm = nullptr;
     int64_t last_n = 0;
     int last_depth = 0;
@@ -154,7 +155,17 @@ void dfree(T*& p) {
 
 vfmm_status ensure_ops(vfmm_ctx* c) {
     if (c->ops_p == c->prm.p && c->ops_levels == c->prm.image_levels) return VFMM_OK;
-    build_host_ops(c->prm.p, c->prm.image_levels, &c->hops);
+    // nothing may throw across the C ABI: host table construction allocates (bad_alloc) and
+    // checks its own invariants (runtime_error)
+    try {
+        build_host_ops(c->prm.p, c->prm.image_levels, &c->hops);
+    } catch (const std::bad_alloc&) {
+        c->err = "host operator tables: out of memory";
+        return VFMM_ENOMEM;
+    } catch (const std::exception& ex) {
+        c->err = std::string("host operator tables: ") + ex.what();
+        return VFMM_ESTATE;
+    }
     dfree(c->d_m2m);
     dfree(c->d_l2l);
     dfree(c->d_m2l);
@@ -174,18 +185,20 @@ vfmm_status ensure_ops(vfmm_ctx* c) {
     dfree(c->side_scratch);
     {
         // largest op-split partial set: M2M of < 296 x 32 parents (< 2 tiles per SM) x 8
-        // children, or a SIMT M2L level with < 296 tiles (slices x 8 children x parents)
-        size_t need = (size_t)8 * 4096;
+        // children (main stream only), or a SIMT M2L level with < 296 tiles (slices x 8
+        // children x parents; main stream for level L, side stream for the coarse levels)
+        size_t need_m2l = 0;
         for (int64_t pc = 1; pc <= 4096; pc *= 8) {
             const int64_t tiles = 8 * ((pc + 31) / 32) * (c->hops.NR / 128);
             const int64_t os = tiles >= 296 ? 1 : std::min<int64_t>(27, (296 + tiles - 1) / tiles);
-            if (os > 1) need = std::max(need, (size_t)(os * 8 * pc));
+            if (os > 1) need_m2l = std::max(need_m2l, (size_t)(os * 8 * pc));
         }
-        c->m2m_scratch_floats = need * 3 * c->hops.nc;
+        c->m2m_scratch_floats = std::max<size_t>((size_t)8 * 4096, need_m2l) * 3 * c->hops.nc;
+        c->side_scratch_floats = std::max<size_t>(need_m2l, 1) * 3 * c->hops.nc;
     }
     CK(cudaMalloc((void**)&c->m2m_scratch, c->m2m_scratch_floats * sizeof(float)),
        "alloc op-split scratch");
-    CK(cudaMalloc((void**)&c->side_scratch, c->m2m_scratch_floats * sizeof(float)),
+    CK(cudaMalloc((void**)&c->side_scratch, c->side_scratch_floats * sizeof(float)),
        "alloc op-split scratch");
     {
         auto upi = [&](const std::vector<int>& h, int** d) -> cudaError_t {
@@ -545,6 +558,11 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
     CK(cudaSetDevice(c->device), "set device");
     (void)cudaGetLastError();  // drop stale non-sticky errors of unrelated earlier calls
     cudaStream_t st = (cudaStream_t)stream;
+    // the workspace is shared by every evaluate of this context: work on a new stream waits
+    // for the previous evaluate (its last event) before touching it
+    if (c->last_stream != st && c->have_last)
+        CK(cudaStreamWaitEvent(st, c->ev[vfmm_ctx::NEV - 1], 0), "order after last evaluate");
+    c->have_last = true;
     if (c->dist) {  // distributed evaluation over NCCL (this process = one rank)
         ensure_rank_states(c, c->R, c->rank, 1);
         DistShared D = make_shared(c, c->R);
@@ -682,7 +700,7 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
                 nl += launch_m2l(c->d_m2l, c->d_slots, p, H.KP, H.NR, Mlev(l), Llev(l), l,
                                  P.image_levels > 0, 0, (int64_t)1 << (3 * (l - 1)),
                                  l == depth ? c->m2m_scratch : c->side_scratch,
-                                 c->m2m_scratch_floats, sl);
+                                 l == depth ? c->m2m_scratch_floats : c->side_scratch_floats, sl);
             }
             S.n_m2l += (int64_t)189 << (3 * l);
         }
@@ -758,7 +776,12 @@ vfmm_status vfmm_evaluate_host(vfmm_ctx* c, int64_t n, const float* pos_h, const
     }
     vfmm_status s = vfmm_evaluate(c, n, dp, dg, dv, ds, st);
     c->gamma_pending = false;
-    if (s != VFMM_OK) return s;
+    if (s != VFMM_OK) {
+        // the caller's buffers may still be read by queued H2D copies: drain before returning
+        cudaStreamSynchronize(st);
+        cudaStreamSynchronize(c->side);
+        return s;
+    }
     CK(cudaMemcpyAsync(vel_h, dv, 3 * n * sizeof(float), cudaMemcpyDeviceToHost, st), "d2h");
     CK(cudaMemcpyAsync(dgamma_h, ds, 3 * n * sizeof(float), cudaMemcpyDeviceToHost, st), "d2h");
     return vfmm_sync_status(c);

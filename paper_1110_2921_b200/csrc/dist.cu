@@ -352,7 +352,8 @@ vfmm_status dist_phase1(RankState& S, const DistShared& D, cudaStream_t st, std:
         dfree(S.counts_all);
         dfree(S.gstart);
         DCK(cudaMalloc((void**)&S.lstart, (nleaf + 1) * 4), "alloc lstart");
-        DCK(cudaMalloc((void**)&S.counts_own, (nleaf / R) * 4), "alloc counts");
+        // sized for R = 1 (the largest owned range): R may change between calls at one depth
+        DCK(cudaMalloc((void**)&S.counts_own, nleaf * 4), "alloc counts");
         DCK(cudaMalloc((void**)&S.counts_all, nleaf * 4), "alloc counts");
         DCK(cudaMalloc((void**)&S.gstart, (nleaf + 1) * 4), "alloc gstart");
     }

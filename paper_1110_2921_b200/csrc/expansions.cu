@@ -577,15 +577,15 @@ __global__ void zsum_kernel(const float* __restrict__ part, int64_t stride, int 
 }
 
 void translate_attrs() {
-    static bool done = false;
-    if (done) return;
-    cudaFuncSetAttribute(translate_kernel<OP_M2M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)TRANSLATE_SMEM);
-    cudaFuncSetAttribute(translate_kernel<OP_L2L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)TRANSLATE_SMEM);
-    cudaFuncSetAttribute(translate_kernel<OP_M2L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)TRANSLATE_SMEM);
-    done = true;
+    static PerDeviceOnce once;
+    once([] {
+        cudaFuncSetAttribute(translate_kernel<OP_M2M>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)TRANSLATE_SMEM);
+        cudaFuncSetAttribute(translate_kernel<OP_L2L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)TRANSLATE_SMEM);
+        cudaFuncSetAttribute(translate_kernel<OP_M2L>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)TRANSLATE_SMEM);
+    });
 }
 
 }  // namespace
@@ -594,15 +594,14 @@ void launch_p2m(const float* sorted6, int64_t n, const int* leaf_start, int p, f
                 float* M_leaf, int64_t leaf_lo, int64_t leaf_cnt, cudaStream_t st) {
     const int nc = (p + 1) * (p + 1);
     const size_t smem = sizeof(float) * (nc * 36 + 3 * 32);
-    static bool attr = false;
-    if (!attr) {
+    static PerDeviceOnce once;
+    once([] {
         const void* ks[] = {(const void*)p2m_kernel<0>, (const void*)p2m_kernel<4>,
                             (const void*)p2m_kernel<6>, (const void*)p2m_kernel<8>,
                             (const void*)p2m_kernel<10>};
         for (const void* k : ks)
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        attr = true;
-    }
+    });
     if (leaf_cnt <= 0) return;
     auto go = [&](auto kern) {
         kern<<<(unsigned)leaf_cnt, 64, smem, st>>>(sorted6, n, leaf_start, p, inv_a, M_leaf,
@@ -692,18 +691,16 @@ void launch_l2p_combine(const L2PMap& map, const float* sorted6, const float* ne
     const size_t smem = sizeof(float) * (ng * 12 + 3 * nc);
     if (leaf_cnt <= 0) return;
     const float inv_a = 1.f / a;
-    static bool attr = false;
-    if (!attr) {
+    static PerDeviceOnce once;
+    once([] {
         const void* ks[] = {(const void*)l2p_combine_kernel<0, 4>, (const void*)l2p_combine_kernel<1, 4>,
                             (const void*)l2p_combine_kernel<0, 6>, (const void*)l2p_combine_kernel<1, 6>,
                             (const void*)l2p_combine_kernel<0, 8>, (const void*)l2p_combine_kernel<1, 8>,
                             (const void*)l2p_combine_kernel<0, 10>, (const void*)l2p_combine_kernel<1, 10>,
                             (const void*)l2p_combine_kernel<0, 0>, (const void*)l2p_combine_kernel<1, 0>};
-        for (const void* k : ks) {
+        for (const void* k : ks)
             cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-        }
-        attr = true;
-    }
+    });
     auto go = [&](auto kern) {
         kern<<<(unsigned)leaf_cnt, 64, smem, st>>>(sorted6, near6, perm, n, leaf_start, p, inv_a,
                                                    L_leaf, use_near, use_far, vel, dgam, leaf_lo,

@@ -654,14 +654,13 @@ int launch_m2l_tc(const TcOps& ops, const int* il_slots, int p, const float* M_l
                 CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return -3;
     }
-    static bool attr = false;
-    if (!attr) {
+    static PerDeviceOnce once;
+    once([] {
         cudaFuncSetAttribute(m2l_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)TC_SMEM);
         cudaFuncSetAttribute(m2l_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)TC_SMEM);
-        attr = true;
-    }
+    });
     TcParams P;
     P.nP = nP;
     P.XT = XT;

@@ -623,16 +623,15 @@ void launch_p2p(const float* sorted6, int64_t n, const int* leaf_start, int dept
                 unsigned long long* npairs, int64_t plo, int64_t pcnt, cudaStream_t st) {
     const size_t smem_sj = (size_t)(p2p_cap<true>() + P2P_PAD) * (2 * sizeof(float4) + sizeof(float));
     const size_t smem_x = (size_t)(p2p_cap<false>() + P2P_PAD) * (sizeof(float4) + sizeof(float2));
-    static bool attr = false;
-    if (!attr) {
+    static PerDeviceOnce once;
+    once([&] {
         cudaFuncSetAttribute(p2p_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem_sj);
         cudaFuncSetAttribute(p2p_kernel<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem_x);
         cudaFuncSetAttribute(p2p_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)smem_x);
-        attr = true;
-    }
+    });
     if (pcnt <= 0) return;
     // default: per-pair cross products gamma_j x d (FP32-faithful rounding); VFMM_P2P=sj: the
     // classical scheme with staged source cross products (~3% faster at c4, 2-4x the rounding)

@@ -3,6 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -13,6 +14,23 @@ namespace vfmm {
 constexpr int kPMax = VFMM_PMAX;
 
 inline int ncoef(int p) { return (p + 1) * (p + 1); }
+
+// Runs f() once per CUDA device (the current one), thread-safe.  Kernel attributes such as
+// cudaFuncAttributeMaxDynamicSharedMemorySize are per device, so a process driving several
+// devices must set them on each.
+struct PerDeviceOnce {
+    std::mutex m;
+    uint64_t done = 0;
+    template <class F>
+    void operator()(F&& f) {
+        int d = 0;
+        cudaGetDevice(&d);
+        std::lock_guard<std::mutex> g(m);
+        if (d < 0 || d > 63 || ((done >> d) & 1)) return;
+        f();
+        done |= uint64_t(1) << d;
+    }
+};
 
 // Packed real coefficient index:
 // Re(n,0) -> n^2 ; Re(n,m) -> n^2 + 2m - 1 ; Im(n,m) -> n^2 + 2m   (m >= 1)

@@ -10,7 +10,9 @@ particle fields the paper's runs use (section 4.2, :183-191):
   E(k) ~ k^4 exp(-2k^2/k_p^2), k_p = 4 (Rogallo), normalised so the
   large-eddy turnover time T = L/u' = 2; omega is the exact spectral curl
   evaluated at cell centres (reading R15, instead of the paper's 4th-order differences);
-* c5 stand-in: a von Karman-Pao spectrum with more small-scale content (reading R14).
+* c5 stand-in: a von Karman-Pao spectrum with more small-scale content (reading R14);
+* robustness fields (not timed): jittered lattices, clustered random points (non-uniform
+  leaves: empty and overfull), dense leaves, distinct coincident particles.
 
 Everything is float32 on output (the GPU path's precision); the box is
 lo = float32(-pi), len = float32(2 pi) (reading R8).
@@ -132,8 +134,10 @@ def isotropic(n: int, seed: int = 11102921, kind: str = "pp", kp: float = 4.0,
                  f"isotropic_{kind}_{n}_s{seed}")
 
 
-def jitter(f: Field, frac: float = 0.25, seed: int = 2) -> Field:
-    """Move each particle uniformly by +-frac*h per axis and re-wrap into [lo, lo+len)."""
+def jitter(f: Field, frac: float = 0.75, seed: int = 2) -> Field:
+    """Move each particle uniformly by +-frac*h per axis and re-wrap into [lo, lo+len).
+    frac > 0.5 moves particles across lattice cells (and leaf faces), so leaves hold unequal
+    counts, some leaves can be empty, and pairs come arbitrarily close."""
     rng = np.random.default_rng(seed)
     h = f.box_len / f.n
     p = f.pos.astype(np.float64) + rng.uniform(-frac * h, frac * h, f.pos.shape)
@@ -186,3 +190,34 @@ def sample_targets(n_total: int, count: int, seed: int = 3, n_lattice: int | Non
     while len(out) < count:
         out.add(int(rng.integers(0, n_total)))
     return np.array(sorted(out), np.int64)
+
+
+def clustered(n: int, n_clusters: int = 12, spread: float = 0.25, seed: int = 31,
+              sigma: float = 0.05, strength: float = 1e-3) -> Field:
+    """n random points in Gaussian clusters (std `spread`, wrapped into the box) around
+    uniform random centres, plus normal strengths: strongly non-uniform leaf occupancy (many
+    empty leaves, some with hundreds of particles) for robustness tests."""
+    rng = np.random.default_rng(seed)
+    lo, ln = float(BOX_LO), float(BOX_LEN)
+    centres = rng.uniform(lo, lo + ln, (3, n_clusters))
+    which = rng.integers(0, n_clusters, n)
+    p = centres[:, which] + rng.normal(0.0, spread, (3, n))
+    p = lo + np.mod(p - lo, ln)
+    p32 = p.astype(np.float32)
+    hi = np.float32(BOX_LO + BOX_LEN)
+    p32 = np.where(p32 >= hi, np.float32(BOX_LO), p32)
+    p32 = np.where(p32 < BOX_LO, np.float32(BOX_LO), p32)
+    gam = (rng.normal(size=(3, n)) * strength).astype(np.float32)
+    return Field(p32, gam, float(np.float32(sigma)), float(BOX_LO), float(BOX_LEN), 0,
+                 f"clustered{n}_s{seed}")
+
+
+def with_coincident(f: Field, count: int = 16, seed: int = 41) -> Field:
+    """Copy of f in which `count` particles are moved exactly onto other particles' positions
+    (distinct coincident pairs: the r -> 0 limits of Eqs. 5 and 8, reading R7)."""
+    rng = np.random.default_rng(seed)
+    n = f.pos.shape[1]
+    idx = rng.choice(n, 2 * count, replace=False)
+    pos = f.pos.copy()
+    pos[:, idx[:count]] = pos[:, idx[count:]]
+    return Field(pos, f.gamma.copy(), f.sigma, f.box_lo, f.box_len, f.n, f.name + "_coinc")

@@ -110,14 +110,121 @@ def test_direct_mode_vs_oracle(lam, scheme):
 def test_near_only_depth1_free_space_equals_direct(scheme, p2p, monkeypatch):
     """Depth 1, free space: all octants are neighbours, so P2P alone is the whole sum.
     Classical scheme in both P2P accumulations (default / VFMM_P2P=cross: per-pair gamma_j x d;
-    VFMM_P2P=sj: staged gamma_j x x_j, looser FP32 rounding bound)."""
+    VFMM_P2P=sj: staged gamma_j x x_j, looser FP32 rounding bound).  The jittered lattice
+    (+-0.75 h) has unequal leaves and close pairs; 16 distinct coincident pairs exercise the
+    r -> 0 limits (reading R7)."""
     monkeypatch.setenv("VFMM_P2P", p2p)
-    f = synthgen.jitter(synthgen.taylor_green(12), seed=5)
+    f = synthgen.with_coincident(synthgen.jitter(synthgen.taylor_green(12), seed=5))
     v, s, ev = run(f, p=2, depth=1, image_levels=0, scheme=scheme, mode=vf.MODE_NEAR_ONLY)
     vo, so = oracle.direct(f.pos, f.gamma, f.sigma, f.box_lo, f.box_len, 0, scheme)
     tol = TOL.NEAR_VS_ORACLE_SJ if (scheme == 0 and p2p == "sj") else TOL.NEAR_VS_ORACLE
     assert rel(v, vo) < tol[0] and rel(s, so) < tol[1], (rel(v, vo), rel(s, so))
     ev.close()
+
+
+@pytest.mark.parametrize("scheme", [0, 1])
+def test_near_only_dense_leaves_multiwindow_equals_direct(scheme):
+    """Dense leaves: 20000 clustered points at depth 1 (thousands per leaf) -- the P2P kernel
+    stages the 64-leaf region in several shared-memory windows (> 4352 sources) and loops over
+    many 64-target chunks per warp.  Free space, so NEAR_ONLY is the whole direct sum."""
+    f = synthgen.with_coincident(synthgen.clustered(20000, seed=33, sigma=0.2), count=8)
+    v, s, ev = run(f, p=2, depth=1, image_levels=0, scheme=scheme, mode=vf.MODE_NEAR_ONLY)
+    keys, perm, ls = ev.debug_tree(1)
+    assert np.diff(ls).max() > 2 * 4352 // 8  # several windows per region
+    tg = np.arange(0, 20000, 61)
+    vo, so = oracle.direct(f.pos, f.gamma, f.sigma, f.box_lo, f.box_len, 0, scheme, targets=tg,
+                           batched=True)
+    assert rel(v[:, tg], vo) < TOL.NEAR_VS_ORACLE[0] and rel(s[:, tg], so) < TOL.NEAR_VS_ORACLE[1], \
+        (rel(v[:, tg], vo), rel(s[:, tg], so))
+    ev.close()
+
+
+def test_dense_leaves_fmm_vs_direct():
+    """64^3 lattice at depth 3 (512 particles per leaf; 64 x 512 staged sources per region in
+    8 windows), p = 8, one image level, against O1 on stratified targets."""
+    f = synthgen.isotropic(64, seed=15)
+    v, s, ev = run(f, p=8, depth=3, image_levels=1)
+    tg = synthgen.sample_targets(64 ** 3, 32, n_lattice=64, leaf=8)
+    vo, so = oracle.direct(f.pos, f.gamma, f.sigma, f.box_lo, f.box_len, 1, 0, targets=tg,
+                           batched=True)
+    tu, ts = TOL.FMM_VS_DIRECT[8]
+    assert rel(v[:, tg], vo) < tu and rel(s[:, tg], so) < ts, (rel(v[:, tg], vo), rel(s[:, tg], so))
+    ev.close()
+
+
+def test_clustered_field_vs_direct():
+    """Non-uniform leaves (SURVEY 8(d) robustness fields): 20000 points in 12 Gaussian clusters
+    at depth 3 -- 318 of 512 leaves empty, up to 1105 particles in one leaf -- with coincident
+    pairs, p = 10, one image level.  The fp64 FMM oracle's own error here is 4.0e-6 / 3.8e-6."""
+    f = synthgen.with_coincident(synthgen.clustered(20000), count=8)
+    v, s, ev = run(f, p=10, depth=3, image_levels=1)
+    tg = np.arange(0, 20000, 97)
+    vo, so = oracle.direct(f.pos, f.gamma, f.sigma, f.box_lo, f.box_len, 1, 0, targets=tg,
+                           batched=True)
+    eu, es = rel(v[:, tg], vo), rel(s[:, tg], so)
+    print(f"clustered p=10: u {eu:.2e} sdot {es:.2e}")
+    tu, ts = TOL.FMM_VS_DIRECT[10]
+    assert eu < tu and es < ts, (eu, es)
+    ev.close()
+
+
+def test_periodic_27cubed_images_vs_direct():
+    """The benched image count (27^3 boxes, image_levels = 3) against O1
+    over the same cube, isotropic 32^3, p = 10, depth 3.  On this field O1 at lambda = 2 differs
+    from lambda = 3 by 7.2e-4 (u), so a wrong or missing outer supercell ring fails."""
+    f = synthgen.isotropic(32, seed=12)
+    tg = synthgen.sample_targets(32 ** 3, 48, n_lattice=32)
+    vo, so = oracle.direct(f.pos, f.gamma, f.sigma, f.box_lo, f.box_len, 3, 0, targets=tg,
+                           batched=True)
+    for engine in ("f16", "simt"):
+        import os
+        os.environ["VFMM_M2L"] = engine
+        try:
+            v, s, ev = run(f, p=10, depth=3, image_levels=3)
+        finally:
+            os.environ.pop("VFMM_M2L", None)
+        eu, es = rel(v[:, tg], vo), rel(s[:, tg], so)
+        print(f"iso32 lambda=3 p=10 {engine}: u {eu:.2e} sdot {es:.2e}")
+        tu, ts = TOL.FMM_VS_DIRECT[10]
+        assert eu < tu and es < ts, (engine, eu, es)
+        ev.close()
+
+
+def test_m2m_split_levels_per_stage_depth5():
+    """Depth 5: the level-4 M2M (4096 parents, < 2 tiles per SM) runs as the deterministic
+    8-way child split + ordered sum.  Per-stage check of every level's multipoles against the
+    fp64 M2M operators (oracle.fmm_ref.m2m_matrix) applied to the GPU's own child level."""
+    f = synthgen.isotropic(32, seed=6)
+    p, depth = 6, 5
+    v, s, ev = run(f, p=p, depth=depth, image_levels=1, mode=vf.MODE_FAR_ONLY)
+    for l in range(depth - 1, -1, -1):
+        child = _unpack(ev.debug_expansions(0, l + 1), p, (f.box_len / (1 << (l + 1))) ** np.arange(p + 1.0))
+        got = _unpack(ev.debug_expansions(0, l), p, (f.box_len / (1 << l)) ** np.arange(p + 1.0))
+        want = np.zeros_like(got)
+        mag = np.zeros(got.shape)  # sum of |terms|: FP32 rounding scale under cancellation
+        w = f.box_len / (1 << (l + 1))
+        for ch in range(8):
+            d = np.array([(ch & 1) - 0.5, ((ch >> 1) & 1) - 0.5, ((ch >> 2) & 1) - 0.5]) * w
+            t = child[ch::8] @ F.m2m_matrix(d, p).T
+            want += t
+            mag += np.abs(t)
+        err = np.linalg.norm(got - want) / np.linalg.norm(mag)
+        assert err < 1e-6, (l, err)
+    ev.close()
+
+
+def _unpack(P, p, scale_n):
+    """packed real [cell][comp][(p+1)^2] -> complex [cell][comp][(n,m) full], times scale_n[n]
+    (negative m from the real-source symmetry C_n^{-m} = (-1)^m conj(C_n^m))."""
+    out = np.zeros(P.shape[:2] + ((p + 1) ** 2,), np.complex128)
+    P = P.astype(np.float64)
+    for n in range(p + 1):
+        out[..., F.kidx(n, 0)] = P[..., n * n] * scale_n[n]
+        for m in range(1, n + 1):
+            c = (P[..., n * n + 2 * m - 1] + 1j * P[..., n * n + 2 * m]) * scale_n[n]
+            out[..., F.kidx(n, m)] = c
+            out[..., F.kidx(n, -m)] = (-1) ** m * np.conj(c)
+    return out
 
 
 def test_near_plus_far_equals_fmm():
@@ -331,6 +438,36 @@ def test_c4_full_size_sampled_targets(cfg):
     ev.close()
 
 
+@pytest.mark.slow
+@pytest.mark.parametrize("cfg", ["c4", "c5"])
+def test_bench_config_vs_golden_o1_27cubed(cfg):
+    """Exactly the benched configuration (bench.py: p = 10, depth 6, image_levels = 3 = the
+    paper's 27^3 boxes, default tensor-core M2L engine) against O1 reference values for 16
+    stratified targets computed once by scripts/make_golden.py (oracle/ only) and stored in
+    tests/golden/<cfg>_lam3_s0_o1.json (PAPER.md:164, :174, :361)."""
+    import hashlib
+    import json
+    import os
+
+    path = os.path.join(os.path.dirname(__file__), "golden", f"{cfg}_lam3_s0_o1.json")
+    if not os.path.exists(path):
+        pytest.skip(f"{path} not generated yet (scripts/make_golden.py {cfg})")
+    g = json.load(open(path))
+    f = synthgen.make(cfg)
+    h = hashlib.sha256()
+    h.update(np.ascontiguousarray(f.pos, np.float32).tobytes())
+    h.update(np.ascontiguousarray(f.gamma, np.float32).tobytes())
+    assert h.hexdigest() == g["field_sha256"], "generator output differs from the golden field"
+    v, s, ev = run(f, p=10, depth=6, image_levels=3)
+    tg = np.array(g["targets"], np.int64)
+    vo, so = np.array(g["vel"]), np.array(g["dgamma"])
+    eu, es = rel(v[:, tg], vo), rel(s[:, tg], so)
+    print(f"{cfg} bench config vs O1 (27^3 images): u {eu:.3e} sdot {es:.3e}")
+    tu, ts = TOL.FMM_VS_DIRECT[10]
+    assert eu < tu and es < ts, (eu, es)
+    ev.close()
+
+
 # ------------------------------------------------------------------ tensor-core M2L (tcgen05)
 
 @pytest.mark.parametrize("engine", ["tf32", "f16"])
@@ -352,3 +489,34 @@ def test_m2l_tensor_core_matches_simt(n, depth, p, lam, engine, monkeypatch):
     assert rel(v1, v2) < 3e-5 and rel(s1, s2) < 5e-5, (rel(v1, v2), rel(s1, s2))
     ev1.close()
     ev2.close()
+
+
+# ------------------------------------------------------------------ compute-sanitizer
+
+@pytest.mark.slow
+@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck"])
+def test_compute_sanitizer_c1(tool):
+    """compute-sanitizer over one full evaluation (examples/vfmm_c_example: 16^3 lattice, p = 6,
+    depth 2, 27^3 images, host buffers through the C ABI) -- every kernel of the pipeline,
+    including the tcgen05 / TMA / mbarrier M2L."""
+    import os
+    import shutil
+    import subprocess
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    exe = os.path.join(root, "examples", "vfmm_c_example")
+    san = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
+    if not os.path.exists(san):
+        pytest.skip("compute-sanitizer not installed")
+    if not os.path.exists(exe):
+        lib = os.path.join(root, "paper_1110_2921_b200", "lib")
+        subprocess.check_call(["gcc", "-O2", "-I", os.path.join(root, "include"), exe + ".c",
+                               "-L", lib, "-lvfmm", f"-Wl,-rpath,{lib}", "-lm", "-o", exe])
+    cmd = [san, "--tool", tool, "--error-exitcode", "99"]
+    if tool == "memcheck":
+        cmd += ["--leak-check", "full"]
+    r = subprocess.run(cmd + [exe, "16"], capture_output=True, text=True, timeout=1200)
+    tail = (r.stdout + r.stderr)[-3000:]
+    print(tail)
+    assert r.returncode == 0, tail
+    assert "ERROR SUMMARY: 0 errors" in r.stdout + r.stderr, tail
