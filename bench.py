@@ -202,12 +202,13 @@ def main():
     kw = dict(p=p, depth=depth, image_levels=3, sigma=f.sigma, box_lo=f.box_lo,
               box_len=f.box_len)
     if world > 1:
-        # this rank's share of the one problem: particles in its Morton leaf range
-        lo, hi = vf.partition(depth, world, rank)
-        leaf = vf.leaf_of(f.pos, depth, f.box_lo, f.box_len)
-        mine = np.nonzero((leaf >= lo) & (leaf < hi))[0]
-        f.pos = np.ascontiguousarray(f.pos[:, mine])
-        f.gamma = np.ascontiguousarray(f.gamma[:, mine])
+        # this rank's share of the one problem: a contiguous chunk of the input order (particles
+        # anywhere in the box); the library redistributes them to their Morton owners and
+        # returns the results
+        lo = n_total * rank // world
+        hi = n_total * (rank + 1) // world
+        f.pos = np.ascontiguousarray(f.pos[:, lo:hi])
+        f.gamma = np.ascontiguousarray(f.gamma[:, lo:hi])
         ev = vf.init_distributed(**kw)
     else:
         ev = vf.Evaluator(device=local, **kw)

@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define VFMM_ABI_VERSION 1
+#define VFMM_ABI_VERSION 2 /* 2: distributed inputs anywhere in the box; ms_comm fields */
 #define VFMM_PMAX 16 /* highest supported expansion order p */
 
 typedef struct vfmm_ctx vfmm_ctx; /* opaque: workspace, operator tables, streams */
@@ -89,7 +89,11 @@ typedef struct {
     int64_t n_m2m, n_l2l; /* child-parent translations                                     */
     int32_t depth_used;
     int32_t n_kernel_launches; /* kernels launched by the last evaluate                  */
-    int64_t bytes_sent, bytes_recv; /* distributed contexts: LET + halo bytes of this rank */
+    int64_t bytes_sent, bytes_recv; /* distributed contexts: bytes this rank sent / received
+                                       (redistribution both ways, halo particles, LET cells) */
+    double ms_comm;         /* distributed contexts: device time of the exchanges (NCCL or
+                               logical-rank copies), summed                                  */
+    double ms_comm_exposed; /* part of ms_comm the compute stream waited for (not overlapped) */
 } vfmm_stats;
 
 /* ABI version this library was built with (VFMM_ABI_VERSION). */
@@ -120,10 +124,14 @@ vfmm_status vfmm_evaluate(vfmm_ctx* ctx, int64_t n, const float* pos, const floa
 /* ---- multi-GPU: Morton-range spatial decomposition + local-essential-tree exchange ----
    (the paper's multi-GPU runs.)  Rank r of R
    (R in {1, 2, 4, 8}) owns the Morton leaf range [r 8^L/R, (r+1) 8^L/R) at depth L
-   (vfmm_partition); every rank passes only particles inside its range (others are flagged
-   VFMM_EDOMAIN) and gets u, dgamma for them in its own input order.  depth must be set
-   explicitly (>= 2).  Halo particles and LET multipoles travel over NCCL (grouped
-   send/recv + all-gather on the compute stream). */
+   (vfmm_partition).  Every rank passes its own n (possibly different, possibly 0) particles
+   ANYWHERE in the box and gets u, dgamma for them in its own input order: the library
+   redistributes them to their owners and returns the results (device-side Morton sort + grouped
+   NCCL send/recv both ways).  The result equals a single-context evaluation of the rank-order
+   concatenation of all ranks' inputs (same per-target summation order; the tensor-core M2L's
+   per-rank f16 staging scale can change the last bits).  depth must be set explicitly (>= 2).
+   Halo particles and LET multipoles travel over NCCL on a communication stream that overlaps
+   the upward pass and the M2L; two host syncs per evaluation read message sizes. */
 
 /* Write a fresh NCCL unique id (128 bytes) to host memory `out128` (call on one rank and
    broadcast it, e.g. with torch.distributed).  VFMM_ENCCL if libnccl.so.2 is unavailable. */
@@ -141,12 +149,19 @@ vfmm_status vfmm_partition(int depth, int nranks, int rank, int64_t* leaf_lo, in
 
 /* Test mode: run the distributed algorithm for `nranks` LOGICAL ranks on this context's one
    GPU -- every phase of every rank in lockstep, exchanges as device-to-device copies -- so
-   the partition / halo / LET logic can be validated on a single GPU.  Arrays are per rank:
-   n[r] particles at device pointers pos[r], gamma[r] (inside rank r's range), results to
-   vel[r], dgamma[r].  Asynchronous on `cuda_stream` apart from two host syncs per phase. */
+   the redistribution / partition / halo / LET logic can be validated on a single GPU.  Arrays
+   are per rank: n[r] >= 0 particles anywhere in the box at device pointers pos[r], gamma[r],
+   results to vel[r], dgamma[r] in rank r's input order.  Synchronizes `cuda_stream`. */
 vfmm_status vfmm_evaluate_logical(vfmm_ctx* ctx, int nranks, const int64_t* n,
                                   const float* const* pos, const float* const* gamma,
                                   float* const* vel, float* const* dgamma, void* cuda_stream);
+
+/* Host-only routing of the redistribution (no GPU needed): for n HOST positions (3 x n SoA
+   float32, anywhere in [lo, lo+len)^3) write counts[q] = how many fall in rank q's Morton range
+   at depth L (q < nranks) -- the send counts this rank's evaluate uses.  VFMM_EDOMAIN if a
+   position lies outside the box (the counts are then still written, clamped). */
+vfmm_status vfmm_route_counts(int depth, int nranks, int64_t n, const float* pos_h, float box_lo,
+                              float box_len, int64_t* counts);
 
 /* Host-only introspection of the static exchange plan of `rank` (no GPU needed): kind 0 =
    halo particle leaves (depth level), kind k in [2, depth] = LET multipole cells of level k;

@@ -51,7 +51,8 @@ class c_stats(ctypes.Structure):
                  "ms_l2l", "ms_l2p", "ms_p2p")] + \
                [(k, ctypes.c_int64) for k in ("n_p2p_pairs", "n_m2l", "n_m2m", "n_l2l")] + \
                [("depth_used", ctypes.c_int32), ("n_kernel_launches", ctypes.c_int32),
-                ("bytes_sent", ctypes.c_int64), ("bytes_recv", ctypes.c_int64)]
+                ("bytes_sent", ctypes.c_int64), ("bytes_recv", ctypes.c_int64),
+                ("ms_comm", ctypes.c_double), ("ms_comm_exposed", ctypes.c_double)]
 
 
 _LIB = None
@@ -60,7 +61,8 @@ EXPORTS = ["vfmm_abi_version", "vfmm_params_default", "vfmm_create", "vfmm_evalu
            "vfmm_evaluate_host", "vfmm_sync_status", "vfmm_get_stats", "vfmm_set_params",
            "vfmm_debug_tree", "vfmm_debug_expansions", "vfmm_strerror",
            "vfmm_last_error_message", "vfmm_destroy", "vfmm_nccl_get_unique_id",
-           "vfmm_create_nccl", "vfmm_partition", "vfmm_evaluate_logical", "vfmm_dist_plan"]
+           "vfmm_create_nccl", "vfmm_partition", "vfmm_evaluate_logical", "vfmm_dist_plan",
+           "vfmm_route_counts"]
 
 
 def load_library(path: str = LIB_PATH):
@@ -93,8 +95,9 @@ def load_library(path: str = LIB_PATH):
     L.vfmm_partition.argtypes = [i32, i32, i32, ctypes.POINTER(i64), ctypes.POINTER(i64)]
     L.vfmm_evaluate_logical.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp]
     L.vfmm_dist_plan.argtypes = [i32, i32, i32, i32, i32, i32, i32, vp, i64, ctypes.POINTER(i64)]
+    L.vfmm_route_counts.argtypes = [i32, i32, i64, vp, ctypes.c_float, ctypes.c_float, vp]
     for f in ("vfmm_nccl_get_unique_id", "vfmm_create_nccl", "vfmm_partition",
-              "vfmm_evaluate_logical", "vfmm_dist_plan"):
+              "vfmm_evaluate_logical", "vfmm_dist_plan", "vfmm_route_counts"):
         getattr(L, f).restype = ctypes.c_int
     for f in ("vfmm_create", "vfmm_evaluate", "vfmm_evaluate_host", "vfmm_sync_status",
               "vfmm_get_stats", "vfmm_set_params", "vfmm_debug_tree", "vfmm_debug_expansions"):
@@ -137,17 +140,17 @@ def partition(depth: int, nranks: int, rank: int):
     return lo.value, hi.value
 
 
-def leaf_of(pos, depth: int, box_lo: float, box_len: float):
-    """Morton leaf index of each particle (input plumbing for partitioning a field across
-    ranks; the same float32 quantization the keys kernel uses)."""
-    pos = np.asarray(pos, np.float32)
-    inv = np.float32((1 << depth) / float(np.float32(box_len)))
-    q = np.floor((pos - np.float32(box_lo)) * inv).astype(np.int64).clip(0, (1 << depth) - 1)
-    key = np.zeros(pos.shape[1], np.int64)
-    for b in range(depth):
-        for a in range(3):
-            key |= ((q[a] >> b) & 1) << (3 * b + a)
-    return key
+def route_counts(pos, depth: int, nranks: int, box_lo: float, box_len: float):
+    """Host routing of the redistribution (C ABI vfmm_route_counts): how many of these (3, n)
+    float32 host positions each rank's Morton range receives.  Returns (counts, status)."""
+    L = load_library()
+    pos = np.ascontiguousarray(pos, np.float32)
+    out = np.zeros(nranks, np.int64)
+    st = L.vfmm_route_counts(depth, nranks, pos.shape[1], pos.ctypes.data, box_lo, box_len,
+                             out.ctypes.data)
+    if st not in (VFMM_OK, VFMM_EDOMAIN):
+        _check(L, None, st)
+    return out, st
 
 
 def dist_plan(depth, nranks, rank, periodic, kind, direction, peer):
@@ -245,7 +248,8 @@ class Evaluator:
 
     def evaluate_logical(self, pos_list, gamma_list, stream=None):
         """Distributed algorithm with len(pos_list) logical ranks on this one GPU (tests):
-        pos_list[r], gamma_list[r]: (3, n_r) float32 CUDA tensors inside rank r's range."""
+        pos_list[r], gamma_list[r]: (3, n_r) float32 CUDA tensors, anywhere in the box (n_r may
+        be 0).  Returns per-rank (vel, dgamma) lists in each rank's input order."""
         import torch
 
         R = len(pos_list)

@@ -76,6 +76,12 @@ struct vfmm_ctx {
     std::vector<vfmm::RankState*> ranks;
     static constexpr int NEV = 10;
     cudaEvent_t ev[NEV] = {};
+    // distributed contexts: communication stream (all NCCL calls) and exchange timing events
+    cudaStream_t comm_st = nullptr;
+    static constexpr int NCE = 20;
+    cudaEvent_t evc[NCE] = {};
+    bool comm_timed = false;  // evc hold the exchanges of the last evaluate
+    bool comm_overlap = false;  // NCCL mode: X2 / X3 overlapped (exposed part from evc 11-16)
 };
 
 namespace {
@@ -337,17 +343,20 @@ void ensure_rank_states(vfmm_ctx* c, int R, int first_rank, int count) {
         S->rank = first_rank + i;
         const int per = c->prm.image_levels > 0;
         if (S->plan.L != c->prm.depth || S->plan.R != R || S->plan.rank != S->rank ||
-            S->plan.periodic != per || S->plan.p_send.empty())
+            S->plan.periodic != per || S->plan.p_send.empty()) {
             build_dist_plan(c->prm.depth, R, S->rank, per, &S->plan);
+            S->plan_dirty = true;
+        }
     }
 }
 
 vfmm_status dist_sticky(vfmm_ctx* c, RankState* S) {
     int flag = 0;
+    if (!S->d_err) return VFMM_OK;
     CK(cudaMemcpy(&flag, S->d_err, sizeof(int), cudaMemcpyDeviceToHost), "read flag");
     if (flag) {
         CK(cudaMemset(S->d_err, 0, sizeof(int)), "clear flag");
-        c->err = "a particle lies outside the box or outside its rank's Morton range";
+        c->err = "a particle lies outside the box (or is not finite)";
         return VFMM_EDOMAIN;
     }
     return VFMM_OK;
@@ -400,6 +409,11 @@ vfmm_status vfmm_create_nccl(vfmm_ctx** out, const vfmm_params* prm, int device,
     // every NCCL context runs the distributed phases, also with one rank (a 1-rank
     // communicator: the all-gathers degenerate to copies), so the NCCL plumbing is exercised
     c->dist = true;
+    if (cudaStreamCreateWithFlags(&c->comm_st, cudaStreamNonBlocking) != cudaSuccess) {
+        vfmm_destroy(c);
+        *out = nullptr;
+        return VFMM_ECUDA;
+    }
     {
         s = nccl_init(&c->comm, nranks, rank, nccl_id128);
         if (s != VFMM_OK) {
@@ -420,6 +434,9 @@ vfmm_status vfmm_evaluate_logical(vfmm_ctx* c, int nranks, const int64_t* n,
     CK(cudaSetDevice(c->device), "set device");
     (void)cudaGetLastError();
     cudaStream_t st = (cudaStream_t)stream;
+    if (c->last_stream != st && c->have_last)
+        CK(cudaStreamWaitEvent(st, c->ev[vfmm_ctx::NEV - 1], 0), "order after last evaluate");
+    c->have_last = true;
     ensure_rank_states(c, nranks, 0, nranks);
     CK(cudaEventRecord(c->ev[0], st), "event");
     DistShared D = make_shared(c, nranks);
@@ -427,29 +444,53 @@ vfmm_status vfmm_evaluate_logical(vfmm_ctx* c, int nranks, const int64_t* n,
     for (int r = 0; r < nranks; ++r) {
         if (n[r] < 0 || (n[r] > 0 && (!pos[r] || !gamma[r] || !vel[r] || !dgamma[r])))
             return VFMM_EINVAL;
-        S[r]->n_local = n[r];
-        S[r]->pos = pos[r];
-        S[r]->gam = gamma[r];
-        S[r]->vel = vel[r];
-        S[r]->dg = dgamma[r];
+        S[r]->n_in = n[r];
+        S[r]->in_pos = pos[r];
+        S[r]->in_gam = gamma[r];
+        S[r]->in_vel = vel[r];
+        S[r]->in_dg = dgamma[r];
     }
     vfmm_status s;
-    for (int r = 0; r < nranks; ++r)
-        if ((s = dist_phase1(*S[r], D, st, &c->err)) != VFMM_OK) return s;
-    if ((s = logical_x1(S, D, st)) != VFMM_OK) return s;
-    for (int r = 0; r < nranks; ++r)
-        if ((s = dist_phase2(*S[r], D, st, &c->err)) != VFMM_OK) return s;
-    if ((s = logical_x2(S, D, st)) != VFMM_OK) return s;
-    for (int r = 0; r < nranks; ++r)
-        if ((s = dist_phase3(*S[r], D, st, &c->err)) != VFMM_OK) return s;
-    if ((s = logical_x3(S, D, st)) != VFMM_OK) return s;
-    for (int r = 0; r < nranks; ++r)
-        if ((s = dist_phase4(*S[r], D, st, &c->err)) != VFMM_OK) return s;
+    int ce = 0;  // exchange timing events: (start, end) pairs on the one stream
+    auto phase = [&](vfmm_status (*f)(RankState&, const DistShared&, cudaStream_t, std::string*)) {
+        for (int r = 0; r < nranks; ++r) {
+            vfmm_status t = f(*S[r], D, st, &c->err);
+            if (t != VFMM_OK) return t;
+        }
+        return VFMM_OK;
+    };
+    auto xchg = [&](vfmm_status (*f)(std::vector<RankState*>&, const DistShared&, cudaStream_t)) {
+        cudaEventRecord(c->evc[ce++], st);
+        vfmm_status t = f(S, D, st);
+        cudaEventRecord(c->evc[ce++], st);
+        return t;
+    };
+    if ((s = phase(dist_phase0a)) != VFMM_OK) return s;
+    if ((s = xchg(logical_x0a)) != VFMM_OK) return s;
+    if ((s = phase(dist_phase0b)) != VFMM_OK) return s;
+    if ((s = xchg(logical_x0b)) != VFMM_OK) return s;
+    if ((s = phase(dist_phase0c)) != VFMM_OK) return s;
+    if ((s = phase(dist_phase1)) != VFMM_OK) return s;
+    if ((s = xchg(logical_x1)) != VFMM_OK) return s;
+    if ((s = phase(dist_phase2)) != VFMM_OK) return s;
+    if ((s = xchg(logical_x2)) != VFMM_OK) return s;
+    if ((s = phase(dist_unpack_halo)) != VFMM_OK) return s;
+    if ((s = phase(dist_phase3)) != VFMM_OK) return s;
+    if ((s = xchg(logical_x3)) != VFMM_OK) return s;
+    if ((s = phase(dist_unpack_let)) != VFMM_OK) return s;
+    if ((s = phase(dist_phase4_far)) != VFMM_OK) return s;
+    if ((s = phase(dist_phase4_near)) != VFMM_OK) return s;
+    if ((s = phase(dist_phase5a)) != VFMM_OK) return s;
+    if ((s = xchg(logical_x5)) != VFMM_OK) return s;
+    if ((s = phase(dist_phase5b)) != VFMM_OK) return s;
     for (int i = 1; i < vfmm_ctx::NEV; ++i) CK(cudaEventRecord(c->ev[i], st), "event");
     c->last_stream = st;
     c->have_tree = false;
     c->have_exp = false;
+    c->comm_timed = true;
+    c->comm_overlap = false;
     memset(&c->stats, 0, sizeof(c->stats));
+    c->stats.depth_used = c->prm.depth;
     for (int r = 0; r < nranks; ++r) {
         c->stats.bytes_sent += S[r]->bytes_sent;
         c->stats.bytes_recv += S[r]->bytes_recv;
@@ -460,6 +501,23 @@ vfmm_status vfmm_evaluate_logical(vfmm_ctx* c, int nranks, const int64_t* n,
     return VFMM_OK;
 }
 
+vfmm_status vfmm_route_counts(int depth, int nranks, int64_t n, const float* pos_h, float box_lo,
+                              float box_len, int64_t* counts) {
+    if (!valid_R(nranks) || depth < 1 || depth > 10 || n < 0 || !counts || (n > 0 && !pos_h) ||
+        !(box_len > 0.f))
+        return VFMM_EINVAL;
+    const int64_t per = ((int64_t)1 << (3 * depth)) / nranks;
+    for (int q = 0; q < nranks; ++q) counts[q] = 0;
+    bool all_in = true;
+    for (int64_t i = 0; i < n; ++i) {
+        bool in = true;
+        const int64_t leaf = host_leaf_of(pos_h[i], pos_h[n + i], pos_h[2 * n + i], depth, box_lo,
+                                          box_len, &in);
+        all_in &= in;
+        counts[leaf / per] += 1;
+    }
+    return all_in ? VFMM_OK : VFMM_EDOMAIN;
+}
 
 int32_t vfmm_abi_version(void) { return VFMM_ABI_VERSION; }
 
@@ -520,6 +578,7 @@ vfmm_status vfmm_create(vfmm_ctx** out, const vfmm_params* prm, int device) {
         if (e2 == cudaSuccess) e2 = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
         if (e2 == cudaSuccess) e2 = cudaEventCreateWithFlags(&c->ev_gamma, cudaEventDisableTiming);
         for (int i = 0; i < vfmm_ctx::NEV && e2 == cudaSuccess; ++i) e2 = cudaEventCreate(&c->ev[i]);
+        for (int i = 0; i < vfmm_ctx::NCE && e2 == cudaSuccess; ++i) e2 = cudaEventCreate(&c->evc[i]);
         if (e2 != cudaSuccess) s = cuda_fail(c, e2, "create");
     }
     if (s != VFMM_OK) {
@@ -543,7 +602,8 @@ vfmm_status vfmm_set_params(vfmm_ctx* c, const vfmm_params* prm) {
 
 vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float* gamma,
                           float* vel, float* dgamma, void* stream) {
-    if (!c || n < 1 || !pos || !gamma || !vel || !dgamma) return VFMM_EINVAL;
+    if (!c || n < 0 || (n == 0 && !c->dist)) return VFMM_EINVAL;
+    if (n > 0 && (!pos || !gamma || !vel || !dgamma)) return VFMM_EINVAL;
     if (n > ((int64_t)1 << 31) - 1) return VFMM_EINVAL;
     // outputs must not alias inputs or each other
     auto overlap = [n](const void* a, const void* b) {
@@ -567,20 +627,62 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
         ensure_rank_states(c, c->R, c->rank, 1);
         DistShared D = make_shared(c, c->R);
         RankState& R0 = *c->ranks[0];
-        R0.n_local = n;
-        R0.pos = pos;
-        R0.gam = gamma;
-        R0.vel = vel;
-        R0.dg = dgamma;
+        R0.n_in = n;
+        R0.in_pos = pos;
+        R0.in_gam = gamma;
+        R0.in_vel = vel;
+        R0.in_dg = dgamma;
+        cudaStream_t cs = c->comm_st;
+        cudaEvent_t* E = c->evc;
         vfmm_status s;
+        // every NCCL call runs on the communication stream cs, ordered by events; X0/X1/X5
+        // are waited for at once, X2 (halo particles) overlaps P2M / M2M / M2L and X3 (LET
+        // multipoles) overlaps the LET packing tail until the M2L needs it
+        auto to_comm = [&](int e_ready) {
+            CK(cudaEventRecord(E[e_ready], st), "event");
+            CK(cudaStreamWaitEvent(cs, E[e_ready], 0), "wait");
+            CK(cudaEventRecord(E[e_ready + 1], cs), "event");
+            return VFMM_OK;
+        };
         CK(cudaEventRecord(c->ev[0], st), "event");
+        if ((s = dist_phase0a(R0, D, st, &c->err)) != VFMM_OK) return s;
+        if ((s = to_comm(0)) != VFMM_OK) return s;
+        if ((s = nccl_x0a(R0, D, c->comm, cs)) != VFMM_OK) return s;
+        CK(cudaEventRecord(E[2], cs), "event");
+        CK(cudaStreamWaitEvent(st, E[2], 0), "wait");
+        if ((s = dist_phase0b(R0, D, st, &c->err)) != VFMM_OK) return s;
+        if ((s = to_comm(3)) != VFMM_OK) return s;
+        if ((s = nccl_x0b(R0, D, c->comm, cs)) != VFMM_OK) return s;
+        CK(cudaEventRecord(E[5], cs), "event");
+        CK(cudaStreamWaitEvent(st, E[5], 0), "wait");
+        if ((s = dist_phase0c(R0, D, st, &c->err)) != VFMM_OK) return s;
         if ((s = dist_phase1(R0, D, st, &c->err)) != VFMM_OK) return s;
-        if ((s = nccl_x1(R0, D, c->comm, st)) != VFMM_OK) return s;
+        if ((s = to_comm(6)) != VFMM_OK) return s;
+        if ((s = nccl_x1(R0, D, c->comm, cs)) != VFMM_OK) return s;
+        CK(cudaEventRecord(E[8], cs), "event");
+        CK(cudaStreamWaitEvent(st, E[8], 0), "wait");
         if ((s = dist_phase2(R0, D, st, &c->err)) != VFMM_OK) return s;
-        if ((s = nccl_x2(R0, D, c->comm, st)) != VFMM_OK) return s;
+        if ((s = to_comm(9)) != VFMM_OK) return s;
+        if ((s = nccl_x2(R0, D, c->comm, cs)) != VFMM_OK) return s;
+        if ((s = dist_unpack_halo(R0, D, cs, &c->err)) != VFMM_OK) return s;
+        CK(cudaEventRecord(E[11], cs), "event");
         if ((s = dist_phase3(R0, D, st, &c->err)) != VFMM_OK) return s;
-        if ((s = nccl_x3(R0, D, c->comm, st)) != VFMM_OK) return s;
-        if ((s = dist_phase4(R0, D, st, &c->err)) != VFMM_OK) return s;
+        if ((s = to_comm(12)) != VFMM_OK) return s;
+        if ((s = nccl_x3(R0, D, c->comm, cs)) != VFMM_OK) return s;
+        if ((s = dist_unpack_let(R0, D, cs, &c->err)) != VFMM_OK) return s;
+        CK(cudaEventRecord(E[14], cs), "event");
+        CK(cudaEventRecord(E[15], st), "event");  // compute stream ready for the LET
+        CK(cudaStreamWaitEvent(st, E[14], 0), "wait");
+        if ((s = dist_phase4_far(R0, D, st, &c->err)) != VFMM_OK) return s;
+        CK(cudaEventRecord(E[16], st), "event");  // compute stream ready for the halo
+        CK(cudaStreamWaitEvent(st, E[11], 0), "wait");
+        if ((s = dist_phase4_near(R0, D, st, &c->err)) != VFMM_OK) return s;
+        if ((s = dist_phase5a(R0, D, st, &c->err)) != VFMM_OK) return s;
+        if ((s = to_comm(17)) != VFMM_OK) return s;
+        if ((s = nccl_x5(R0, D, c->comm, cs)) != VFMM_OK) return s;
+        CK(cudaEventRecord(E[19], cs), "event");
+        CK(cudaStreamWaitEvent(st, E[19], 0), "wait");
+        if ((s = dist_phase5b(R0, D, st, &c->err)) != VFMM_OK) return s;
         for (int i = 1; i < vfmm_ctx::NEV; ++i) CK(cudaEventRecord(c->ev[i], st), "event");
         memset(&c->stats, 0, sizeof(c->stats));
         c->stats.bytes_sent = R0.bytes_sent;
@@ -589,11 +691,14 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
         c->last_stream = st;
         c->have_tree = false;
         c->have_exp = false;
+        c->comm_timed = true;
+        c->comm_overlap = true;
         return VFMM_OK;
     }
     const vfmm_params& P = c->prm;
     vfmm_stats& S = c->stats;
     memset(&S, 0, sizeof(S));
+    c->comm_timed = false;
     c->last_stream = st;
     c->last_n = n;
     const KernelConsts kc = make_kernel_consts(P.sigma);
@@ -791,6 +896,10 @@ vfmm_status vfmm_sync_status(vfmm_ctx* c) {
     if (!c) return VFMM_EINVAL;
     CK(cudaSetDevice(c->device), "set device");
     CK(cudaStreamSynchronize(c->last_stream), "sync");
+    if (c->dist) {
+        vfmm_status s = nccl_async_error(c->comm, &c->err);
+        if (s != VFMM_OK) return s;
+    }
     if (c->dist && !c->ranks.empty()) {
         vfmm_status s = dist_sticky(c, c->ranks[0]);
         if (s != VFMM_OK) return s;
@@ -825,6 +934,23 @@ vfmm_status vfmm_get_stats(vfmm_ctx* c, vfmm_stats* out) {
     float tot = 0;
     CK(cudaEventElapsedTime(&tot, c->ev[0], c->ev[vfmm_ctx::NEV - 1]), "elapsed");
     S.ms_total = tot;
+    if (c->comm_timed) {
+        auto el = [&](int a, int b) {
+            float t = 0.f;
+            return cudaEventElapsedTime(&t, c->evc[a], c->evc[b]) == cudaSuccess ? (double)t : 0.0;
+        };
+        if (c->comm_overlap) {  // NCCL: (start, end) of X0a, X0b, X1, X2, X3, X5 on the comm stream
+            const double x0a = el(1, 2), x0b = el(4, 5), x1 = el(7, 8), x2 = el(10, 11),
+                         x3 = el(13, 14), x5 = el(18, 19);
+            S.ms_comm = x0a + x0b + x1 + x2 + x3 + x5;
+            S.ms_comm_exposed = x0a + x0b + x1 + x5 + std::max(0.0, el(15, 14)) +
+                                std::max(0.0, el(16, 11));
+        } else {  // logical ranks: six (start, end) pairs on the one stream, all exposed
+            double t = 0;
+            for (int i = 0; i < 12; i += 2) t += el(i, i + 1);
+            S.ms_comm = S.ms_comm_exposed = t;
+        }
+    }
     if (c->prm.mode == VFMM_MODE_FMM || c->prm.mode == VFMM_MODE_NEAR_ONLY) {
         unsigned long long pairs = 0;
         CK(cudaMemcpy(&pairs, c->d_pairs, sizeof(pairs), cudaMemcpyDeviceToHost), "copy pairs");
@@ -903,6 +1029,9 @@ void vfmm_destroy(vfmm_ctx* c) {
     dfree(c->hbuf);
     for (int i = 0; i < vfmm_ctx::NEV; ++i)
         if (c->ev[i]) cudaEventDestroy(c->ev[i]);
+    for (int i = 0; i < vfmm_ctx::NCE; ++i)
+        if (c->evc[i]) cudaEventDestroy(c->evc[i]);
+    if (c->comm_st) cudaStreamDestroy(c->comm_st);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     if (c->side) cudaStreamDestroy(c->side);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);

@@ -4,26 +4,34 @@
 //
 // Rank r of R (R in {1, 2, 4, 8}) owns the contiguous Morton range of leaves
 // [r 8^L/R, (r+1) 8^L/R), i.e. 8/R whole octants; at every level >= 1 its cells form a box.
-// One evaluation:
-//   1  local Morton keys + stable sort of the rank's particles (which must lie in its range)
-//   X1 all-gather of owned leaf counts -> global leaf_start on every rank (+ one D2H copy so
-//      the host knows halo message sizes)
-//   2  owned particles -> their global sorted positions; pack halo leaves for the peers
+// Each rank passes any particles (anywhere in the box).  One evaluation:
+//   0  C1: Morton keys + stable sort of the caller's particles, cut at the rank boundaries;
+//      X0 counts matrix all-gather (one D2H copy: message sizes) and the particles to their
+//      owners (grouped send/recv); the owner evaluates them in received order
+//   1  keys + stable sort of the owned particles (ties: sender rank, then the sender's input
+//      order = the global input order of the concatenated per-rank inputs)
+//   X1 all-gather of owned leaf counts -> compact leaf_start over the rank's owned + halo
+//      leaves (+ one D2H copy so the host knows halo message sizes)
+//   2  owned particles -> their compact sorted positions; pack halo leaves for the peers
 //   X2 halo particle exchange (leaves within one leaf of a peer's range, periodic)
 //   3  P2M, M2M over owned cells (levels L-1 .. 1); pack halo multipoles
 //   X3 all-gather of level-1 multipoles + LET multipole exchange for levels 2..L (cells in a
 //      peer's 189-cell interaction lists)
-//   4  root M2M, periodic images and L2L redundantly on every rank; M2L, L2L, P2P, L2P for
-//      owned cells; results back to the caller's input order on the same rank.
-// The exchange plans are static for (L, R, periodic) and built once on the host.
-// Transport: NCCL (grouped ncclSend/ncclRecv, ncclAllGather on the compute stream, library
-// loaded with dlopen -- the same libnccl.so.2 torch uses), or "logical ranks": all R ranks'
-// phases run on one GPU in lockstep and exchanges are device-to-device copies (tests).
+//   4  root M2M, periodic images and L2L redundantly on every rank; M2L, L2L for owned cells
+//      (after X3), P2P (after X2), L2P
+//   5  results back to their senders (reverse trip of X0) and to the caller's input order.
+// The exchange plans are static for (L, R, periodic) and built once on the host; the static
+// device tables (halo leaf mask, LET cell lists) are uploaded once per plan.
+// Transport: NCCL (grouped ncclSend/ncclRecv and ncclAllGather on a communication stream,
+// X2 overlapping P2M / M2M / M2L and X3 overlapping the M2L-independent work; library loaded
+// with dlopen -- the same libnccl.so.2 torch uses), or "logical ranks": all R ranks' phases run
+// on one GPU in lockstep and exchanges are device-to-device copies (tests).
 #include <cuda_runtime.h>
 #include <dlfcn.h>
 #include <nccl.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 #include <memory>
 #include <string>
@@ -49,6 +57,7 @@ struct NcclApi {
     ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t,
                               cudaStream_t) = nullptr;
     const char* (*GetErrorString)(ncclResult_t) = nullptr;
+    ncclResult_t (*CommGetAsyncError)(ncclComm_t, ncclResult_t*) = nullptr;
     bool load() {
         if (h) return true;
         h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
@@ -62,6 +71,7 @@ struct NcclApi {
         Recv = (decltype(Recv))dlsym(h, "ncclRecv");
         AllGather = (decltype(AllGather))dlsym(h, "ncclAllGather");
         GetErrorString = (decltype(GetErrorString))dlsym(h, "ncclGetErrorString");
+        CommGetAsyncError = (decltype(CommGetAsyncError))dlsym(h, "ncclCommGetAsyncError");
         return GetUniqueId && CommInitRank && CommDestroy && GroupStart && GroupEnd && Send &&
                Recv && AllGather;
     }
@@ -70,8 +80,10 @@ NcclApi g_nccl;
 
 // ---- kernels -------------------------------------------------------------------------
 
-// exclusive scan of counts[0..m) -> start[0..m]; one block (small m, once per evaluation)
-__global__ void scan_counts_kernel(const int* __restrict__ counts, int64_t m, int* __restrict__ start) {
+// exclusive scan of counts[0..m) (times need[i] if given) -> start[0..m]; one block (small m,
+// once per evaluation)
+__global__ void scan_counts_kernel(const int* __restrict__ counts, const uint8_t* __restrict__ need,
+                                   int64_t m, int* __restrict__ start) {
     __shared__ int wsum[32];
     __shared__ int carry;
     if (threadIdx.x == 0) carry = 0;
@@ -79,7 +91,7 @@ __global__ void scan_counts_kernel(const int* __restrict__ counts, int64_t m, in
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
     for (int64_t b = 0; b < m; b += blockDim.x) {
         const int64_t i = b + threadIdx.x;
-        const int v = i < m ? counts[i] : 0;
+        const int v = i < m ? (need && !need[i] ? 0 : counts[i]) : 0;
         int x = v;
         for (int o = 1; o < 32; o <<= 1) {
             const int y = __shfl_up_sync(0xffffffffu, x, o);
@@ -158,6 +170,57 @@ __global__ void unpack_cells_kernel(float* __restrict__ M, int cellsz, const int
          k += (int64_t)gridDim.x * blockDim.x) {
         const int64_t c = k / cellsz;
         M[(int64_t)cells[c] * cellsz + (k - c * cellsz)] = buf[k];
+    }
+}
+
+// C1: particles per destination rank from the sorted keys (lower bounds of the rank
+// boundaries); one thread per rank
+__global__ void dest_counts_kernel(const uint32_t* __restrict__ keys, int64_t n, int R,
+                                   int64_t nleaf, int* __restrict__ crow) {
+    const int q = threadIdx.x;
+    if (q >= R) return;
+    auto lb = [&](int64_t c) {
+        int64_t lo = 0, hi = n;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if ((int64_t)keys[mid] < c) lo = mid + 1;
+            else hi = mid;
+        }
+        return lo;
+    };
+    const int64_t a = lb(nleaf / R * q), b = q == R - 1 ? n : lb(nleaf / R * (q + 1));
+    crow[q] = (int)(b - a);
+}
+// AoS6 [k] = (a[perm[k]], b[perm[k]]) for SoA3 a, b of length n (perm null: identity)
+__global__ void pack_aos6_kernel(const float* __restrict__ a, const float* __restrict__ b,
+                                 int64_t n, const uint32_t* __restrict__ perm,
+                                 float* __restrict__ out) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = perm ? (int64_t)perm[k] : k;
+        float* o = out + k * 6;
+        o[0] = a[i];
+        o[1] = a[n + i];
+        o[2] = a[2 * n + i];
+        o[3] = b[i];
+        o[4] = b[n + i];
+        o[5] = b[2 * n + i];
+    }
+}
+// SoA3 a[perm[k]], b[perm[k]] = AoS6 [k] (perm null: identity)
+__global__ void unpack_aos6_kernel(const float* __restrict__ in, int64_t n,
+                                   const uint32_t* __restrict__ perm, float* __restrict__ a,
+                                   float* __restrict__ b) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t i = perm ? (int64_t)perm[k] : k;
+        const float* v = in + k * 6;
+        a[i] = v[0];
+        a[n + i] = v[1];
+        a[2 * n + i] = v[2];
+        b[i] = v[3];
+        b[n + i] = v[4];
+        b[2 * n + i] = v[5];
     }
 }
 
@@ -265,12 +328,21 @@ void RankState::release() {
     for (int b = 0; b < 2; ++b) {
         dfree(keys[b]);
         dfree(vals[b]);
+        dfree(ikeys[b]);
+        dfree(ivals[b]);
     }
     dfree(radix_tmp);
+    dfree(itmp);
+    dfree(isend);
+    dfree(irecv);
+    dfree(own);
+    dfree(d_crow);
+    dfree(d_cmat);
     dfree(lstart);
     dfree(counts_own);
     dfree(counts_all);
     dfree(gstart);
+    dfree(d_need);
     dfree(sorted6);
     dfree(near6);
     dfree(Mall);
@@ -287,10 +359,32 @@ void RankState::release() {
     dfree(g_hi);
     dfree(g_lo);
     dfree(tcmax);
-    cap_local = cap_total = 0;
+    cap_in = cap_own = cap_local = cap_total = 0;
     cap_send = cap_recv = 0;
     cap_segs = cap_cells = 0;
     g_cap = 0;
+    cap_depth = cap_p = cap_R = -1;
+    plan_dirty = true;
+}
+
+int64_t host_leaf_of(float x, float y, float z, int depth, float lo, float len, bool* inside) {
+    const int side = 1 << depth;
+    const float inv = (float)((double)side / (double)len);
+    const float hi = lo + len;
+    const float v[3] = {x, y, z};
+    int64_t key = 0;
+    bool in = true;
+    for (int a = 0; a < 3; ++a) {
+        if (!(v[a] >= lo && v[a] < hi)) in = false;
+        volatile float d = v[a] - lo;  // single RN subtract, single RN multiply
+        volatile float s = d * inv;
+        const float fl = std::floor((float)s);
+        int q = fl >= 0.f ? (int)fl : 0;
+        if (q > side - 1) q = side - 1;
+        for (int b = 0; b < depth; ++b) key |= (int64_t)((q >> b) & 1) << (3 * b + a);
+    }
+    if (inside) *inside = in;
+    return key;
 }
 
 // ---------------------------------------------------------------------------------------
@@ -317,6 +411,16 @@ cudaError_t grow(T*& p, size_t& cap, size_t need) {
     if (e == cudaSuccess) cap = need;
     return e;
 }
+template <class T>
+cudaError_t grow64(T*& p, int64_t& cap, int64_t need, size_t per) {
+    if (need <= cap && p) return cudaSuccess;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    cudaError_t e = cudaMalloc((void**)&p, (size_t)std::max<int64_t>(need, 1) * per * sizeof(T));
+    if (e == cudaSuccess) cap = need;
+    return e;
+}
 
 int grid_of(int64_t work, int bs = 256) {
     int64_t g = (work + bs - 1) / bs;
@@ -326,7 +430,118 @@ int grid_of(int64_t work, int bs = 256) {
 int64_t owned_lo(int l, int R, int r) { return ((int64_t)r << (3 * l)) / R; }
 int64_t owned_cnt(int l, int R) { return ((int64_t)1 << (3 * l)) / R; }
 
+Geom geom_of(const DistShared& D) {
+    const vfmm_params& P = D.prm;
+    return Geom{P.box_lo, P.box_len, (double)P.box_lo, (double)P.box_len, D.depth,
+                P.image_levels > 0};
+}
+
 }  // namespace
+
+// ---- 0: C1 redistribution of the caller's particles ------------------------------------
+
+vfmm_status dist_phase0a(RankState& S, const DistShared& D, cudaStream_t st, std::string* err) {
+    const int L = D.depth, R = D.R;
+    const int64_t n = S.n_in;
+    if (n > S.cap_in) {
+        for (int b = 0; b < 2; ++b) {
+            dfree(S.ikeys[b]);
+            dfree(S.ivals[b]);
+        }
+        dfree(S.itmp);
+        dfree(S.isend);
+        S.cap_in = 0;
+        for (int b = 0; b < 2; ++b) {
+            DCK(cudaMalloc((void**)&S.ikeys[b], n * 4), "alloc keys");
+            DCK(cudaMalloc((void**)&S.ivals[b], n * 4), "alloc vals");
+        }
+        DCK(cudaMalloc(&S.itmp, radix_temp_bytes(n)), "alloc radix");
+        DCK(cudaMalloc((void**)&S.isend, 6 * n * sizeof(float)), "alloc c1 send");
+        S.cap_in = n;
+    }
+    if (!S.d_err) {
+        DCK(cudaMalloc((void**)&S.d_err, sizeof(int)), "alloc err");
+        DCK(cudaMemset(S.d_err, 0, sizeof(int)), "memset err");
+        DCK(cudaMalloc((void**)&S.d_pairs, sizeof(unsigned long long)), "alloc pairs");
+    }
+    if (S.cap_R != R) {
+        dfree(S.d_crow);
+        dfree(S.d_cmat);
+        DCK(cudaMalloc((void**)&S.d_crow, R * sizeof(int)), "alloc counts");
+        DCK(cudaMalloc((void**)&S.d_cmat, R * R * sizeof(int)), "alloc counts");
+        S.cap_R = R;
+    }
+    const int64_t nleaf = (int64_t)1 << (3 * L);
+    if (n > 0) {
+        int nl = 0;
+        launch_keys(S.in_pos, n, geom_of(D), S.ikeys[0], S.ivals[0], S.d_err, st);
+        launch_radix_sort(S.ikeys[0], S.ivals[0], S.ikeys[1], S.ivals[1], n, 3 * L, S.itmp, st,
+                          &S.ikeys_sorted, &S.iperm, &nl);
+        dest_counts_kernel<<<1, 32, 0, st>>>(S.ikeys_sorted, n, R, nleaf, S.d_crow);
+    } else {
+        DCK(cudaMemsetAsync(S.d_crow, 0, R * sizeof(int), st), "memset counts");
+    }
+    DCK(cudaGetLastError(), "phase0a kernels");
+    return VFMM_OK;
+}
+
+vfmm_status dist_phase0b(RankState& S, const DistShared& D, cudaStream_t st, std::string* err) {
+    const int R = D.R, r = S.rank;
+    S.h_cmat.resize((size_t)R * R);
+    DCK(cudaMemcpyAsync(S.h_cmat.data(), S.d_cmat, R * R * sizeof(int), cudaMemcpyDeviceToHost,
+                        st),
+        "copy counts");
+    DCK(cudaStreamSynchronize(st), "sync counts");  // host sync 1 of 2: C1 message sizes
+    S.c1_send_off.assign(R, 0);
+    S.c1_send_cnt.assign(R, 0);
+    S.c1_recv_off.assign(R, 0);
+    S.c1_recv_cnt.assign(R, 0);
+    int64_t so = 0, ro = 0;
+    for (int q = 0; q < R; ++q) {
+        S.c1_send_off[q] = so;
+        S.c1_send_cnt[q] = S.h_cmat[(size_t)r * R + q];
+        so += S.c1_send_cnt[q];
+        S.c1_recv_off[q] = ro;
+        S.c1_recv_cnt[q] = S.h_cmat[(size_t)q * R + r];
+        ro += S.c1_recv_cnt[q];
+    }
+    if (so != S.n_in) {
+        if (err) *err = "C1 counts do not add up to the rank's particles";
+        return VFMM_ESTATE;
+    }
+    S.n_own = ro;
+    if (S.n_own > S.cap_own) {
+        dfree(S.irecv);
+        dfree(S.own);
+        S.cap_own = 0;
+        DCK(cudaMalloc((void**)&S.irecv, 6 * S.n_own * sizeof(float)), "alloc c1 recv");
+        DCK(cudaMalloc((void**)&S.own, 12 * S.n_own * sizeof(float)), "alloc owned");
+        S.cap_own = S.n_own;
+    }
+    if (S.n_in > 0)
+        pack_aos6_kernel<<<grid_of(S.n_in), 256, 0, st>>>(S.in_pos, S.in_gam, S.n_in, S.iperm,
+                                                          S.isend);
+    DCK(cudaGetLastError(), "phase0b kernels");
+    S.bytes_sent = (so - S.c1_send_cnt[r]) * 24;
+    S.bytes_recv = (ro - S.c1_recv_cnt[r]) * 24;
+    return VFMM_OK;
+}
+
+vfmm_status dist_phase0c(RankState& S, const DistShared& D, cudaStream_t st, std::string* err) {
+    (void)D;
+    const int64_t m = S.n_own;
+    if (m > 0)
+        unpack_aos6_kernel<<<grid_of(m), 256, 0, st>>>(S.irecv, m, nullptr, S.own, S.own + 3 * m);
+    DCK(cudaGetLastError(), "phase0c kernels");
+    S.n_local = m;
+    S.pos = S.own;
+    S.gam = S.own + 3 * m;
+    S.vel = S.own + 6 * m;
+    S.dg = S.own + 9 * m;
+    return VFMM_OK;
+}
+
+// ---- 1-4: the FMM on the owned particles ----------------------------------------------
 
 vfmm_status dist_phase1(RankState& S, const DistShared& D, cudaStream_t st, std::string* err) {
     const int L = D.depth, R = D.R;
@@ -340,10 +555,10 @@ vfmm_status dist_phase1(RankState& S, const DistShared& D, cudaStream_t st, std:
         dfree(S.radix_tmp);
         S.cap_local = 0;
         for (int b = 0; b < 2; ++b) {
-            DCK(cudaMalloc((void**)&S.keys[b], std::max<int64_t>(n, 1) * 4), "alloc keys");
-            DCK(cudaMalloc((void**)&S.vals[b], std::max<int64_t>(n, 1) * 4), "alloc vals");
+            DCK(cudaMalloc((void**)&S.keys[b], n * 4), "alloc keys");
+            DCK(cudaMalloc((void**)&S.vals[b], n * 4), "alloc vals");
         }
-        DCK(cudaMalloc(&S.radix_tmp, radix_temp_bytes(std::max<int64_t>(n, 1))), "alloc radix");
+        DCK(cudaMalloc(&S.radix_tmp, radix_temp_bytes(n)), "alloc radix");
         S.cap_local = n;
     }
     if (S.cap_depth != L) {
@@ -351,22 +566,18 @@ vfmm_status dist_phase1(RankState& S, const DistShared& D, cudaStream_t st, std:
         dfree(S.counts_own);
         dfree(S.counts_all);
         dfree(S.gstart);
+        dfree(S.d_need);
         DCK(cudaMalloc((void**)&S.lstart, (nleaf + 1) * 4), "alloc lstart");
         // sized for R = 1 (the largest owned range): R may change between calls at one depth
         DCK(cudaMalloc((void**)&S.counts_own, nleaf * 4), "alloc counts");
         DCK(cudaMalloc((void**)&S.counts_all, nleaf * 4), "alloc counts");
         DCK(cudaMalloc((void**)&S.gstart, (nleaf + 1) * 4), "alloc gstart");
+        DCK(cudaMalloc((void**)&S.d_need, nleaf), "alloc need mask");
+        S.plan_dirty = true;
     }
-    if (!S.d_err) {
-        DCK(cudaMalloc((void**)&S.d_err, sizeof(int)), "alloc err");
-        DCK(cudaMemset(S.d_err, 0, sizeof(int)), "memset err");
-        DCK(cudaMalloc((void**)&S.d_pairs, sizeof(unsigned long long)), "alloc pairs");
-    }
-    const vfmm_params& P = D.prm;
-    Geom g{P.box_lo, P.box_len, (double)P.box_lo, (double)P.box_len, L, P.image_levels > 0};
     int nl = 0;
     if (n > 0) {
-        launch_keys(S.pos, n, g, S.keys[0], S.vals[0], S.d_err, st);
+        launch_keys(S.pos, n, geom_of(D), S.keys[0], S.vals[0], S.d_err, st);
         launch_radix_sort(S.keys[0], S.vals[0], S.keys[1], S.vals[1], n, 3 * L, S.radix_tmp, st,
                           &S.keys_sorted, &S.perm, &nl);
         launch_leaf_ranges(S.keys_sorted, n, L, S.lstart, st);
@@ -380,41 +591,75 @@ vfmm_status dist_phase1(RankState& S, const DistShared& D, cudaStream_t st, std:
     return VFMM_OK;
 }
 
+// static device tables of the plan: the need mask (owned + halo leaves) and the LET cell lists
+static vfmm_status upload_plan(RankState& S, const DistShared& D, cudaStream_t st,
+                               std::string* err) {
+    const int L = D.depth, R = D.R, r = S.rank;
+    const int64_t nleaf = (int64_t)1 << (3 * L);
+    std::vector<uint8_t> need(nleaf, 0);
+    for (int64_t c = owned_lo(L, R, r); c < owned_lo(L, R, r) + owned_cnt(L, R); ++c) need[c] = 1;
+    for (int q = 0; q < R; ++q)
+        for (int leaf : S.plan.p_recv[q]) need[leaf] = 1;
+    std::vector<int> cells;
+    for (int q = 0; q < R; ++q)
+        for (int l = 2; l <= L; ++l)
+            for (int cidx : S.plan.m_send[l][q]) cells.push_back(cidx);
+    const int nsend_cells = (int)cells.size();
+    for (int q = 0; q < R; ++q)
+        for (int l = 2; l <= L; ++l)
+            for (int cidx : S.plan.m_recv[l][q]) cells.push_back(cidx);
+    S.n_recv_cells_off = nsend_cells;
+    S.n_recv_cells = (int)cells.size() - nsend_cells;
+    DCK(grow(S.d_cells, S.cap_cells, cells.size()), "alloc cells");
+    // synchronous uploads (once per plan): the host vectors die at return
+    DCK(cudaStreamSynchronize(st), "sync before plan upload");
+    DCK(cudaMemcpy(S.d_need, need.data(), nleaf, cudaMemcpyHostToDevice), "upload need mask");
+    if (!cells.empty())
+        DCK(cudaMemcpy(S.d_cells, cells.data(), cells.size() * sizeof(int), cudaMemcpyHostToDevice),
+            "upload cells");
+    S.plan_dirty = false;
+    return VFMM_OK;
+}
+
 vfmm_status dist_phase2(RankState& S, const DistShared& D, cudaStream_t st, std::string* err) {
     const int L = D.depth, R = D.R, r = S.rank;
     const int64_t nleaf = (int64_t)1 << (3 * L);
-    scan_counts_kernel<<<1, 1024, 0, st>>>(S.counts_all, nleaf, S.gstart);
+    if (S.plan_dirty) {
+        vfmm_status s = upload_plan(S, D, st, err);
+        if (s != VFMM_OK) return s;
+    }
+    scan_counts_kernel<<<1, 1024, 0, st>>>(S.counts_all, S.d_need, nleaf, S.gstart);
     S.hstart.resize(nleaf + 1);
     DCK(cudaMemcpyAsync(S.hstart.data(), S.gstart, (nleaf + 1) * 4, cudaMemcpyDeviceToHost, st),
         "copy gstart");
-    DCK(cudaStreamSynchronize(st), "sync gstart");
+    DCK(cudaStreamSynchronize(st), "sync gstart");  // host sync 2 of 2: halo message sizes
     S.n_total = S.hstart[nleaf];
     S.gbase = S.hstart[owned_lo(L, R, r)];
     const int nc = ncoef(D.prm.p);
-    if (S.n_total > S.cap_total || S.cap_depth != L || S.cap_p != D.prm.p) {
+    if (S.n_total > S.cap_total) {
         dfree(S.sorted6);
         dfree(S.near6);
-        dfree(S.Mall);
-        dfree(S.Lall);
         S.cap_total = 0;
         const int64_t nt = std::max<int64_t>(S.n_total, 1);
         DCK(cudaMalloc((void**)&S.sorted6, 6 * nt * 4), "alloc sorted6");
         DCK(cudaMalloc((void**)&S.near6, 6 * nt * 4), "alloc near6");
+        S.cap_total = S.n_total;
+    }
+    if (S.cap_depth != L || S.cap_p != D.prm.p) {
+        dfree(S.Mall);
+        dfree(S.Lall);
         const int64_t cells = level_offset(L + 1);
         DCK(cudaMalloc((void**)&S.Mall, cells * 3 * nc * 4), "alloc M");
         DCK(cudaMalloc((void**)&S.Lall, cells * 3 * nc * 4), "alloc L");
         DCK(cudaMemset(S.Mall, 0, cells * 3 * nc * 4), "memset M");
-        S.cap_total = S.n_total;
         S.cap_depth = L;
         S.cap_p = D.prm.p;
     }
-    const vfmm_params& P = D.prm;
-    Geom g{P.box_lo, P.box_len, (double)P.box_lo, (double)P.box_len, L, P.image_levels > 0};
     if (S.n_local > 0)
-        launch_gather(S.pos, S.gam, S.perm, S.keys_sorted, S.n_local, g, S.sorted6, S.n_total,
-                      S.gbase, st);
-    // ---- pack halo particles for every peer ----
-    std::vector<Seg> segs;
+        launch_gather(S.pos, S.gam, S.perm, S.keys_sorted, S.n_local, geom_of(D), S.sorted6,
+                      S.n_total, S.gbase, st);
+    // ---- pack halo particles for every peer (segments in compact sorted order) ----
+    S.h_segs.clear();
     S.p_send_off.assign(R, 0);
     S.p_send_cnt.assign(R, 0);
     int64_t off = 0;
@@ -422,12 +667,12 @@ vfmm_status dist_phase2(RankState& S, const DistShared& D, cudaStream_t st, std:
         S.p_send_off[q] = off;
         for (int leaf : S.plan.p_send[q]) {
             const int64_t c = S.hstart[leaf + 1] - S.hstart[leaf];
-            if (c) segs.push_back({S.hstart[leaf], c, off});
+            if (c) S.h_segs.push_back({S.hstart[leaf], c, off});
             off += c;
         }
         S.p_send_cnt[q] = off - S.p_send_off[q];
     }
-    const int nsend_segs = (int)segs.size();
+    const int nsend_segs = (int)S.h_segs.size();
     S.n_send_segs = nsend_segs;
     S.p_recv_off.assign(R, 0);
     S.p_recv_cnt.assign(R, 0);
@@ -436,28 +681,36 @@ vfmm_status dist_phase2(RankState& S, const DistShared& D, cudaStream_t st, std:
         S.p_recv_off[q] = roff;
         for (int leaf : S.plan.p_recv[q]) {
             const int64_t c = S.hstart[leaf + 1] - S.hstart[leaf];
-            if (c) segs.push_back({S.hstart[leaf], c, roff});
+            if (c) S.h_segs.push_back({S.hstart[leaf], c, roff});
             roff += c;
         }
         S.p_recv_cnt[q] = roff - S.p_recv_off[q];
     }
     S.p_recv_total = roff;
-    S.n_recv_segs = (int)segs.size() - nsend_segs;
-    DCK(grow(S.d_segs, S.cap_segs, segs.size()), "alloc segs");
-    if (!segs.empty())
-        DCK(cudaMemcpyAsync(S.d_segs, segs.data(), segs.size() * sizeof(Seg), cudaMemcpyHostToDevice,
-                            st),
+    S.n_recv_segs = (int)S.h_segs.size() - nsend_segs;
+    DCK(grow(S.d_segs, S.cap_segs, S.h_segs.size()), "alloc segs");
+    // pageable upload: staged before the call returns, and h_segs outlives it anyway
+    if (!S.h_segs.empty())
+        DCK(cudaMemcpyAsync(S.d_segs, S.h_segs.data(), S.h_segs.size() * sizeof(Seg),
+                            cudaMemcpyHostToDevice, st),
             "copy segs");
     DCK(grow(S.sendbuf, S.cap_send, (size_t)std::max<int64_t>(off * 6, 1)), "alloc send");
     DCK(grow(S.recvbuf, S.cap_recv, (size_t)std::max<int64_t>(roff * 6, 1)), "alloc recv");
     if (nsend_segs)
         pack_particles_kernel<<<std::min(nsend_segs, 148 * 8), 256, 0, st>>>(
             S.sorted6, S.n_total, S.d_segs, nsend_segs, S.sendbuf);
-    // the host segment vector must stay alive until the async copy is done
-    DCK(cudaStreamSynchronize(st), "sync segs");
     DCK(cudaGetLastError(), "phase2 kernels");
-    S.bytes_sent = off * 24;
-    S.bytes_recv = roff * 24;
+    S.bytes_sent += off * 24;
+    S.bytes_recv += roff * 24;
+    return VFMM_OK;
+}
+
+vfmm_status dist_unpack_halo(RankState& S, const DistShared& D, cudaStream_t st, std::string* err) {
+    (void)D;
+    if (S.n_recv_segs)
+        unpack_particles_kernel<<<std::min(S.n_recv_segs, 148 * 8), 256, 0, st>>>(
+            S.sorted6, S.n_total, S.d_segs + S.n_send_segs, S.n_recv_segs, S.recvbuf);
+    DCK(cudaGetLastError(), "halo unpack");
     return VFMM_OK;
 }
 
@@ -465,12 +718,6 @@ vfmm_status dist_phase3(RankState& S, const DistShared& D, cudaStream_t st, std:
     const int L = D.depth, R = D.R, r = S.rank;
     const int p = D.prm.p, nc = ncoef(p);
     const int cellsz = 3 * nc;
-    const int64_t nleaf = (int64_t)1 << (3 * L);
-    // halo particles into their global positions
-    if (S.n_recv_segs)
-        unpack_particles_kernel<<<std::min(S.n_recv_segs, 148 * 8), 256, 0, st>>>(
-            S.sorted6, S.n_total, S.d_segs + S.n_send_segs, S.n_recv_segs, S.recvbuf);
-    (void)nleaf;
     const float a = (float)((double)D.prm.box_len / (double)(1 << L));
     auto Mlev = [&](int l) { return S.Mall + level_offset(l) * cellsz; };
     launch_p2m(S.sorted6, S.n_total, S.gstart, p, 1.f / a, Mlev(L), owned_lo(L, R, r),
@@ -478,43 +725,24 @@ vfmm_status dist_phase3(RankState& S, const DistShared& D, cudaStream_t st, std:
     for (int l = L - 1; l >= 1; --l)
         launch_m2m(D.m2m, p, D.KP, D.NR, Mlev(l + 1), Mlev(l), l, owned_lo(l, R, r),
                    owned_cnt(l, R), D.m2m_scratch, D.m2m_scratch_floats, st);
-    // ---- pack LET multipoles (levels 2..L) per peer ----
-    std::vector<int> cells;
+    // ---- pack LET multipoles (levels 2..L) per peer (cell lists uploaded with the plan) ----
     S.m_send_off.assign(R, 0);
     S.m_send_cnt.assign(R, 0);
     int64_t off = 0;  // floats
-    std::vector<std::pair<int, int>> send_runs;  // (level, count) in order, for the pack launch
     for (int q = 0; q < R; ++q) {
         S.m_send_off[q] = off;
-        for (int l = 2; l <= L; ++l) {
-            const auto& v = S.plan.m_send[l][q];
-            for (int cidx : v) cells.push_back(cidx);
-            send_runs.push_back({l, (int)v.size()});
-            off += (int64_t)v.size() * cellsz;
-        }
+        for (int l = 2; l <= L; ++l) off += (int64_t)S.plan.m_send[l][q].size() * cellsz;
         S.m_send_cnt[q] = off - S.m_send_off[q];
     }
-    const int nsend_cells = (int)cells.size();
     S.m_recv_off.assign(R, 0);
     S.m_recv_cnt.assign(R, 0);
     int64_t roff = 0;
     for (int q = 0; q < R; ++q) {
         S.m_recv_off[q] = roff;
-        for (int l = 2; l <= L; ++l) {
-            const auto& v = S.plan.m_recv[l][q];
-            for (int cidx : v) cells.push_back(cidx);
-            roff += (int64_t)v.size() * cellsz;
-        }
+        for (int l = 2; l <= L; ++l) roff += (int64_t)S.plan.m_recv[l][q].size() * cellsz;
         S.m_recv_cnt[q] = roff - S.m_recv_off[q];
     }
     S.m_recv_floats = roff;
-    S.n_recv_cells_off = nsend_cells;
-    S.n_recv_cells = (int)cells.size() - nsend_cells;
-    DCK(grow(S.d_cells, S.cap_cells, cells.size()), "alloc cells");
-    if (!cells.empty())
-        DCK(cudaMemcpyAsync(S.d_cells, cells.data(), cells.size() * sizeof(int),
-                            cudaMemcpyHostToDevice, st),
-            "copy cells");
     DCK(grow(S.msend, S.cap_msend, (size_t)std::max<int64_t>(off, 1)), "alloc msend");
     DCK(grow(S.mrecv, S.cap_mrecv, (size_t)std::max<int64_t>(roff, 1)), "alloc mrecv");
     int64_t coff = 0, boff = 0;
@@ -527,22 +755,16 @@ vfmm_status dist_phase3(RankState& S, const DistShared& D, cudaStream_t st, std:
             coff += cnt;
             boff += (int64_t)cnt * cellsz;
         }
-    DCK(cudaStreamSynchronize(st), "sync cells");
     DCK(cudaGetLastError(), "phase3 kernels");
     S.bytes_sent += off * 4;
     S.bytes_recv += roff * 4;
     return VFMM_OK;
 }
 
-vfmm_status dist_phase4(RankState& S, const DistShared& D, cudaStream_t st, std::string* err) {
-    const int L = D.depth, R = D.R, r = S.rank;
-    const int p = D.prm.p, nc = ncoef(p);
-    const int cellsz = 3 * nc;
-    const vfmm_params& P = D.prm;
-    const int periodic = P.image_levels > 0;
+vfmm_status dist_unpack_let(RankState& S, const DistShared& D, cudaStream_t st, std::string* err) {
+    const int L = D.depth, R = D.R;
+    const int cellsz = 3 * ncoef(D.prm.p);
     auto Mlev = [&](int l) { return S.Mall + level_offset(l) * cellsz; };
-    auto Llev = [&](int l) { return S.Lall + level_offset(l) * cellsz; };
-    // LET multipoles into place
     int64_t coff = S.n_recv_cells_off, boff = 0;
     for (int q = 0; q < R; ++q)
         for (int l = 2; l <= L; ++l) {
@@ -553,6 +775,18 @@ vfmm_status dist_phase4(RankState& S, const DistShared& D, cudaStream_t st, std:
             coff += cnt;
             boff += (int64_t)cnt * cellsz;
         }
+    DCK(cudaGetLastError(), "LET unpack");
+    return VFMM_OK;
+}
+
+vfmm_status dist_phase4_far(RankState& S, const DistShared& D, cudaStream_t st, std::string* err) {
+    const int L = D.depth, R = D.R, r = S.rank;
+    const int p = D.prm.p, nc = ncoef(p);
+    const int cellsz = 3 * nc;
+    const vfmm_params& P = D.prm;
+    const int periodic = P.image_levels > 0;
+    auto Mlev = [&](int l) { return S.Mall + level_offset(l) * cellsz; };
+    auto Llev = [&](int l) { return S.Lall + level_offset(l) * cellsz; };
     // root multipole (every rank, from the all-gathered level 1)
     launch_m2m(D.m2m, p, D.KP, D.NR, Mlev(1), Mlev(0), 0, 0, 1, D.m2m_scratch,
                D.m2m_scratch_floats, st);
@@ -605,25 +839,91 @@ vfmm_status dist_phase4(RankState& S, const DistShared& D, cudaStream_t st, std:
         const int64_t pcnt = l == 1 ? 1 : owned_cnt(l - 1, R);
         launch_l2l(D.l2l, p, D.KP, D.NR, Llev(l - 1), Llev(l), l, plo, pcnt, st);
     }
+    DCK(cudaGetLastError(), "phase4 far kernels");
+    return VFMM_OK;
+}
+
+vfmm_status dist_phase4_near(RankState& S, const DistShared& D, cudaStream_t st, std::string* err) {
+    const int L = D.depth, R = D.R, r = S.rank;
+    const int p = D.prm.p;
+    const vfmm_params& P = D.prm;
+    const int periodic = P.image_levels > 0;
     const KernelConsts kc = make_kernel_consts(P.sigma);
     const float a = (float)((double)P.box_len / (double)(1 << L));
     const bool use_far = P.mode == VFMM_MODE_FMM || P.mode == VFMM_MODE_FAR_ONLY;
     const bool use_near = P.mode == VFMM_MODE_FMM || P.mode == VFMM_MODE_NEAR_ONLY;
+    const int cellsz = 3 * ncoef(p);
     DCK(cudaMemsetAsync(S.d_pairs, 0, sizeof(unsigned long long), st), "memset pairs");
     if (use_near)
         launch_p2p(S.sorted6, S.n_total, S.gstart, L, a, periodic, P.scheme, kc, S.near6, S.d_pairs,
                    owned_lo(L - 1, R, r), owned_cnt(L - 1, R), st);
     if (S.n_local > 0)
-        launch_l2p_combine(D.l2p, S.sorted6, S.near6, S.perm, S.n_total, S.gstart, p, a, Llev(L), P.scheme,
-                           use_near, use_far, S.vel, S.dg, owned_lo(L, R, r), owned_cnt(L, R),
-                           S.gbase, S.n_local, st);
-    DCK(cudaGetLastError(), "phase4 kernels");
+        launch_l2p_combine(D.l2p, S.sorted6, S.near6, S.perm, S.n_total, S.gstart, p, a,
+                           S.Lall + level_offset(L) * cellsz, P.scheme, use_near, use_far, S.vel,
+                           S.dg, owned_lo(L, R, r), owned_cnt(L, R), S.gbase, S.n_local, st);
+    DCK(cudaGetLastError(), "phase4 near kernels");
+    return VFMM_OK;
+}
+
+// ---- 5: results back to the caller ----------------------------------------------------
+
+vfmm_status dist_phase5a(RankState& S, const DistShared& D, cudaStream_t st, std::string* err) {
+    (void)D;
+    const int64_t m = S.n_own;  // results in received order -> AoS for the return trip
+    if (m > 0)
+        pack_aos6_kernel<<<grid_of(m), 256, 0, st>>>(S.vel, S.dg, m, nullptr, S.irecv);
+    DCK(cudaGetLastError(), "phase5a kernels");
+    return VFMM_OK;
+}
+
+vfmm_status dist_phase5b(RankState& S, const DistShared& D, cudaStream_t st, std::string* err) {
+    (void)D;
+    const int64_t n = S.n_in;  // isend now holds the results in local Morton order
+    if (n > 0)
+        unpack_aos6_kernel<<<grid_of(n), 256, 0, st>>>(S.isend, n, S.iperm, S.in_vel, S.in_dg);
+    DCK(cudaGetLastError(), "phase5b kernels");
+    S.bytes_sent += (S.n_own - S.c1_recv_cnt[S.rank]) * 24;
+    S.bytes_recv += (S.n_in - S.c1_send_cnt[S.rank]) * 24;
     return VFMM_OK;
 }
 
 // ---------------------------------------------------------------------------------------
 // exchanges: logical ranks (device copies within one process)
 // ---------------------------------------------------------------------------------------
+vfmm_status logical_x0a(std::vector<RankState*>& S, const DistShared& D, cudaStream_t st) {
+    const int R = D.R;
+    for (int r = 0; r < R; ++r)
+        for (int q = 0; q < R; ++q)
+            if (cudaMemcpyAsync(S[r]->d_cmat + q * R, S[q]->d_crow, R * sizeof(int),
+                                cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+                return VFMM_ECUDA;
+    return VFMM_OK;
+}
+vfmm_status logical_x0b(std::vector<RankState*>& S, const DistShared& D, cudaStream_t st) {
+    const int R = D.R;
+    for (int r = 0; r < R; ++r)
+        for (int q = 0; q < R; ++q) {  // q sends its run for r
+            const int64_t c = S[r]->c1_recv_cnt[q];
+            if (c != S[q]->c1_send_cnt[r]) return VFMM_ESTATE;
+            if (c && cudaMemcpyAsync(S[r]->irecv + S[r]->c1_recv_off[q] * 6,
+                                     S[q]->isend + S[q]->c1_send_off[r] * 6, c * 24,
+                                     cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+                return VFMM_ECUDA;
+        }
+    return VFMM_OK;
+}
+vfmm_status logical_x5(std::vector<RankState*>& S, const DistShared& D, cudaStream_t st) {
+    const int R = D.R;
+    for (int r = 0; r < R; ++r)
+        for (int q = 0; q < R; ++q) {  // r returns q's results
+            const int64_t c = S[r]->c1_recv_cnt[q];
+            if (c && cudaMemcpyAsync(S[q]->isend + S[q]->c1_send_off[r] * 6,
+                                     S[r]->irecv + S[r]->c1_recv_off[q] * 6, c * 24,
+                                     cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+                return VFMM_ECUDA;
+        }
+    return VFMM_OK;
+}
 vfmm_status logical_x1(std::vector<RankState*>& S, const DistShared& D, cudaStream_t st) {
     const int R = D.R;
     const int64_t per = ((int64_t)1 << (3 * D.depth)) / R;
@@ -675,7 +975,7 @@ vfmm_status logical_x3(std::vector<RankState*>& S, const DistShared& D, cudaStre
 }
 
 // ---------------------------------------------------------------------------------------
-// exchanges: NCCL (grouped point-to-point + all-gather on the compute stream)
+// exchanges: NCCL (grouped point-to-point + all-gather on the given stream)
 // ---------------------------------------------------------------------------------------
 bool nccl_available() { return g_nccl.load(); }
 
@@ -695,8 +995,78 @@ vfmm_status nccl_init(void** comm, int nranks, int rank, const void* id128) {
     *comm = (void*)c;
     return VFMM_OK;
 }
+vfmm_status nccl_async_error(void* comm, std::string* err) {
+    if (!comm || !g_nccl.CommGetAsyncError) return VFMM_OK;
+    ncclResult_t a = ncclSuccess;
+    if (g_nccl.CommGetAsyncError((ncclComm_t)comm, &a) != ncclSuccess || a != ncclSuccess) {
+        if (err)
+            *err = std::string("NCCL asynchronous error: ") +
+                   (g_nccl.GetErrorString ? g_nccl.GetErrorString(a) : "unknown");
+        return VFMM_ENCCL;
+    }
+    return VFMM_OK;
+}
 void nccl_destroy(void* comm) {
     if (comm && g_nccl.h) g_nccl.CommDestroy((ncclComm_t)comm);
+}
+
+namespace {
+// grouped point-to-point exchange: send[q] / recv[q] = (pointer, floats); every return code
+// is checked, and the group is always closed
+vfmm_status nccl_p2p_group(int R, int self, const std::vector<std::pair<const float*, int64_t>>& snd,
+                           const std::vector<std::pair<float*, int64_t>>& rcv, ncclComm_t comm,
+                           cudaStream_t st, const float* ag_send = nullptr, float* ag_recv = nullptr,
+                           int64_t ag_count = 0) {
+    if (g_nccl.GroupStart() != ncclSuccess) return VFMM_ENCCL;
+    ncclResult_t r = ncclSuccess;
+    if (ag_recv && r == ncclSuccess)
+        r = g_nccl.AllGather(ag_send, ag_recv, (size_t)ag_count, ncclFloat32, comm, st);
+    for (int q = 0; q < R && r == ncclSuccess; ++q) {
+        if (q == self) continue;
+        if (snd[q].second && r == ncclSuccess)
+            r = g_nccl.Send(snd[q].first, (size_t)snd[q].second, ncclFloat32, q, comm, st);
+        if (rcv[q].second && r == ncclSuccess)
+            r = g_nccl.Recv(rcv[q].first, (size_t)rcv[q].second, ncclFloat32, q, comm, st);
+    }
+    const ncclResult_t e = g_nccl.GroupEnd();
+    return (r == ncclSuccess && e == ncclSuccess) ? VFMM_OK : VFMM_ENCCL;
+}
+}  // namespace
+
+vfmm_status nccl_x0a(RankState& S, const DistShared& D, void* comm, cudaStream_t st) {
+    if (g_nccl.AllGather(S.d_crow, S.d_cmat, (size_t)D.R, ncclInt32, (ncclComm_t)comm, st) !=
+        ncclSuccess)
+        return VFMM_ENCCL;
+    return VFMM_OK;
+}
+vfmm_status nccl_x0b(RankState& S, const DistShared& D, void* comm, cudaStream_t st) {
+    const int R = D.R, r = S.rank;
+    std::vector<std::pair<const float*, int64_t>> snd(R);
+    std::vector<std::pair<float*, int64_t>> rcv(R);
+    for (int q = 0; q < R; ++q) {
+        snd[q] = {S.isend + S.c1_send_off[q] * 6, S.c1_send_cnt[q] * 6};
+        rcv[q] = {S.irecv + S.c1_recv_off[q] * 6, S.c1_recv_cnt[q] * 6};
+    }
+    // the rank's own run stays local
+    if (S.c1_send_cnt[r] &&
+        cudaMemcpyAsync(rcv[r].first, snd[r].first, S.c1_send_cnt[r] * 24,
+                        cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        return VFMM_ECUDA;
+    return nccl_p2p_group(R, r, snd, rcv, (ncclComm_t)comm, st);
+}
+vfmm_status nccl_x5(RankState& S, const DistShared& D, void* comm, cudaStream_t st) {
+    const int R = D.R, r = S.rank;
+    std::vector<std::pair<const float*, int64_t>> snd(R);
+    std::vector<std::pair<float*, int64_t>> rcv(R);
+    for (int q = 0; q < R; ++q) {  // reverse of X0b
+        snd[q] = {S.irecv + S.c1_recv_off[q] * 6, S.c1_recv_cnt[q] * 6};
+        rcv[q] = {S.isend + S.c1_send_off[q] * 6, S.c1_send_cnt[q] * 6};
+    }
+    if (S.c1_send_cnt[r] &&
+        cudaMemcpyAsync(rcv[r].first, snd[r].first, S.c1_send_cnt[r] * 24,
+                        cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+        return VFMM_ECUDA;
+    return nccl_p2p_group(R, r, snd, rcv, (ncclComm_t)comm, st);
 }
 vfmm_status nccl_x1(RankState& S, const DistShared& D, void* comm, cudaStream_t st) {
     const int64_t per = ((int64_t)1 << (3 * D.depth)) / D.R;
@@ -707,38 +1077,28 @@ vfmm_status nccl_x1(RankState& S, const DistShared& D, void* comm, cudaStream_t 
 }
 vfmm_status nccl_x2(RankState& S, const DistShared& D, void* comm, cudaStream_t st) {
     const int R = D.R;
-    if (g_nccl.GroupStart() != ncclSuccess) return VFMM_ENCCL;
+    std::vector<std::pair<const float*, int64_t>> snd(R);
+    std::vector<std::pair<float*, int64_t>> rcv(R);
     for (int q = 0; q < R; ++q) {
-        if (q == S.rank) continue;
-        if (S.p_send_cnt[q])
-            g_nccl.Send(S.sendbuf + S.p_send_off[q] * 6, S.p_send_cnt[q] * 6, ncclFloat32, q,
-                        (ncclComm_t)comm, st);
-        if (S.p_recv_cnt[q])
-            g_nccl.Recv(S.recvbuf + S.p_recv_off[q] * 6, S.p_recv_cnt[q] * 6, ncclFloat32, q,
-                        (ncclComm_t)comm, st);
+        snd[q] = {S.sendbuf + S.p_send_off[q] * 6, S.p_send_cnt[q] * 6};
+        rcv[q] = {S.recvbuf + S.p_recv_off[q] * 6, S.p_recv_cnt[q] * 6};
     }
-    if (g_nccl.GroupEnd() != ncclSuccess) return VFMM_ENCCL;
-    return VFMM_OK;
+    return nccl_p2p_group(R, S.rank, snd, rcv, (ncclComm_t)comm, st);
 }
 vfmm_status nccl_x3(RankState& S, const DistShared& D, void* comm, cudaStream_t st) {
     const int R = D.R;
     const int cellsz = 3 * ncoef(D.prm.p);
     const int64_t per1 = 8 / R;
     float* l1 = S.Mall + level_offset(1) * cellsz;
-    if (g_nccl.GroupStart() != ncclSuccess) return VFMM_ENCCL;
-    g_nccl.AllGather(l1 + S.rank * per1 * cellsz, l1, per1 * cellsz, ncclFloat32,
-                     (ncclComm_t)comm, st);  // in place
+    std::vector<std::pair<const float*, int64_t>> snd(R);
+    std::vector<std::pair<float*, int64_t>> rcv(R);
     for (int q = 0; q < R; ++q) {
-        if (q == S.rank) continue;
-        if (S.m_send_cnt[q])
-            g_nccl.Send(S.msend + S.m_send_off[q], S.m_send_cnt[q], ncclFloat32, q,
-                        (ncclComm_t)comm, st);
-        if (S.m_recv_cnt[q])
-            g_nccl.Recv(S.mrecv + S.m_recv_off[q], S.m_recv_cnt[q], ncclFloat32, q,
-                        (ncclComm_t)comm, st);
+        snd[q] = {S.msend + S.m_send_off[q], S.m_send_cnt[q]};
+        rcv[q] = {S.mrecv + S.m_recv_off[q], S.m_recv_cnt[q]};
     }
-    if (g_nccl.GroupEnd() != ncclSuccess) return VFMM_ENCCL;
-    return VFMM_OK;
+    // level-1 multipoles all-gathered in place, in the same group as the LET exchange
+    return nccl_p2p_group(R, S.rank, snd, rcv, (ncclComm_t)comm, st, l1 + S.rank * per1 * cellsz,
+                          l1, per1 * cellsz);
 }
 
 }  // namespace vfmm

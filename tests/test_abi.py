@@ -28,7 +28,8 @@ def test_library_exports_every_declared_symbol():
 
 def test_host_only_functions():
     L = vf.load_library()
-    assert L.vfmm_abi_version() == 1
+    assert L.vfmm_abi_version() == 2
+    assert ctypes.sizeof(vf.c_stats) == 10 * 8 + 4 * 8 + 2 * 4 + 2 * 8 + 2 * 8
     p = vf.c_params()
     L.vfmm_params_default(ctypes.byref(p))
     assert p.p == 10 and p.image_levels == 3 and p.depth == 0

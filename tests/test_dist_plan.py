@@ -100,11 +100,64 @@ def test_plans_agree_across_processes_gloo():
     assert out[0] and out[1]
 
 
-def test_partition_and_leaf_of():
+def test_partition_and_route_counts():
     lo, hi = vf.partition(4, 8, 3)
     assert (lo, hi) == (3 * 512, 4 * 512)
     with pytest.raises(vf.VfmmError):
         vf.partition(4, 3, 0)
-    pos = np.array([[-3.0, 3.0], [-3.0, 3.0], [-3.0, 3.0]], np.float32)
-    k = vf.leaf_of(pos, 2, np.float32(-np.pi), np.float32(2 * np.pi))
-    assert k[0] == 0 and k[1] == 63
+    lo_, ln = float(np.float32(-np.pi)), float(np.float32(2 * np.pi))
+    pos = np.array([[-3.0, 3.0, 3.0], [-3.0, 3.0, -3.0], [-3.0, 3.0, -3.0]], np.float32)
+    c, st = vf.route_counts(pos, 2, 8, lo_, ln)
+    assert st == vf.VFMM_OK
+    # octant of each point: x fastest in the Morton bits -> (0,0,0) rank 0, (1,1,1) rank 7,
+    # (1,0,0) rank 1
+    assert c.tolist() == [1, 1, 0, 0, 0, 0, 0, 1]
+    pos[1, 0] = np.float32(lo_ + ln)  # upper face: outside the half-open box
+    _, st = vf.route_counts(pos, 2, 8, lo_, ln)
+    assert st == vf.VFMM_EDOMAIN
+
+
+def _route_worker(rank, world, port, out):
+    """Each process holds arbitrary particles; the send counts (vfmm_route_counts) of every
+    rank, all-gathered over gloo, form the C1 count matrix: column sums are what each owner
+    evaluates, and they equal an independent count by brute-force octant membership."""
+    import torch
+    import torch.distributed as dist
+
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    rng = np.random.default_rng(100 + rank)
+    n = 3000 + 777 * rank
+    lo_, ln = float(np.float32(-np.pi)), float(np.float32(2 * np.pi))
+    pos = rng.uniform(lo_, lo_ + ln, (3, n)).astype(np.float32)
+    pos = np.minimum(pos, np.nextafter(np.float32(lo_ + ln), np.float32(0)))
+    depth, R = 3, 4
+    cnt, st = vf.route_counts(pos, depth, R, lo_, ln)
+    rows = [torch.zeros(R, dtype=torch.int64) for _ in range(world)]
+    dist.all_gather(rows, torch.from_numpy(cnt))
+    mat = torch.stack(rows)
+    allpos = [None] * world
+    dist.all_gather_object(allpos, pos)
+    ok = st == vf.VFMM_OK and int(mat[rank].sum()) == n
+    # brute force: rank R's range at depth 3 with R = 4 is two level-1 octants, i.e. the top
+    # Morton bits (z1, y1) of the particle's octant = rank (x fastest, so octant = x + 2y + 4z)
+    for q in range(R):
+        want = 0
+        for P_ in allpos:
+            ix = np.floor((P_ - np.float32(lo_)) * np.float32(8 / ln)).astype(int).clip(0, 7)
+            octant = (ix[0] >> 2) + 2 * (ix[1] >> 2) + 4 * (ix[2] >> 2)
+            want += int(np.sum(octant // 2 == q))
+        ok &= int(mat[:, q].sum()) == want
+    out[rank] = bool(ok)
+    dist.destroy_process_group()
+
+
+def test_route_counts_across_processes_gloo():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_route_worker, args=(2, port, out), nprocs=2, join=True)
+    assert out[0] and out[1]

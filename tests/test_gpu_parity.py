@@ -134,8 +134,8 @@ def test_near_only_dense_leaves_multiwindow_equals_direct(scheme):
     tg = np.arange(0, 20000, 61)
     vo, so = oracle.direct(f.pos, f.gamma, f.sigma, f.box_lo, f.box_len, 0, scheme, targets=tg,
                            batched=True)
-    assert rel(v[:, tg], vo) < TOL.NEAR_VS_ORACLE[0] and rel(s[:, tg], so) < TOL.NEAR_VS_ORACLE[1], \
-        (rel(v[:, tg], vo), rel(s[:, tg], so))
+    tu, ts = TOL.NEAR_VS_ORACLE_DENSE
+    assert rel(v[:, tg], vo) < tu and rel(s[:, tg], so) < ts, (rel(v[:, tg], vo), rel(s[:, tg], so))
     ev.close()
 
 
@@ -485,38 +485,10 @@ def test_m2l_tensor_core_matches_simt(n, depth, p, lam, engine, monkeypatch):
     v2, s2, ev2 = run(f, p=p, depth=depth, image_levels=lam, mode=vf.MODE_FAR_ONLY)
     for l in range(depth - 1, depth + 1):
         a, b = ev1.debug_expansions(1, l), ev2.debug_expansions(1, l)
+        print(f"tc {engine} vs simt n={n} L={depth} p={p} lam={lam}: level {l} "
+              f"{rel(a[..., 1:], b[..., 1:]):.2e}")
         assert rel(a[..., 1:], b[..., 1:]) < 3e-5, (l, rel(a[..., 1:], b[..., 1:]))
+    print(f"tc {engine} vs simt n={n}: u {rel(v1, v2):.2e} sdot {rel(s1, s2):.2e}")
     assert rel(v1, v2) < 3e-5 and rel(s1, s2) < 5e-5, (rel(v1, v2), rel(s1, s2))
     ev1.close()
     ev2.close()
-
-
-# ------------------------------------------------------------------ compute-sanitizer
-
-@pytest.mark.slow
-@pytest.mark.parametrize("tool", ["memcheck", "racecheck", "synccheck", "initcheck"])
-def test_compute_sanitizer_c1(tool):
-    """compute-sanitizer over one full evaluation (examples/vfmm_c_example: 16^3 lattice, p = 6,
-    depth 2, 27^3 images, host buffers through the C ABI) -- every kernel of the pipeline,
-    including the tcgen05 / TMA / mbarrier M2L."""
-    import os
-    import shutil
-    import subprocess
-
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    exe = os.path.join(root, "examples", "vfmm_c_example")
-    san = shutil.which("compute-sanitizer") or "/usr/local/cuda/bin/compute-sanitizer"
-    if not os.path.exists(san):
-        pytest.skip("compute-sanitizer not installed")
-    if not os.path.exists(exe):
-        lib = os.path.join(root, "paper_1110_2921_b200", "lib")
-        subprocess.check_call(["gcc", "-O2", "-I", os.path.join(root, "include"), exe + ".c",
-                               "-L", lib, "-lvfmm", f"-Wl,-rpath,{lib}", "-lm", "-o", exe])
-    cmd = [san, "--tool", tool, "--error-exitcode", "99"]
-    if tool == "memcheck":
-        cmd += ["--leak-check", "full"]
-    r = subprocess.run(cmd + [exe, "16"], capture_output=True, text=True, timeout=1200)
-    tail = (r.stdout + r.stderr)[-3000:]
-    print(tail)
-    assert r.returncode == 0, tail
-    assert "ERROR SUMMARY: 0 errors" in r.stdout + r.stderr, tail

@@ -23,3 +23,7 @@ NEAR_VS_ORACLE = (2e-6, 5e-6)
 # scripts/p2p_precision.py, 7.3e-7 / 1.4e-6 with the default per-pair cross products).  Still
 # an order of magnitude below the FMM truncation error at p = 10 (FMM_VS_DIRECT).
 NEAR_VS_ORACLE_SJ = (4.5e-6, 1e-5)
+# NEAR_ONLY over very long source lists (20000 sources per target, the dense-leaf test): FP32
+# accumulation in sequence grows like sqrt(n) 2^-24 ~ 8e-6 relative to the sum of |terms|
+# (measured 2.5e-6 / 3.5e-6 on the B200), so the per-target bound scales with the list length.
+NEAR_VS_ORACLE_DENSE = (1e-5, 1.5e-5)
