@@ -121,6 +121,21 @@ vfmm_status vfmm_create(vfmm_ctx** ctx, const vfmm_params* prm, int device);
 vfmm_status vfmm_evaluate(vfmm_ctx* ctx, int64_t n, const float* pos, const float* gamma,
                           float* vel, float* dgamma, void* cuda_stream);
 
+/* One forward-Euler time step of the vortex particle method (section 2; forward
+   Euler), the three updates simultaneous:
+     x_i     += u_i dt          convection, Eq. (7) PAPER.md:91 (wrapped into the box when
+                                image_levels > 0; positions stay in [lo, lo+len))
+     gamma_i += dgamma_i/dt dt  stretching, Eq. (8)
+     sigma^2 += 2 nu dt         diffusion by core spreading, Eq. (9)
+   u and dgamma/dt are evaluated as vfmm_evaluate does at the current (x, gamma, sigma)
+   and written to vel / dgamma (device, 3 x n, may be NULL); pos and gamma (device, 3 x n) are
+   updated in place.  The context's sigma becomes sqrt(sigma^2 + 2 nu dt) (uniform core,
+   reading R4) for the next step; *sigma_out (may be NULL) receives it.  Asynchronous on
+   `cuda_stream`; dt must be finite, nu >= 0.  Distributed contexts: every rank steps its own
+   particles (collective). */
+vfmm_status vfmm_step(vfmm_ctx* ctx, int64_t n, float* pos, float* gamma, float dt, float nu,
+                      float* vel, float* dgamma, float* sigma_out, void* cuda_stream);
+
 /* ---- multi-GPU: Morton-range spatial decomposition + local-essential-tree exchange ----
    (the paper's multi-GPU runs.)  Rank r of R
    (R in {1, 2, 4, 8}) owns the Morton leaf range [r 8^L/R, (r+1) 8^L/R) at depth L

@@ -62,7 +62,7 @@ EXPORTS = ["vfmm_abi_version", "vfmm_params_default", "vfmm_create", "vfmm_evalu
            "vfmm_debug_tree", "vfmm_debug_expansions", "vfmm_strerror",
            "vfmm_last_error_message", "vfmm_destroy", "vfmm_nccl_get_unique_id",
            "vfmm_create_nccl", "vfmm_partition", "vfmm_evaluate_logical", "vfmm_dist_plan",
-           "vfmm_route_counts"]
+           "vfmm_route_counts", "vfmm_step"]
 
 
 def load_library(path: str = LIB_PATH):
@@ -96,6 +96,9 @@ def load_library(path: str = LIB_PATH):
     L.vfmm_evaluate_logical.argtypes = [vp, i32, vp, vp, vp, vp, vp, vp]
     L.vfmm_dist_plan.argtypes = [i32, i32, i32, i32, i32, i32, i32, vp, i64, ctypes.POINTER(i64)]
     L.vfmm_route_counts.argtypes = [i32, i32, i64, vp, ctypes.c_float, ctypes.c_float, vp]
+    L.vfmm_step.argtypes = [vp, i64, vp, vp, ctypes.c_float, ctypes.c_float, vp, vp,
+                            ctypes.POINTER(ctypes.c_float), vp]
+    L.vfmm_step.restype = ctypes.c_int
     for f in ("vfmm_nccl_get_unique_id", "vfmm_create_nccl", "vfmm_partition",
               "vfmm_evaluate_logical", "vfmm_dist_plan", "vfmm_route_counts"):
         getattr(L, f).restype = ctypes.c_int
@@ -229,6 +232,30 @@ class Evaluator:
         vel = torch.empty_like(pos)
         dg = torch.empty_like(pos)
         return self.evaluate_into(pos, gamma, vel, dg, stream)
+
+    def step(self, pos, gamma, dt: float, nu: float = 0.0, vel=None, dgamma=None, stream=None):
+        """One forward-Euler step of the vortex method (C ABI vfmm_step, PAPER.md:67, :91,
+        :100, :107, :114): pos and gamma ((3, N) float32 CUDA tensors) are updated in place,
+        the core radius sigma grows by core spreading (sigma^2 += 2 nu dt).  Returns the
+        (vel, dgamma) evaluated at the start of the step."""
+        import torch
+
+        for t in (pos, gamma):
+            if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()
+                    and t.dim() == 2 and t.shape[0] == 3):
+                raise ValueError("expected contiguous float32 CUDA tensors of shape (3, N)")
+        vel = torch.empty_like(pos) if vel is None else vel
+        dgamma = torch.empty_like(pos) if dgamma is None else dgamma
+        if stream is None:
+            stream = torch.cuda.current_stream(pos.device)
+        sig = ctypes.c_float()
+        _check(self._L, self._ctx, self._L.vfmm_step(
+            self._ctx, pos.shape[1], pos.data_ptr(), gamma.data_ptr(), float(dt), float(nu),
+            vel.data_ptr(), dgamma.data_ptr(), ctypes.byref(sig),
+            ctypes.c_void_p(stream.cuda_stream)))
+        self.params.sigma = sig.value
+        self._n = pos.shape[1]
+        return vel, dgamma
 
     def evaluate_host(self, pos, gamma):
         """Host (numpy) in/out: H2D copy, evaluate, D2H copy inside the library."""

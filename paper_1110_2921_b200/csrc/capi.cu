@@ -59,6 +59,8 @@ struct vfmm_ctx {
     // host-API staging
     int64_t cap_host_n = 0;
     float* hbuf = nullptr;  // 12 x n
+    int64_t cap_step_n = 0;
+    float* step_buf = nullptr;  // vfmm_step: u and dgamma/dt when the caller passes no buffers
     cudaStream_t own_stream = nullptr;
     // last evaluate
     cudaStream_t last_stream = nullptr;
@@ -851,6 +853,38 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
     return VFMM_OK;
 }
 
+vfmm_status vfmm_step(vfmm_ctx* c, int64_t n, float* pos, float* gamma, float dt, float nu,
+                      float* vel, float* dgamma, float* sigma_out, void* stream) {
+    if (!c || !std::isfinite(dt) || !std::isfinite(nu) || !(nu >= 0.f)) return VFMM_EINVAL;
+    if (n < 0 || (n == 0 && !c->dist) || (n > 0 && (!pos || !gamma))) return VFMM_EINVAL;
+    const double s2 = (double)c->prm.sigma * (double)c->prm.sigma + 2.0 * (double)nu * (double)dt;
+    if (!(s2 > 0.0) || !std::isfinite((float)std::sqrt(s2))) return VFMM_EINVAL;
+    CK(cudaSetDevice(c->device), "set device");
+    float* v = vel;
+    float* s = dgamma;
+    if (n > 0 && (!v || !s)) {
+        if (n > c->cap_step_n) {
+            dfree(c->step_buf);
+            c->cap_step_n = 0;
+            CK(cudaMalloc((void**)&c->step_buf, 6 * n * sizeof(float)), "alloc step buffers");
+            c->cap_step_n = n;
+        }
+        if (!v) v = c->step_buf;
+        if (!s) s = c->step_buf + 3 * n;
+    }
+    vfmm_status st = vfmm_evaluate(c, n, pos, gamma, v, s, stream);
+    if (st != VFMM_OK) return st;
+    if (n > 0) {
+        launch_euler_update(pos, gamma, v, s, n, dt, c->prm.box_lo, c->prm.box_len,
+                            c->prm.image_levels > 0, (cudaStream_t)stream);
+        CK(cudaGetLastError(), "euler update kernel");
+        c->stats.n_kernel_launches += 1;
+    }
+    c->prm.sigma = (float)std::sqrt(s2);  // core spreading, uniform core (Eq. 9)
+    if (sigma_out) *sigma_out = c->prm.sigma;
+    return VFMM_OK;
+}
+
 vfmm_status vfmm_evaluate_host(vfmm_ctx* c, int64_t n, const float* pos_h, const float* gamma_h,
                                float* vel_h, float* dgamma_h) {
     if (!c || n < 1 || !pos_h || !gamma_h || !vel_h || !dgamma_h) return VFMM_EINVAL;
@@ -1027,6 +1061,7 @@ void vfmm_destroy(vfmm_ctx* c) {
     dfree(c->d_err);
     dfree(c->d_pairs);
     dfree(c->hbuf);
+    dfree(c->step_buf);
     for (int i = 0; i < vfmm_ctx::NEV; ++i)
         if (c->ev[i]) cudaEventDestroy(c->ev[i]);
     for (int i = 0; i < vfmm_ctx::NCE; ++i)

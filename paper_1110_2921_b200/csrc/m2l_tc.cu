@@ -26,9 +26,11 @@
 //
 // Accuracy: the tensor core accumulates with truncation, so a TMEM chain over all
 // 189 offsets x 16 K-steps x 3 products (~9000 accumulations) drifts by ~1e-4.  The chain is
-// therefore cut after every group (<= 3 offsets x 4 K-steps x K chunks x 3 products): the MMA
+// therefore cut after every (offset, K chunk) -- 4 K-steps x 3 products = 12 MMAs: the MMA
 // warp alternates between two TMEM buffers and the epilogue warps add each finished buffer
-// into FP32 registers (round-to-nearest), so the result keeps ~FP32 accuracy.
+// into FP32 registers (round-to-nearest, packed f32x2 adds), so the result keeps ~FP32
+// accuracy (scripts/m2l_precision.py models the truncation: 3x less error than per-group
+// chains of up to 72 MMAs).
 //
 // Warp roles (320 threads): warp 0 = TMA producer, warp 1 = TMEM alloc + MMA issuer,
 // warps 2-9 = epilogue (TMEM -> FP32 register sums -> L in Morton order).
@@ -332,15 +334,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         const uint64_t slab_step = (uint64_t)((P.N * 128) >> 4);  // descriptor units (16 B)
         int sa = 0, sb = 0;
         uint32_t pa = 0, pb = 0;
-        int grp = 0;
+        int chain = 0;  // one TMEM accumulation chain per (offset, K chunk): 4 K-steps x 3 products
         for (int gi = 0; gi < 72; ++gi) {
             const int mask = P.groups[pi * 72 + gi].x & 7;
             if (!mask) continue;
-            const int buf = grp & 1;
-            mbar_wait(&acc_empty[buf], ((grp >> 1) & 1) ^ 1);  // epilogue drained this buffer
-            tc_fence_after();
-            const uint32_t d = tmem + (uint32_t)(buf * 256);
-            bool first = true;
             for (int kc = 0; kc < tc_nkc<F16>(); ++kc) {
                 mbar_wait(&b_full[sb], pb);
                 tc_fence_after();
@@ -349,8 +346,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
                 for (int dd = 0; dd < 3; ++dd) {
                     if (!((mask >> dd) & 1)) continue;
+                    const int buf = chain & 1;
+                    mbar_wait(&acc_empty[buf], ((chain >> 1) & 1) ^ 1);  // epilogue drained it
                     mbar_wait(&a_full[sa], pa);
                     tc_fence_after();
+                    const uint32_t d = tmem + (uint32_t)(buf * 256);
                     const uint64_t ahi = sw128_desc(Abuf + (sa * 2 + 0) * A_BYTES);
                     const uint64_t alo = sw128_desc(Abuf + (sa * 2 + 1) * A_BYTES);
                     const uint64_t bsh = (uint64_t)dd * slab_step;
@@ -358,7 +358,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
                         for (int ks = 0; ks < 4; ++ks) {  // K = 8 tf32 / 16 f16 = 32 B per MMA
                             const uint64_t adv = (uint64_t)(ks * 2);
-                            const uint32_t acc = (first && ks == 0) ? 0u : 1u;
+                            const uint32_t acc = ks == 0 ? 0u : 1u;
                             if (F16) {
                                 mma_f16(d, ahi + adv, bhi + bsh + adv, idesc, acc);
                                 mma_f16(d, ahi + adv, blo + bsh + adv, idesc, 1u);
@@ -370,9 +370,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
                             }
                         }
                         mma_commit_mc(&a_empty[sa], (uint16_t)3);  // release in both CTAs
+                        mma_commit(&acc_full[buf]);
                     }
                     __syncwarp();
-                    first = false;
+                    ++chain;
                     if (++sa == TC_AST) {
                         sa = 0;
                         pa ^= 1;
@@ -385,9 +386,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
                     pb ^= 1;
                 }
             }
-            if (lane == 0) mma_commit(&acc_full[buf]);
-            __syncwarp();
-            ++grp;
         }
     } else {
         // ===================== epilogue: TMEM groups -> FP32 register sums -> L =====================
@@ -397,37 +395,48 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         const int ncol = (P.T / 2) * P.N;  // <= 96 columns per warp
         const int col0 = half * ncol;
         const int r = quarter * 32 + lane;
-        float acc[96];
+        // each finished chain (one offset x one K chunk, <= 12 MMAs: truncating TMEM
+        // accumulation) is added into FP32 registers with round-to-nearest, packed two at a time
+        unsigned long long acc2[48];
 #pragma unroll
-        for (int j = 0; j < 96; ++j) acc[j] = 0.f;
-        int ngroups = 0;
-        for (int gi = 0; gi < 72; ++gi) ngroups += (P.groups[pi * 72 + gi].x & 7) != 0;
-        for (int grp = 0; grp < ngroups; ++grp) {
-            const int buf = grp & 1;
-            mbar_wait(&acc_full[buf], (grp >> 1) & 1);
+        for (int j = 0; j < 48; ++j) acc2[j] = 0ull;
+        int nchains = 0;
+        for (int gi = 0; gi < 72; ++gi) nchains += __popc(P.groups[pi * 72 + gi].x & 7);
+        nchains *= tc_nkc<F16>();
+        for (int ch = 0; ch < nchains; ++ch) {
+            const int buf = ch & 1;
+            mbar_wait(&acc_full[buf], (ch >> 1) & 1);
             tc_fence_after();
 #pragma unroll
             for (int c = 0; c < 6; ++c) {
                 if (c * 16 < ncol) {
-                    uint32_t v[16];
+                    unsigned long long v[8];
                     const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) +
                                            (uint32_t)(buf * 256 + col0 + c * 16);
+                    uint32_t w[16];
                     asm volatile(
                         "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, "
                         "%8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
-                        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
-                          "=r"(v[6]), "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]),
-                          "=r"(v[12]), "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+                        : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]),
+                          "=r"(w[6]), "=r"(w[7]), "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]),
+                          "=r"(w[12]), "=r"(w[13]), "=r"(w[14]), "=r"(w[15])
                         : "r"(taddr));
                     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) acc[c * 16 + j] += __uint_as_float(v[j]);
+                    for (int j = 0; j < 8; ++j) {
+                        asm("mov.b64 %0, {%1, %2};" : "=l"(v[j]) : "r"(w[2 * j]), "r"(w[2 * j + 1]));
+                        asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc2[c * 8 + j]) : "l"(acc2[c * 8 + j]), "l"(v[j]));
+                    }
                 }
             }
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[buf]);
         }
+        float acc[96];
+#pragma unroll
+        for (int j = 0; j < 48; ++j)
+            asm("mov.b64 {%0, %1}, %2;" : "=f"(acc[2 * j]), "=f"(acc[2 * j + 1]) : "l"(acc2[j]));
         if (r < P.nc) {
             if (F16) {  // undo the balancing: row r times rs[r] / s
                 const float f = P.rs[r] * ldexpf(1.f, -h16_scale_exp(*P.maxbits));

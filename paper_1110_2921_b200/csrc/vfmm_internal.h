@@ -168,6 +168,9 @@ KernelConsts make_kernel_consts(float sigma);
 void launch_p2p(const float* sorted6, int64_t n, const int* leaf_start, int depth, float a,
                 int periodic, int scheme, KernelConsts kc, float* near6,
                 unsigned long long* npairs, int64_t plo, int64_t pcnt, cudaStream_t st);
+// step.cu: x += u dt (wrapped into the box when periodic), gamma += dgamma dt
+void launch_euler_update(float* pos, float* gamma, const float* vel, const float* dgamma,
+                         int64_t n, float dt, float lo, float len, int periodic, cudaStream_t st);
 void launch_direct(const float* pos, const float* gamma, int64_t n, float len, int image_levels,
                    int scheme, KernelConsts kc, float* vel, float* dgam, cudaStream_t st);
 

@@ -470,14 +470,38 @@ def test_bench_config_vs_golden_o1_27cubed(cfg):
 
 # ------------------------------------------------------------------ tensor-core M2L (tcgen05)
 
+@pytest.mark.parametrize("engine", ["simt", "f16", "tf32"])
+@pytest.mark.parametrize("n,depth,p,lam", [(32, 3, 10, 1), (32, 3, 6, 3), (64, 4, 8, 1)])
+def test_m2l_engines_vs_fp64_fmm_oracle(n, depth, p, lam, engine, monkeypatch):
+    """Every M2L engine -- SIMT FP32, tcgen05 scaled 3xFP16 (default), tcgen05 3xTF32 -- against
+    the float64 step-by-step FMM oracle running the same algorithm: the local expansions of
+    every level and the velocity / stretching differ by FP32 rounding only.  The tensor core
+    accumulates with truncation; chains are cut after every (offset, K chunk) and summed in
+    FP32 registers (DESIGN.md "tcgen05 M2L accuracy")."""
+    f = synthgen.isotropic(n, seed=21)
+    monkeypatch.setenv("VFMM_M2L", engine)
+    v, s, ev = run(f, p=p, depth=depth, image_levels=lam)
+    vo, so, st = F.evaluate(f.pos, f.gamma, f.sigma, f.box_lo, f.box_len, depth, p, lam,
+                            return_stages=True)
+    line = [f"{engine} n={n} L={depth} p={p} lam={lam}: u {rel(v, vo):.2e} sdot {rel(s, so):.2e}"]
+    for l in range(1, depth + 1):
+        al = f.box_len / (1 << l)
+        got = ev.debug_expansions(1, l)[..., 1:]
+        want = _pack(st["L"][l], p, al ** (np.arange(p + 1.0) + 1))[..., 1:]
+        line.append(f"L{l} {rel(got, want):.2e}")
+        assert rel(got, want) < 5e-6, (l, rel(got, want))
+    print(" ".join(line))
+    assert rel(v, vo) < 3e-6 and rel(s, so) < 3e-6, (rel(v, vo), rel(s, so))
+    ev.close()
+
+
 @pytest.mark.parametrize("engine", ["tf32", "f16"])
 @pytest.mark.parametrize("n,depth,p,lam", [(64, 5, 10, 3), (48, 5, 6, 0), (128, 6, 8, 1)])
 def test_m2l_tensor_core_matches_simt(n, depth, p, lam, engine, monkeypatch):
-    """Levels >= 2 run M2L on tcgen05 (3xTF32, or the balanced 3xFP16 split); the SIMT FP32
-    gather-GEMM (validated against the fp64 FMM oracle above) computes the same translations.
-    The tensor core accumulates with truncation (round toward zero), so even with the TMEM chain
-    cut after every offset the two differ by ~1e-5 (DESIGN.md "tcgen05 M2L accuracy"), not FP32
-    round-off."""
+    """Deeper trees than the fp64 oracle reaches: levels >= 2 on tcgen05 (3xTF32, or the
+    balanced 3xFP16 split) against the SIMT FP32 gather-GEMM (itself validated against the fp64
+    FMM oracle above) on the far field: velocity and stretching within 5e-6; the finest local
+    expansions, where both engines' FP32 rounding shows, within 1e-5."""
     f = synthgen.isotropic(n, seed=21)
     monkeypatch.setenv("VFMM_M2L", engine)
     v1, s1, ev1 = run(f, p=p, depth=depth, image_levels=lam, mode=vf.MODE_FAR_ONLY)
@@ -487,8 +511,8 @@ def test_m2l_tensor_core_matches_simt(n, depth, p, lam, engine, monkeypatch):
         a, b = ev1.debug_expansions(1, l), ev2.debug_expansions(1, l)
         print(f"tc {engine} vs simt n={n} L={depth} p={p} lam={lam}: level {l} "
               f"{rel(a[..., 1:], b[..., 1:]):.2e}")
-        assert rel(a[..., 1:], b[..., 1:]) < 3e-5, (l, rel(a[..., 1:], b[..., 1:]))
+        assert rel(a[..., 1:], b[..., 1:]) < 1e-5, (l, rel(a[..., 1:], b[..., 1:]))
     print(f"tc {engine} vs simt n={n}: u {rel(v1, v2):.2e} sdot {rel(s1, s2):.2e}")
-    assert rel(v1, v2) < 3e-5 and rel(s1, s2) < 5e-5, (rel(v1, v2), rel(s1, s2))
+    assert rel(v1, v2) < 5e-6 and rel(s1, s2) < 5e-6, (rel(v1, v2), rel(s1, s2))
     ev1.close()
     ev2.close()

@@ -459,3 +459,54 @@ def test_fmm_oracle_supercell_rings_vs_direct_sum_at_27_cubed():
     # the same FMM at lambda = 2 is far from the lambda = 3 sum (the ring is what matters)
     vf2, _ = F.evaluate(f.pos, f.gamma, f.sigma, f.box_lo, f.box_len, 1, 12, 2)
     assert np.linalg.norm(vf2 - v3) / np.linalg.norm(v3) > 1e-3
+
+
+# ---------------------------------------------------------------- time stepping (NEXT-1)
+
+def test_euler_step_taylor_green_closed_form():
+    """One forward-Euler step (PAPER.md:91 Eq. 7, :100 Eq. 8, :107 Eq. 9, :114) of the lattice
+    Taylor-Green field: the displacement is dt e^{-3 s^2/2} u_TG(x_i) and the strength change
+    dt h^3 e^{-3 s^2/2} (w.grad)u_TG (the closed forms of test_taylor_green_closed_form_image_sum,
+    SURVEY App. B), the core grows as sigma^2 + 2 nu dt."""
+    from oracle.euler import euler_step
+
+    f = synthgen.make("c1")
+    dt, nu = 0.05, 0.01
+    x1, g1, s1, u, dg = euler_step(f.pos, f.gamma, f.sigma, nu, dt, f.box_lo, f.box_len, 2)
+    x, y, z = (f.pos[i].astype(np.float64) for i in range(3))
+    damp = math.exp(-1.5 * f.sigma ** 2)
+    h = f.box_len / f.n
+    u_tg = np.stack([np.sin(x) * np.cos(y) * np.cos(z), -np.cos(x) * np.sin(y) * np.cos(z),
+                     0 * x]) * damp
+    s_tg = np.stack([-0.25 * np.sin(2 * y) * np.sin(2 * z), 0.25 * np.sin(2 * x) * np.sin(2 * z),
+                     0 * x]) * damp * h ** 3
+    disp = x1 - f.pos.astype(np.float64)
+    disp -= f.box_len * np.round(disp / f.box_len)  # undo the wrap
+    # lambda = 2 instead of 3: the outer shell changes the sum by ~2e-5 relative (SURVEY 8c)
+    assert np.abs(disp - dt * u_tg).max() < 5e-5 * dt * np.abs(u_tg).max()
+    assert np.abs((g1 - f.gamma) - dt * s_tg).max() < 5e-5 * dt * np.abs(s_tg).max()
+    assert s1 == pytest.approx(math.sqrt(f.sigma ** 2 + 2 * nu * dt), rel=1e-15)
+    assert np.all(x1 >= f.box_lo) and np.all(x1 < f.box_lo + f.box_len)
+
+
+def test_euler_step_lone_particle_and_zero_dt():
+    """A lone particle in the periodic box is at rest with constant strength (its images
+    cancel); dt = 0 is the identity; free space: no wrap."""
+    from oracle.euler import euler_step
+
+    pos = np.array([[0.7], [-1.1], [2.0]])
+    gam = np.array([[0.4], [0.9], [-0.3]])
+    x1, g1, s1, _, _ = euler_step(pos, gam, 0.3, 0.02, 0.1, -math.pi, 2 * math.pi, 2)
+    assert np.abs(x1 - pos).max() < 1e-14 and np.abs(g1 - gam).max() < 1e-14
+    assert s1 == pytest.approx(math.sqrt(0.09 + 0.004))
+    rng = np.random.default_rng(3)
+    p = rng.uniform(-3, 3, (3, 20))
+    g = rng.normal(size=(3, 20))
+    x1, g1, s1, _, _ = euler_step(p, g, 0.4, 0.0, 0.0, -math.pi, 2 * math.pi, 1)
+    assert np.abs(x1 - p).max() < 1e-15 and np.array_equal(g1, g) and s1 == 0.4
+    # free space, two particles: the step moves each by dt u (antisymmetric pair, Eq. 7)
+    p2 = np.array([[0.3, -0.4], [0.1, 0.5], [-0.2, 0.25]])
+    g2 = np.array([[0.2, 0.2], [-0.1, -0.1], [0.7, 0.7]])
+    x1, _, _, u, _ = euler_step(p2, g2, 0.3, 0.0, 0.2, -math.pi, 2 * math.pi, 0)
+    assert np.allclose(x1 - p2, 0.2 * u, rtol=0, atol=1e-15)
+    assert np.allclose(u[:, 0], -u[:, 1], rtol=1e-12)
