@@ -121,6 +121,17 @@ vfmm_status vfmm_create(vfmm_ctx** ctx, const vfmm_params* prm, int device);
 vfmm_status vfmm_evaluate(vfmm_ctx* ctx, int64_t n, const float* pos, const float* gamma,
                           float* vel, float* dgamma, void* cuda_stream);
 
+/* Velocity at target points that are not particles (NEXT-3: e.g. the velocity on an n^3
+   lattice for the energy spectrum): u(t_k) = sum_n sum_j gamma_j x grad(G
+   g_sigma)(t_k - x_j - n len) (Eq. 5) from n_src particles (pos, gamma: device,
+   3 x n_src) at n_tgt targets (tpos: device, 3 x n_tgt, inside the box) -> tvel (device,
+   3 x n_tgt).  The targets join the tree as zero-strength particles (they contribute nothing as
+   sources) and take the same near / far path as the particles; the particles' own velocities
+   are not returned.  Asynchronous on `cuda_stream`.  Distributed contexts: collective, each rank
+   passes its own sources and targets. */
+vfmm_status vfmm_evaluate_at(vfmm_ctx* ctx, int64_t n_src, const float* pos, const float* gamma,
+                             int64_t n_tgt, const float* tpos, float* tvel, void* cuda_stream);
+
 /* One forward-Euler time step of the vortex particle method (section 2; forward
    Euler), the three updates simultaneous:
      x_i     += u_i dt          convection, Eq. (7) PAPER.md:91 (wrapped into the box when

@@ -62,7 +62,7 @@ EXPORTS = ["vfmm_abi_version", "vfmm_params_default", "vfmm_create", "vfmm_evalu
            "vfmm_debug_tree", "vfmm_debug_expansions", "vfmm_strerror",
            "vfmm_last_error_message", "vfmm_destroy", "vfmm_nccl_get_unique_id",
            "vfmm_create_nccl", "vfmm_partition", "vfmm_evaluate_logical", "vfmm_dist_plan",
-           "vfmm_route_counts", "vfmm_step"]
+           "vfmm_route_counts", "vfmm_step", "vfmm_evaluate_at"]
 
 
 def load_library(path: str = LIB_PATH):
@@ -99,6 +99,8 @@ def load_library(path: str = LIB_PATH):
     L.vfmm_step.argtypes = [vp, i64, vp, vp, ctypes.c_float, ctypes.c_float, vp, vp,
                             ctypes.POINTER(ctypes.c_float), vp]
     L.vfmm_step.restype = ctypes.c_int
+    L.vfmm_evaluate_at.argtypes = [vp, i64, vp, vp, i64, vp, vp, vp]
+    L.vfmm_evaluate_at.restype = ctypes.c_int
     for f in ("vfmm_nccl_get_unique_id", "vfmm_create_nccl", "vfmm_partition",
               "vfmm_evaluate_logical", "vfmm_dist_plan", "vfmm_route_counts"):
         getattr(L, f).restype = ctypes.c_int
@@ -232,6 +234,24 @@ class Evaluator:
         vel = torch.empty_like(pos)
         dg = torch.empty_like(pos)
         return self.evaluate_into(pos, gamma, vel, dg, stream)
+
+    def evaluate_at(self, pos, gamma, tpos, stream=None):
+        """Velocity at target points tpos ((3, T) float32 CUDA tensor) induced by the particles
+        (pos, gamma) -- C ABI vfmm_evaluate_at (targets enter the tree with zero strength)."""
+        import torch
+
+        for t in (pos, gamma, tpos):
+            if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()
+                    and t.dim() == 2 and t.shape[0] == 3):
+                raise ValueError("expected contiguous float32 CUDA tensors of shape (3, N)")
+        tvel = torch.empty_like(tpos)
+        if stream is None:
+            stream = torch.cuda.current_stream(pos.device)
+        _check(self._L, self._ctx, self._L.vfmm_evaluate_at(
+            self._ctx, pos.shape[1], pos.data_ptr(), gamma.data_ptr(), tpos.shape[1],
+            tpos.data_ptr(), tvel.data_ptr(), ctypes.c_void_p(stream.cuda_stream)))
+        self._n = pos.shape[1] + tpos.shape[1]
+        return tvel
 
     def step(self, pos, gamma, dt: float, nu: float = 0.0, vel=None, dgamma=None, stream=None):
         """One forward-Euler step of the vortex method (C ABI vfmm_step, PAPER.md:67, :91,

@@ -59,6 +59,8 @@ struct vfmm_ctx {
     // host-API staging
     int64_t cap_host_n = 0;
     float* hbuf = nullptr;  // 12 x n
+    int64_t cap_at_n = 0;
+    float* at_buf = nullptr;    // vfmm_evaluate_at: sources + targets, 12 x (n_src + n_tgt)
     int64_t cap_step_n = 0;
     float* step_buf = nullptr;  // vfmm_step: u and dgamma/dt when the caller passes no buffers
     cudaStream_t own_stream = nullptr;
@@ -853,6 +855,48 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
     return VFMM_OK;
 }
 
+vfmm_status vfmm_evaluate_at(vfmm_ctx* c, int64_t n_src, const float* pos, const float* gamma,
+                             int64_t n_tgt, const float* tpos, float* tvel, void* stream) {
+    if (!c || n_src < 0 || n_tgt < 0 || (n_src > 0 && (!pos || !gamma)) ||
+        (n_tgt > 0 && (!tpos || !tvel)))
+        return VFMM_EINVAL;
+    const int64_t N = n_src + n_tgt;
+    if (N == 0 && !c->dist) return VFMM_EINVAL;
+    if (N > ((int64_t)1 << 31) - 1) return VFMM_EINVAL;
+    CK(cudaSetDevice(c->device), "set device");
+    cudaStream_t st = (cudaStream_t)stream;
+    if (c->last_stream != st && c->have_last)  // at_buf may still be read by the last evaluate
+        CK(cudaStreamWaitEvent(st, c->ev[vfmm_ctx::NEV - 1], 0), "order after last evaluate");
+    if (N > c->cap_at_n) {
+        if (c->last_stream) CK(cudaStreamSynchronize(c->last_stream), "sync");
+        dfree(c->at_buf);
+        c->cap_at_n = 0;
+        CK(cudaMalloc((void**)&c->at_buf, 12 * std::max<int64_t>(N, 1) * sizeof(float)),
+           "alloc target buffers");
+        c->cap_at_n = N;
+    }
+    float* P = c->at_buf;        // positions: sources then targets, per component
+    float* G = P + 3 * N;        // strengths: targets carry zero strength
+    float* V = G + 3 * N;
+    float* S = V + 3 * N;
+    for (int a = 0; a < 3; ++a) {
+        if (n_src) {
+            CK(cudaMemcpyAsync(P + a * N, pos + a * n_src, n_src * 4, cudaMemcpyDeviceToDevice, st), "copy");
+            CK(cudaMemcpyAsync(G + a * N, gamma + a * n_src, n_src * 4, cudaMemcpyDeviceToDevice, st), "copy");
+        }
+        if (n_tgt) {
+            CK(cudaMemcpyAsync(P + a * N + n_src, tpos + a * n_tgt, n_tgt * 4, cudaMemcpyDeviceToDevice, st), "copy");
+            CK(cudaMemsetAsync(G + a * N + n_src, 0, n_tgt * 4, st), "zero");
+        }
+    }
+    vfmm_status s = vfmm_evaluate(c, N, P, G, V, S, stream);
+    if (s != VFMM_OK) return s;
+    for (int a = 0; a < 3 && n_tgt; ++a)
+        CK(cudaMemcpyAsync(tvel + a * n_tgt, V + a * N + n_src, n_tgt * 4, cudaMemcpyDeviceToDevice, st),
+           "copy");
+    return VFMM_OK;
+}
+
 vfmm_status vfmm_step(vfmm_ctx* c, int64_t n, float* pos, float* gamma, float dt, float nu,
                       float* vel, float* dgamma, float* sigma_out, void* stream) {
     if (!c || !std::isfinite(dt) || !std::isfinite(nu) || !(nu >= 0.f)) return VFMM_EINVAL;
@@ -865,6 +909,7 @@ vfmm_status vfmm_step(vfmm_ctx* c, int64_t n, float* pos, float* gamma, float dt
     if (n > 0 && (!v || !s)) {
         if (n > c->cap_step_n) {
             dfree(c->step_buf);
+    dfree(c->at_buf);
             c->cap_step_n = 0;
             CK(cudaMalloc((void**)&c->step_buf, 6 * n * sizeof(float)), "alloc step buffers");
             c->cap_step_n = n;

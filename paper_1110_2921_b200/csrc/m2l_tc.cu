@@ -407,25 +407,40 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
             const int buf = ch & 1;
             mbar_wait(&acc_full[buf], (ch >> 1) & 1);
             tc_fence_after();
+            // two halves of 48 columns: three 16-column loads in flight, one wait each
 #pragma unroll
-            for (int c = 0; c < 6; ++c) {
-                if (c * 16 < ncol) {
-                    unsigned long long v[8];
-                    const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) +
-                                           (uint32_t)(buf * 256 + col0 + c * 16);
-                    uint32_t w[16];
-                    asm volatile(
-                        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, "
-                        "%8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
-                        : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]),
-                          "=r"(w[6]), "=r"(w[7]), "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]),
-                          "=r"(w[12]), "=r"(w[13]), "=r"(w[14]), "=r"(w[15])
-                        : "r"(taddr));
-                    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+            for (int hh = 0; hh < 2; ++hh) {
+                uint32_t w[48];
 #pragma unroll
-                    for (int j = 0; j < 8; ++j) {
-                        asm("mov.b64 %0, {%1, %2};" : "=l"(v[j]) : "r"(w[2 * j]), "r"(w[2 * j + 1]));
-                        asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc2[c * 8 + j]) : "l"(acc2[c * 8 + j]), "l"(v[j]));
+                for (int c = 0; c < 3; ++c) {
+                    const int col = (hh * 3 + c) * 16;
+                    if (col < ncol) {
+                        const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) +
+                                               (uint32_t)(buf * 256 + col0 + col);
+                        asm volatile(
+                            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, "
+                            "%7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
+                            : "=r"(w[c * 16 + 0]), "=r"(w[c * 16 + 1]), "=r"(w[c * 16 + 2]),
+                              "=r"(w[c * 16 + 3]), "=r"(w[c * 16 + 4]), "=r"(w[c * 16 + 5]),
+                              "=r"(w[c * 16 + 6]), "=r"(w[c * 16 + 7]), "=r"(w[c * 16 + 8]),
+                              "=r"(w[c * 16 + 9]), "=r"(w[c * 16 + 10]), "=r"(w[c * 16 + 11]),
+                              "=r"(w[c * 16 + 12]), "=r"(w[c * 16 + 13]), "=r"(w[c * 16 + 14]),
+                              "=r"(w[c * 16 + 15])
+                            : "r"(taddr));
+                    }
+                }
+                asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+                for (int c = 0; c < 3; ++c) {
+                    if ((hh * 3 + c) * 16 < ncol) {
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            unsigned long long v;
+                            asm("mov.b64 %0, {%1, %2};" : "=l"(v) : "r"(w[c * 16 + 2 * j]),
+                                "r"(w[c * 16 + 2 * j + 1]));
+                            const int a = (hh * 3 + c) * 8 + j;
+                            asm("add.rn.f32x2 %0, %1, %2;" : "=l"(acc2[a]) : "l"(acc2[a]), "l"(v));
+                        }
                     }
                 }
             }
