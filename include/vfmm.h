@@ -147,6 +147,34 @@ vfmm_status vfmm_evaluate_at(vfmm_ctx* ctx, int64_t n_src, const float* pos, con
 vfmm_status vfmm_step(vfmm_ctx* ctx, int64_t n, float* pos, float* gamma, float dt, float nu,
                       float* vel, float* dgamma, float* sigma_out, void* cuda_stream);
 
+/* ---- NEXT-2: reinitialization by RBF interpolation ----
+   Moves the vorticity of n_old particles (pos_old, gamma_old: device 3 x n_old, core radius
+   sigma_old, typically grown by core spreading) onto n_new new particles (pos_new: device
+   3 x n_new, usually the cell-centre lattice) of core radius sigma_new (= h):
+     omega_i = sum_j gamma_j zeta_sigma_old(x_i - x_j)                  Eq. (3) at the new points
+     solve     sum_j gamma'_j zeta_sigma_new(x_i - x_j) = omega_i  for gamma'
+   by GMRES(restart) in matrix-free form, the Gaussian sums over neighbour leaves only
+   (reading R18: neighbour radius ws with ws a >= 6 sigma, truncation < 1.5e-8),
+   initial guess gamma' = omega dx^3 with dx^3 = box_len^3 / n_new, exit when the residual has
+   dropped by `tol` relative to that guess's residual, per strength component,
+   or after max_iter iterations.  Outputs (device, 3 x n_new, input order of pos_new):
+   gamma_new (required), omega_new (may be NULL).  Uses the context's box, image_levels (> 0:
+   periodic neighbours) and depth (0 = auto for n_new); sets the context's sigma to sigma_new.
+   Synchronous (the GMRES recurrences run on the host); all vector work on `cuda_stream`. */
+typedef struct {
+    int32_t iterations;      /* GMRES iterations (matrix-vector products after the residual) */
+    int32_t converged;       /* 1 if every component reached tol                            */
+    double rel_residual[3];  /* final ||omega - A gamma'|| / ||omega - A gamma'_0|| per comp.  */
+    double ms;               /* device time of the whole reinitialization                    */
+    int32_t depth_used, ws_old, ws_new;
+} vfmm_reinit_info;
+
+vfmm_status vfmm_reinit(vfmm_ctx* ctx, int64_t n_old, const float* pos_old,
+                        const float* gamma_old, float sigma_old, int64_t n_new,
+                        const float* pos_new, float sigma_new, float tol, int32_t max_iter,
+                        int32_t restart, float* gamma_new, float* omega_new,
+                        vfmm_reinit_info* info, void* cuda_stream);
+
 /* ---- multi-GPU: Morton-range spatial decomposition + local-essential-tree exchange ----
    (the paper's multi-GPU runs.)  Rank r of R
    (R in {1, 2, 4, 8}) owns the Morton leaf range [r 8^L/R, (r+1) 8^L/R) at depth L

@@ -62,7 +62,14 @@ EXPORTS = ["vfmm_abi_version", "vfmm_params_default", "vfmm_create", "vfmm_evalu
            "vfmm_debug_tree", "vfmm_debug_expansions", "vfmm_strerror",
            "vfmm_last_error_message", "vfmm_destroy", "vfmm_nccl_get_unique_id",
            "vfmm_create_nccl", "vfmm_partition", "vfmm_evaluate_logical", "vfmm_dist_plan",
-           "vfmm_route_counts", "vfmm_step", "vfmm_evaluate_at"]
+           "vfmm_route_counts", "vfmm_step", "vfmm_evaluate_at", "vfmm_reinit"]
+
+
+class c_reinit_info(ctypes.Structure):
+    _fields_ = [("iterations", ctypes.c_int32), ("converged", ctypes.c_int32),
+                ("rel_residual", ctypes.c_double * 3), ("ms", ctypes.c_double),
+                ("depth_used", ctypes.c_int32), ("ws_old", ctypes.c_int32),
+                ("ws_new", ctypes.c_int32)]
 
 
 def load_library(path: str = LIB_PATH):
@@ -101,6 +108,10 @@ def load_library(path: str = LIB_PATH):
     L.vfmm_step.restype = ctypes.c_int
     L.vfmm_evaluate_at.argtypes = [vp, i64, vp, vp, i64, vp, vp, vp]
     L.vfmm_evaluate_at.restype = ctypes.c_int
+    L.vfmm_reinit.argtypes = [vp, i64, vp, vp, ctypes.c_float, i64, vp, ctypes.c_float,
+                              ctypes.c_float, ctypes.c_int32, ctypes.c_int32, vp, vp,
+                              ctypes.POINTER(c_reinit_info), vp]
+    L.vfmm_reinit.restype = ctypes.c_int
     for f in ("vfmm_nccl_get_unique_id", "vfmm_create_nccl", "vfmm_partition",
               "vfmm_evaluate_logical", "vfmm_dist_plan", "vfmm_route_counts"):
         getattr(L, f).restype = ctypes.c_int
@@ -252,6 +263,31 @@ class Evaluator:
             tpos.data_ptr(), tvel.data_ptr(), ctypes.c_void_p(stream.cuda_stream)))
         self._n = pos.shape[1] + tpos.shape[1]
         return tvel
+
+    def reinit(self, pos_old, gamma_old, sigma_old: float, pos_new, sigma_new: float,
+               tol: float = 1e-5, max_iter: int = 50, restart: int = 30, stream=None):
+        """RBF reinitialization onto new particles (C ABI vfmm_reinit):
+        returns (gamma_new, omega_new, info dict); the context's sigma becomes sigma_new."""
+        import torch
+
+        for t in (pos_old, gamma_old, pos_new):
+            if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()
+                    and t.dim() == 2 and t.shape[0] == 3):
+                raise ValueError("expected contiguous float32 CUDA tensors of shape (3, N)")
+        g = torch.empty_like(pos_new)
+        om = torch.empty_like(pos_new)
+        info = c_reinit_info()
+        if stream is None:
+            stream = torch.cuda.current_stream(pos_new.device)
+        _check(self._L, self._ctx, self._L.vfmm_reinit(
+            self._ctx, pos_old.shape[1], pos_old.data_ptr(), gamma_old.data_ptr(),
+            float(sigma_old), pos_new.shape[1], pos_new.data_ptr(), float(sigma_new), float(tol),
+            int(max_iter), int(restart), g.data_ptr(), om.data_ptr(), ctypes.byref(info),
+            ctypes.c_void_p(stream.cuda_stream)))
+        self.params.sigma = float(sigma_new)
+        d = {k: getattr(info, k) for k, _ in c_reinit_info._fields_}
+        d["rel_residual"] = list(info.rel_residual)
+        return g, om, d
 
     def step(self, pos, gamma, dt: float, nu: float = 0.0, vel=None, dgamma=None, stream=None):
         """One forward-Euler step of the vortex method (C ABI vfmm_step, PAPER.md:67, :91,

@@ -19,6 +19,27 @@
 
 using namespace vfmm;
 
+// reinitialization workspace (vfmm_reinit): trees of the old and new particles, Krylov basis
+struct RbfWs {
+    int64_t cap_old = 0, cap_new = 0;
+    int cap_depth = -1, cap_m = -1;
+    uint32_t *ok[2] = {nullptr, nullptr}, *ov[2] = {nullptr, nullptr};
+    uint32_t *nk[2] = {nullptr, nullptr}, *nv[2] = {nullptr, nullptr};
+    void *otmp = nullptr, *ntmp = nullptr;
+    float *o6 = nullptr, *n6 = nullptr;
+    int *ols = nullptr, *nls = nullptr;
+    float *V = nullptr, *w = nullptr, *x = nullptr, *om = nullptr;
+    double *part = nullptr, *dots = nullptr, *coef = nullptr;
+    void release() {
+        for (void* p : {(void*)ok[0], (void*)ok[1], (void*)ov[0], (void*)ov[1], (void*)nk[0],
+                        (void*)nk[1], (void*)nv[0], (void*)nv[1], otmp, ntmp, (void*)o6, (void*)n6,
+                        (void*)ols, (void*)nls, (void*)V, (void*)w, (void*)x, (void*)om,
+                        (void*)part, (void*)dots, (void*)coef})
+            if (p) cudaFree(p);
+        *this = RbfWs();
+    }
+};
+
 struct vfmm_ctx {
     vfmm_params prm{};
     int device = 0;
@@ -59,6 +80,7 @@ struct vfmm_ctx {
     // host-API staging
     int64_t cap_host_n = 0;
     float* hbuf = nullptr;  // 12 x n
+    RbfWs rbf;
     int64_t cap_at_n = 0;
     float* at_buf = nullptr;    // vfmm_evaluate_at: sources + targets, 12 x (n_src + n_tgt)
     int64_t cap_step_n = 0;
@@ -870,6 +892,7 @@ vfmm_status vfmm_evaluate_at(vfmm_ctx* c, int64_t n_src, const float* pos, const
     if (N > c->cap_at_n) {
         if (c->last_stream) CK(cudaStreamSynchronize(c->last_stream), "sync");
         dfree(c->at_buf);
+    c->rbf.release();
         c->cap_at_n = 0;
         CK(cudaMalloc((void**)&c->at_buf, 12 * std::max<int64_t>(N, 1) * sizeof(float)),
            "alloc target buffers");
@@ -894,6 +917,268 @@ vfmm_status vfmm_evaluate_at(vfmm_ctx* c, int64_t n_src, const float* pos, const
     for (int a = 0; a < 3 && n_tgt; ++a)
         CK(cudaMemcpyAsync(tvel + a * n_tgt, V + a * N + n_src, n_tgt * 4, cudaMemcpyDeviceToDevice, st),
            "copy");
+    return VFMM_OK;
+}
+
+vfmm_status vfmm_reinit(vfmm_ctx* c, int64_t n_old, const float* pos_old,
+                        const float* gamma_old, float sigma_old, int64_t n_new,
+                        const float* pos_new, float sigma_new, float tol, int32_t max_iter,
+                        int32_t restart, float* gamma_new, float* omega_new,
+                        vfmm_reinit_info* info, void* stream) {
+    if (!c || c->dist || n_old < 1 || n_new < 1 || !pos_old || !gamma_old || !pos_new ||
+        !gamma_new || !finite_pos(sigma_old) || !finite_pos(sigma_new) || !(tol > 0.f) ||
+        !std::isfinite(tol) || max_iter < 1 || restart < 1 || restart > 200)
+        return VFMM_EINVAL;
+    if (n_old > ((int64_t)1 << 31) - 1 || n_new > ((int64_t)1 << 31) - 1) return VFMM_EINVAL;
+    CK(cudaSetDevice(c->device), "set device");
+    (void)cudaGetLastError();
+    cudaStream_t st = (cudaStream_t)stream;
+    if (c->last_stream != st && c->have_last)
+        CK(cudaStreamWaitEvent(st, c->ev[vfmm_ctx::NEV - 1], 0), "order after last evaluate");
+    const vfmm_params& P = c->prm;
+    const int depth = P.depth > 0 ? P.depth : auto_depth(P, n_new);
+    const int64_t nleaf = (int64_t)1 << (3 * depth);
+    const float a = (float)((double)P.box_len / (double)(1 << depth));
+    const int periodic = P.image_levels > 0;
+    const int ws_old = rbf_ws(a, sigma_old), ws_new = rbf_ws(a, sigma_new);
+    // (a neighbour cube wider than the periodic box visits further images of the same leaves:
+    // each offset is a distinct image, so the truncated periodic sum stays exact)
+    const int m = restart;
+    RbfWs& W = c->rbf;
+    const int64_t n = n_new;
+    // ---- workspace ----
+    if (n_old > W.cap_old) {
+        for (int b = 0; b < 2; ++b) {
+            dfree(W.ok[b]);
+            dfree(W.ov[b]);
+        }
+        dfree(W.otmp);
+        dfree(W.o6);
+        W.cap_old = 0;
+        for (int b = 0; b < 2; ++b) {
+            CK(cudaMalloc((void**)&W.ok[b], n_old * 4), "alloc rbf");
+            CK(cudaMalloc((void**)&W.ov[b], n_old * 4), "alloc rbf");
+        }
+        CK(cudaMalloc(&W.otmp, radix_temp_bytes(n_old)), "alloc rbf");
+        CK(cudaMalloc((void**)&W.o6, 6 * n_old * sizeof(float)), "alloc rbf");
+        W.cap_old = n_old;
+    }
+    if (n_new > W.cap_new || m > W.cap_m) {
+        for (int b = 0; b < 2; ++b) {
+            dfree(W.nk[b]);
+            dfree(W.nv[b]);
+        }
+        dfree(W.ntmp);
+        dfree(W.n6);
+        dfree(W.V);
+        dfree(W.w);
+        dfree(W.x);
+        dfree(W.om);
+        dfree(W.part);
+        dfree(W.dots);
+        dfree(W.coef);
+        W.cap_new = 0;
+        W.cap_m = -1;
+        const int64_t nn = std::max(n_new, W.cap_new);
+        for (int b = 0; b < 2; ++b) {
+            CK(cudaMalloc((void**)&W.nk[b], nn * 4), "alloc rbf");
+            CK(cudaMalloc((void**)&W.nv[b], nn * 4), "alloc rbf");
+        }
+        CK(cudaMalloc(&W.ntmp, radix_temp_bytes(nn)), "alloc rbf");
+        CK(cudaMalloc((void**)&W.n6, 6 * nn * sizeof(float)), "alloc rbf");
+        CK(cudaMalloc((void**)&W.V, (size_t)(m + 1) * 3 * nn * sizeof(float)), "alloc Krylov basis");
+        CK(cudaMalloc((void**)&W.w, 3 * nn * sizeof(float)), "alloc rbf");
+        CK(cudaMalloc((void**)&W.x, 3 * nn * sizeof(float)), "alloc rbf");
+        CK(cudaMalloc((void**)&W.om, 3 * nn * sizeof(float)), "alloc rbf");
+        CK(cudaMalloc((void**)&W.part, rbf_dot_part_doubles(m + 1) * sizeof(double)), "alloc rbf");
+        CK(cudaMalloc((void**)&W.dots, 3 * (m + 1) * sizeof(double)), "alloc rbf");
+        CK(cudaMalloc((void**)&W.coef, 3 * (m + 1) * sizeof(double)), "alloc rbf");
+        W.cap_new = nn;
+        W.cap_m = m;
+    }
+    if (depth != W.cap_depth) {
+        dfree(W.ols);
+        dfree(W.nls);
+        W.cap_depth = -1;
+        CK(cudaMalloc((void**)&W.ols, (nleaf + 1) * 4), "alloc rbf");
+        CK(cudaMalloc((void**)&W.nls, (nleaf + 1) * 4), "alloc rbf");
+        W.cap_depth = depth;
+    }
+    CK(cudaEventRecord(c->ev[0], st), "event");
+    // ---- trees of the old and the new particles (same depth) ----
+    Geom g{P.box_lo, P.box_len, (double)P.box_lo, (double)P.box_len, depth, periodic};
+    int nl = 0;
+    uint32_t *oks = nullptr, *operm = nullptr, *nks = nullptr, *nperm = nullptr;
+    launch_keys(pos_old, n_old, g, W.ok[0], W.ov[0], c->d_err, st);
+    launch_radix_sort(W.ok[0], W.ov[0], W.ok[1], W.ov[1], n_old, 3 * depth, W.otmp, st, &oks,
+                      &operm, &nl);
+    launch_leaf_ranges(oks, n_old, depth, W.ols, st);
+    launch_gather(pos_old, gamma_old, operm, oks, n_old, g, W.o6, n_old, 0, st);
+    launch_keys(pos_new, n_new, g, W.nk[0], W.nv[0], c->d_err, st);
+    launch_radix_sort(W.nk[0], W.nv[0], W.nk[1], W.nv[1], n_new, 3 * depth, W.ntmp, st, &nks,
+                      &nperm, &nl);
+    launch_leaf_ranges(nks, n_new, depth, W.nls, st);
+    // the new particles carry no strength yet: the gather's strength rows are unused
+    launch_gather(pos_new, pos_new, nperm, nks, n_new, g, W.n6, n_new, 0, st);
+    CK(cudaGetLastError(), "reinit tree kernels");
+    // ---- right-hand side: omega at the new points (Eq. 3), initial guess omega dx^3 ----
+    launch_gauss(W.n6, n, W.nls, W.o6, n_old, W.ols, nullptr, depth, a, periodic, ws_old,
+                 sigma_old, W.om, st);
+    const double dx3 = (double)P.box_len * (double)P.box_len * (double)P.box_len / (double)n_new;
+    {
+        const double al[3] = {dx3, dx3, dx3}, be[3] = {0, 0, 0};
+        launch_scale3(W.om, nullptr, W.x, n, al, be, st);
+    }
+    CK(cudaGetLastError(), "reinit rhs kernels");
+    // ---- GMRES(m), the three components in lockstep (same matrix) ----
+    auto matvec = [&](const float* v, float* out) {  // out = A v
+        launch_gauss(W.n6, n, W.nls, W.n6, n, W.nls, v, depth, a, periodic, ws_new, sigma_new, out,
+                     st);
+    };
+    std::vector<double> hd(3 * (m + 1));
+    auto dots = [&](const float* X, int nv, const float* Y) -> vfmm_status {
+        launch_multidot(X, 3 * n, nv, Y, n, W.part, W.dots, st);
+        CK(cudaMemcpyAsync(hd.data(), W.dots, 3 * nv * sizeof(double), cudaMemcpyDeviceToHost, st),
+           "copy dots");
+        CK(cudaStreamSynchronize(st), "sync dots");
+        return VFMM_OK;
+    };
+    double beta0[3] = {0, 0, 0}, res[3] = {0, 0, 0};
+    int total = 0;
+    bool conv = false;
+    std::vector<double> H(3 * (size_t)(m + 1) * m), gv(3 * (m + 1)), cs(3 * m), sn(3 * m);
+    auto Hc = [&](int c, int i, int k) -> double& { return H[((size_t)c * (m + 1) + i) * m + k]; };
+    vfmm_status sres;
+    for (int cycle = 0;; ++cycle) {
+        // r = omega - A x -> V_0
+        matvec(W.x, W.w);
+        {
+            const double al[3] = {1, 1, 1}, be[3] = {-1, -1, -1};
+            launch_scale3(W.om, W.w, W.V, n, al, be, st);
+        }
+        if ((sres = dots(W.V, 1, W.V)) != VFMM_OK) return sres;
+        double beta[3];
+        bool done[3];
+        for (int cc = 0; cc < 3; ++cc) {
+            beta[cc] = std::sqrt(std::max(hd[cc], 0.0));
+            if (cycle == 0) beta0[cc] = beta[cc];
+            res[cc] = beta0[cc] > 0 ? beta[cc] / beta0[cc] : 0.0;
+            done[cc] = beta0[cc] == 0 || beta[cc] <= (double)tol * beta0[cc];
+        }
+        conv = done[0] && done[1] && done[2];
+        if (conv || total >= max_iter) break;
+        {
+            double al[3], be[3] = {0, 0, 0};
+            for (int cc = 0; cc < 3; ++cc) al[cc] = done[cc] ? 0.0 : 1.0 / beta[cc];
+            launch_scale3(W.V, nullptr, W.V, n, al, be, st);
+        }
+        std::fill(H.begin(), H.end(), 0.0);
+        std::fill(gv.begin(), gv.end(), 0.0);
+        for (int cc = 0; cc < 3; ++cc) gv[cc * (m + 1)] = done[cc] ? 0.0 : beta[cc];
+        bool active[3] = {!done[0], !done[1], !done[2]};
+        int kused = 0;
+        for (int k = 0; k < m && total < max_iter; ++k) {
+            float* vk = W.V + (size_t)k * 3 * n;
+            matvec(vk, W.w);
+            ++total;
+            for (int pass = 0; pass < 2; ++pass) {  // classical Gram-Schmidt, twice
+                if ((sres = dots(W.V, k + 1, W.w)) != VFMM_OK) return sres;
+                std::vector<double> coef(3 * (k + 1));
+                for (int i = 0; i <= k; ++i)
+                    for (int cc = 0; cc < 3; ++cc) {
+                        const double h = active[cc] ? hd[i * 3 + cc] : 0.0;
+                        Hc(cc, i, k) += h;
+                        coef[i * 3 + cc] = -h;
+                    }
+                CK(cudaMemcpyAsync(W.coef, coef.data(), coef.size() * sizeof(double),
+                                   cudaMemcpyHostToDevice, st),
+                   "copy coef");
+                launch_multiaxpy(W.V, 3 * n, k + 1, W.coef, W.w, n, st);
+                CK(cudaStreamSynchronize(st), "sync coef");  // coef (host) reused next pass
+            }
+            if ((sres = dots(W.w, 1, W.w)) != VFMM_OK) return sres;
+            double al[3], be[3] = {0, 0, 0};
+            bool all = true;
+            for (int cc = 0; cc < 3; ++cc) {
+                const double hn = std::sqrt(std::max(hd[cc], 0.0));
+                al[cc] = 0.0;
+                if (!active[cc]) continue;
+                Hc(cc, k + 1, k) = hn;
+                al[cc] = hn > 1e-300 ? 1.0 / hn : 0.0;
+                // Givens rotations on column k
+                double* csc = &cs[cc * m];
+                double* snc = &sn[cc * m];
+                for (int i = 0; i < k; ++i) {
+                    const double t = csc[i] * Hc(cc, i, k) + snc[i] * Hc(cc, i + 1, k);
+                    Hc(cc, i + 1, k) = -snc[i] * Hc(cc, i, k) + csc[i] * Hc(cc, i + 1, k);
+                    Hc(cc, i, k) = t;
+                }
+                const double hk = Hc(cc, k, k), hk1 = Hc(cc, k + 1, k);
+                const double r = std::hypot(hk, hk1);
+                csc[k] = r > 0 ? hk / r : 1.0;
+                snc[k] = r > 0 ? hk1 / r : 0.0;
+                Hc(cc, k, k) = r;
+                Hc(cc, k + 1, k) = 0.0;
+                double* gc = &gv[cc * (m + 1)];
+                gc[k + 1] = -snc[k] * gc[k];
+                gc[k] = csc[k] * gc[k];
+                res[cc] = std::fabs(gc[k + 1]) / beta0[cc];
+                if (res[cc] <= (double)tol || hn <= 1e-300) active[cc] = false;
+                all = all && !active[cc];
+            }
+            launch_scale3(W.w, nullptr, W.V + (size_t)(k + 1) * 3 * n, n, al, be, st);
+            kused = k + 1;
+            if (all) break;
+        }
+        // x += V y, H y = g (upper triangular, per component)
+        std::vector<double> coef(3 * kused, 0.0);
+        for (int cc = 0; cc < 3; ++cc) {
+            if (done[cc]) continue;
+            std::vector<double> y(kused, 0.0);
+            for (int i = kused - 1; i >= 0; --i) {
+                double t = gv[cc * (m + 1) + i];
+                for (int j = i + 1; j < kused; ++j) t -= Hc(cc, i, j) * y[j];
+                y[i] = Hc(cc, i, i) != 0 ? t / Hc(cc, i, i) : 0.0;
+            }
+            for (int i = 0; i < kused; ++i) coef[i * 3 + cc] = y[i];
+        }
+        if (kused) {
+            CK(cudaMemcpyAsync(W.coef, coef.data(), coef.size() * sizeof(double),
+                               cudaMemcpyHostToDevice, st),
+               "copy coef");
+            launch_multiaxpy(W.V, 3 * n, kused, W.coef, W.x, n, st);
+            CK(cudaStreamSynchronize(st), "sync coef");
+        }
+    }
+    // ---- outputs in the input order of the new particles ----
+    launch_unpermute3(W.x, nperm, n, gamma_new, st);
+    if (omega_new) launch_unpermute3(W.om, nperm, n, omega_new, st);
+    CK(cudaGetLastError(), "reinit kernels");
+    for (int i = 1; i < vfmm_ctx::NEV; ++i) CK(cudaEventRecord(c->ev[i], st), "event");
+    CK(cudaStreamSynchronize(st), "sync");
+    c->last_stream = st;
+    c->have_last = true;
+    c->have_tree = false;
+    c->have_exp = false;
+    c->prm.sigma = sigma_new;
+    if (info) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, c->ev[0], c->ev[vfmm_ctx::NEV - 1]);
+        info->iterations = total;
+        info->converged = conv ? 1 : 0;
+        for (int cc = 0; cc < 3; ++cc) info->rel_residual[cc] = res[cc];
+        info->ms = ms;
+        info->depth_used = depth;
+        info->ws_old = ws_old;
+        info->ws_new = ws_new;
+    }
+    int flag = 0;
+    CK(cudaMemcpy(&flag, c->d_err, sizeof(int), cudaMemcpyDeviceToHost), "read flag");
+    if (flag) {
+        CK(cudaMemset(c->d_err, 0, sizeof(int)), "clear flag");
+        c->err = "reinit: a position outside the box or non-finite";
+        return VFMM_EDOMAIN;
+    }
     return VFMM_OK;
 }
 

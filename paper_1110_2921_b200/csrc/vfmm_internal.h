@@ -168,6 +168,21 @@ KernelConsts make_kernel_consts(float sigma);
 void launch_p2p(const float* sorted6, int64_t n, const int* leaf_start, int depth, float a,
                 int periodic, int scheme, KernelConsts kc, float* near6,
                 unsigned long long* npairs, int64_t plo, int64_t pcnt, cudaStream_t st);
+// rbf.cu (reinitialization): Gaussian sums over the ws-neighbour leaves, BLAS-1 for GMRES
+void launch_gauss(const float* t6, int64_t nt, const int* tls, const float* s6, int64_t ns,
+                  const int* sls, const float* sg, int depth, float a, int periodic, int ws,
+                  float sigma, float* out, cudaStream_t st);
+int rbf_ws(float a, float sigma);
+size_t rbf_dot_part_doubles(int nv);
+void launch_multidot(const float* X, int64_t xs, int nv, const float* Y, int64_t n, double* part,
+                     double* dots, cudaStream_t st);
+void launch_multiaxpy(const float* X, int64_t xs, int nv, const double* coef, float* Y, int64_t n,
+                      cudaStream_t st);
+void launch_scale3(const float* X, const float* Z, float* Y, int64_t n, const double al[3],
+                   const double be[3], cudaStream_t st);
+void launch_unpermute3(const float* in, const uint32_t* perm, int64_t n, float* out,
+                       cudaStream_t st);
+
 // step.cu: x += u dt (wrapped into the box when periodic), gamma += dgamma dt
 void launch_euler_update(float* pos, float* gamma, const float* vel, const float* dgamma,
                          int64_t n, float dt, float lo, float len, int periodic, cudaStream_t st);

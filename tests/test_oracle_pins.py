@@ -510,3 +510,53 @@ def test_euler_step_lone_particle_and_zero_dt():
     x1, _, _, u, _ = euler_step(p2, g2, 0.3, 0.0, 0.2, -math.pi, 2 * math.pi, 0)
     assert np.allclose(x1 - p2, 0.2 * u, rtol=0, atol=1e-15)
     assert np.allclose(u[:, 0], -u[:, 1], rtol=1e-12)
+
+
+# ---------------------------------------------------------------- RBF reinitialization (NEXT-2)
+
+def test_rbf_oracle_fourier_mode_closed_form():
+    """On the cell-centre lattice with sigma = h a Fourier mode is an eigenvector
+    of the Gaussian sum (Eq. 3): sum_j h^3 sin(k.x_j) zeta(x_i - x_j) = e^{-|k|^2 s^2/2} sin(k.x_i)
+    up to lattice aliasing, here e^{-|k - (2 pi/h) e_x|^2 s^2 / 2} = 3e-8 (Poisson summation;
+    16^3, k = (1, 1, 0)).  So the RBF solve of omega = sin(k.x) is
+    gamma = h^3 e^{|k|^2 s^2/2} sin(k.x)."""
+    from oracle import rbf
+
+    n = 16
+    L = 2 * math.pi
+    h = L / n
+    c = -math.pi + h * (np.arange(n) + 0.5)  # exact float64 lattice (Poisson summation)
+    zz, yy, xx = np.meshgrid(c, c, c, indexing="ij")
+    x = np.stack([xx.ravel(), yy.ravel(), zz.ravel()])
+    s = h
+    f = synthgen.Field(x, x, s, -math.pi, L, n, "lattice")
+    k = np.array([1.0, 1.0, 0.0])
+    mode = np.sin(k @ x)
+    w = np.stack([mode, 0.5 * mode, -mode]) * h ** 3
+    om = rbf.gaussian_sum(x, x, w, s, f.box_len)
+    damp = math.exp(-0.5 * (k @ k) * s * s)
+    assert np.abs(om - damp * w / h ** 3).max() < 2e-7 * np.abs(w / h ** 3).max()
+    A = rbf.rbf_matrix(x, s, f.box_len)
+    g2 = np.linalg.solve(A, mode)
+    assert np.abs(g2 - h ** 3 * mode / damp).max() < 5e-6 * np.abs(h ** 3 * mode / damp).max()
+    g, _ = rbf.reinit(x, w, s, x, s, f.box_len)
+    assert np.abs(g - w).max() < 1e-9 * np.abs(w).max()   # the same particles back
+
+
+def test_rbf_oracle_single_particle_and_partition_of_unity():
+    """A particle already on a lattice point with the new core size is its own interpolant;
+    the lattice quadrature of one Gaussian sums to 1 (Eq. 4 integrates to 1)."""
+    from oracle import rbf
+
+    f = synthgen.taylor_green(8)
+    x = f.pos.astype(np.float64)
+    h = f.box_len / 8
+    p = 77
+    g_old = np.array([[0.3], [-0.2], [0.9]])
+    g, _ = rbf.reinit(x[:, p:p + 1], g_old, f.sigma, x, f.sigma, f.box_len)
+    want = np.zeros_like(g)
+    want[:, p] = g_old[:, 0]
+    assert np.abs(g - want).max() < 1e-9
+    one = rbf.gaussian_sum(np.array([[0.123], [-0.4], [1.0]]), x, np.ones_like(x) * h ** 3,
+                           f.sigma, f.box_len)
+    assert one == pytest.approx(np.ones((3, 1)), rel=1e-8)
