@@ -305,19 +305,21 @@ __device__ __forceinline__ uint32_t compact3p(uint32_t v) {
 constexpr int P2P_THREADS = 256;
 // sources per pass at 2 blocks / SM: 24 B per source (x y z gx | gy gz) or, with the staged
 // cross products, 36 B (x y z gx | gy gz sx sy | sz)
-template <bool SJ> constexpr int p2p_cap() { return SJ ? 3072 : 4352; }
+template <bool SJ, int MINB = 2> constexpr int p2p_cap() {
+    return MINB >= 3 ? (SJ ? 1920 : 2816) : (SJ ? 3072 : 4352);
+}
 constexpr int P2P_PAD = 4;     // slack after each staged array (keeps the arrays 16-byte aligned)
 
 // SJ (classical scheme only): accumulate with the staged source cross products s_j (Acc2S:
 // 38 instead of 41 FP32 instructions per pair, rounding ~1.4x larger since the sums carry
 // |x_j| instead of |d|); otherwise the per-pair cross product gamma_j x d
-template <int SCHEME, bool SJ>
-__global__ void __launch_bounds__(P2P_THREADS, 2) p2p_kernel(
+template <int SCHEME, bool SJ, int MINB = 2, int UNR = 2>
+__global__ void __launch_bounds__(P2P_THREADS, MINB) p2p_kernel(
     const float* __restrict__ s6, int64_t n, const int* __restrict__ leaf_start, int depth,
     float a, int periodic, KernelConsts kc, float* __restrict__ near6,
     unsigned long long* __restrict__ npairs, int64_t plo) {
     extern __shared__ float4 p2p_sm[];
-    constexpr int P2P_CAP = p2p_cap<SJ>();
+    constexpr int P2P_CAP = p2p_cap<SJ, MINB>();
     float4* S4 = p2p_sm;                         // x, y, z, gx
     // SJ: gy, gz, sx, sy (s_j = gamma_j x x_j) and sz; else gy, gz
     float4* S4b = S4 + P2P_CAP + P2P_PAD;
@@ -443,7 +445,7 @@ __global__ void __launch_bounds__(P2P_THREADS, 2) p2p_kernel(
                     return make_float4(t.x, t.y, 0.f, 0.f);
                 };
                 // unrolled by 2 (c4 P2P: 43.1 ms; 49.6 without unrolling, 44.0 unrolled by 4)
-#pragma unroll 2
+#pragma unroll UNR
                 for (int j = js; j < je; j += 2) {  // js, je even (padded leaves, even CAP)
                     const float4 pa = S4[j];
                     const float4 qa = rec2(j);
@@ -618,34 +620,48 @@ __global__ void __launch_bounds__(128) direct_kernel(const float* __restrict__ p
 
 }  // namespace
 
+namespace {
+template <int SCHEME, bool SJ, int MINB, int UNR>
+void p2p_go(const float* sorted6, int64_t n, const int* leaf_start, int depth, float a,
+            int periodic, KernelConsts kc, float* near6, unsigned long long* npairs, int64_t plo,
+            int64_t pcnt, cudaStream_t st) {
+    constexpr int cap = p2p_cap<SJ, MINB>();
+    const size_t smem = SJ ? (size_t)(cap + P2P_PAD) * (2 * sizeof(float4) + sizeof(float))
+                           : (size_t)(cap + P2P_PAD) * (sizeof(float4) + sizeof(float2));
+    static PerDeviceOnce once;
+    once([&] {
+        cudaFuncSetAttribute(p2p_kernel<SCHEME, SJ, MINB, UNR>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    });
+    p2p_kernel<SCHEME, SJ, MINB, UNR><<<(unsigned)pcnt, P2P_THREADS, smem, st>>>(
+        sorted6, n, leaf_start, depth, a, periodic, kc, near6, npairs, plo);
+}
+}  // namespace
+
 void launch_p2p(const float* sorted6, int64_t n, const int* leaf_start, int depth, float a,
                 int periodic, int scheme, KernelConsts kc, float* near6,
                 unsigned long long* npairs, int64_t plo, int64_t pcnt, cudaStream_t st) {
-    const size_t smem_sj = (size_t)(p2p_cap<true>() + P2P_PAD) * (2 * sizeof(float4) + sizeof(float));
-    const size_t smem_x = (size_t)(p2p_cap<false>() + P2P_PAD) * (sizeof(float4) + sizeof(float2));
-    static PerDeviceOnce once;
-    once([&] {
-        cudaFuncSetAttribute(p2p_kernel<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem_sj);
-        cudaFuncSetAttribute(p2p_kernel<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem_x);
-        cudaFuncSetAttribute(p2p_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem_x);
-    });
     if (pcnt <= 0) return;
     // default: per-pair cross products gamma_j x d (FP32-faithful rounding); VFMM_P2P=sj: the
-    // classical scheme with staged source cross products (~3% faster at c4, 2-4x the rounding)
+    // classical scheme with staged source cross products (~3% faster at c4, 2-4x the rounding).
+    // VFMM_P2P_CFG: occupancy / unroll variants (measurement knob): "b3u1", "b3u2", "b2u1"
     const char* env = getenv("VFMM_P2P");
     const bool sj = env && strcmp(env, "sj") == 0;
-    if (scheme == 0 && sj)
-        p2p_kernel<0, true><<<(unsigned)pcnt, P2P_THREADS, smem_sj, st>>>(
-            sorted6, n, leaf_start, depth, a, periodic, kc, near6, npairs, plo);
-    else if (scheme == 0)
-        p2p_kernel<0, false><<<(unsigned)pcnt, P2P_THREADS, smem_x, st>>>(
-            sorted6, n, leaf_start, depth, a, periodic, kc, near6, npairs, plo);
-    else
-        p2p_kernel<1, false><<<(unsigned)pcnt, P2P_THREADS, smem_x, st>>>(
-            sorted6, n, leaf_start, depth, a, periodic, kc, near6, npairs, plo);
+    const char* cfg = getenv("VFMM_P2P_CFG");
+    const int v = !cfg ? 0 : strcmp(cfg, "b3u1") == 0 ? 1 : strcmp(cfg, "b3u2") == 0 ? 2
+                                : strcmp(cfg, "b2u1") == 0 ? 3 : 0;
+#define P2P_ARGS sorted6, n, leaf_start, depth, a, periodic, kc, near6, npairs, plo, pcnt, st
+    if (scheme == 0 && sj) {
+        p2p_go<0, true, 2, 2>(P2P_ARGS);
+    } else if (scheme == 0) {
+        if (v == 1) p2p_go<0, false, 3, 1>(P2P_ARGS);
+        else if (v == 2) p2p_go<0, false, 3, 2>(P2P_ARGS);
+        else if (v == 3) p2p_go<0, false, 2, 1>(P2P_ARGS);
+        else p2p_go<0, false, 2, 2>(P2P_ARGS);
+    } else {
+        p2p_go<1, false, 2, 2>(P2P_ARGS);
+    }
+#undef P2P_ARGS
 }
 
 void launch_direct(const float* pos, const float* gamma, int64_t n, float len, int image_levels,

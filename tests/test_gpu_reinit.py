@@ -39,20 +39,30 @@ def test_reinit_jittered_particles_onto_the_lattice():
     s_old, s_new = float(np.float32(1.25 * h)), float(np.float32(h))
     ev = vf.Evaluator(p=4, depth=2, image_levels=1, sigma=s_old, box_lo=f0.box_lo,
                       box_len=f0.box_len)
-    g, om, info = ev.reinit(_t(old.pos), _t(old.gamma), s_old, _t(f0.pos), s_new, tol=1e-6,
-                            max_iter=60)
-    g = g.cpu().numpy().astype(np.float64)
-    om = om.cpu().numpy().astype(np.float64)
     g_o, om_o = rbf.reinit(old.pos, old.gamma, s_old, f0.pos, s_new, f0.box_len)
-    e_om, e_g = rel(om, om_o), rel(g, g_o)
-    print(f"reinit 16^3: omega {e_om:.2e}, gamma {e_g:.2e}, {info['iterations']} iterations, "
-          f"residual {max(info['rel_residual']):.1e}, ws {info['ws_old']}/{info['ws_new']}, "
-          f"{info['ms']:.2f} ms")
-    assert info["converged"] == 1
-    assert e_om < 2e-6, e_om
-    # FP32 matrix-vector products; the RBF matrix at h / sigma = 1 has a condition number
-    # ~e^{pi^2/2} = 139, so the solve keeps ~1e-5 of the FP32 residual floor
-    assert e_g < 5e-5, e_g
+    A = rbf.rbf_matrix(f0.pos, s_new, f0.box_len)
+    x0 = om_o * (f0.box_len ** 3 / n ** 3)          # the paper's initial guess
+    r0 = np.linalg.norm(om_o - x0 @ A.T, axis=1)
+    for tol in (1e-3, 1e-5):
+        g, om, info = ev.reinit(_t(old.pos), _t(old.gamma), s_old, _t(f0.pos), s_new, tol=tol,
+                                max_iter=400, restart=60)
+        g = g.cpu().numpy().astype(np.float64)
+        om = om.cpu().numpy().astype(np.float64)
+        res = np.linalg.norm(om_o - g @ A.T, axis=1) / r0   # true residual, dense matrix
+        e_om, e_g = rel(om, om_o), rel(g, g_o)
+        print(f"reinit 16^3 tol {tol:g}: omega {e_om:.2e}, true residual {res.max():.2e} "
+              f"(GMRES {max(info['rel_residual']):.2e}), gamma vs dense solve {e_g:.2e}, "
+              f"{info['iterations']} iterations, ws {info['ws_old']}/{info['ws_new']}, "
+              f"{info['ms']:.2f} ms")
+        assert info["converged"] == 1
+        assert e_om < 2e-6, e_om
+        # the exit test holds for the true (float64, untruncated) residual too, up to the
+        # FP32 floor of the matrix-vector products (~1e-6 of omega)
+        assert res.max() < 1.5 * tol + 2e-5, res
+    # at the tight tolerance the strengths approach the exact solve; the RBF matrix's highest
+    # lattice modes are damped by up to e^{-3 pi^2 / 2} (condition ~1e5), which GMRES only
+    # resolves as far as the residual asks
+    assert e_g < 1e-2, e_g
     assert ev.params.sigma == pytest.approx(s_new)
     ev.close()
 
@@ -73,11 +83,11 @@ def test_reinit_fourier_mode_closed_form():
     g_true = np.stack([mode, -mode, 0.5 * mode]) * h ** 3 / damp
     ev = vf.Evaluator(p=4, depth=3, image_levels=1, sigma=f.sigma, box_lo=f.box_lo,
                       box_len=f.box_len)
-    g, om, info = ev.reinit(_t(f.pos), _t(g_true), f.sigma, _t(f.pos), f.sigma, tol=1e-6)
+    g, om, info = ev.reinit(_t(f.pos), _t(g_true), f.sigma, _t(f.pos), f.sigma, tol=1e-4)
     g = g.cpu().numpy()
     om = om.cpu().numpy()
     print(f"fourier mode: {info['iterations']} iterations, gamma {rel(g, g_true):.2e}")
     assert rel(om, np.stack([mode, -mode, 0.5 * mode])) < 1e-5
-    assert rel(g, g_true) < 2e-5
-    assert info["iterations"] <= 12
+    assert rel(g, g_true) < 1e-4
+    assert info["iterations"] <= 10  # "converges in 5-10 iterations"
     ev.close()
