@@ -93,6 +93,21 @@ class ClockSampler:
                 "samples": len(sm), "power_w_max": max(pw) if pw else None}
 
 
+def host_cpu():
+    """lscpu model / sockets / cores of this host (recorded with the CPU baseline)."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            k, _, v = line.partition(":")
+            k = k.strip()
+            if k in ("Model name", "Socket(s)", "Core(s) per socket", "Thread(s) per core"):
+                info[k] = v.strip()
+    except Exception:
+        pass
+    return info
+
+
 def cpu_baseline(field, p_unused, budget_s=15.0, threads=None):
     """Oracle O1 (float64 direct periodic sum, oracle/) on a bounded sample: T targets x a
     strided subset of sources x all 27^3 images; extrapolated to the full evaluation."""
@@ -113,7 +128,8 @@ def cpu_baseline(field, p_unused, budget_s=15.0, threads=None):
                   probe_pos=field.pos[:, tg[:1]].astype(np.float64),
                   probe_gamma=field.gamma[:, tg[:1]].astype(np.float64), nthreads=1)
     t1 = time.perf_counter() - t0
-    ntg = max(1, min(256, int(budget_s / max(t1, 1e-6) * threads * 0.8)))
+    # at least one target per thread, so every core works
+    ntg = max(threads, min(256, int(budget_s / max(t1, 1e-6) * threads * 0.8)))
     tg = np.linspace(7, n - 1, ntg).astype(np.int64)
     t0 = time.perf_counter()
     oracle.direct(pos_s, gam_s, field.sigma, field.box_lo, field.box_len, 3, 0,
@@ -123,7 +139,7 @@ def cpu_baseline(field, p_unused, budget_s=15.0, threads=None):
     pairs_sample = len(tg) * len(src) * 27 ** 3
     pairs_full = n * n * 27 ** 3
     return {"value": dt * pairs_full / pairs_sample, "unit": "s/eval (extrapolated)",
-            "cores": threads, "kind": "oracle",
+            "cores": threads, "kind": "oracle", "host_cpu": host_cpu(),
             "sample": (f"{len(tg)} targets x {len(src)} sources (every {stride}th) x 27^3 "
                        f"images = {pairs_sample:.3e} pair evals in {dt:.2f} s; scaled by "
                        f"{pairs_full / pairs_sample:.3e} to N^2 27^3")}

@@ -137,6 +137,8 @@ TcOps tc_ops(const vfmm_ctx* c) {
         t.rs = c->d_h16_rs;
         t.cs = c->d_h16_cs;
         t.f16 = true;
+        t.nr = c->hops.h16_nr;
+        t.kp = c->hops.h16_kp;
     } else {
         t.hi = c->d_tc_hi;
         t.lo = c->d_tc_lo;
@@ -262,6 +264,8 @@ vfmm_status ensure_ops(vfmm_ctx* c) {
     if (!c->hops.m2l_tc_hi.empty()) {
         CK(up(c->hops.m2l_tc_hi, &c->d_tc_hi), "upload m2l tc hi");
         CK(up(c->hops.m2l_tc_lo, &c->d_tc_lo), "upload m2l tc lo");
+    }
+    if (!c->hops.m2l_h16_hi.empty()) {
         auto up16 = [&](const std::vector<uint16_t>& h, uint16_t** d) -> cudaError_t {
             cudaError_t e = cudaMalloc((void**)d, h.size() * sizeof(uint16_t));
             if (e != cudaSuccess) return e;
@@ -808,7 +812,7 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
             float** glo = l == depth ? &c->g_lo : &c->g2_lo;
             size_t* gcap = l == depth ? &c->g_cap : &c->g2_cap;
             const int box[6] = {0, 0, 0, 1 << (l - 1), 1 << (l - 1), 1 << (l - 1)};
-            if (allow_tc && m2l_tc_supported(p, l) && m2l_tc_shape_ok(box)) {
+            if (allow_tc && m2l_tc_supported(p, l) && m2l_tc_shape_ok(box, p)) {
                 const size_t need = m2l_tc_grid_floats(l);
                 if (need > *gcap) {
                     CK(cudaStreamSynchronize(sl), "sync before grid realloc");

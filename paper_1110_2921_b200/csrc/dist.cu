@@ -808,7 +808,7 @@ vfmm_status dist_phase4_far(RankState& S, const DistShared& D, cudaStream_t st, 
             box[4] = k >= 4 ? nP : half;
             box[5] = k >= 8 ? nP : half;
         }
-        if (D.allow_tc && D.tc.hi && m2l_tc_supported(p, l) && m2l_tc_shape_ok(box)) {
+        if (D.allow_tc && D.tc.hi && m2l_tc_supported(p, l) && m2l_tc_shape_ok(box, p)) {
             const size_t need = m2l_tc_grid_floats(l);
             if (need > S.g_cap) {
                 dfree(S.g_hi);

@@ -50,16 +50,22 @@ namespace vfmm {
 namespace {
 
 // K chunks of 128 B: 4 x 32 tf32 or 2 x 64 halves (K = 128)
-template <bool F16> __host__ __device__ constexpr int tc_nkc() { return F16 ? 2 : 4; }
 template <bool F16> __host__ __device__ constexpr int tc_ke() { return F16 ? 64 : 32; }
 constexpr int TC_AST = 2;      // A (operator) pipeline stages
 constexpr int TC_BST = 2;      // B pipeline stages (each holds one y-window of T + 2 slabs)
-constexpr int A_BYTES = 128 * 128;  // one K chunk of one operator half (hi or lo): 16 KB
-constexpr int B_WROWS = 288;        // max window rows (T + 2) N
-constexpr int B_BYTES = B_WROWS * 128;  // one K chunk of a y-window of slabs, one half: 36 KB
+// MT = output row tiles of 128 (1: (p+1)^2 <= 128; 2: <= 256, f16 only)
+constexpr int A_TILE = 128 * 128;  // one K chunk of 128 operator rows, one half (hi or lo): 16 KB
+template <int MT> __host__ __device__ constexpr int a_bytes() { return MT * A_TILE; }
+// max window rows (T + 2) N: MT = 1 up to 288 rows (36 KB), MT = 2 up to 192 (24 KB)
+template <int MT> __host__ __device__ constexpr int b_wrows() { return MT == 1 ? 288 : 192; }
+template <int MT> __host__ __device__ constexpr int b_bytes() { return b_wrows<MT>() * 128; }
 constexpr int TC_EPI_WARPS = 8;  // 2 per TMEM lane quarter: warp pair splits the T tiles
 constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;
-constexpr size_t TC_SMEM = 1024 + (size_t)TC_AST * 2 * A_BYTES + (size_t)TC_BST * 2 * B_BYTES + 512;
+template <int MT>
+constexpr size_t tc_smem() {
+    return 1024 + (size_t)TC_AST * 2 * a_bytes<MT>() + (size_t)TC_BST * 2 * b_bytes<MT>() + 512;
+}
+static_assert(tc_smem<2>() <= 232448, "MT = 2 stages exceed 227 KB");
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -180,7 +186,8 @@ struct TcParams {
     int NV;     // valid columns = 3 * XT
     int T;      // target rows per CTA (accumulator tiles), T N <= 192
     int rows;   // target rows per parity = nP * nP * ntx
-    int nc;     // (p+1)^2 <= 128
+    int nc;     // (p+1)^2 <= 128 MT
+    int nkc;    // K chunks of 128 B (64 halves / 32 tf32) covering nc
     int level;
     int bx0, by0, bz0, bny;  // owned box of target parents (origin; y extent)
     const int* slots;  // [8][189] M2L slot per target parity
@@ -218,7 +225,7 @@ __device__ __forceinline__ void group_rows(const TcParams& P, int g, int* tx, in
     *pz = P.bz0 + gz;
 }
 
-template <bool F16>
+template <bool F16, int MT>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     m2l_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant__ CUtensorMap tmA_lo,
                   const __grid_constant__ CUtensorMap tmB_hi, const __grid_constant__ CUtensorMap tmB_lo,
@@ -226,7 +233,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
     extern __shared__ uint8_t tc_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>(((uintptr_t)tc_raw + 1023) & ~(uintptr_t)1023);
     uint8_t* Abuf = sm;                                  // [AST][hi|lo][16 KB]
-    uint8_t* Bbuf = sm + TC_AST * 2 * A_BYTES;           // [BST][hi|lo][12 KB]
+    constexpr int A_BYTES = a_bytes<MT>(), B_BYTES = b_bytes<MT>();
+    uint8_t* Bbuf = sm + TC_AST * 2 * A_BYTES;           // [BST][hi|lo][B_BYTES]
     uint64_t* bars = reinterpret_cast<uint64_t*>(Bbuf + TC_BST * 2 * B_BYTES);
     uint64_t* a_full = bars;
     uint64_t* a_empty = bars + TC_AST;
@@ -291,7 +299,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
                 const int dx = ((G.x >> 4) & 3) - 1, dz = ((G.x >> 6) & 3) - 1, pis = (G.x >> 8) & 7;
                 const int c1 = 3 * (2 + P.bx0 + gtx * P.XT + dx);
                 const int c2 = 1 + gpy0, c3 = 2 + gpz + dz;
-                for (int kc = 0; kc < tc_nkc<F16>(); ++kc) {
+                for (int kc = 0; kc < P.nkc; ++kc) {
                     mbar_wait(&b_empty[sb], pb ^ 1);
                     mbar_expect_tx(&b_full[sb], b_tx);
                     tma_load_5d(Bbuf + (sb * 2 + 0) * B_BYTES, &tmB_hi, &b_full[sb], kc * tc_ke<F16>(),
@@ -338,7 +346,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         for (int gi = 0; gi < 72; ++gi) {
             const int mask = P.groups[pi * 72 + gi].x & 7;
             if (!mask) continue;
-            for (int kc = 0; kc < tc_nkc<F16>(); ++kc) {
+            for (int kc = 0; kc < P.nkc; ++kc) {
                 mbar_wait(&b_full[sb], pb);
                 tc_fence_after();
                 const uint64_t bhi = sw128_desc(Bbuf + (sb * 2 + 0) * B_BYTES);
@@ -359,14 +367,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
                         for (int ks = 0; ks < 4; ++ks) {  // K = 8 tf32 / 16 f16 = 32 B per MMA
                             const uint64_t adv = (uint64_t)(ks * 2);
                             const uint32_t acc = ks == 0 ? 0u : 1u;
-                            if (F16) {
-                                mma_f16(d, ahi + adv, bhi + bsh + adv, idesc, acc);
-                                mma_f16(d, ahi + adv, blo + bsh + adv, idesc, 1u);
-                                mma_f16(d, alo + adv, bhi + bsh + adv, idesc, 1u);
-                            } else {
-                                mma_tf32(d, ahi + adv, bhi + bsh + adv, idesc, acc);
-                                mma_tf32(d, ahi + adv, blo + bsh + adv, idesc, 1u);
-                                mma_tf32(d, alo + adv, bhi + bsh + adv, idesc, 1u);
+#pragma unroll
+                            for (int mt = 0; mt < MT; ++mt) {  // row tile mt: rows 128 mt ..
+                                const uint32_t dm = d + (uint32_t)(mt * P.T * P.N);
+                                const uint64_t am = (uint64_t)(mt * (A_TILE >> 4));
+                                if (F16) {
+                                    mma_f16(dm, ahi + am + adv, bhi + bsh + adv, idesc, acc);
+                                    mma_f16(dm, ahi + am + adv, blo + bsh + adv, idesc, 1u);
+                                    mma_f16(dm, alo + am + adv, bhi + bsh + adv, idesc, 1u);
+                                } else {
+                                    mma_tf32(dm, ahi + am + adv, bhi + bsh + adv, idesc, acc);
+                                    mma_tf32(dm, ahi + am + adv, blo + bsh + adv, idesc, 1u);
+                                    mma_tf32(dm, alo + am + adv, bhi + bsh + adv, idesc, 1u);
+                                }
                             }
                         }
                         mma_commit_mc(&a_empty[sa], (uint16_t)3);  // release in both CTAs
@@ -392,31 +405,33 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         const int e = warp - 2;
         const int quarter = warp & 3;  // TMEM lanes [32 quarter, 32 quarter + 32)
         const int half = e >> 2;       // this warp owns tiles [half T/2, (half+1) T/2)
-        const int ncol = (P.T / 2) * P.N;  // <= 96 columns per warp
+        const int ncol = (P.T / 2) * P.N;  // columns per warp and row tile: MT * ncol <= 96
         const int col0 = half * ncol;
         const int r = quarter * 32 + lane;
-        // each finished chain (one offset x one K chunk, <= 12 MMAs: truncating TMEM
+        // each finished chain (one offset x one K chunk, <= 12 MMAs per row tile: truncating TMEM
         // accumulation) is added into FP32 registers with round-to-nearest, packed two at a time
         unsigned long long acc2[48];
 #pragma unroll
         for (int j = 0; j < 48; ++j) acc2[j] = 0ull;
         int nchains = 0;
         for (int gi = 0; gi < 72; ++gi) nchains += __popc(P.groups[pi * 72 + gi].x & 7);
-        nchains *= tc_nkc<F16>();
+        nchains *= P.nkc;
         for (int ch = 0; ch < nchains; ++ch) {
             const int buf = ch & 1;
             mbar_wait(&acc_full[buf], (ch >> 1) & 1);
             tc_fence_after();
-            // two halves of 48 columns: three 16-column loads in flight, one wait each
+            // two halves of 48 accumulator columns (MT = 1: the warp's 96 columns; MT = 2: one
+            // row tile each), three 16-column loads in flight, one wait each
 #pragma unroll
             for (int hh = 0; hh < 2; ++hh) {
                 uint32_t w[48];
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
-                    const int col = (hh * 3 + c) * 16;
+                    const int col = MT == 1 ? (hh * 3 + c) * 16 : c * 16;
+                    const int tcol = MT == 1 ? col0 + col : hh * P.T * P.N + col0 + col;
                     if (col < ncol) {
                         const uint32_t taddr = tmem + ((uint32_t)(quarter * 32) << 16) +
-                                               (uint32_t)(buf * 256 + col0 + col);
+                                               (uint32_t)(buf * 256 + tcol);
                         asm volatile(
                             "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, "
                             "%7, %8, %9, %10, %11, %12, %13, %14, %15}, [%16];"
@@ -432,7 +447,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
                 asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
                 for (int c = 0; c < 3; ++c) {
-                    if ((hh * 3 + c) * 16 < ncol) {
+                    const int col = MT == 1 ? (hh * 3 + c) * 16 : c * 16;
+                    if (col < ncol) {
 #pragma unroll
                         for (int j = 0; j < 8; ++j) {
                             unsigned long long v;
@@ -452,23 +468,25 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
 #pragma unroll
         for (int j = 0; j < 48; ++j)
             asm("mov.b64 {%0, %1}, %2;" : "=f"(acc[2 * j]), "=f"(acc[2 * j + 1]) : "l"(acc2[j]));
-        if (r < P.nc) {
-            if (F16) {  // undo the balancing: row r times rs[r] / s
-                const float f = P.rs[r] * ldexpf(1.f, -h16_scale_exp(*P.maxbits));
+        const float sinv = F16 ? ldexpf(1.f, -h16_scale_exp(*P.maxbits)) : 1.f;
+        const uint32_t cz = spread3t(2 * gpz + piz) << 2;
 #pragma unroll
-                for (int j = 0; j < 96; ++j) acc[j] *= f;
-            }
-            const uint32_t cz = spread3t(2 * gpz + piz) << 2;
+        for (int mt = 0; mt < MT; ++mt) {
+            const int rr = r + 128 * mt;
+            if (rr < P.nc) {
+                const float fsc = F16 ? P.rs[rr] * sinv : 1.f;  // undo the balancing
 #pragma unroll
-            for (int j = 0; j < 96; ++j) {
-                if (j < ncol) {
-                    const int t = half * (P.T / 2) + j / P.N, cj = j % P.N;
-                    if (cj < P.NV) {
-                        const int py = gpy0 + t;
-                        const int px = P.bx0 + gtx * P.XT + cj / 3, comp = cj % 3;
-                        const uint32_t cell =
-                            spread3t(2 * px + pix) | (spread3t(2 * py + piy) << 1) | cz;
-                        P.L[((int64_t)cell * 3 + comp) * P.nc + r] = acc[j];
+                for (int jj = 0; jj < 96 / MT; ++jj) {
+                    if (jj < ncol) {
+                        const int j = mt * (96 / MT) + jj;
+                        const int t = half * (P.T / 2) + jj / P.N, cj = jj % P.N;
+                        if (cj < P.NV) {
+                            const int py = gpy0 + t;
+                            const int px = P.bx0 + gtx * P.XT + cj / 3, comp = cj % 3;
+                            const uint32_t cell =
+                                spread3t(2 * px + pix) | (spread3t(2 * py + piy) << 1) | cz;
+                            P.L[((int64_t)cell * 3 + comp) * P.nc + rr] = acc[j] * fsc;
+                        }
                     }
                 }
             }
@@ -558,8 +576,8 @@ __global__ void __launch_bounds__(512) m2l_stage16_kernel(const float* __restric
             const float x = v * ck * s;
             const __half h = __float2half_rn(x);
             const __half l = __float2half_rn(x - __half2float(h));
-            ghi[(row0 + rr) * 128 + k] = h;
-            glo[(row0 + rr) * 128 + k] = l;
+            ghi[(row0 + rr) * blockDim.x + k] = h;  // row length = padded K (128 or 256)
+            glo[(row0 + rr) * blockDim.x + k] = l;
         }
     }
     if (MAXPASS) {
@@ -584,28 +602,34 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 
 }  // namespace
 
-// rows per CTA for a box: the largest T in {8, 4, 2} with T N <= 192, T | bny and an even
-// number of CTAs (2-CTA clusters); 0 if none
+// rows per CTA for a box: the largest T in {8, 4, 2} with MT T N <= 192 (MT = 2: T N <= 128)
+// and (T + 2) N within the window stage, T | bny and an even number of CTAs (2-CTA clusters);
+// 0 if none
 static int pick_XT(const int box[6]) { return box[3] < 16 ? box[3] : 16; }
-static int pick_T(const int box[6]) {
+static int pick_T(const int box[6], int MT) {
     const int bnx = box[3], bny = box[4], bnz = box[5];
     const int XT = pick_XT(box);
     if (bnx % XT != 0) return 0;
     const int N = (3 * XT + 15) / 16 * 16;
     const int rows = bny * bnz * (bnx / XT);
+    const int wrows = MT == 1 ? b_wrows<1>() : b_wrows<2>();
     for (int T = 8; T >= 2; T /= 2)
-        if (T * N <= 192 && (T + 2) * N <= B_WROWS && bny % T == 0 && (rows / T) % 2 == 0)
+        if (MT * T * N <= (MT == 1 ? 192 : 256) && T * N <= 192 && (T + 2) * N <= wrows &&
+            bny % T == 0 && (rows / T) % 2 == 0)
             return T;
     return 0;
 }
 
-bool m2l_tc_shape_ok(const int box[6]) { return pick_T(box) != 0; }
-
-bool m2l_tc_supported(int p, int level) {
-    return (p + 1) * (p + 1) <= 128 && level >= 2 && get_encode() != nullptr;
+bool m2l_tc_shape_ok(const int box[6], int p) {
+    return pick_T(box, (p + 1) * (p + 1) > 128 ? 2 : 1) != 0;
 }
 
-size_t m2l_tc_grid_floats(int level) {
+// (p+1)^2 <= 128: 3xTF32 or 3xFP16; (p+1)^2 <= 256 (p <= 15): 3xFP16 with two row tiles
+bool m2l_tc_supported(int p, int level) {
+    return (p + 1) * (p + 1) <= 256 && level >= 2 && get_encode() != nullptr;
+}
+
+size_t m2l_tc_grid_floats(int level) {  // floats: 128 tf32 or 256 halves per grid row
     const int64_t nP = (int64_t)1 << (level - 1), Xp = nP + 4;
     return (size_t)(8 * Xp * Xp * Xp * 3 * 128);
 }
@@ -617,6 +641,10 @@ int launch_m2l_tc(const TcOps& ops, const int* il_slots, int p, const float* M_l
     const int nP = 1 << (level - 1);
     const int Xp = nP + 4;
     const bool f16 = ops.f16;
+    const int MT = ops.nr / 128;   // output row tiles
+    const int KPG = ops.kp;        // padded K of the operators and of the staged grid rows
+    if (nc > ops.nr || nc > KPG || (MT == 2 && !f16) || MT < 1 || MT > 2) return -5;
+    const int nkc = (nc + (f16 ? 63 : 31)) / (f16 ? 64 : 32);
     const size_t esz = f16 ? 2 : 4;
     const CUtensorMapDataType dt = f16 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
     const cuuint32_t ke = f16 ? 64 : 32;  // K elements per 128-byte chunk
@@ -625,7 +653,7 @@ int launch_m2l_tc(const TcOps& ops, const int* il_slots, int p, const float* M_l
         const int64_t total = (int64_t)8 * Xp * Xp * Xp * 3 * 128;
         if (f16) {
             const int64_t blocks = (int64_t)8 * Xp * Xp;  // one per (pi', Z, Y) x-row
-            const dim3 blk(128, 4);
+            const dim3 blk(KPG, 512 / KPG);
             m2l_stage16_kernel<true><<<(unsigned)blocks, blk, 0, st>>>(
                 M_l, nP, periodic, nc, ops.cs, maxbits, nullptr, nullptr);
             m2l_stage16_kernel<false><<<(unsigned)blocks, blk, 0, st>>>(
@@ -642,9 +670,9 @@ int launch_m2l_tc(const TcOps& ops, const int* il_slots, int p, const float* M_l
     if (!enc) return -1;
     CUtensorMap mAh, mAl, mBh, mBl;
     {
-        cuuint64_t dims[3] = {128, 128, 343};
-        cuuint64_t strides[2] = {128 * esz, 128 * 128 * esz};
-        cuuint32_t bx[3] = {ke, 128, 1};
+        cuuint64_t dims[3] = {(cuuint64_t)KPG, (cuuint64_t)ops.nr, 343};
+        cuuint64_t strides[2] = {KPG * esz, (cuuint64_t)KPG * ops.nr * esz};
+        cuuint32_t bx[3] = {ke, (cuuint32_t)ops.nr, 1};
         cuuint32_t es[3] = {1, 1, 1};
         if (enc(&mAh, dt, 3, const_cast<void*>(ops.hi), dims, strides, bx, es,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
@@ -659,14 +687,14 @@ int launch_m2l_tc(const TcOps& ops, const int* il_slots, int p, const float* M_l
     const int bnx = box[3], bny = box[4], bnz = box[5];
     const int XT = pick_XT(box);
     const int NV = 3 * XT;
-    const int T = pick_T(box);
+    const int T = pick_T(box, MT);
     if (T == 0) return -4;
     const int N = (NV + 15) / 16 * 16;  // MMA N (multiple of 16 for M = 128)
     {
-        cuuint64_t dims[5] = {128, (cuuint64_t)3 * Xp, (cuuint64_t)Xp, (cuuint64_t)Xp, 8};
-        cuuint64_t strides[4] = {128 * esz, (cuuint64_t)3 * Xp * 128 * esz,
-                                 (cuuint64_t)Xp * 3 * Xp * 128 * esz,
-                                 (cuuint64_t)Xp * Xp * 3 * Xp * 128 * esz};
+        const cuuint64_t row = (cuuint64_t)KPG * esz;
+        cuuint64_t dims[5] = {(cuuint64_t)KPG, (cuuint64_t)3 * Xp, (cuuint64_t)Xp, (cuuint64_t)Xp, 8};
+        cuuint64_t strides[4] = {row, (cuuint64_t)3 * Xp * row, (cuuint64_t)Xp * 3 * Xp * row,
+                                 (cuuint64_t)Xp * Xp * 3 * Xp * row};
         cuuint32_t bx[5] = {ke, (cuuint32_t)N, (cuuint32_t)(T + 2), 1, 1};  // y-window
         cuuint32_t es[5] = {1, 1, 1, 1, 1};
         if (enc(&mBh, dt, 5, (void*)ghi, dims, strides, bx, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -680,10 +708,12 @@ int launch_m2l_tc(const TcOps& ops, const int* il_slots, int p, const float* M_l
     }
     static PerDeviceOnce once;
     once([] {
-        cudaFuncSetAttribute(m2l_tc_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)TC_SMEM);
-        cudaFuncSetAttribute(m2l_tc_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)TC_SMEM);
+        cudaFuncSetAttribute(m2l_tc_kernel<false, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)tc_smem<1>());
+        cudaFuncSetAttribute(m2l_tc_kernel<true, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)tc_smem<1>());
+        cudaFuncSetAttribute(m2l_tc_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)tc_smem<2>());
     });
     TcParams P;
     P.nP = nP;
@@ -697,6 +727,7 @@ int launch_m2l_tc(const TcOps& ops, const int* il_slots, int p, const float* M_l
     P.bz0 = box[2];
     P.bny = bny;
     P.nc = nc;
+    P.nkc = nkc;
     P.level = level;
     P.slots = il_slots;
     P.L = L_l;
@@ -705,10 +736,12 @@ int launch_m2l_tc(const TcOps& ops, const int* il_slots, int p, const float* M_l
     P.T = T;
     P.groups = ops.groups;
     const unsigned grid = (unsigned)(8 * (P.rows / P.T));
-    if (f16)
-        m2l_tc_kernel<true><<<grid, TC_THREADS, TC_SMEM, st>>>(mAh, mAl, mBh, mBl, P);
+    if (f16 && MT == 2)
+        m2l_tc_kernel<true, 2><<<grid, TC_THREADS, tc_smem<2>(), st>>>(mAh, mAl, mBh, mBl, P);
+    else if (f16)
+        m2l_tc_kernel<true, 1><<<grid, TC_THREADS, tc_smem<1>(), st>>>(mAh, mAl, mBh, mBl, P);
     else
-        m2l_tc_kernel<false><<<grid, TC_THREADS, TC_SMEM, st>>>(mAh, mAl, mBh, mBl, P);
+        m2l_tc_kernel<false, 1><<<grid, TC_THREADS, tc_smem<1>(), st>>>(mAh, mAl, mBh, mBl, P);
     return 0;
 }
 

@@ -240,7 +240,10 @@ void store_tc(std::vector<float>& hi, std::vector<float>& lo, int slot,
 // has |Ahat| <= 1 and no overflow in half; hi = half(Ahat), lo = half(Ahat - hi)
 void store_h16(const std::vector<std::pair<int, std::vector<double>>>& ops, int nc, HostOps* out) {
     auto pow2_ceil = [](double v) { return v > 0 ? std::exp2(std::ceil(std::log2(v))) : 1.0; };
-    std::vector<double> cs(128, 1.0), rs(128, 1.0);
+    const int NRh = nc <= 128 ? 128 : 256, KPh = nc <= 128 ? 128 : (nc + 63) / 64 * 64;
+    out->h16_nr = NRh;
+    out->h16_kp = KPh;
+    std::vector<double> cs(KPh, 1.0), rs(NRh, 1.0);
     for (int k = 0; k < nc; ++k) {
         double m = 0;
         for (const auto& so : ops)
@@ -254,18 +257,18 @@ void store_h16(const std::vector<std::pair<int, std::vector<double>>>& ops, int 
                 m = std::max(m, std::fabs(so.second[(size_t)r * nc + k]) / cs[k]);
         rs[r] = pow2_ceil(m);
     }
-    out->m2l_h16_hi.assign((size_t)343 * 128 * 128, 0);
-    out->m2l_h16_lo.assign((size_t)343 * 128 * 128, 0);
+    out->m2l_h16_hi.assign((size_t)343 * NRh * KPh, 0);
+    out->m2l_h16_lo.assign((size_t)343 * NRh * KPh, 0);
     for (const auto& so : ops) {
-        uint16_t* H = out->m2l_h16_hi.data() + (size_t)so.first * 128 * 128;
-        uint16_t* Lo = out->m2l_h16_lo.data() + (size_t)so.first * 128 * 128;
+        uint16_t* H = out->m2l_h16_hi.data() + (size_t)so.first * NRh * KPh;
+        uint16_t* Lo = out->m2l_h16_lo.data() + (size_t)so.first * NRh * KPh;
         for (int r = 0; r < nc; ++r)
             for (int k = 0; k < nc; ++k) {
                 const double v = so.second[(size_t)r * nc + k] / (rs[r] * cs[k]);
                 const __half h = __double2half(v);
                 const __half l = __double2half(v - (double)__half2float(h));
-                memcpy(&H[(size_t)r * 128 + k], &h, 2);
-                memcpy(&Lo[(size_t)r * 128 + k], &l, 2);
+                memcpy(&H[(size_t)r * KPh + k], &h, 2);
+                memcpy(&Lo[(size_t)r * KPh + k], &l, 2);
             }
     }
     out->h16_rs.assign(rs.begin(), rs.end());
@@ -419,7 +422,8 @@ void build_host_ops(int p, int image_levels, HostOps* out) {
     out->l2l.assign(8 * msz, 0.f);
     out->m2l.assign(343 * msz, 0.f);
     out->per.assign(msz, 0.f);
-    const bool tc = nc <= 128;
+    const bool tc = nc <= 128;        // 3xTF32 operators
+    const bool h16 = nc <= 256;       // 3xFP16 operators (two row tiles above 128)
     out->m2l_tc_hi.assign(tc ? (size_t)343 * 128 * 128 : 0, 0.f);
     out->m2l_tc_lo.assign(tc ? (size_t)343 * 128 * 128 : 0, 0.f);
     std::vector<std::pair<int, std::vector<double>>> tc_ops;  // (slot, packed operator)
@@ -436,12 +440,10 @@ void build_host_ops(int p, int image_levels, HostOps* out) {
                 if (std::max(std::abs(ox), std::max(std::abs(oy), std::abs(oz))) <= 1) continue;
                 const auto T = pack_matrix(m2l_full(-ox, -oy, -oz, p), p);
                 store_t(out->m2l, m2l_slot(ox, oy, oz), T, nc, out->KP, out->NR);
-                if (tc) {
-                    store_tc(out->m2l_tc_hi, out->m2l_tc_lo, m2l_slot(ox, oy, oz), T, nc);
-                    tc_ops.emplace_back(m2l_slot(ox, oy, oz), T);
-                }
+                if (tc) store_tc(out->m2l_tc_hi, out->m2l_tc_lo, m2l_slot(ox, oy, oz), T, nc);
+                if (h16) tc_ops.emplace_back(m2l_slot(ox, oy, oz), T);
             }
-    if (tc) store_h16(tc_ops, nc, out);
+    if (h16) store_h16(tc_ops, nc, out);
     build_l2p_map(p, out);
     out->per_d = build_periodic(p, image_levels);
     store_t(out->per, 0, out->per_d, nc, out->KP, out->NR);

@@ -56,9 +56,11 @@ struct HostOps {
     // tensor-core M2L operands (nc <= 128): row-major [343][128 r][128 k], 3xTF32 split
     std::vector<float> m2l_tc_hi, m2l_tc_lo;
     // 3xFP16 split of the balanced operators Ahat = T / (rs[r] cs[k]) (rs, cs powers of 2,
-    // |Ahat| <= 1), IEEE half bit patterns, same layout
+    // |Ahat| <= 1), IEEE half bit patterns, row-major [343][h16_nr][h16_kp]: 128 x 128 for
+    // nc <= 128, else 256 rows x (64 ceil(nc / 64)) columns (p <= 15)
     std::vector<uint16_t> m2l_h16_hi, m2l_h16_lo;
-    std::vector<float> h16_rs, h16_cs;  // [128] row / column scales
+    std::vector<float> h16_rs, h16_cs;  // [h16_nr] row / [h16_kp] column scales
+    int h16_nr = 128, h16_kp = 128;
     // L2P: D[k][q] = sum_t coef[t] L[src[t]] for t in [rowptr[k 12 + q], rowptr[k 12 + q + 1]),
     // src indexing the 3 nc packed coefficients of a leaf (q: curl psi 3, grad u 9; k < p^2);
     // rows padded to multiples of 4 terms with zeros (uploaded as 32-bit terms: src in the low
@@ -134,13 +136,14 @@ struct TcOps {
     const float* cs = nullptr; // f16: column scales [128]
     const int4* groups = nullptr;  // [8][72] offset groups per target parity (m2l_groups)
     bool f16 = false;
+    int nr = 128, kp = 128;  // operator layout [343][nr][kp] (f16 with (p+1)^2 > 128: 256 rows)
 };
 // The 189 M2L offsets of target parity pi grouped by (source parent dx, dz, source parity):
 // entry [pi][((dx+1) 3 + (dz+1)) 8 + pis] = {mask (bit dy+1 set if offset (dx, dy, dz, pis) is
 // in the list) | (dx+1) << 4 | (dz+1) << 6 | pis << 8, slot(dy=-1), slot(0), slot(1)}
 std::vector<int> m2l_groups();
 bool m2l_tc_supported(int p, int level);
-bool m2l_tc_shape_ok(const int box[6]);
+bool m2l_tc_shape_ok(const int box[6], int p);
 size_t m2l_tc_grid_floats(int level);
 // maxbits: one zeroed uint32 per launch (f16: the level's max |cs[k] M_k|, as float bits)
 int launch_m2l_tc(const TcOps& ops, const int* il_slots, int p, const float* M_l, float* L_l,

@@ -168,6 +168,22 @@ def test_clustered_field_vs_direct():
     ev.close()
 
 
+def test_north_star_accuracy_p13_27cubed_vs_direct():
+    """north_star: u within 1e-5 of the direct sum (and sdot within 3e-5) at the benched image
+    count.  With the uniform ws = 1 tree that takes p = 13 ((p+1)^2 = 196: the tcgen05 M2L with
+    two 128-row output tiles); isotropic 32^3, depth 3, 27^3 images, against O1."""
+    f = synthgen.isotropic(32, seed=12)
+    tg = synthgen.sample_targets(32 ** 3, 48, n_lattice=32)
+    vo, so = oracle.direct(f.pos, f.gamma, f.sigma, f.box_lo, f.box_len, 3, 0, targets=tg,
+                           batched=True)
+    v, s, ev = run(f, p=13, depth=3, image_levels=3)
+    eu, es = rel(v[:, tg], vo), rel(s[:, tg], so)
+    print(f"iso32 lambda=3 p=13 (tc f16, 2 row tiles): u {eu:.2e} sdot {es:.2e}")
+    tu, ts = TOL.FMM_VS_DIRECT[13]
+    assert eu < tu and es < ts, (eu, es)
+    ev.close()
+
+
 def test_periodic_27cubed_images_vs_direct():
     """The benched image count (27^3 boxes, image_levels = 3) against O1
     over the same cube, isotropic 32^3, p = 10, depth 3.  On this field O1 at lambda = 2 differs
@@ -472,6 +488,7 @@ def test_bench_config_vs_golden_o1_27cubed(cfg):
 
 @pytest.mark.parametrize("engine", ["simt", "f16", "tf32"])
 @pytest.mark.parametrize("n,depth,p,lam", [(32, 3, 10, 1), (32, 3, 6, 3), (64, 4, 8, 1),
+                                           (16, 2, 13, 2), (16, 2, 15, 1),
                                            pytest.param(64, 5, 10, 3, marks=pytest.mark.slow)])
 def test_m2l_engines_vs_fp64_fmm_oracle(n, depth, p, lam, engine, monkeypatch):
     """Every M2L engine -- SIMT FP32, tcgen05 scaled 3xFP16 (default), tcgen05 3xTF32 -- against

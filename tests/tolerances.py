@@ -13,6 +13,9 @@ FMM_VS_DIRECT = {  # p: (velocity, stretching)
     6: (2.5e-3, 1e-2),
     8: (8e-4, 2e-3),
     10: (1e-4, 3e-4),
+    # north_star's "<= 1e-5 at p = 10" is reached at p = 13 with ws = 1 (fp64 FMM oracle on the
+    # isotropic 32^3 field at 27^3 images: 3.7e-6 / 1.8e-5; p = 12: 9.0e-6 / 4.0e-5)
+    13: (1e-5, 3e-5),
 }
 FMM_VS_FMM_ORACLE = (2e-5, 5e-5)
 DIRECT_VS_ORACLE = (2e-6, 5e-6)
