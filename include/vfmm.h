@@ -44,7 +44,7 @@ typedef struct vfmm_ctx vfmm_ctx; /* opaque: workspace, operator tables, streams
 typedef enum {
     VFMM_OK = 0,
     VFMM_EINVAL = -1,  /* bad parameter: n < 1, p < 1 or p > VFMM_PMAX, sigma <= 0 or not
-                          finite, depth out of [1, 10], image_levels out of [0, 6], box_len <= 0,
+                          finite, depth out of [-1, 10], image_levels out of [0, 6], box_len <= 0,
                           NULL pointer, aliasing outputs */
     VFMM_EDOMAIN = -2, /* device-detected (sticky until vfmm_sync_status): a position outside
                           [lo, lo+len)^3 or a non-finite input; outputs are unspecified then */
@@ -72,7 +72,10 @@ typedef struct {
     int32_t p;            /* expansion order: degrees n = 0..p, (p+1)^2 coefficients per
                              component (PAPER.md:123 Eq. 10; paper default p = 10, :163)       */
     int32_t depth;        /* uniform octree depth L >= 1: 8^L leaves ("number of
-                             levels"); 0 = auto (about 64 particles per leaf)                  */
+                             levels"); 0 = auto (about 64 particles per leaf); -1 = tuned: the
+                             first evaluate of a new n times the auto depth and its two
+                             neighbours and keeps the fastest ("automatically choosing the
+                             number of particles per box")                    */
     int32_t image_levels; /* 0 = free space; k >= 1: image cube {-m..m}^3, m = (3^k - 1)/2;
                              k = 3 gives the paper's 27^3 boxes           */
     int32_t scheme;       /* vfmm_scheme                                                       */

@@ -89,6 +89,11 @@ struct vfmm_ctx {
     // last evaluate
     cudaStream_t last_stream = nullptr;
     bool have_last = false;  // ev[NEV-1] marks the end of an earlier evaluate
+    // depth = -1: depth chosen by timing ("automatically choosing the number
+    // of particles per box"), cached per (n, p, mode, image_levels)
+    int64_t tuned_n = -1;
+    int tuned_p = -1, tuned_mode = -1, tuned_levels = -1, tuned_depth = 0;
+    float tuned_ms[3] = {0, 0, 0};
     uint32_t *keys_sorted = nullptr, *perm = nullptr;
     int64_t last_n = 0;
     int last_depth = 0;
@@ -162,7 +167,7 @@ bool finite_pos(float x) { return std::isfinite(x) && x > 0.f; }
 vfmm_status validate(const vfmm_params* p) {
     if (!p) return VFMM_EINVAL;
     if (p->p < 1 || p->p > VFMM_PMAX) return VFMM_EINVAL;
-    if (p->depth < 0 || p->depth > 10) return VFMM_EINVAL;
+    if (p->depth < -1 || p->depth > 10) return VFMM_EINVAL;
     if (p->image_levels < 0 || p->image_levels > 6) return VFMM_EINVAL;
     if (p->scheme != 0 && p->scheme != 1) return VFMM_EINVAL;
     if (p->mode < 0 || p->mode > 3) return VFMM_EINVAL;
@@ -749,7 +754,53 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
         c->have_exp = false;
         return VFMM_OK;
     }
-    const int depth = P.depth > 0 ? P.depth : auto_depth(P, n);
+    if (P.depth == -1 && !(c->tuned_n == n && c->tuned_p == P.p && c->tuned_mode == P.mode &&
+                           c->tuned_levels == P.image_levels)) {
+        // time the default depth and its two neighbours once (the paper's auto-tuning picks
+        // the particles per box by measurement), keep the fastest
+        const int L0 = auto_depth(P, n);
+        float best = 1e30f;
+        int bestL = L0;
+        cudaEvent_t t0, t1;
+        CK(cudaEventCreate(&t0), "event");
+        CK(cudaEventCreate(&t1), "event");
+        for (int k = 0; k < 3; ++k) {
+            const int L = L0 - 1 + k;
+            c->tuned_ms[k] = 0.f;
+            if (L < 1 || L > 10) continue;
+            if ((double)P.box_len / (double)(1 << L) < 4.0 * (double)P.sigma * (1.0 - 1e-6)) continue;
+            if (((int64_t)1 << (3 * L)) > 64 * n + 8) continue;  // hardly any particle per leaf
+            c->prm.depth = L;
+            vfmm_status s0 = vfmm_evaluate(c, n, pos, gamma, vel, dgamma, stream);  // warm-up
+            if (s0 == VFMM_OK) {
+                cudaEventRecord(t0, st);
+                s0 = vfmm_evaluate(c, n, pos, gamma, vel, dgamma, stream);
+                cudaEventRecord(t1, st);
+            }
+            c->prm.depth = -1;
+            if (s0 != VFMM_OK) {
+                cudaEventDestroy(t0);
+                cudaEventDestroy(t1);
+                return s0;
+            }
+            CK(cudaEventSynchronize(t1), "sync");
+            float ms = 0.f;
+            cudaEventElapsedTime(&ms, t0, t1);
+            c->tuned_ms[k] = ms;
+            if (ms < best) {
+                best = ms;
+                bestL = L;
+            }
+        }
+        cudaEventDestroy(t0);
+        cudaEventDestroy(t1);
+        c->tuned_n = n;
+        c->tuned_p = P.p;
+        c->tuned_mode = P.mode;
+        c->tuned_levels = P.image_levels;
+        c->tuned_depth = bestL;
+    }
+    const int depth = P.depth > 0 ? P.depth : (P.depth == -1 ? c->tuned_depth : auto_depth(P, n));
     vfmm_status s = ensure_ws(c, n, depth);
     if (s != VFMM_OK) return s;
     c->last_depth = depth;

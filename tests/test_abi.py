@@ -42,7 +42,7 @@ def test_create_rejects_bad_params_without_touching_the_gpu():
     L = vf.load_library()
     ctx = ctypes.c_void_p()
     for bad in (dict(p=0), dict(p=17), dict(sigma=0.0), dict(sigma=float("nan")),
-                dict(depth=11), dict(image_levels=7), dict(scheme=2), dict(mode=9),
+                dict(depth=11), dict(depth=-2), dict(image_levels=7), dict(scheme=2), dict(mode=9),
                 dict(box_len=-1.0)):
         prm = vf.Params(**bad).to_c()
         assert L.vfmm_create(ctypes.byref(ctx), ctypes.byref(prm), 0) == vf.VFMM_EINVAL

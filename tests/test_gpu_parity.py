@@ -325,6 +325,25 @@ def test_auto_depth_matches_explicit():
     ev1.close()
 
 
+def test_tuned_depth_is_timed_and_consistent():
+    """depth = -1: the first evaluate of a new N times the auto depth and its neighbours and
+    keeps the fastest (PAPER.md:152 "automatically choosing the number of particles per box");
+    the result equals an explicit evaluation at the chosen depth, and the choice is cached."""
+    f = synthgen.isotropic(64, seed=4)
+    v0, s0, ev0 = run(f, p=6, depth=-1, image_levels=2)
+    L = ev0.stats()["depth_used"]
+    assert L in (3, 4, 5)
+    v1, s1, ev1 = run(f, p=6, depth=L, image_levels=2)
+    assert np.array_equal(v0, v1) and np.array_equal(s0, s1)
+    pos = torch.from_numpy(f.pos).to(DEV)
+    gam = torch.from_numpy(f.gamma).to(DEV)
+    ev0.evaluate(pos, gam)
+    assert ev0.stats()["depth_used"] == L
+    print(f"tuned depth for 64^3 at p = 6: {L}")
+    ev0.close()
+    ev1.close()
+
+
 @pytest.mark.parametrize("engine", ["f16", "simt"])
 def test_evaluation_is_deterministic(engine, monkeypatch):
     """No atomics on the value path (op splits reduce partials in a fixed order): two
