@@ -57,6 +57,8 @@ struct vfmm_ctx {
     float *g2_hi = nullptr, *g2_lo = nullptr;      // staging for the side stream (levels < L)
     size_t g2_cap = 0;
     cudaStream_t side = nullptr;                   // coarse M2L levels run here, joined by events
+    cudaStream_t far_st = nullptr;  // co-resident mode: the far-field chain (high priority)
+    cudaEvent_t ev_tree = nullptr, ev_far = nullptr;
     cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
     cudaEvent_t ev_gamma = nullptr;  // evaluate_host: strengths copied on the side stream
     bool gamma_pending = false;      // the next evaluate waits for ev_gamma before the gather
@@ -609,6 +611,10 @@ vfmm_status vfmm_create(vfmm_ctx** out, const vfmm_params* prm, int device) {
         if (e2 == cudaSuccess) e2 = cudaDeviceGetStreamPriorityRange(&prio_least, &prio_greatest);
         if (e2 == cudaSuccess)
             e2 = cudaStreamCreateWithPriority(&c->side, cudaStreamNonBlocking, prio_greatest);
+        if (e2 == cudaSuccess)
+            e2 = cudaStreamCreateWithPriority(&c->far_st, cudaStreamNonBlocking, prio_greatest);
+        if (e2 == cudaSuccess) e2 = cudaEventCreateWithFlags(&c->ev_tree, cudaEventDisableTiming);
+        if (e2 == cudaSuccess) e2 = cudaEventCreateWithFlags(&c->ev_far, cudaEventDisableTiming);
         if (e2 == cudaSuccess) e2 = cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming);
         if (e2 == cudaSuccess) e2 = cudaEventCreateWithFlags(&c->ev_join, cudaEventDisableTiming);
         if (e2 == cudaSuccess) e2 = cudaEventCreateWithFlags(&c->ev_gamma, cudaEventDisableTiming);
@@ -831,34 +837,52 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
     const HostOps& H = c->hops;
     auto Mlev = [&](int l) { return c->Mall + level_offset(l) * 3 * nc; };
     auto Llev = [&](int l) { return c->Lall + level_offset(l) * 3 * nc; };
+    // Co-resident mode (VFMM_CORES=1): the near field (FP32 pipe) runs on the caller's stream
+    // concurrently with the far-field chain (tensor pipe) on a high-priority stream; the lean
+    // kernel variants (P2P 61.5 KB, tcgen05 M2L 161 KB / 192 threads) let one block of each
+    // share an SM.  Otherwise everything runs in sequence on the caller's stream.
+    const char* cores_env = getenv("VFMM_CORES");
+    const bool cores = cores_env && cores_env[0] == '1' && use_far && use_near;
+    cudaStream_t fs = st;  // stream of the far-field chain
+    if (cores) {
+        CK(cudaEventRecord(c->ev_tree, st), "event");
+        CK(cudaStreamWaitEvent(c->far_st, c->ev_tree, 0), "fork far field");
+        fs = c->far_st;
+        CK(cudaMemsetAsync(c->d_pairs, 0, sizeof(unsigned long long), st), "memset pairs");
+        launch_p2p(c->sorted6, n, c->leaf_start, depth, a, P.image_levels > 0, P.scheme, kc,
+                   c->near6, c->d_pairs, 0, (int64_t)1 << (3 * (depth - 1)), st, true);
+        ++nl;
+        CK(cudaGetLastError(), "p2p kernel");
+    }
     // ---- upward pass ----
     if (use_far) {
         launch_p2m(c->sorted6, n, c->leaf_start, p, 1.f / a, Mlev(depth), 0,
-                   (int64_t)1 << (3 * depth), st);
+                   (int64_t)1 << (3 * depth), fs);
         ++nl;
     }
     CK(cudaEventRecord(c->ev[4], st), "event");
     if (use_far) {
         for (int l = depth - 1; l >= 0; --l) {
             nl += launch_m2m(c->d_m2m, p, H.KP, H.NR, Mlev(l + 1), Mlev(l), l, 0,
-                             (int64_t)1 << (3 * l), c->m2m_scratch, c->m2m_scratch_floats, st);
+                             (int64_t)1 << (3 * l), c->m2m_scratch, c->m2m_scratch_floats, fs);
             S.n_m2m += (int64_t)8 << (3 * l);
         }
         CK(cudaGetLastError(), "upward kernels");
     }
-    CK(cudaEventRecord(c->ev[5], st), "event");
+    CK(cudaEventRecord(c->ev[5], fs), "event");
     // ---- M2L at every level (writes L_l), then periodic images + L2L top-down (adds) ----
     // The levels are independent: levels 1..L-1 (few CTAs each, latency bound) and the
     // periodic-image operator run on a side stream concurrently with level L (fork/join by
     // events), each stream with its own tensor-core staging buffer.
     if (use_far) {
-        const TcOps tco = tc_ops(c);
+        TcOps tco = tc_ops(c);
+        tco.lean = cores;
         const bool allow_tc = m2l_env_mode() != 0 && tco.hi;
-        CK(cudaMemsetAsync(c->d_tcmax, 0, 32 * sizeof(uint32_t), st), "memset tc max");
-        CK(cudaEventRecord(c->ev_fork, st), "fork");
+        CK(cudaMemsetAsync(c->d_tcmax, 0, 32 * sizeof(uint32_t), fs), "memset tc max");
+        CK(cudaEventRecord(c->ev_fork, fs), "fork");
         CK(cudaStreamWaitEvent(c->side, c->ev_fork, 0), "fork");
         for (int l = depth; l >= 1; --l) {
-            cudaStream_t sl = l == depth ? st : c->side;
+            cudaStream_t sl = l == depth ? fs : c->side;
             float** ghi = l == depth ? &c->g_hi : &c->g2_hi;
             float** glo = l == depth ? &c->g_lo : &c->g2_lo;
             size_t* gcap = l == depth ? &c->g_cap : &c->g2_cap;
@@ -897,24 +921,28 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
             CK(cudaMemsetAsync(Llev(0), 0, 3 * nc * sizeof(float), c->side), "memset L0");
         }
         CK(cudaEventRecord(c->ev_join, c->side), "join");
-        CK(cudaStreamWaitEvent(st, c->ev_join, 0), "join");
+        CK(cudaStreamWaitEvent(fs, c->ev_join, 0), "join");
         CK(cudaGetLastError(), "m2l kernels");
     }
-    CK(cudaEventRecord(c->ev[6], st), "event");
+    CK(cudaEventRecord(c->ev[6], fs), "event");
     if (use_far) {
         for (int l = 1; l <= depth; ++l) {
             launch_l2l(c->d_l2l, p, H.KP, H.NR, Llev(l - 1), Llev(l), l, 0,
-                       (int64_t)1 << (3 * (l - 1)), st);
+                       (int64_t)1 << (3 * (l - 1)), fs);
             ++nl;
             S.n_l2l += (int64_t)1 << (3 * l);
         }
         CK(cudaGetLastError(), "downward kernels");
         c->have_exp = true;
     }
-    CK(cudaEventRecord(c->ev[7], st), "event");
+    CK(cudaEventRecord(c->ev[7], fs), "event");
+    if (cores) {  // join the far-field chain
+        CK(cudaEventRecord(c->ev_far, fs), "event");
+        CK(cudaStreamWaitEvent(st, c->ev_far, 0), "join far field");
+    }
     if (getenv("VFMM_DEBUG_SYNC")) CK(cudaStreamSynchronize(st), "debug sync");
     // ---- near field ----
-    if (use_near) {
+    if (use_near && !cores) {
         CK(cudaMemsetAsync(c->d_pairs, 0, sizeof(unsigned long long), st), "memset pairs");
         launch_p2p(c->sorted6, n, c->leaf_start, depth, a, P.image_levels > 0, P.scheme, kc,
                    c->near6, c->d_pairs, 0, (int64_t)1 << (3 * (depth - 1)), st);
@@ -1454,6 +1482,9 @@ void vfmm_destroy(vfmm_ctx* c) {
     if (c->comm_st) cudaStreamDestroy(c->comm_st);
     if (c->own_stream) cudaStreamDestroy(c->own_stream);
     if (c->side) cudaStreamDestroy(c->side);
+    if (c->far_st) cudaStreamDestroy(c->far_st);
+    if (c->ev_tree) cudaEventDestroy(c->ev_tree);
+    if (c->ev_far) cudaEventDestroy(c->ev_far);
     if (c->ev_fork) cudaEventDestroy(c->ev_fork);
     if (c->ev_join) cudaEventDestroy(c->ev_join);
     if (c->ev_gamma) cudaEventDestroy(c->ev_gamma);

@@ -59,13 +59,21 @@ template <int MT> __host__ __device__ constexpr int a_bytes() { return MT * A_TI
 // max window rows (T + 2) N: MT = 1 up to 288 rows (36 KB), MT = 2 up to 192 (24 KB)
 template <int MT> __host__ __device__ constexpr int b_wrows() { return MT == 1 ? 288 : 192; }
 template <int MT> __host__ __device__ constexpr int b_bytes() { return b_wrows<MT>() * 128; }
-constexpr int TC_EPI_WARPS = 8;  // 2 per TMEM lane quarter: warp pair splits the T tiles
-constexpr int TC_THREADS = 64 + 32 * TC_EPI_WARPS;
-template <int MT>
+// Epilogue warps: 8 (2 per TMEM lane quarter, the warp pair splits the T tiles) or, in the
+// LEAN variant, 4 (one per quarter, T = 2 row tiles of N = 48: 96 columns each) with 192-row
+// y-windows -- 161 KB of shared memory and 192 threads, so one P2P block (62 KB) fits beside
+// it on the same SM (tensor pipe and FP32 pipe busy at once, capi.cu "co-resident mode")
+template <bool LEAN> __host__ __device__ constexpr int tc_epi() { return LEAN ? 4 : 8; }
+template <bool LEAN> __host__ __device__ constexpr int tc_threads() { return 64 + 32 * tc_epi<LEAN>(); }
+template <int MT, bool LEAN = false> __host__ __device__ constexpr int b_bytes_v() {
+    return LEAN ? 192 * 128 : b_bytes<MT>();
+}
+template <int MT, bool LEAN = false>
 constexpr size_t tc_smem() {
-    return 1024 + (size_t)TC_AST * 2 * a_bytes<MT>() + (size_t)TC_BST * 2 * b_bytes<MT>() + 512;
+    return 1024 + (size_t)TC_AST * 2 * a_bytes<MT>() + (size_t)TC_BST * 2 * b_bytes_v<MT, LEAN>() + 512;
 }
 static_assert(tc_smem<2>() <= 232448, "MT = 2 stages exceed 227 KB");
+static_assert(tc_smem<1, true>() <= 166 * 1024, "LEAN stages exceed 166 KB");
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
     return (uint32_t)__cvta_generic_to_shared(p);
@@ -225,15 +233,15 @@ __device__ __forceinline__ void group_rows(const TcParams& P, int g, int* tx, in
     *pz = P.bz0 + gz;
 }
 
-template <bool F16, int MT>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
+template <bool F16, int MT, bool LEAN = false>
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc_threads<LEAN>(), 1)
     m2l_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant__ CUtensorMap tmA_lo,
                   const __grid_constant__ CUtensorMap tmB_hi, const __grid_constant__ CUtensorMap tmB_lo,
                   TcParams P) {
     extern __shared__ uint8_t tc_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>(((uintptr_t)tc_raw + 1023) & ~(uintptr_t)1023);
     uint8_t* Abuf = sm;                                  // [AST][hi|lo][16 KB]
-    constexpr int A_BYTES = a_bytes<MT>(), B_BYTES = b_bytes<MT>();
+    constexpr int A_BYTES = a_bytes<MT>(), B_BYTES = b_bytes_v<MT, LEAN>();
     uint8_t* Bbuf = sm + TC_AST * 2 * A_BYTES;           // [BST][hi|lo][B_BYTES]
     uint64_t* bars = reinterpret_cast<uint64_t*>(Bbuf + TC_BST * 2 * B_BYTES);
     uint64_t* a_full = bars;
@@ -267,7 +275,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&acc_full[i], 1);
-            mbar_init(&acc_empty[i], TC_EPI_WARPS);
+            mbar_init(&acc_empty[i], tc_epi<LEAN>());
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
@@ -362,9 +370,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
                     const uint64_t ahi = sw128_desc(Abuf + (sa * 2 + 0) * A_BYTES);
                     const uint64_t alo = sw128_desc(Abuf + (sa * 2 + 1) * A_BYTES);
                     const uint64_t bsh = (uint64_t)dd * slab_step;
+                    // K steps holding real coefficients: the last chunk of a padded K
+                    // (e.g. (p+1)^2 = 196 in 4 chunks of 64) skips its all-zero steps
+                    const int kleft = P.nc - kc * tc_ke<F16>();
+                    const int nks = min(4, (kleft + tc_ke<F16>() / 4 - 1) / (tc_ke<F16>() / 4));
                     if (lane == 0) {
 #pragma unroll
                         for (int ks = 0; ks < 4; ++ks) {  // K = 8 tf32 / 16 f16 = 32 B per MMA
+                            if (ks >= nks) break;
                             const uint64_t adv = (uint64_t)(ks * 2);
                             const uint32_t acc = ks == 0 ? 0u : 1u;
 #pragma unroll
@@ -404,8 +417,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
         // ===================== epilogue: TMEM groups -> FP32 register sums -> L =====================
         const int e = warp - 2;
         const int quarter = warp & 3;  // TMEM lanes [32 quarter, 32 quarter + 32)
-        const int half = e >> 2;       // this warp owns tiles [half T/2, (half+1) T/2)
-        const int ncol = (P.T / 2) * P.N;  // columns per warp and row tile: MT * ncol <= 96
+        const int half = LEAN ? 0 : e >> 2;  // this warp owns tiles [half T/2, (half+1) T/2)
+        const int tpw = LEAN ? P.T : P.T / 2;  // tiles per warp
+        const int ncol = tpw * P.N;    // columns per warp and row tile: MT * ncol <= 96
         const int col0 = half * ncol;
         const int r = quarter * 32 + lane;
         // each finished chain (one offset x one K chunk, <= 12 MMAs per row tile: truncating TMEM
@@ -479,7 +493,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(TC_THREADS, 1)
                 for (int jj = 0; jj < 96 / MT; ++jj) {
                     if (jj < ncol) {
                         const int j = mt * (96 / MT) + jj;
-                        const int t = half * (P.T / 2) + jj / P.N, cj = jj % P.N;
+                        const int t = half * tpw + jj / P.N, cj = jj % P.N;
                         if (cj < P.NV) {
                             const int py = gpy0 + t;
                             const int px = P.bx0 + gtx * P.XT + cj / 3, comp = cj % 3;
@@ -606,15 +620,16 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 // and (T + 2) N within the window stage, T | bny and an even number of CTAs (2-CTA clusters);
 // 0 if none
 static int pick_XT(const int box[6]) { return box[3] < 16 ? box[3] : 16; }
-static int pick_T(const int box[6], int MT) {
+static int pick_T(const int box[6], int MT, bool lean = false) {
     const int bnx = box[3], bny = box[4], bnz = box[5];
     const int XT = pick_XT(box);
     if (bnx % XT != 0) return 0;
     const int N = (3 * XT + 15) / 16 * 16;
     const int rows = bny * bnz * (bnx / XT);
-    const int wrows = MT == 1 ? b_wrows<1>() : b_wrows<2>();
+    const int wrows = lean ? 192 : (MT == 1 ? b_wrows<1>() : b_wrows<2>());
+    const int maxcols = lean ? 96 : 192;  // columns one epilogue warp set covers
     for (int T = 8; T >= 2; T /= 2)
-        if (MT * T * N <= (MT == 1 ? 192 : 256) && T * N <= 192 && (T + 2) * N <= wrows &&
+        if (MT * T * N <= (MT == 1 ? 192 : 256) && T * N <= maxcols && (T + 2) * N <= wrows &&
             bny % T == 0 && (rows / T) % 2 == 0)
             return T;
     return 0;
@@ -687,7 +702,8 @@ int launch_m2l_tc(const TcOps& ops, const int* il_slots, int p, const float* M_l
     const int bnx = box[3], bny = box[4], bnz = box[5];
     const int XT = pick_XT(box);
     const int NV = 3 * XT;
-    const int T = pick_T(box, MT);
+    const bool lean = ops.lean && MT == 1 && f16 && pick_T(box, 1, true) != 0;
+    const int T = pick_T(box, MT, lean);
     if (T == 0) return -4;
     const int N = (NV + 15) / 16 * 16;  // MMA N (multiple of 16 for M = 128)
     {
@@ -714,6 +730,8 @@ int launch_m2l_tc(const TcOps& ops, const int* il_slots, int p, const float* M_l
                              (int)tc_smem<1>());
         cudaFuncSetAttribute(m2l_tc_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)tc_smem<2>());
+        cudaFuncSetAttribute(m2l_tc_kernel<true, 1, true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem<1, true>());
     });
     TcParams P;
     P.nP = nP;
@@ -737,11 +755,14 @@ int launch_m2l_tc(const TcOps& ops, const int* il_slots, int p, const float* M_l
     P.groups = ops.groups;
     const unsigned grid = (unsigned)(8 * (P.rows / P.T));
     if (f16 && MT == 2)
-        m2l_tc_kernel<true, 2><<<grid, TC_THREADS, tc_smem<2>(), st>>>(mAh, mAl, mBh, mBl, P);
+        m2l_tc_kernel<true, 2><<<grid, tc_threads<false>(), tc_smem<2>(), st>>>(mAh, mAl, mBh, mBl, P);
+    else if (lean)
+        m2l_tc_kernel<true, 1, true><<<grid, tc_threads<true>(), tc_smem<1, true>(), st>>>(
+            mAh, mAl, mBh, mBl, P);
     else if (f16)
-        m2l_tc_kernel<true, 1><<<grid, TC_THREADS, tc_smem<1>(), st>>>(mAh, mAl, mBh, mBl, P);
+        m2l_tc_kernel<true, 1><<<grid, tc_threads<false>(), tc_smem<1>(), st>>>(mAh, mAl, mBh, mBl, P);
     else
-        m2l_tc_kernel<false, 1><<<grid, TC_THREADS, tc_smem<1>(), st>>>(mAh, mAl, mBh, mBl, P);
+        m2l_tc_kernel<false, 1><<<grid, tc_threads<false>(), tc_smem<1>(), st>>>(mAh, mAl, mBh, mBl, P);
     return 0;
 }
 

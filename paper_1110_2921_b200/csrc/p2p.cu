@@ -305,8 +305,10 @@ __device__ __forceinline__ uint32_t compact3p(uint32_t v) {
 constexpr int P2P_THREADS = 256;
 // sources per pass at 2 blocks / SM: 24 B per source (x y z gx | gy gz) or, with the staged
 // cross products, 36 B (x y z gx | gy gz sx sy | sz)
+// MINB = 1: the lean variant (2 blocks / SM on their own, 2560 sources = 61.5 KB of shared
+// memory so one block fits beside a lean tensor-core M2L block, capi.cu co-resident mode)
 template <bool SJ, int MINB = 2> constexpr int p2p_cap() {
-    return MINB >= 3 ? (SJ ? 1920 : 2816) : (SJ ? 3072 : 4352);
+    return MINB == 1 ? (SJ ? 1664 : 2560) : MINB >= 3 ? (SJ ? 1920 : 2816) : (SJ ? 3072 : 4352);
 }
 constexpr int P2P_PAD = 4;     // slack after each staged array (keeps the arrays 16-byte aligned)
 
@@ -314,7 +316,7 @@ constexpr int P2P_PAD = 4;     // slack after each staged array (keeps the array
 // 38 instead of 41 FP32 instructions per pair, rounding ~1.4x larger since the sums carry
 // |x_j| instead of |d|); otherwise the per-pair cross product gamma_j x d
 template <int SCHEME, bool SJ, int MINB = 2, int UNR = 2>
-__global__ void __launch_bounds__(P2P_THREADS, MINB) p2p_kernel(
+__global__ void __launch_bounds__(P2P_THREADS, MINB == 1 ? 2 : MINB) p2p_kernel(
     const float* __restrict__ s6, int64_t n, const int* __restrict__ leaf_start, int depth,
     float a, int periodic, KernelConsts kc, float* __restrict__ near6,
     unsigned long long* __restrict__ npairs, int64_t plo) {
@@ -640,7 +642,8 @@ void p2p_go(const float* sorted6, int64_t n, const int* leaf_start, int depth, f
 
 void launch_p2p(const float* sorted6, int64_t n, const int* leaf_start, int depth, float a,
                 int periodic, int scheme, KernelConsts kc, float* near6,
-                unsigned long long* npairs, int64_t plo, int64_t pcnt, cudaStream_t st) {
+                unsigned long long* npairs, int64_t plo, int64_t pcnt, cudaStream_t st,
+                bool lean) {
     if (pcnt <= 0) return;
     // default: per-pair cross products gamma_j x d (FP32-faithful rounding); VFMM_P2P=sj: the
     // classical scheme with staged source cross products (~3% faster at c4, 2-4x the rounding).
@@ -653,6 +656,9 @@ void launch_p2p(const float* sorted6, int64_t n, const int* leaf_start, int dept
 #define P2P_ARGS sorted6, n, leaf_start, depth, a, periodic, kc, near6, npairs, plo, pcnt, st
     if (scheme == 0 && sj) {
         p2p_go<0, true, 2, 2>(P2P_ARGS);
+    } else if (lean) {
+        if (scheme == 0) p2p_go<0, false, 1, 2>(P2P_ARGS);
+        else p2p_go<1, false, 1, 2>(P2P_ARGS);
     } else if (scheme == 0) {
         if (v == 1) p2p_go<0, false, 3, 1>(P2P_ARGS);
         else if (v == 2) p2p_go<0, false, 3, 2>(P2P_ARGS);

@@ -137,6 +137,7 @@ struct TcOps {
     const int4* groups = nullptr;  // [8][72] offset groups per target parity (m2l_groups)
     bool f16 = false;
     int nr = 128, kp = 128;  // operator layout [343][nr][kp] (f16 with (p+1)^2 > 128: 256 rows)
+    bool lean = false;       // f16, (p+1)^2 <= 128: the 161 KB / 192-thread variant (T = 2)
 };
 // The 189 M2L offsets of target parity pi grouped by (source parent dx, dz, source parity):
 // entry [pi][((dx+1) 3 + (dz+1)) 8 + pis] = {mask (bit dy+1 set if offset (dx, dy, dz, pis) is
@@ -170,7 +171,8 @@ struct KernelConsts {
 KernelConsts make_kernel_consts(float sigma);
 void launch_p2p(const float* sorted6, int64_t n, const int* leaf_start, int depth, float a,
                 int periodic, int scheme, KernelConsts kc, float* near6,
-                unsigned long long* npairs, int64_t plo, int64_t pcnt, cudaStream_t st);
+                unsigned long long* npairs, int64_t plo, int64_t pcnt, cudaStream_t st,
+                bool lean = false);
 // rbf.cu (reinitialization): Gaussian sums over the ws-neighbour leaves, BLAS-1 for GMRES
 void launch_gauss(const float* t6, int64_t nt, const int* tls, const float* s6, int64_t ns,
                   const int* sls, const float* sg, int depth, float a, int periodic, int ws,

@@ -325,6 +325,23 @@ def test_auto_depth_matches_explicit():
     ev1.close()
 
 
+def test_coresident_mode_matches_sequential(monkeypatch):
+    """VFMM_CORES=1: P2P on the caller's stream concurrently with the far-field chain on a
+    high-priority stream, both in their lean variants (one block of each per SM): the same
+    result as the sequential pipeline up to the P2P's FP32 summation order (its staging windows
+    are smaller), the tensor-core M2L bitwise unchanged."""
+    f = synthgen.isotropic(32, seed=14)
+    v0, s0, ev0 = run(f, p=10, depth=3, image_levels=3)
+    L0 = ev0.debug_expansions(1, 3)
+    monkeypatch.setenv("VFMM_CORES", "1")
+    v1, s1, ev1 = run(f, p=10, depth=3, image_levels=3)
+    L1 = ev1.debug_expansions(1, 3)
+    assert np.array_equal(L0, L1)
+    assert rel(v1, v0) < 1e-6 and rel(s1, s0) < 1e-6, (rel(v1, v0), rel(s1, s0))
+    ev0.close()
+    ev1.close()
+
+
 def test_tuned_depth_is_timed_and_consistent():
     """depth = -1: the first evaluate of a new N times the auto depth and its neighbours and
     keeps the fastest (PAPER.md:152 "automatically choosing the number of particles per box");
