@@ -627,11 +627,14 @@ static int pick_T(const int box[6], int MT, bool lean = false) {
     const int N = (3 * XT + 15) / 16 * 16;
     const int rows = bny * bnz * (bnx / XT);
     const int wrows = lean ? 192 : (MT == 1 ? b_wrows<1>() : b_wrows<2>());
-    const int maxcols = lean ? 96 : 192;  // columns one epilogue warp set covers
-    for (int T = 8; T >= 2; T /= 2)
-        if (MT * T * N <= (MT == 1 ? 192 : 256) && T * N <= maxcols && (T + 2) * N <= wrows &&
+    for (int T = 8; T >= 2; T /= 2) {
+        // accumulator columns per epilogue warp (its tiles x N x row tiles) fit its 96
+        // registers; one TMEM buffer (MT T N columns) fits half of the 512 columns
+        const int warp_cols = (lean ? T : T / 2) * N * MT;
+        if (warp_cols <= 96 && MT * T * N <= 256 && (T + 2) * N <= wrows &&
             bny % T == 0 && (rows / T) % 2 == 0)
             return T;
+    }
     return 0;
 }
 

@@ -552,7 +552,8 @@ def test_m2l_engines_vs_fp64_fmm_oracle(n, depth, p, lam, engine, monkeypatch):
 
 
 @pytest.mark.parametrize("engine", ["tf32", "f16"])
-@pytest.mark.parametrize("n,depth,p,lam", [(48, 5, 6, 0), (128, 6, 8, 1)])
+@pytest.mark.parametrize("n,depth,p,lam", [(48, 5, 6, 0), (128, 6, 8, 1), (32, 4, 13, 1),
+                                           (64, 5, 12, 3)])
 def test_m2l_tensor_core_matches_simt(n, depth, p, lam, engine, monkeypatch):
     """Deeper trees than the fp64 oracle reaches: levels >= 2 on tcgen05 (3xTF32, or the
     balanced 3xFP16 split) against the SIMT FP32 gather-GEMM (itself validated against the fp64
