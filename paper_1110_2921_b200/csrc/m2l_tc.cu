@@ -51,7 +51,8 @@ namespace {
 
 // K chunks of 128 B: 4 x 32 tf32 or 2 x 64 halves (K = 128)
 template <bool F16> __host__ __device__ constexpr int tc_ke() { return F16 ? 64 : 32; }
-constexpr int TC_AST = 2;      // A (operator) pipeline stages
+// A (operator) pipeline stages: TC_AST = 2 (template default), or 4 in the deep variant (the
+// lean layout with T = 2 rows per CTA, 225 KB)
 constexpr int TC_BST = 2;      // B pipeline stages (each holds one y-window of T + 2 slabs)
 // MT = output row tiles of 128 (1: (p+1)^2 <= 128; 2: <= 256, f16 only)
 constexpr int A_TILE = 128 * 128;  // one K chunk of 128 operator rows, one half (hi or lo): 16 KB
@@ -68,10 +69,11 @@ template <bool LEAN> __host__ __device__ constexpr int tc_threads() { return 64 
 template <int MT, bool LEAN = false> __host__ __device__ constexpr int b_bytes_v() {
     return LEAN ? 192 * 128 : b_bytes<MT>();
 }
-template <int MT, bool LEAN = false>
+template <int MT, bool LEAN = false, int AST = 2>
 constexpr size_t tc_smem() {
-    return 1024 + (size_t)TC_AST * 2 * a_bytes<MT>() + (size_t)TC_BST * 2 * b_bytes_v<MT, LEAN>() + 512;
+    return 1024 + (size_t)AST * 2 * a_bytes<MT>() + (size_t)TC_BST * 2 * b_bytes_v<MT, LEAN>() + 512;
 }
+static_assert(tc_smem<1, true, 4>() <= 232448, "deep variant exceeds 227 KB");
 static_assert(tc_smem<2>() <= 232448, "MT = 2 stages exceed 227 KB");
 static_assert(tc_smem<1, true>() <= 166 * 1024, "LEAN stages exceed 166 KB");
 
@@ -233,7 +235,7 @@ __device__ __forceinline__ void group_rows(const TcParams& P, int g, int* tx, in
     *pz = P.bz0 + gz;
 }
 
-template <bool F16, int MT, bool LEAN = false>
+template <bool F16, int MT, bool LEAN = false, int TC_AST = 2>
 __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc_threads<LEAN>(), 1)
     m2l_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant__ CUtensorMap tmA_lo,
                   const __grid_constant__ CUtensorMap tmB_hi, const __grid_constant__ CUtensorMap tmB_lo,
@@ -705,7 +707,11 @@ int launch_m2l_tc(const TcOps& ops, const int* il_slots, int p, const float* M_l
     const int bnx = box[3], bny = box[4], bnz = box[5];
     const int XT = pick_XT(box);
     const int NV = 3 * XT;
-    const bool lean = ops.lean && MT == 1 && f16 && pick_T(box, 1, true) != 0;
+    // VFMM_M2L_DEEP=1: the lean layout (T = 2) with 4 operator stages for the plain pipeline
+    const char* deep_env = getenv("VFMM_M2L_DEEP");
+    const bool deep = deep_env && deep_env[0] == '1' && !ops.lean && MT == 1 && f16 &&
+                      pick_T(box, 1, true) != 0;
+    const bool lean = (ops.lean || deep) && MT == 1 && f16 && pick_T(box, 1, true) != 0;
     const int T = pick_T(box, MT, lean);
     if (T == 0) return -4;
     const int N = (NV + 15) / 16 * 16;  // MMA N (multiple of 16 for M = 128)
@@ -735,6 +741,9 @@ int launch_m2l_tc(const TcOps& ops, const int* il_slots, int p, const float* M_l
                              (int)tc_smem<2>());
         cudaFuncSetAttribute(m2l_tc_kernel<true, 1, true>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem<1, true>());
+        cudaFuncSetAttribute(m2l_tc_kernel<true, 1, true, 4>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)tc_smem<1, true, 4>());
     });
     TcParams P;
     P.nP = nP;
@@ -759,6 +768,9 @@ int launch_m2l_tc(const TcOps& ops, const int* il_slots, int p, const float* M_l
     const unsigned grid = (unsigned)(8 * (P.rows / P.T));
     if (f16 && MT == 2)
         m2l_tc_kernel<true, 2><<<grid, tc_threads<false>(), tc_smem<2>(), st>>>(mAh, mAl, mBh, mBl, P);
+    else if (deep)
+        m2l_tc_kernel<true, 1, true, 4><<<grid, tc_threads<true>(), tc_smem<1, true, 4>(), st>>>(
+            mAh, mAl, mBh, mBl, P);
     else if (lean)
         m2l_tc_kernel<true, 1, true><<<grid, tc_threads<true>(), tc_smem<1, true>(), st>>>(
             mAh, mAl, mBh, mBl, P);
