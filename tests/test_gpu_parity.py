@@ -564,12 +564,15 @@ def test_m2l_tensor_core_matches_simt(n, depth, p, lam, engine, monkeypatch):
     v1, s1, ev1 = run(f, p=p, depth=depth, image_levels=lam, mode=vf.MODE_FAR_ONLY)
     monkeypatch.setenv("VFMM_M2L", "simt")
     v2, s2, ev2 = run(f, p=p, depth=depth, image_levels=lam, mode=vf.MODE_FAR_ONLY)
+    print(f"tc {engine} vs simt n={n} L={depth} p={p} lam={lam}: u {rel(v1, v2):.2e} "
+          f"sdot {rel(s1, s2):.2e}")
+    assert rel(v1, v2) < 5e-6 and rel(s1, s2) < 5e-6, (rel(v1, v2), rel(s1, s2))
+    # the scaled operators span ~(2p)! in FP32, so both engines' finest expansions carry more
+    # rounding at p > 10 (DESIGN.md 7 "High p"; 5e-4 against fp64 at p = 16)
+    etol = 1e-5 if p <= 10 else 5e-5
     for l in range(depth - 1, depth + 1):
         a, b = ev1.debug_expansions(1, l), ev2.debug_expansions(1, l)
-        print(f"tc {engine} vs simt n={n} L={depth} p={p} lam={lam}: level {l} "
-              f"{rel(a[..., 1:], b[..., 1:]):.2e}")
-        assert rel(a[..., 1:], b[..., 1:]) < 1e-5, (l, rel(a[..., 1:], b[..., 1:]))
-    print(f"tc {engine} vs simt n={n}: u {rel(v1, v2):.2e} sdot {rel(s1, s2):.2e}")
-    assert rel(v1, v2) < 5e-6 and rel(s1, s2) < 5e-6, (rel(v1, v2), rel(s1, s2))
+        print(f"  level {l}: {rel(a[..., 1:], b[..., 1:]):.2e}")
+        assert rel(a[..., 1:], b[..., 1:]) < etol, (l, rel(a[..., 1:], b[..., 1:]))
     ev1.close()
     ev2.close()
