@@ -39,6 +39,7 @@
 // row groups): each loads one half (hi or lo) of an operator chunk with TMA multicast into
 // both CTAs, halving operator traffic; operator stages are released by both MMA warps.
 #include <cuda.h>
+#include <algorithm>
 #include <cudaTypedefs.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -603,6 +604,27 @@ __global__ void __launch_bounds__(512) m2l_stage16_kernel(const float* __restric
     }
 }
 
+// the level's max |cs[k] M_k| straight over the Morton array (every cell once, coalesced;
+// the halo copies of the staged grid repeat these values or are zero)
+__global__ void __launch_bounds__(256) m2l_max_kernel(const float* __restrict__ M, int64_t count,
+                                                      int nc, const float* __restrict__ cs,
+                                                      uint32_t* __restrict__ maxbits) {
+    float mx = 0.f;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x)
+        mx = fmaxf(mx, fabsf(M[i] * cs[(int)(i % nc)]));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+    __shared__ float wm[8];
+    if ((threadIdx.x & 31) == 0) wm[threadIdx.x >> 5] = mx;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float b = 0.f;
+        for (int w = 0; w < 8; ++w) b = fmaxf(b, wm[w]);
+        if (b > 0.f) atomicMax(maxbits, __float_as_uint(b));
+    }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     if (!fn) {
@@ -674,8 +696,9 @@ int launch_m2l_tc(const TcOps& ops, const int* il_slots, int p, const float* M_l
         if (f16) {
             const int64_t blocks = (int64_t)8 * Xp * Xp;  // one per (pi', Z, Y) x-row
             const dim3 blk(KPG, 512 / KPG);
-            m2l_stage16_kernel<true><<<(unsigned)blocks, blk, 0, st>>>(
-                M_l, nP, periodic, nc, ops.cs, maxbits, nullptr, nullptr);
+            const int64_t cnt = ((int64_t)1 << (3 * level)) * 3 * nc;
+            const int64_t mb = std::min<int64_t>((cnt + 255) / 256, 148 * 8);
+            m2l_max_kernel<<<(unsigned)mb, 256, 0, st>>>(M_l, cnt, nc, ops.cs, maxbits);
             m2l_stage16_kernel<false><<<(unsigned)blocks, blk, 0, st>>>(
                 M_l, nP, periodic, nc, ops.cs, maxbits, reinterpret_cast<__half*>(ghi),
                 reinterpret_cast<__half*>(glo));
