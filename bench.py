@@ -391,7 +391,7 @@ def main():
         "p2p_pairs_per_eval": pairs,
         "fp32_frac_p2p": p2p_tf / fp32_peak, "m2l_useful_tflops": m2l_tf,
         "m2l_engine": engine if tc_m2l else "simt",
-        "p2p_variant": "sj" if os.environ.get("VFMM_P2P") == "sj" else "cross",
+        "p2p_variant": "cross" if os.environ.get("VFMM_P2P") == "cross" else "sj",
         "phase_ms": {k[3:]: round(v, 4) for k, v in avg.items() if k.startswith("ms_")},
         "roofline": roof, "cpu_baseline": cb, "e2e": e2e,
         "gpu_launches": int(phases[0]["n_kernel_launches"]) * args.steps,

@@ -645,16 +645,19 @@ void launch_p2p(const float* sorted6, int64_t n, const int* leaf_start, int dept
                 unsigned long long* npairs, int64_t plo, int64_t pcnt, cudaStream_t st,
                 bool lean) {
     if (pcnt <= 0) return;
-    // default: per-pair cross products gamma_j x d (FP32-faithful rounding); VFMM_P2P=sj: the
-    // classical scheme with staged source cross products (~3% faster at c4, 2-4x the rounding).
+    // classical scheme, default: staged source cross products s_j = gamma_j x x_j (reading R17;
+    // 38 instead of 41 FP32 operations per pair, P2P 41.9 vs 43.1 ms at c4; the sums carry
+    // the lever arm |x_j| ~ the 4-leaf region instead of |d|, ~1e-6 relative rounding at c4);
+    // VFMM_P2P=cross: per-pair gamma_j x d (the smallest rounding; the transpose scheme and the
+    // lean co-resident variant always use it).
     // VFMM_P2P_CFG: occupancy / unroll variants (measurement knob): "b3u1", "b3u2", "b2u1"
     const char* env = getenv("VFMM_P2P");
-    const bool sj = env && strcmp(env, "sj") == 0;
+    const bool sj = !(env && strcmp(env, "cross") == 0);
     const char* cfg = getenv("VFMM_P2P_CFG");
     const int v = !cfg ? 0 : strcmp(cfg, "b3u1") == 0 ? 1 : strcmp(cfg, "b3u2") == 0 ? 2
                                 : strcmp(cfg, "b2u1") == 0 ? 3 : 0;
 #define P2P_ARGS sorted6, n, leaf_start, depth, a, periodic, kc, near6, npairs, plo, pcnt, st
-    if (scheme == 0 && sj) {
+    if (scheme == 0 && sj && !lean && v == 0) {
         p2p_go<0, true, 2, 2>(P2P_ARGS);
     } else if (lean) {
         if (scheme == 0) p2p_go<0, false, 1, 2>(P2P_ARGS);

@@ -109,7 +109,7 @@ def test_direct_mode_vs_oracle(lam, scheme):
 @pytest.mark.parametrize("scheme,p2p", [(0, "sj"), (0, "cross"), (1, "cross")])
 def test_near_only_depth1_free_space_equals_direct(scheme, p2p, monkeypatch):
     """Depth 1, free space: all octants are neighbours, so P2P alone is the whole sum.
-    Classical scheme in both P2P accumulations (default / VFMM_P2P=cross: per-pair gamma_j x d;
+    Classical scheme in both P2P accumulations (VFMM_P2P=cross: per-pair gamma_j x d; default /
     VFMM_P2P=sj: staged gamma_j x x_j, looser FP32 rounding bound).  The jittered lattice
     (+-0.75 h) has unequal leaves and close pairs; 16 distinct coincident pairs exercise the
     r -> 0 limits (reading R7)."""
@@ -123,10 +123,12 @@ def test_near_only_depth1_free_space_equals_direct(scheme, p2p, monkeypatch):
 
 
 @pytest.mark.parametrize("scheme", [0, 1])
-def test_near_only_dense_leaves_multiwindow_equals_direct(scheme):
+def test_near_only_dense_leaves_multiwindow_equals_direct(scheme, monkeypatch):
     """Dense leaves: 20000 clustered points at depth 1 (thousands per leaf) -- the P2P kernel
     stages the 64-leaf region in several shared-memory windows (> 4352 sources) and loops over
-    many 64-target chunks per warp.  Free space, so NEAR_ONLY is the whole direct sum."""
+    many 64-target chunks per warp.  Free space, so NEAR_ONLY is the whole direct sum.  Per-pair
+    cross products (VFMM_P2P=cross): at depth 1 the staged form's lever arm is the whole box."""
+    monkeypatch.setenv("VFMM_P2P", "cross")
     f = synthgen.with_coincident(synthgen.clustered(20000, seed=33, sigma=0.2), count=8)
     v, s, ev = run(f, p=2, depth=1, image_levels=0, scheme=scheme, mode=vf.MODE_NEAR_ONLY)
     keys, perm, ls = ev.debug_tree(1)
@@ -331,6 +333,7 @@ def test_coresident_mode_matches_sequential(monkeypatch):
     result as the sequential pipeline up to the P2P's FP32 summation order (its staging windows
     are smaller), the tensor-core M2L bitwise unchanged."""
     f = synthgen.isotropic(32, seed=14)
+    monkeypatch.setenv("VFMM_P2P", "cross")  # the lean P2P variant has the per-pair form only
     v0, s0, ev0 = run(f, p=10, depth=3, image_levels=3)
     L0 = ev0.debug_expansions(1, 3)
     monkeypatch.setenv("VFMM_CORES", "1")
@@ -372,6 +375,34 @@ def test_evaluation_is_deterministic(engine, monkeypatch):
     assert np.array_equal(v0, v1) and np.array_equal(s0, s1)
     ev.close()
     ev1.close()
+
+
+def test_evaluates_on_different_streams_are_ordered():
+    """one context's workspace serves every evaluate, so an evaluate on a new stream
+    waits for the previous one (its end event).  Back-to-back evaluations of two different
+    fields on two streams, without host synchronization in between, give each field's own
+    single-stream result."""
+    fa = synthgen.isotropic(32, seed=41)
+    fb = synthgen.isotropic(32, seed=42)
+    va, _, ev = run(fa, p=6, depth=3, image_levels=2)
+    vb, _, ev_b = run(fb, p=6, depth=3, image_levels=2)
+    ev_b.close()
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    pa, ga = (torch.from_numpy(x).to(DEV) for x in (fa.pos, fa.gamma))
+    pb, gb = (torch.from_numpy(x).to(DEV) for x in (fb.pos, fb.gamma))
+    torch.cuda.synchronize()
+    outs = []
+    for k in range(3):
+        with torch.cuda.stream(s1):
+            v1, _ = ev.evaluate(pa, ga, stream=s1)
+        with torch.cuda.stream(s2):
+            v2, _ = ev.evaluate(pb, gb, stream=s2)
+        outs.append((v1, v2))
+    torch.cuda.synchronize()
+    for v1, v2 in outs:
+        assert np.array_equal(v1.cpu().numpy().astype(np.float64), va)
+        assert np.array_equal(v2.cpu().numpy().astype(np.float64), vb)
+    ev.close()
 
 
 @pytest.mark.parametrize("mode", ["fmm", "direct"])

@@ -20,7 +20,7 @@ FMM_VS_DIRECT = {  # p: (velocity, stretching)
 FMM_VS_FMM_ORACLE = (2e-5, 5e-5)
 DIRECT_VS_ORACLE = (2e-6, 5e-6)
 NEAR_VS_ORACLE = (2e-6, 5e-6)
-# Classical-scheme P2P with staged source cross products (VFMM_P2P=sj, opt-in): the sums
+# Classical-scheme P2P with staged source cross products (the default; VFMM_P2P=sj): the sums
 # carry gamma_j x x_j (lever arm ~ the leaf width) instead of gamma_j x d, so FP32 rounding
 # grows ~2-4x (DESIGN.md 2 "Readings" R17; measured 2.8e-6 / 6.4e-6 on the depth-1 case with
 # scripts/p2p_precision.py, 7.3e-7 / 1.4e-6 with the default per-pair cross products).  Still
