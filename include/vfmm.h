@@ -178,6 +178,14 @@ vfmm_status vfmm_reinit(vfmm_ctx* ctx, int64_t n_old, const float* pos_old,
                         int32_t restart, float* gamma_new, float* omega_new,
                         vfmm_reinit_info* info, void* cuda_stream);
 
+/* Per-particle core radius (NEXT-4): as vfmm_evaluate, with sigma_j of every particle (device,
+   n floats > 0, input order) in the cutoff of Eq. (6) -- PAPER.md:86 writes the source's
+   sigma_j -- for the near field (P2P) and DIRECT mode; the far field drops the cutoff
+    as before.  The context's sigma must be >= max sigma_j: the automatic depth
+   keeps the leaf width >= 4 sigma with it (reading R3).  Single-GPU contexts only. */
+vfmm_status vfmm_evaluate_sigma(vfmm_ctx* ctx, int64_t n, const float* pos, const float* gamma,
+                                const float* sigma, float* vel, float* dgamma, void* cuda_stream);
+
 /* ---- multi-GPU: Morton-range spatial decomposition + local-essential-tree exchange ----
    (the paper's multi-GPU runs.)  Rank r of R
    (R in {1, 2, 4, 8}) owns the Morton leaf range [r 8^L/R, (r+1) 8^L/R) at depth L

@@ -55,9 +55,10 @@ def _lib(native: bool = False):
         dp = ctypes.POINTER(ctypes.c_double)
         L.vfmm_oracle_kernels.argtypes = [ctypes.c_double, ctypes.c_double, dp, dp, dp, dp]
         L.vfmm_oracle_kernels.restype = None
-        for fn in (L.vfmm_oracle_eval, L.vfmm_oracle_eval_batched):
+        for fn in (L.vfmm_oracle_eval, L.vfmm_oracle_eval_batched, L.vfmm_oracle_eval_sigma):
             fn.argtypes = [
-                ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_double,
+                ctypes.c_int64, ctypes.c_void_p, ctypes.c_void_p,
+                ctypes.c_void_p if fn is L.vfmm_oracle_eval_sigma else ctypes.c_double,
                 ctypes.c_double, ctypes.c_double, ctypes.c_int, ctypes.c_int, ctypes.c_int64,
                 ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p, ctypes.c_void_p,
                 ctypes.c_void_p, ctypes.c_int,
@@ -86,6 +87,13 @@ def _c(a, dtype):
 
 def direct(pos, gamma, sigma, box_lo, box_len, image_levels=3, scheme=0, targets=None,
            probe_pos=None, probe_gamma=None, nthreads=0, batched=False, native=False):
+    """see _direct; sigma may be an array of per-source core radii (Eq. 6's sigma_j)"""
+    return _direct(pos, gamma, sigma, box_lo, box_len, image_levels, scheme, targets,
+                   probe_pos, probe_gamma, nthreads, batched, native)
+
+
+def _direct(pos, gamma, sigma, box_lo, box_len, image_levels=3, scheme=0, targets=None,
+            probe_pos=None, probe_gamma=None, nthreads=0, batched=False, native=False):
     """Direct periodic-image sum (oracle O1).
 
     pos, gamma: (3, N) arrays (SoA); values are widened exactly to float64.
@@ -109,11 +117,17 @@ def direct(pos, gamma, sigma, box_lo, box_len, image_levels=3, scheme=0, targets
     vel = np.zeros((3, nt), np.float64)
     dg = np.zeros((3, nt), np.float64)
     L = _lib(native)
-    rc = (L.vfmm_oracle_eval_batched if batched else L.vfmm_oracle_eval)(
-        n, pos.ctypes.data, gamma.ctypes.data, float(sigma), float(box_lo), float(box_len),
-        int(image_levels), int(scheme), nt, None if tidx is None else tidx.ctypes.data,
-        None if tp is None else tp.ctypes.data, None if tg is None else tg.ctypes.data,
-        vel.ctypes.data, dg.ctypes.data, int(nthreads))
+    tail = (float(box_lo), float(box_len), int(image_levels), int(scheme), nt,
+            None if tidx is None else tidx.ctypes.data, None if tp is None else tp.ctypes.data,
+            None if tg is None else tg.ctypes.data, vel.ctypes.data, dg.ctypes.data,
+            int(nthreads))
+    if np.ndim(sigma) > 0:  # per-source core radii (plain loop nest)
+        sig = _c(np.broadcast_to(np.asarray(sigma, np.float64), (n,)), np.float64)
+        rc = L.vfmm_oracle_eval_sigma(n, pos.ctypes.data, gamma.ctypes.data, sig.ctypes.data,
+                                      *tail)
+    else:
+        rc = (L.vfmm_oracle_eval_batched if batched else L.vfmm_oracle_eval)(
+            n, pos.ctypes.data, gamma.ctypes.data, float(sigma), *tail)
     if rc != 0:
         raise ValueError(f"vfmm_oracle_eval failed: {rc}")
     return vel, dg

@@ -136,15 +136,26 @@ static inline void or_pair(int scheme, double f, double q, double d0, double d1,
  * vel, dgam: SoA 3 x n_tgt, overwritten.
  * Returns 0, or -1 on bad parameters.
  */
-int vfmm_oracle_eval(int64_t n_src, const double* src_pos, const double* src_gam,
-                     double sigma, double box_lo, double box_len, int image_levels, int scheme,
-                     int64_t n_tgt, const int64_t* tgt_idx, const double* tgt_pos,
-                     const double* tgt_gam, double* vel, double* dgam, int nthreads)
+/* The direct sum with the core radius of every source given (sig_src[j], Eq. 6 has sigma_j,
+   PAPER.md:86; zeta0 per source) or uniform (sig_src == NULL: sigma). */
+static int or_eval(int64_t n_src, const double* src_pos, const double* src_gam,
+                   double sigma, const double* sig_src, double box_lo, double box_len,
+                   int image_levels, int scheme, int64_t n_tgt, const int64_t* tgt_idx,
+                   const double* tgt_pos, const double* tgt_gam, double* vel, double* dgam,
+                   int nthreads)
 {
     (void)box_lo; /* only differences of positions enter the sum */
     if (n_src < 1 || !(sigma > 0.0) || !(box_len > 0.0) || image_levels < 0 ||
         image_levels > 6 || (scheme != 0 && scheme != 1) || n_tgt < 0)
         return -1;
+    double* z0_src = NULL;
+    if (sig_src) {
+        for (int64_t j = 0; j < n_src; ++j)
+            if (!(sig_src[j] > 0.0)) return -1;
+        z0_src = (double*)malloc(sizeof(double) * (size_t)n_src);
+        if (!z0_src) return -2;
+        for (int64_t j = 0; j < n_src; ++j) z0_src[j] = or_zeta0(sig_src[j]);
+    }
     if (tgt_idx == NULL && (tgt_pos == NULL || tgt_gam == NULL)) return -1;
     int m = 0;
     for (int l = 0; l < image_levels; ++l) m = 3 * m + 1; /* m = (3^L - 1)/2 */
@@ -186,7 +197,10 @@ int vfmm_oracle_eval(int64_t n_src, const double* src_pos, const double* src_gam
                 const double d2 = xi[2] - src_pos[j + 2 * n_src] - sz;
                 const double r = sqrt(d0 * d0 + d1 * d1 + d2 * d2);
                 double zeta, g, f, q;
-                or_kernels(r, sigma, zeta0, &zeta, &g, &f, &q);
+                if (sig_src)
+                    or_kernels(r, sig_src[j], z0_src[j], &zeta, &g, &f, &q);
+                else
+                    or_kernels(r, sigma, zeta0, &zeta, &g, &f, &q);
                 or_pair(scheme, f, q, d0, d1, d2, src_gam[j], src_gam[j + n_src],
                         src_gam[j + 2 * n_src], gi, u, s);
             }
@@ -200,7 +214,30 @@ int vfmm_oracle_eval(int64_t n_src, const double* src_pos, const double* src_gam
             dgam[t + k * n_tgt] = S[k];
         }
     }
+    free(z0_src);
     return 0;
+}
+
+int vfmm_oracle_eval(int64_t n_src, const double* src_pos, const double* src_gam,
+                     double sigma, double box_lo, double box_len, int image_levels, int scheme,
+                     int64_t n_tgt, const int64_t* tgt_idx, const double* tgt_pos,
+                     const double* tgt_gam, double* vel, double* dgam, int nthreads)
+{
+    return or_eval(n_src, src_pos, src_gam, sigma, NULL, box_lo, box_len, image_levels, scheme,
+                   n_tgt, tgt_idx, tgt_pos, tgt_gam, vel, dgam, nthreads);
+}
+
+/* Per-particle core radius sigma_j of the source (Eq. 6 as written, sigma_j; NEXT-4):
+   sig_src[n_src] > 0; otherwise as vfmm_oracle_eval. */
+int vfmm_oracle_eval_sigma(int64_t n_src, const double* src_pos, const double* src_gam,
+                           const double* sig_src, double box_lo, double box_len,
+                           int image_levels, int scheme, int64_t n_tgt, const int64_t* tgt_idx,
+                           const double* tgt_pos, const double* tgt_gam, double* vel,
+                           double* dgam, int nthreads)
+{
+    if (!sig_src) return -1;
+    return or_eval(n_src, src_pos, src_gam, 1.0, sig_src, box_lo, box_len, image_levels, scheme,
+                   n_tgt, tgt_idx, tgt_pos, tgt_gam, vel, dgam, nthreads);
 }
 
 /*

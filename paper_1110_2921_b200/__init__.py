@@ -62,7 +62,8 @@ EXPORTS = ["vfmm_abi_version", "vfmm_params_default", "vfmm_create", "vfmm_evalu
            "vfmm_debug_tree", "vfmm_debug_expansions", "vfmm_strerror",
            "vfmm_last_error_message", "vfmm_destroy", "vfmm_nccl_get_unique_id",
            "vfmm_create_nccl", "vfmm_partition", "vfmm_evaluate_logical", "vfmm_dist_plan",
-           "vfmm_route_counts", "vfmm_step", "vfmm_evaluate_at", "vfmm_reinit"]
+           "vfmm_route_counts", "vfmm_step", "vfmm_evaluate_at", "vfmm_reinit",
+           "vfmm_evaluate_sigma"]
 
 
 class c_reinit_info(ctypes.Structure):
@@ -107,6 +108,8 @@ def load_library(path: str = LIB_PATH):
                             ctypes.POINTER(ctypes.c_float), vp]
     L.vfmm_step.restype = ctypes.c_int
     L.vfmm_evaluate_at.argtypes = [vp, i64, vp, vp, i64, vp, vp, vp]
+    L.vfmm_evaluate_sigma.argtypes = [vp, i64, vp, vp, vp, vp, vp, vp]
+    L.vfmm_evaluate_sigma.restype = ctypes.c_int
     L.vfmm_evaluate_at.restype = ctypes.c_int
     L.vfmm_reinit.argtypes = [vp, i64, vp, vp, ctypes.c_float, i64, vp, ctypes.c_float,
                               ctypes.c_float, ctypes.c_int32, ctypes.c_int32, vp, vp,
@@ -238,6 +241,24 @@ class Evaluator:
             ctypes.c_void_p(stream.cuda_stream)))
         self._n = n
         return vel, dgamma
+
+    def evaluate_sigma(self, pos, gamma, sigma, stream=None):
+        """Per-particle core radii sigma ((N,) float32 CUDA tensor, Eq. 6's sigma_j) in the near
+        field -- C ABI vfmm_evaluate_sigma; the context's sigma must be >= max sigma."""
+        import torch
+
+        if not (sigma.is_cuda and sigma.dtype == torch.float32 and sigma.is_contiguous()
+                and sigma.dim() == 1 and sigma.shape[0] == pos.shape[1]):
+            raise ValueError("sigma: contiguous float32 CUDA tensor of shape (N,)")
+        vel = torch.empty_like(pos)
+        dg = torch.empty_like(pos)
+        if stream is None:
+            stream = torch.cuda.current_stream(pos.device)
+        _check(self._L, self._ctx, self._L.vfmm_evaluate_sigma(
+            self._ctx, pos.shape[1], pos.data_ptr(), gamma.data_ptr(), sigma.data_ptr(),
+            vel.data_ptr(), dg.data_ptr(), ctypes.c_void_p(stream.cuda_stream)))
+        self._n = pos.shape[1]
+        return vel, dg
 
     def evaluate(self, pos, gamma, stream=None):
         import torch

@@ -86,6 +86,8 @@ struct vfmm_ctx {
     int64_t cap_at_n = 0;
     float* at_buf = nullptr;    // vfmm_evaluate_at: sources + targets, 12 x (n_src + n_tgt)
     int64_t cap_step_n = 0;
+    int64_t cap_sig_n = 0;
+    float* sorted_sig = nullptr;  // vfmm_evaluate_sigma: per-particle sigma in Morton order
     float* step_buf = nullptr;  // vfmm_step: u and dgamma/dt when the caller passes no buffers
     cudaStream_t own_stream = nullptr;
     // last evaluate
@@ -641,8 +643,22 @@ vfmm_status vfmm_set_params(vfmm_ctx* c, const vfmm_params* prm) {
     return ensure_ops(c);
 }
 
+static vfmm_status evaluate_impl(vfmm_ctx* c, int64_t n, const float* pos, const float* gamma,
+                                 const float* sig, float* vel, float* dgamma, void* stream);
+
 vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float* gamma,
                           float* vel, float* dgamma, void* stream) {
+    return evaluate_impl(c, n, pos, gamma, nullptr, vel, dgamma, stream);
+}
+
+vfmm_status vfmm_evaluate_sigma(vfmm_ctx* c, int64_t n, const float* pos, const float* gamma,
+                                const float* sigma, float* vel, float* dgamma, void* stream) {
+    if (!c || !sigma || c->dist) return VFMM_EINVAL;
+    return evaluate_impl(c, n, pos, gamma, sigma, vel, dgamma, stream);
+}
+
+static vfmm_status evaluate_impl(vfmm_ctx* c, int64_t n, const float* pos, const float* gamma,
+                                 const float* sig, float* vel, float* dgamma, void* stream) {
     if (!c || n < 0 || (n == 0 && !c->dist)) return VFMM_EINVAL;
     if (n > 0 && (!pos || !gamma || !vel || !dgamma)) return VFMM_EINVAL;
     if (n > ((int64_t)1 << 31) - 1) return VFMM_EINVAL;
@@ -749,7 +765,11 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
             CK(cudaStreamWaitEvent(st, c->ev_gamma, 0), "wait h2d");
             c->gamma_pending = false;
         }
-        launch_direct(pos, gamma, n, P.box_len, P.image_levels, P.scheme, kc, vel, dgamma, st);
+        if (sig)
+            launch_direct_sigma(pos, gamma, sig, n, P.box_len, P.image_levels, P.scheme, vel,
+                                dgamma, st);
+        else
+            launch_direct(pos, gamma, n, P.box_len, P.image_levels, P.scheme, kc, vel, dgamma, st);
         CK(cudaGetLastError(), "direct kernel");
         for (int i = 1; i < vfmm_ctx::NEV; ++i) CK(cudaEventRecord(c->ev[i], st), "event");
         int m = 0;
@@ -777,10 +797,10 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
             if ((double)P.box_len / (double)(1 << L) < 4.0 * (double)P.sigma * (1.0 - 1e-6)) continue;
             if (((int64_t)1 << (3 * L)) > 64 * n + 8) continue;  // hardly any particle per leaf
             c->prm.depth = L;
-            vfmm_status s0 = vfmm_evaluate(c, n, pos, gamma, vel, dgamma, stream);  // warm-up
+            vfmm_status s0 = evaluate_impl(c, n, pos, gamma, sig, vel, dgamma, stream);  // warm-up
             if (s0 == VFMM_OK) {
                 cudaEventRecord(t0, st);
-                s0 = vfmm_evaluate(c, n, pos, gamma, vel, dgamma, stream);
+                s0 = evaluate_impl(c, n, pos, gamma, sig, vel, dgamma, stream);
                 cudaEventRecord(t1, st);
             }
             c->prm.depth = -1;
@@ -842,7 +862,7 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
     // kernel variants (P2P 61.5 KB, tcgen05 M2L 161 KB / 192 threads) let one block of each
     // share an SM.  Otherwise everything runs in sequence on the caller's stream.
     const char* cores_env = getenv("VFMM_CORES");
-    const bool cores = cores_env && cores_env[0] == '1' && use_far && use_near;
+    const bool cores = cores_env && cores_env[0] == '1' && use_far && use_near && !sig;
     cudaStream_t fs = st;  // stream of the far-field chain
     if (cores) {
         CK(cudaEventRecord(c->ev_tree, st), "event");
@@ -944,6 +964,19 @@ vfmm_status vfmm_evaluate(vfmm_ctx* c, int64_t n, const float* pos, const float*
     // ---- near field ----
     if (use_near && !cores) {
         CK(cudaMemsetAsync(c->d_pairs, 0, sizeof(unsigned long long), st), "memset pairs");
+        if (sig) {  // per-particle core radius: sigma into Morton order, the sigma_j P2P
+            if (n > c->cap_sig_n) {
+                dfree(c->sorted_sig);
+                c->cap_sig_n = 0;
+                CK(cudaMalloc((void**)&c->sorted_sig, n * sizeof(float)), "alloc sorted sigma");
+                c->cap_sig_n = n;
+            }
+            launch_gather1(sig, c->perm, n, c->sorted_sig, st);
+            launch_p2p_sigma(c->sorted6, c->sorted_sig, n, c->leaf_start, depth, a,
+                             P.image_levels > 0, P.scheme, c->near6, c->d_pairs, 0,
+                             (int64_t)1 << (3 * (depth - 1)), st);
+            nl += 2;
+        } else
         launch_p2p(c->sorted6, n, c->leaf_start, depth, a, P.image_levels > 0, P.scheme, kc,
                    c->near6, c->d_pairs, 0, (int64_t)1 << (3 * (depth - 1)), st);
         ++nl;
@@ -1278,6 +1311,7 @@ vfmm_status vfmm_step(vfmm_ctx* c, int64_t n, float* pos, float* gamma, float dt
         if (n > c->cap_step_n) {
             dfree(c->step_buf);
     dfree(c->at_buf);
+    dfree(c->sorted_sig);
             c->cap_step_n = 0;
             CK(cudaMalloc((void**)&c->step_buf, 6 * n * sizeof(float)), "alloc step buffers");
             c->cap_step_n = n;

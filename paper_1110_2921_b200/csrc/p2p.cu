@@ -550,6 +550,278 @@ __global__ void __launch_bounds__(P2P_THREADS, MINB == 1 ? 2 : MINB) p2p_kernel(
     }
 }
 
+// ---- per-particle core radius sigma_j (Eq. 6 as written: the source's sigma, NEXT-4) ----
+// With rt = r / sigma_j, rho = rt / sqrt2 and ez' = zeta0(1) e^{-rho^2} (sigma-independent
+// offset), the closed form of fq_closed2 becomes f = (1/4pi + ez' Qn(rt)) / r^3 with the
+// sigma = 1 polynomial (kc1: make_kernel_consts(1)), q = (ez' / sigma_j^3 - 3 f) / r^2.
+// Per source staged: c_j = -log2(e) / (2 sigma_j^2), 1/sigma_j, 1/sigma_j^3, sigma_j^2 / 2.
+__device__ __forceinline__ void fq_closed2_sig(f2 r2, float cj, float isig, float isig3,
+                                               const KernelConsts& kc1, f2& f, f2& q) {
+    float ra, rb;
+    upk(r2, ra, rb);
+    const f2 rinv = pk(rsqrt_approx(ra), rsqrt_approx(rb));
+    float ea, eb;
+    upk(fma2(r2, bc(cj), bc(kc1.ez_off)), ea, eb);
+    const f2 ez = pk(ex2_approx(ea), ex2_approx(eb));
+    const f2 rt = mul2(mul2(r2, rinv), bc(isig));
+    float da, db;
+    upk(fma2(rt, bc(kc1.t_scale), bc(1.f)), da, db);
+    const f2 t = pk(rcp_approx(da), rcp_approx(db));
+    f2 E = fma2(bc(kc1.en[5]), t, bc(kc1.en[4]));
+    E = fma2(E, t, bc(kc1.en[3]));
+    E = fma2(E, t, bc(kc1.en[2]));
+    E = fma2(E, t, bc(kc1.en[1]));
+    E = fma2(E, t, bc(kc1.en[0]));
+    const f2 Qn = fma2(bc(kc1.qn_scale), rt, E);
+    const f2 g4pi = fma2(ez, Qn, bc(0.0795774715459476679f));
+    const f2 rinv2 = mul2(rinv, rinv);
+    f = mul2(g4pi, mul2(rinv2, rinv));
+    q = mul2(fma2(bc(-3.f), f, mul2(ez, bc(isig3))), rinv2);
+}
+// the Taylor series for rho^2 < 1/4 with sigma_j (exact r -> 0 limits)
+__device__ __forceinline__ void fq_series_sig(float r2, float isig, float isig3,
+                                              const KernelConsts& kc1, float& f, float& q) {
+    KernelConsts k = kc1;  // sigma = 1 constants rescaled to sigma_j
+    k.inv2s2 = 0.5f * isig * isig;
+    k.zeta0 = kc1.zeta0 * isig3;
+    k.zeta0_over_s2 = kc1.zeta0 * isig3 * isig * isig;
+    fq_series(r2, k, f, q);
+}
+
+template <int SCHEME>
+__global__ void __launch_bounds__(P2P_THREADS, 2) p2p_sig_kernel(
+    const float* __restrict__ s6, const float* __restrict__ ssig, int64_t n,
+    const int* __restrict__ leaf_start, int depth, float a, int periodic, KernelConsts kc1,
+    float* __restrict__ near6, unsigned long long* __restrict__ npairs, int64_t plo) {
+    constexpr int CAP = 1024;             // staged sources per window (40 B each)
+    __shared__ float4 S4[CAP], S4b[CAP];  // (x, y, z, gx), (gy, gz, c_j, 1/sigma_j)
+    extern __shared__ float2 p2ps_sm[];
+    float2* S2 = p2ps_sm;                  // (1/sigma_j^3, sigma_j^2 / 2)
+    __shared__ int rstart[65], rcnt[64], rsrc[64];
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const uint32_t parent = (uint32_t)(plo + blockIdx.x);
+    const int side = 1 << depth;
+    const int px = (int)compact3p(parent), py = (int)compact3p(parent >> 1),
+              pz = (int)compact3p(parent >> 2);
+    if (tid < 64) {
+        const int rx = tid & 3, ry = (tid >> 2) & 3, rz = tid >> 4;
+        int gx = 2 * px - 1 + rx, gy = 2 * py - 1 + ry, gz = 2 * pz - 1 + rz;
+        int cnt = 0, st = 0;
+        if (periodic || (gx >= 0 && gx < side && gy >= 0 && gy < side && gz >= 0 && gz < side)) {
+            gx &= side - 1;
+            gy &= side - 1;
+            gz &= side - 1;
+            const uint32_t lf = spread3p(gx) | (spread3p(gy) << 1) | (spread3p(gz) << 2);
+            st = leaf_start[lf];
+            cnt = leaf_start[lf + 1] - st;
+        }
+        rcnt[tid] = cnt;
+        rsrc[tid] = st;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int run = 0;
+        for (int i = 0; i < 64; ++i) {
+            rstart[i] = run;
+            run += rcnt[i];
+        }
+        rstart[64] = run;
+    }
+    __syncthreads();
+    const int bx = w & 1, by = (w >> 1) & 1, bz = (w >> 2) & 1;
+    const uint32_t tleaf = (parent << 3) | (uint32_t)w;
+    const int ts = leaf_start[tleaf], te = leaf_start[tleaf + 1];
+    const float tox = (bx - 0.5f) * a, toy = (by - 0.5f) * a, toz = (bz - 0.5f) * a;
+    const int total = rstart[64];
+    if (lane == 0) {
+        int ns = 0;
+        for (int nb = 0; nb < 27; ++nb)
+            ns += rcnt[(bx + nb % 3) + 4 * (by + (nb / 3) % 3) + 16 * (bz + nb / 9)];
+        if (te > ts) atomicAdd(npairs, (unsigned long long)(te - ts) * (unsigned long long)ns);
+    }
+    const int nchunk = (te - ts + 63) / 64;
+    __shared__ int maxchunk;
+    if (tid == 0) maxchunk = 0;
+    __syncthreads();
+    atomicMax(&maxchunk, nchunk);
+    __syncthreads();
+    const int nch = maxchunk;
+    for (int ch = 0; ch < nch; ++ch) {
+        const int i0 = ts + ch * 64 + lane, i1 = i0 + 32;
+        const bool a0 = i0 < te, a1 = i1 < te;
+        float x0 = 0, y0 = 0, z0 = 0, g0x = 0, g0y = 0, g0z = 0;
+        float x1 = 0, y1 = 0, z1 = 0, g1x = 0, g1y = 0, g1z = 0;
+        if (a0) {
+            x0 = s6[i0] + tox; y0 = s6[n + i0] + toy; z0 = s6[2 * n + i0] + toz;
+            g0x = s6[3 * n + i0]; g0y = s6[4 * n + i0]; g0z = s6[5 * n + i0];
+        }
+        if (a1) {
+            x1 = s6[i1] + tox; y1 = s6[n + i1] + toy; z1 = s6[2 * n + i1] + toz;
+            g1x = s6[3 * n + i1]; g1y = s6[4 * n + i1]; g1z = s6[5 * n + i1];
+        }
+        const f2 X = pk(x0, x1), Y = pk(y0, y1), Z = pk(z0, z1);
+        const f2 GX = pk(g0x, g1x), GY = pk(g0y, g1y), GZ = pk(g0z, g1z);
+        const f2 z2 = pk(0.f, 0.f);
+        Acc2 C = {z2, z2, z2, z2, z2, z2, z2, z2, z2};
+        for (int w0 = 0; w0 < total; w0 += CAP) {
+            const int w1 = min(w0 + CAP, total);
+            __syncthreads();
+            for (int rl = w; rl < 64; rl += P2P_THREADS / 32) {
+                const int lo = max(rstart[rl], w0), hi = min(rstart[rl + 1], w1);
+                if (lo >= hi) continue;
+                const int src = rsrc[rl] + (lo - rstart[rl]);
+                const float ox = ((rl & 3) - 1.5f) * a, oy = (((rl >> 2) & 3) - 1.5f) * a,
+                            oz = ((rl >> 4) - 1.5f) * a;
+                for (int k = lane; k < hi - lo; k += 32) {
+                    const int j = src + k;
+                    const float sg = ssig[j], isg = 1.f / sg;
+                    S4[lo - w0 + k] = make_float4(s6[j] + ox, s6[n + j] + oy, s6[2 * n + j] + oz,
+                                                  s6[3 * n + j]);
+                    S4b[lo - w0 + k] = make_float4(s6[4 * n + j], s6[5 * n + j],
+                                                   -1.4426950408889634f * 0.5f * isg * isg, isg);
+                    S2[lo - w0 + k] = make_float2(isg * isg * isg, 0.5f * sg * sg);
+                }
+            }
+            __syncthreads();
+            for (int nb = 0; nb < 27; ++nb) {
+                const int rx = bx + nb % 3, ry = by + (nb / 3) % 3, rz = bz + nb / 9;
+                const int rl = rx + 4 * ry + 16 * rz;
+                const int js = max(rstart[rl], w0) - w0, je = min(rstart[rl + 1], w1) - w0;
+                for (int j = js; j < je; ++j) {
+                    const float4 pa = S4[j], qa = S4b[j];
+                    const float2 sa = S2[j];
+                    const f2 dx = sub2(X, bc(pa.x)), dy = sub2(Y, bc(pa.y)), dz = sub2(Z, bc(pa.z));
+                    const f2 r2 = fma2(dx, dx, fma2(dy, dy, mul2(dz, dz)));
+                    float r0, r1;
+                    upk(r2, r0, r1);
+                    f2 f, q;
+                    const bool close = (a0 && r0 < sa.y) || (a1 && r1 < sa.y);
+                    if (__any_sync(0xffffffffu, close)) {
+                        float f0, q0, f1, q1;
+                        fq_closed2_sig(r2, qa.z, qa.w, sa.x, kc1, f, q);
+                        upk(f, f0, f1);
+                        upk(q, q0, q1);
+                        if (r0 < sa.y) fq_series_sig(r0, qa.w, sa.x, kc1, f0, q0);
+                        if (r1 < sa.y) fq_series_sig(r1, qa.w, sa.x, kc1, f1, q1);
+                        f = pk(f0, f1);
+                        q = pk(q0, q1);
+                    } else {
+                        fq_closed2_sig(r2, qa.z, qa.w, sa.x, kc1, f, q);
+                    }
+                    accumulate2<SCHEME>(dx, dy, dz, f, q, pa.w, qa.x, qa.y, GX, GY, GZ, C);
+                }
+            }
+        }
+        Acc c0, c1;
+        upk(C.u0, c0.u0, c1.u0);
+        upk(C.u1, c0.u1, c1.u1);
+        upk(C.u2, c0.u2, c1.u2);
+        upk(C.a0, c0.a0, c1.a0);
+        upk(C.a1, c0.a1, c1.a1);
+        upk(C.a2, c0.a2, c1.a2);
+        upk(C.b0, c0.b0, c1.b0);
+        upk(C.b1, c0.b1, c1.b1);
+        upk(C.b2, c0.b2, c1.b2);
+        float o[6];
+        if (a0) {
+            finish<SCHEME>(c0, g0x, g0y, g0z, o);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) near6[k * n + i0] = o[k];
+        }
+        if (a1) {
+            finish<SCHEME>(c1, g1x, g1y, g1z, o);
+#pragma unroll
+            for (int k = 0; k < 6; ++k) near6[k * n + i1] = o[k];
+        }
+    }
+}
+
+// DIRECT mode with per-source sigma_j: scalar pair of the same building blocks
+template <int SCHEME>
+__global__ void __launch_bounds__(128) direct_sig_kernel(const float* __restrict__ pos,
+                                                         const float* __restrict__ gam,
+                                                         const float* __restrict__ sig,
+                                                         int64_t n, double len, int m,
+                                                         KernelConsts kc1,
+                                                         float* __restrict__ vel,
+                                                         float* __restrict__ dgam) {
+    __shared__ double sx[128], sy[128], sz[128];
+    __shared__ float sgx[128], sgy[128], sgz[128], ss[128];
+    const int64_t i = blockIdx.x * (int64_t)128 + threadIdx.x;
+    const bool act = i < n;
+    double xi = 0, yi = 0, zi = 0;
+    float gix = 0, giy = 0, giz = 0;
+    if (act) {
+        xi = pos[i];
+        yi = pos[n + i];
+        zi = pos[2 * n + i];
+        gix = gam[i];
+        giy = gam[n + i];
+        giz = gam[2 * n + i];
+    }
+    double tot[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    const int side = 2 * m + 1;
+    for (int64_t sb = 0; sb < n; sb += 128) {
+        __syncthreads();
+        const int64_t j = sb + threadIdx.x;
+        if (j < n) {
+            sx[threadIdx.x] = pos[j];
+            sy[threadIdx.x] = pos[n + j];
+            sz[threadIdx.x] = pos[2 * n + j];
+            sgx[threadIdx.x] = gam[j];
+            sgy[threadIdx.x] = gam[n + j];
+            sgz[threadIdx.x] = gam[2 * n + j];
+            ss[threadIdx.x] = sig[j];
+        }
+        __syncthreads();
+        const int cnt = (int)min((int64_t)128, n - sb);
+        if (!act) continue;
+        for (int im = 0; im < side * side * side; ++im) {
+            const double shx = (im / (side * side) - m) * len;
+            const double shy = ((im / side) % side - m) * len;
+            const double shz = (im % side - m) * len;
+            Acc acc = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+            for (int qq = 0; qq < cnt; ++qq) {
+                const float dx = (float)(xi - sx[qq] - shx), dy = (float)(yi - sy[qq] - shy),
+                            dz = (float)(zi - sz[qq] - shz);
+                const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+                const float sgq = ss[qq], isg = 1.f / sgq;
+                float f, q;
+                if (r2 < 0.5f * sgq * sgq) {
+                    fq_series_sig(r2, isg, isg * isg * isg, kc1, f, q);
+                } else {
+                    f2 f2v, q2v;
+                    fq_closed2_sig(pk(r2, r2), -1.4426950408889634f * 0.5f * isg * isg, isg,
+                                   isg * isg * isg, kc1, f2v, q2v);
+                    float fb, qb;
+                    upk(f2v, f, fb);
+                    upk(q2v, q, qb);
+                }
+                accumulate<SCHEME>(dx, dy, dz, f, q, sgx[qq], sgy[qq], sgz[qq], gix, giy, giz, acc);
+            }
+            tot[0] += acc.u0;
+            tot[1] += acc.u1;
+            tot[2] += acc.u2;
+            tot[3] += acc.a0;
+            tot[4] += acc.a1;
+            tot[5] += acc.a2;
+            tot[6] += acc.b0;
+            tot[7] += acc.b1;
+            tot[8] += acc.b2;
+        }
+    }
+    if (act) {
+        float o[6];
+        const Acc t = {(float)tot[0], (float)tot[1], (float)tot[2], (float)tot[3], (float)tot[4],
+                       (float)tot[5], (float)tot[6], (float)tot[7], (float)tot[8]};
+        finish<SCHEME>(t, gix, giy, giz, o);
+        for (int k = 0; k < 3; ++k) {
+            vel[k * n + i] = o[k];
+            dgam[k * n + i] = o[3 + k];
+        }
+    }
+}
+
 // DIRECT mode: all pairs over the image cube; targets in input order, 128 per block.
 // d is formed in double from the float inputs, then rounded once (test mode).
 template <int SCHEME>
@@ -671,6 +943,34 @@ void launch_p2p(const float* sorted6, int64_t n, const int* leaf_start, int dept
         p2p_go<1, false, 2, 2>(P2P_ARGS);
     }
 #undef P2P_ARGS
+}
+
+void launch_p2p_sigma(const float* sorted6, const float* sorted_sig, int64_t n,
+                      const int* leaf_start, int depth, float a, int periodic, int scheme,
+                      float* near6, unsigned long long* npairs, int64_t plo, int64_t pcnt,
+                      cudaStream_t st) {
+    if (pcnt <= 0) return;
+    const KernelConsts kc1 = make_kernel_consts(1.f);
+    const size_t smem = 1024 * sizeof(float2);
+    if (scheme == 0)
+        p2p_sig_kernel<0><<<(unsigned)pcnt, P2P_THREADS, smem, st>>>(
+            sorted6, sorted_sig, n, leaf_start, depth, a, periodic, kc1, near6, npairs, plo);
+    else
+        p2p_sig_kernel<1><<<(unsigned)pcnt, P2P_THREADS, smem, st>>>(
+            sorted6, sorted_sig, n, leaf_start, depth, a, periodic, kc1, near6, npairs, plo);
+}
+
+void launch_direct_sigma(const float* pos, const float* gamma, const float* sigma, int64_t n,
+                         float len, int image_levels, int scheme, float* vel, float* dgam,
+                         cudaStream_t st) {
+    int m = 0;
+    for (int l = 0; l < image_levels; ++l) m = 3 * m + 1;
+    const KernelConsts kc1 = make_kernel_consts(1.f);
+    const unsigned grid = (unsigned)((n + 127) / 128);
+    if (scheme == 0)
+        direct_sig_kernel<0><<<grid, 128, 0, st>>>(pos, gamma, sigma, n, (double)len, m, kc1, vel, dgam);
+    else
+        direct_sig_kernel<1><<<grid, 128, 0, st>>>(pos, gamma, sigma, n, (double)len, m, kc1, vel, dgam);
 }
 
 void launch_direct(const float* pos, const float* gamma, int64_t n, float len, int image_levels,

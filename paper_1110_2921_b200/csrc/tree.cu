@@ -263,6 +263,20 @@ void launch_leaf_ranges(const uint32_t* keys_sorted, int64_t n, int depth, int* 
                                                             (int64_t)1 << (3 * depth), leaf_start);
 }
 
+namespace {
+__global__ void gather1_kernel(const float* __restrict__ in, const uint32_t* __restrict__ perm,
+                               int64_t n, float* __restrict__ out) {
+    for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n;
+         k += (int64_t)gridDim.x * blockDim.x)
+        out[k] = in[perm[k]];
+}
+}  // namespace
+
+void launch_gather1(const float* in, const uint32_t* perm, int64_t n, float* out,
+                    cudaStream_t st) {
+    gather1_kernel<<<grid_for(n, 256), 256, 0, st>>>(in, perm, n, out);
+}
+
 void launch_gather(const float* pos, const float* gamma, const uint32_t* perm,
                    const uint32_t* keys_sorted, int64_t n, Geom g, float* sorted6,
                    int64_t ostride, int64_t ooff, cudaStream_t st) {

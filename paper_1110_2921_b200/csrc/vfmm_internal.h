@@ -101,6 +101,10 @@ void launch_gather(const float* pos, const float* gamma, const uint32_t* perm,
                    const uint32_t* keys_sorted, int64_t n, Geom g, float* sorted6,
                    int64_t ostride, int64_t ooff, cudaStream_t st);
 
+// out[k] = in[perm[k]] (one float per particle into Morton order)
+void launch_gather1(const float* in, const uint32_t* perm, int64_t n, float* out,
+                    cudaStream_t st);
+
 // expansions.cu  (ranges: the owned part of the tree; whole tree for one rank)
 void launch_p2m(const float* sorted6, int64_t n, const int* leaf_start, int p, float inv_a,
                 float* M_leaf, int64_t leaf_lo, int64_t leaf_cnt, cudaStream_t st);
@@ -191,6 +195,14 @@ void launch_unpermute3(const float* in, const uint32_t* perm, int64_t n, float* 
 // step.cu: x += u dt (wrapped into the box when periodic), gamma += dgamma dt
 void launch_euler_update(float* pos, float* gamma, const float* vel, const float* dgamma,
                          int64_t n, float dt, float lo, float len, int periodic, cudaStream_t st);
+// per-particle core radius (Eq. 6's sigma_j): near field and DIRECT mode
+void launch_p2p_sigma(const float* sorted6, const float* sorted_sig, int64_t n,
+                      const int* leaf_start, int depth, float a, int periodic, int scheme,
+                      float* near6, unsigned long long* npairs, int64_t plo, int64_t pcnt,
+                      cudaStream_t st);
+void launch_direct_sigma(const float* pos, const float* gamma, const float* sigma, int64_t n,
+                         float len, int image_levels, int scheme, float* vel, float* dgam,
+                         cudaStream_t st);
 void launch_direct(const float* pos, const float* gamma, int64_t n, float len, int image_levels,
                    int scheme, KernelConsts kc, float* vel, float* dgam, cudaStream_t st);
 

@@ -1,0 +1,83 @@
+"""NEXT-4 (part): per-particle core radius sigma_j (Eq. 6 as written) in the near
+field and DIRECT mode (vfmm_evaluate_sigma) against O1 with per-source sigma_j."""
+import numpy as np
+import pytest
+
+import oracle
+import synthgen
+import tolerances as TOL
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+import paper_1110_2921_b200 as vf  # noqa: E402
+
+DEV = torch.device("cuda:0")
+
+
+def rel(a, b):
+    return float(np.linalg.norm(np.asarray(a, np.float64) - b) / np.linalg.norm(b))
+
+
+def _field(n=16, seed=3):
+    f = synthgen.jitter(synthgen.isotropic(n, seed=seed), 0.75, seed=seed)
+    rng = np.random.default_rng(seed)
+    h = f.box_len / n
+    sig = (h * rng.uniform(0.7, 1.3, f.pos.shape[1])).astype(np.float32)
+    return f, sig
+
+
+def _run(f, sig, **kw):
+    ev = vf.Evaluator(sigma=float(sig.max()), box_lo=f.box_lo, box_len=f.box_len, **kw)
+    v, s = ev.evaluate_sigma(torch.from_numpy(f.pos).to(DEV), torch.from_numpy(f.gamma).to(DEV),
+                             torch.from_numpy(sig).to(DEV))
+    ev.sync_status()
+    return v.cpu().numpy().astype(np.float64), s.cpu().numpy().astype(np.float64), ev
+
+
+@pytest.mark.parametrize("scheme", [0, 1])
+def test_sigma_direct_and_near_only_vs_oracle(scheme):
+    f, sig = _field()
+    tg = np.arange(0, f.pos.shape[1], 13)
+    v, s, ev = _run(f, sig, p=2, image_levels=1, scheme=scheme, mode=vf.MODE_DIRECT)
+    vo, so = oracle.direct(f.pos, f.gamma, sig.astype(np.float64), f.box_lo, f.box_len, 1,
+                           scheme, targets=tg)
+    eu, es = rel(v[:, tg], vo), rel(s[:, tg], so)
+    print(f"sigma_j DIRECT scheme {scheme}: u {eu:.2e} sdot {es:.2e}")
+    assert eu < TOL.DIRECT_VS_ORACLE[0] and es < TOL.DIRECT_VS_ORACLE[1], (eu, es)
+    ev.close()
+    # depth 1, free space: the near field alone is the whole sum
+    v, s, ev = _run(f, sig, p=2, depth=1, image_levels=0, scheme=scheme, mode=vf.MODE_NEAR_ONLY)
+    vo, so = oracle.direct(f.pos, f.gamma, sig.astype(np.float64), f.box_lo, f.box_len, 0,
+                           scheme, targets=tg)
+    eu, es = rel(v[:, tg], vo), rel(s[:, tg], so)
+    print(f"sigma_j NEAR_ONLY depth 1 scheme {scheme}: u {eu:.2e} sdot {es:.2e}")
+    assert eu < TOL.NEAR_VS_ORACLE[0] and es < TOL.NEAR_VS_ORACLE[1], (eu, es)
+    ev.close()
+
+
+def test_sigma_fmm_vs_oracle_and_uniform_case():
+    """FMM at p = 10 with sigma_j in [0.7 h, 1.3 h] (leaf width 4 h >= 4 sigma_j up to 1 h, the
+    cutoff omission stays below 1e-3 per far pair) against O1; a uniform sigma_j array equals
+    the uniform-sigma evaluation to FP32 rounding."""
+    f, sig = _field(32, seed=5)
+    tg = synthgen.sample_targets(32 ** 3, 48, n_lattice=32)
+    v, s, ev = _run(f, sig, p=10, depth=3, image_levels=1)
+    vo, so = oracle.direct(f.pos, f.gamma, sig.astype(np.float64), f.box_lo, f.box_len, 1, 0,
+                           targets=tg)
+    eu, es = rel(v[:, tg], vo), rel(s[:, tg], so)
+    print(f"sigma_j FMM p=10: u {eu:.2e} sdot {es:.2e}")
+    tu, ts = TOL.FMM_VS_DIRECT[8]  # the far field omits the cutoff of sigma_j up to 1.3 h
+    assert eu < tu and es < ts, (eu, es)
+    ev.close()
+    uni = np.full_like(sig, np.float32(f.sigma))
+    v1, s1, ev1 = _run(f, uni, p=10, depth=3, image_levels=1)
+    ev2 = vf.Evaluator(sigma=f.sigma, p=10, depth=3, image_levels=1, box_lo=f.box_lo,
+                       box_len=f.box_len)
+    v2, s2 = ev2.evaluate(torch.from_numpy(f.pos).to(DEV), torch.from_numpy(f.gamma).to(DEV))
+    v2, s2 = v2.cpu().numpy(), s2.cpu().numpy()
+    assert rel(v1, v2) < 2e-6 and rel(s1, s2) < 2e-6, (rel(v1, v2), rel(s1, s2))
+    ev1.close()
+    ev2.close()
