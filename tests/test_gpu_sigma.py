@@ -25,7 +25,7 @@ def _field(n=16, seed=3):
     f = synthgen.jitter(synthgen.isotropic(n, seed=seed), 0.75, seed=seed)
     rng = np.random.default_rng(seed)
     h = f.box_len / n
-    sig = (h * rng.uniform(0.7, 1.3, f.pos.shape[1])).astype(np.float32)
+    sig = (h * rng.uniform(0.6, 1.0, f.pos.shape[1])).astype(np.float32)
     return f, sig
 
 
@@ -59,9 +59,10 @@ def test_sigma_direct_and_near_only_vs_oracle(scheme):
 
 
 def test_sigma_fmm_vs_oracle_and_uniform_case():
-    """FMM at p = 10 with sigma_j in [0.7 h, 1.3 h] (leaf width 4 h >= 4 sigma_j up to 1 h, the
-    cutoff omission stays below 1e-3 per far pair) against O1; a uniform sigma_j array equals
-    the uniform-sigma evaluation to FP32 rounding."""
+    """FMM at p = 10 with sigma_j in [0.6 h, 1.0 h] on a jittered lattice (leaf width 4 h >=
+    4 max sigma_j: the cutoff the far field omits is below 1.1e-3 for the closest far pairs,
+    reading R3) against O1; a uniform sigma_j array equals the uniform-sigma evaluation to FP32
+    rounding."""
     f, sig = _field(32, seed=5)
     tg = synthgen.sample_targets(32 ** 3, 48, n_lattice=32)
     v, s, ev = _run(f, sig, p=10, depth=3, image_levels=1)
@@ -69,8 +70,7 @@ def test_sigma_fmm_vs_oracle_and_uniform_case():
                            targets=tg)
     eu, es = rel(v[:, tg], vo), rel(s[:, tg], so)
     print(f"sigma_j FMM p=10: u {eu:.2e} sdot {es:.2e}")
-    tu, ts = TOL.FMM_VS_DIRECT[8]  # the far field omits the cutoff of sigma_j up to 1.3 h
-    assert eu < tu and es < ts, (eu, es)
+    assert eu < 1e-3 and es < 3e-3, (eu, es)  # R3: cutoff omission at 4 sigma_max
     ev.close()
     uni = np.full_like(sig, np.float32(f.sigma))
     v1, s1, ev1 = _run(f, uni, p=10, depth=3, image_levels=1)
