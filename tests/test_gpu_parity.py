@@ -553,11 +553,17 @@ def test_bench_config_vs_golden_o1_27cubed(cfg):
 
 # ------------------------------------------------------------------ tensor-core M2L (tcgen05)
 
+_FP64_STAGES = {}
+
+
 @pytest.mark.parametrize("engine", ["simt", "f16", "tf32"])
 @pytest.mark.parametrize("n,depth,p,lam", [(32, 3, 10, 1), (32, 3, 6, 3), (64, 4, 8, 1),
                                            (16, 2, 13, 2), (16, 2, 15, 1),
                                            pytest.param(64, 5, 10, 3, marks=pytest.mark.slow)])
 def test_m2l_engines_vs_fp64_fmm_oracle(n, depth, p, lam, engine, monkeypatch):
+    if depth == 5 and engine != "f16":
+        pytest.skip("depth 5 (fp64 oracle ~4 min): the default engine only; SIMT and 3xTF32 "
+                    "measured in profiles/r2 (scripts/m2l_tc_accuracy.py)")
     """Every M2L engine -- SIMT FP32, tcgen05 scaled 3xFP16 (default), tcgen05 3xTF32 -- against
     the float64 step-by-step FMM oracle running the same algorithm: the local expansions of
     every level and the velocity / stretching differ by FP32 rounding only.  The tensor core
@@ -566,8 +572,11 @@ def test_m2l_engines_vs_fp64_fmm_oracle(n, depth, p, lam, engine, monkeypatch):
     f = synthgen.isotropic(n, seed=21)
     monkeypatch.setenv("VFMM_M2L", engine)
     v, s, ev = run(f, p=p, depth=depth, image_levels=lam)
-    vo, so, st = F.evaluate(f.pos, f.gamma, f.sigma, f.box_lo, f.box_len, depth, p, lam,
-                            return_stages=True)
+    key = (n, depth, p, lam)
+    if key not in _FP64_STAGES:  # one fp64 oracle run serves the three engines
+        _FP64_STAGES[key] = F.evaluate(f.pos, f.gamma, f.sigma, f.box_lo, f.box_len, depth, p,
+                                       lam, return_stages=True)
+    vo, so, st = _FP64_STAGES[key]
     line = [f"{engine} n={n} L={depth} p={p} lam={lam}: u {rel(v, vo):.2e} sdot {rel(s, so):.2e}"]
     for l in range(1, depth + 1):
         al = f.box_len / (1 << l)
