@@ -780,8 +780,13 @@ static vfmm_status evaluate_impl(vfmm_ctx* c, int64_t n, const float* pos, const
         c->have_exp = false;
         return VFMM_OK;
     }
-    if (P.depth == -1 && !(c->tuned_n == n && c->tuned_p == P.p && c->tuned_mode == P.mode &&
-                           c->tuned_levels == P.image_levels)) {
+    // a cached choice stays valid while its leaf width keeps >= 4 sigma (reading R3; sigma
+    // grows by core spreading in vfmm_step)
+    const bool tuned_valid =
+        c->tuned_n == n && c->tuned_p == P.p && c->tuned_mode == P.mode &&
+        c->tuned_levels == P.image_levels &&
+        (double)P.box_len / (double)(1 << c->tuned_depth) >= 4.0 * (double)P.sigma * (1.0 - 1e-6);
+    if (P.depth == -1 && !tuned_valid) {
         // time the default depth and its two neighbours once (the paper's auto-tuning picks
         // the particles per box by measurement), keep the fastest
         const int L0 = auto_depth(P, n);
