@@ -16,6 +16,7 @@
 #include <cmath>
 #include <cstdlib>
 #include <cstring>
+#include <type_traits>
 
 #include "vfmm_internal.h"
 
@@ -328,6 +329,10 @@ __global__ void __launch_bounds__(P2P_THREADS, MINB == 1 ? 2 : MINB) p2p_kernel(
     float* S1 = reinterpret_cast<float*>(S4b + P2P_CAP + P2P_PAD);
     float2* S2 = reinterpret_cast<float2*>(S4 + P2P_CAP + P2P_PAD);
     __shared__ int rstart[65], rcnt[64], rsrc[64];
+    // bounding box of each staged leaf's real sources in the current window (min xyz, max xyz):
+    // a target chunk and a source leaf whose boxes are further apart than the series threshold
+    // have no close pair, so that leaf runs the pair loop without the per-iteration test
+    __shared__ float sbox[64][6];
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const uint32_t parent = (uint32_t)(plo + blockIdx.x);
     const int side = 1 << depth;
@@ -393,6 +398,22 @@ __global__ void __launch_bounds__(P2P_THREADS, MINB == 1 ? 2 : MINB) p2p_kernel(
             x1 = s6[i1] + tox; y1 = s6[n + i1] + toy; z1 = s6[2 * n + i1] + toz;
             g1x = s6[3 * n + i1]; g1y = s6[4 * n + i1]; g1z = s6[5 * n + i1];
         }
+        // the warp's target box (warp-uniform after the reduction)
+        float tb[6];
+        tb[0] = fminf(a0 ? x0 : 1e30f, a1 ? x1 : 1e30f);
+        tb[1] = fminf(a0 ? y0 : 1e30f, a1 ? y1 : 1e30f);
+        tb[2] = fminf(a0 ? z0 : 1e30f, a1 ? z1 : 1e30f);
+        tb[3] = fmaxf(a0 ? x0 : -1e30f, a1 ? x1 : -1e30f);
+        tb[4] = fmaxf(a0 ? y0 : -1e30f, a1 ? y1 : -1e30f);
+        tb[5] = fmaxf(a0 ? z0 : -1e30f, a1 ? z1 : -1e30f);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                tb[c] = fminf(tb[c], __shfl_xor_sync(0xffffffffu, tb[c], o));
+                tb[c + 3] = fmaxf(tb[c + 3], __shfl_xor_sync(0xffffffffu, tb[c + 3], o));
+            }
+        }
         // targets (i0, i1) packed in the two halves of f2 registers
         const f2 X = pk(x0, x1), Y = pk(y0, y1), Z = pk(z0, z1);
         const f2 GX = pk(g0x, g1x), GY = pk(g0y, g1y), GZ = pk(g0z, g1z);
@@ -413,6 +434,7 @@ __global__ void __launch_bounds__(P2P_THREADS, MINB == 1 ? 2 : MINB) p2p_kernel(
                 const int src = rsrc[rl] + (lo - rstart[rl]);
                 const float ox = ((rl & 3) - 1.5f) * a, oy = (((rl >> 2) & 3) - 1.5f) * a,
                             oz = ((rl >> 4) - 1.5f) * a;
+                float bmin[3] = {1e30f, 1e30f, 1e30f}, bmax[3] = {-1e30f, -1e30f, -1e30f};
                 for (int k = lane; k < hi - lo; k += 32) {
                     // an odd leaf ends with a padding source: far away, zero strength (exact 0
                     // contribution), so the pair loop runs over whole pairs of sources
@@ -420,6 +442,14 @@ __global__ void __launch_bounds__(P2P_THREADS, MINB == 1 ? 2 : MINB) p2p_kernel(
                     const bool real = lo - rstart[rl] + k < rcnt[rl];
                     const float x = real ? s6[j] + ox : 1e4f, y = real ? s6[n + j] + oy : 1e4f,
                                 z = real ? s6[2 * n + j] + oz : 1e4f;
+                    if (real) {
+                        bmin[0] = fminf(bmin[0], x);
+                        bmin[1] = fminf(bmin[1], y);
+                        bmin[2] = fminf(bmin[2], z);
+                        bmax[0] = fmaxf(bmax[0], x);
+                        bmax[1] = fmaxf(bmax[1], y);
+                        bmax[2] = fmaxf(bmax[2], z);
+                    }
                     const float gx = real ? s6[3 * n + j] : 0.f, gy = real ? s6[4 * n + j] : 0.f,
                                 gz = real ? s6[5 * n + j] : 0.f;
                     S4[lo - w0 + k] = make_float4(x, y, z, gx);
@@ -428,6 +458,21 @@ __global__ void __launch_bounds__(P2P_THREADS, MINB == 1 ? 2 : MINB) p2p_kernel(
                         S1[lo - w0 + k] = gx * y - gy * x;
                     } else {
                         S2[lo - w0 + k] = make_float2(gy, gz);
+                    }
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        bmin[c] = fminf(bmin[c], __shfl_xor_sync(0xffffffffu, bmin[c], o));
+                        bmax[c] = fmaxf(bmax[c], __shfl_xor_sync(0xffffffffu, bmax[c], o));
+                    }
+                }
+                if (lane == 0) {
+#pragma unroll
+                    for (int c = 0; c < 3; ++c) {
+                        sbox[rl][c] = bmin[c];
+                        sbox[rl][c + 3] = bmax[c];
                     }
                 }
             }
@@ -446,6 +491,15 @@ __global__ void __launch_bounds__(P2P_THREADS, MINB == 1 ? 2 : MINB) p2p_kernel(
                     const float2 t = S2[jj];
                     return make_float4(t.x, t.y, 0.f, 0.f);
                 };
+                // the source leaf's box apart from the target box by more than the series
+                // threshold: no close pair, no per-iteration test (warp-uniform decision)
+                const float th = kc.r2_series;
+                const float gx_ = fmaxf(0.f, fmaxf(sbox[rl][0] - tb[3], tb[0] - sbox[rl][3]));
+                const float gy_ = fmaxf(0.f, fmaxf(sbox[rl][1] - tb[4], tb[1] - sbox[rl][4]));
+                const float gz_ = fmaxf(0.f, fmaxf(sbox[rl][2] - tb[5], tb[2] - sbox[rl][5]));
+                const bool apart = gx_ * gx_ + gy_ * gy_ + gz_ * gz_ >= th;
+                auto pairs = [&](auto check_tag) {
+                constexpr bool CHECK = decltype(check_tag)::value;
                 // unrolled by 2 (c4 P2P: 43.1 ms; 49.6 without unrolling, 44.0 unrolled by 4)
 #pragma unroll UNR
                 for (int j = js; j < je; j += 2) {  // js, je even (padded leaves, even CAP)
@@ -462,10 +516,13 @@ __global__ void __launch_bounds__(P2P_THREADS, MINB == 1 ? 2 : MINB) p2p_kernel(
                     float ra0, ra1, rb0, rb1;
                     upk(r2a, ra0, ra1);
                     upk(r2b, rb0, rb1);
-                    const float th = kc.r2_series;
-                    const bool close = (a0 && (ra0 < th || rb0 < th)) || (a1 && (ra1 < th || rb1 < th));
+                    const bool close = CHECK && ((a0 && (ra0 < th || rb0 < th)) ||
+                                                 (a1 && (ra1 < th || rb1 < th)));
                     f2 fa, qa2, fb, qb2;
-                    if (SJ) {
+                    if (!CHECK) {
+                        fq_closed2(r2a, kc, fa, qa2);
+                        fq_closed2(r2b, kc, fb, qb2);
+                    } else if (SJ) {
                         // closed form for all pairs, outside the branch (schedules with the
                         // other unrolled iteration); the rare close pairs (self pairs, rho^2 <
                         // 1/4) then get the Taylor series in place (41.9 ms; 42.7 with the
@@ -513,6 +570,9 @@ __global__ void __launch_bounds__(P2P_THREADS, MINB == 1 ? 2 : MINB) p2p_kernel(
                         accumulate2<SCHEME>(dxb, dyb, dzb, fb, qb2, gbx, qb.x, qb.y, GX, GY, GZ, C);
                     }
                 }
+                };
+                if (apart) pairs(std::false_type{});
+                else pairs(std::true_type{});
             }
         }
         if (SJ) {  // u = A x x_i - V, B = Wg x x_i - Ws
