@@ -328,7 +328,8 @@ __global__ void __launch_bounds__(P2P_THREADS, MINB == 1 ? 2 : MINB) p2p_kernel(
     float4* S4b = S4 + P2P_CAP + P2P_PAD;
     float* S1 = reinterpret_cast<float*>(S4b + P2P_CAP + P2P_PAD);
     float2* S2 = reinterpret_cast<float2*>(S4 + P2P_CAP + P2P_PAD);
-    __shared__ int rstart[65], rcnt[64], rsrc[64];
+    __shared__ int rstart[65], rend[64], rcnt[64], rsrc[64];
+    __shared__ int wsplit;
     // bounding box of each staged leaf's real sources in the current window (min xyz, max xyz):
     // a target chunk and a source leaf whose boxes are further apart than the series threshold
     // have no close pair, so that leaf runs the pair loop without the per-iteration test
@@ -356,10 +357,18 @@ __global__ void __launch_bounds__(P2P_THREADS, MINB == 1 ? 2 : MINB) p2p_kernel(
     }
     __syncthreads();
     if (tid == 0) {  // staged offsets: every leaf padded to an even count (see staging)
+        // z-layers in the order 1, 2, 0, 3: every warp's 27 neighbours span the two middle
+        // layers plus one outer layer, so a region staged in two windows (middle | outer)
+        // gives every warp 18 + 9 leaves -- balanced windows, short barrier waits
         int run = 0;
-        for (int i = 0; i < 64; ++i) {
-            rstart[i] = run;
-            run += (rcnt[i] + 1) & ~1;
+        for (int li = 0; li < 4; ++li) {
+            const int rz = li == 0 ? 1 : li == 1 ? 2 : li == 2 ? 0 : 3;
+            if (li == 2) wsplit = run;
+            for (int i = 16 * rz; i < 16 * rz + 16; ++i) {
+                rstart[i] = run;
+                run += (rcnt[i] + 1) & ~1;
+                rend[i] = run;
+            }
         }
         rstart[64] = run;
     }
@@ -425,11 +434,14 @@ __global__ void __launch_bounds__(P2P_THREADS, MINB == 1 ? 2 : MINB) p2p_kernel(
         // windows [w0, w1) of the concatenated region sources, P2P_CAP at a time (a warp idle
         // at a window barrier leaves the pipes to the SM's other block; balanced two-phase
         // staging by source layers measured 1.5% slower for its 25% extra staging)
-        for (int w0 = 0; w0 < total; w0 += P2P_CAP) {
-            const int w1 = min(w0 + P2P_CAP, total);
+        // windows: the whole region, or middle | outer layers when each fits, else P2P_CAP
+        // chunks (dense leaves)
+        const bool split2 = total > P2P_CAP && wsplit <= P2P_CAP && total - wsplit <= P2P_CAP;
+        for (int w0 = 0, w1 = 0; w0 < total; w0 = w1) {
+            w1 = split2 ? (w0 == 0 ? wsplit : total) : min(w0 + P2P_CAP, total);
             __syncthreads();
             for (int rl = w; rl < 64; rl += P2P_THREADS / 32) {
-                const int lo = max(rstart[rl], w0), hi = min(rstart[rl + 1], w1);
+                const int lo = max(rstart[rl], w0), hi = min(rend[rl], w1);
                 if (lo >= hi) continue;
                 const int src = rsrc[rl] + (lo - rstart[rl]);
                 const float ox = ((rl & 3) - 1.5f) * a, oy = (((rl >> 2) & 3) - 1.5f) * a,
@@ -480,7 +492,7 @@ __global__ void __launch_bounds__(P2P_THREADS, MINB == 1 ? 2 : MINB) p2p_kernel(
             for (int nb = 0; nb < 27; ++nb) {
                 const int rx = bx + nb % 3, ry = by + (nb / 3) % 3, rz = bz + nb / 9;
                 const int rl = rx + 4 * ry + 16 * rz;
-                const int js = max(rstart[rl], w0) - w0, je = min(rstart[rl + 1], w1) - w0;
+                const int js = max(rstart[rl], w0) - w0, je = min(rend[rl], w1) - w0;
                 if (js >= je) continue;  // leaf not in this window
                 // two sources per iteration; each source x two targets = one packed pair
                 // (SJ: the 4-wide second record; else the 2-wide one, zero-extended).  Loads
