@@ -58,7 +58,7 @@ def test_sigma_direct_and_near_only_vs_oracle(scheme):
     ev.close()
 
 
-def test_sigma_fmm_vs_oracle_and_uniform_case():
+def test_sigma_fmm_vs_oracle_and_uniform_case(monkeypatch):
     """FMM at p = 10 with sigma_j in [0.6 h, 1.0 h] on a jittered lattice (leaf width 4 h >=
     4 max sigma_j: the cutoff the far field omits is below 1.1e-3 for the closest far pairs,
     reading R3) against O1; a uniform sigma_j array equals the uniform-sigma evaluation to FP32
@@ -72,6 +72,7 @@ def test_sigma_fmm_vs_oracle_and_uniform_case():
     print(f"sigma_j FMM p=10: u {eu:.2e} sdot {es:.2e}")
     assert eu < 1e-3 and es < 3e-3, (eu, es)  # R3: cutoff omission at 4 sigma_max
     ev.close()
+    monkeypatch.setenv("VFMM_P2P", "cross")  # the sigma_j kernel accumulates per-pair cross products
     uni = np.full_like(sig, np.float32(f.sigma))
     v1, s1, ev1 = _run(f, uni, p=10, depth=3, image_levels=1)
     ev2 = vf.Evaluator(sigma=f.sigma, p=10, depth=3, image_levels=1, box_lo=f.box_lo,
