@@ -999,9 +999,14 @@ void launch_p2p(const float* sorted6, int64_t n, const int* leaf_start, int dept
     const bool sj = !(env && strcmp(env, "cross") == 0);
     const char* cfg = getenv("VFMM_P2P_CFG");
     const int v = !cfg ? 0 : strcmp(cfg, "b3u1") == 0 ? 1 : strcmp(cfg, "b3u2") == 0 ? 2
-                                : strcmp(cfg, "b2u1") == 0 ? 3 : 0;
+                                : strcmp(cfg, "b2u1") == 0 ? 3 : strcmp(cfg, "s4") == 0 ? 4
+                                : strcmp(cfg, "s1") == 0 ? 5 : 0;
 #define P2P_ARGS sorted6, n, leaf_start, depth, a, periodic, kc, near6, npairs, plo, pcnt, st
-    if (scheme == 0 && sj && !lean && v == 0) {
+    if (scheme == 0 && sj && !lean && v == 4) {
+        p2p_go<0, true, 2, 4>(P2P_ARGS);
+    } else if (scheme == 0 && sj && !lean && v == 5) {
+        p2p_go<0, true, 2, 1>(P2P_ARGS);
+    } else if (scheme == 0 && sj && !lean && v == 0) {
         p2p_go<0, true, 2, 2>(P2P_ARGS);
     } else if (lean) {
         if (scheme == 0) p2p_go<0, false, 1, 2>(P2P_ARGS);
