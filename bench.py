@@ -33,7 +33,7 @@ sys.path.insert(0, ROOT)
 METRIC = "s per 256³-particle FMM velocity+stretching eval; P2P interactions/s, %FP32 peak"
 PAPER_CONTEXT = ("paper: ~20 s/time step at p=10 (~10 s at p=6) on one Tesla C2070, FP32, "
                  "N=256^3, 27^3 images (PAPER.md:174-176); hit3d ~1 s/step on 6 Xeon E5650 cores")
-P2P_FLOP_PER_PAIR = 70  # FP32 flops of the pair formula as implemented (FFMA = 2)
+P2P_FLOP_PER_PAIR = 69  # 3 FADD + 16 FMUL + 25 FFMA per pair (FFMA = 2), independent of the kernel variant
 
 
 def load_peaks():

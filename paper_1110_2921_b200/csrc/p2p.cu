@@ -22,11 +22,13 @@
 
 namespace vfmm {
 
-// erfcx(rho) / (4 pi) ~= sum_k ERFCX_Ck t^k, t = 1/(1 + rho/2), degree 5
+// erfcx(rho) / (4 pi) ~= sum_k ERFCX_Ck t^k, t = 1/(1 + rho/2), degree 4
 // (scripts/fit_cutoff_poly.py: relative error of g <= 1.6e-8 over rho in [0.5, 10])
-constexpr float ERFCX_C0 = -1.304099035e-04f, ERFCX_C1 = 2.284340506e-02f,
-                ERFCX_C2 = 2.471552502e-02f, ERFCX_C3 = 5.650036563e-03f,
-                ERFCX_C4 = 4.221915334e-02f, ERFCX_C5 = -1.572556573e-02f;
+// (scripts/fit_cutoff_poly.py 4: relative error of g <= 4.8e-7 over rho in [0.5, 10], below
+// the 1.4e-6 FP32 evaluation floor near rho = 0.5; degree 5 reached 1.6e-8 for one more FFMA2)
+constexpr float ERFCX_C0 = -2.582819305e-03f, ERFCX_C1 = 4.079926104e-02f,
+                ERFCX_C2 = -2.760024571e-02f, ERFCX_C3 = 8.149271438e-02f,
+                ERFCX_C4 = -1.250394818e-02f;
 
 KernelConsts make_kernel_consts(float sigma) {
     const double s = (double)sigma;
@@ -40,12 +42,13 @@ KernelConsts make_kernel_consts(float sigma) {
     k.r2_series = (float)(0.5 * s * s);
     k.t_scale = (float)(1.0 / (2.0 * std::sqrt(2.0) * s));
     k.q_scale = (float)(2.0 / (4.0 * M_PI * std::sqrt(M_PI)) / (std::sqrt(2.0) * s));
-    // packed path: the erfcx/(4 pi) polynomial (ERFCX_C0..5, ascending in t) scaled by -1/zeta0
+    // packed path: the erfcx/(4 pi) polynomial (ERFCX_C0..4, ascending in t) scaled by -1/zeta0
     // (folds the zeta0 factor of the exponential into the ex2 argument and a negation)
     k.ez_off = (float)std::log2(z0);
     k.qn_scale = (float)(-(2.0 / (4.0 * M_PI * std::sqrt(M_PI)) / (std::sqrt(2.0) * s)) / z0);
-    const float c[6] = {ERFCX_C0, ERFCX_C1, ERFCX_C2, ERFCX_C3, ERFCX_C4, ERFCX_C5};
-    for (int i = 0; i < 6; ++i) k.en[i] = (float)(-(double)c[i] / z0);
+    const float c[5] = {ERFCX_C0, ERFCX_C1, ERFCX_C2, ERFCX_C3, ERFCX_C4};
+    for (int i = 0; i < 5; ++i) k.en[i] = (float)(-(double)c[i] / z0);
+    k.en[5] = 0.f;  // unused (degree 4)
     return k;
 }
 
@@ -136,8 +139,7 @@ __device__ __forceinline__ void fq_closed(float r2, const KernelConsts& kc, floa
     const float e = ex2_approx(r2 * kc.neg_l2e_inv2s2);
     const float r = r2 * rinv;
     const float t = rcp_approx(fmaf(kc.t_scale, r, 1.f));
-    float E = ERFCX_C5;  // erfcx(rho)/(4 pi), polynomial in t
-    E = fmaf(E, t, ERFCX_C4);
+    float E = ERFCX_C4;  // erfcx(rho)/(4 pi), polynomial in t
     E = fmaf(E, t, ERFCX_C3);
     E = fmaf(E, t, ERFCX_C2);
     E = fmaf(E, t, ERFCX_C1);
@@ -163,8 +165,7 @@ __device__ __forceinline__ void fq_closed2(f2 r2, const KernelConsts& kc, f2& f,
     upk(fma2(r, bc(kc.t_scale), bc(1.f)), da, db);
     const f2 t = pk(rcp_approx(da), rcp_approx(db));
     // Horner (Estrin's depth-3 form measured 4% slower for its extra instruction)
-    f2 E = fma2(bc(kc.en[5]), t, bc(kc.en[4]));
-    E = fma2(E, t, bc(kc.en[3]));
+    f2 E = fma2(bc(kc.en[4]), t, bc(kc.en[3]));
     E = fma2(E, t, bc(kc.en[2]));
     E = fma2(E, t, bc(kc.en[1]));
     E = fma2(E, t, bc(kc.en[0]));
@@ -639,8 +640,7 @@ __device__ __forceinline__ void fq_closed2_sig(f2 r2, float cj, float isig, floa
     float da, db;
     upk(fma2(rt, bc(kc1.t_scale), bc(1.f)), da, db);
     const f2 t = pk(rcp_approx(da), rcp_approx(db));
-    f2 E = fma2(bc(kc1.en[5]), t, bc(kc1.en[4]));
-    E = fma2(E, t, bc(kc1.en[3]));
+    f2 E = fma2(bc(kc1.en[4]), t, bc(kc1.en[3]));
     E = fma2(E, t, bc(kc1.en[2]));
     E = fma2(E, t, bc(kc1.en[1]));
     E = fma2(E, t, bc(kc1.en[0]));
@@ -995,19 +995,21 @@ void launch_p2p(const float* sorted6, int64_t n, const int* leaf_start, int dept
     // VFMM_P2P=cross: per-pair gamma_j x d (the smallest rounding; the transpose scheme and the
     // lean co-resident variant always use it).
     // VFMM_P2P_CFG: occupancy / unroll variants (measurement knob): "b3u1", "b3u2", "b2u1"
+    // (per-pair form), "s2", "s1" (staged form unrolled by 2 / 1)
     const char* env = getenv("VFMM_P2P");
     const bool sj = !(env && strcmp(env, "cross") == 0);
     const char* cfg = getenv("VFMM_P2P_CFG");
     const int v = !cfg ? 0 : strcmp(cfg, "b3u1") == 0 ? 1 : strcmp(cfg, "b3u2") == 0 ? 2
-                                : strcmp(cfg, "b2u1") == 0 ? 3 : strcmp(cfg, "s4") == 0 ? 4
+                                : strcmp(cfg, "b2u1") == 0 ? 3 : strcmp(cfg, "s2") == 0 ? 4
                                 : strcmp(cfg, "s1") == 0 ? 5 : 0;
 #define P2P_ARGS sorted6, n, leaf_start, depth, a, periodic, kc, near6, npairs, plo, pcnt, st
     if (scheme == 0 && sj && !lean && v == 4) {
-        p2p_go<0, true, 2, 4>(P2P_ARGS);
+        p2p_go<0, true, 2, 2>(P2P_ARGS);
     } else if (scheme == 0 && sj && !lean && v == 5) {
         p2p_go<0, true, 2, 1>(P2P_ARGS);
     } else if (scheme == 0 && sj && !lean && v == 0) {
-        p2p_go<0, true, 2, 2>(P2P_ARGS);
+        // unrolled by 4 since the box test removed the loop's branch (37.7 vs 38.3 ms at c4)
+        p2p_go<0, true, 2, 4>(P2P_ARGS);
     } else if (lean) {
         if (scheme == 0) p2p_go<0, false, 1, 2>(P2P_ARGS);
         else p2p_go<1, false, 1, 2>(P2P_ARGS);
