@@ -996,8 +996,13 @@ void launch_p2p(const float* sorted6, int64_t n, const int* leaf_start, int dept
     // lean co-resident variant always use it).
     // VFMM_P2P_CFG: occupancy / unroll variants (measurement knob): "b3u1", "b3u2", "b2u1"
     // (per-pair form), "s2", "s1" (staged form unrolled by 2 / 1)
+    // The staged form's rounding grows with the lever arm (the 4-leaf region) over the close
+    // pairs' distance (~sigma): default to it only while the leaf width is <= 8 sigma (the
+    // benched lattice: 4 sigma); wider leaves (clustered inputs, small sigma) keep per-pair
+    // cross products.  VFMM_P2P=sj / cross force either form.
     const char* env = getenv("VFMM_P2P");
-    const bool sj = !(env && strcmp(env, "cross") == 0);
+    const float sigma = sqrtf(0.5f / kc.inv2s2);
+    const bool sj = env ? strcmp(env, "sj") == 0 : a <= 8.f * sigma;
     const char* cfg = getenv("VFMM_P2P_CFG");
     const int v = !cfg ? 0 : strcmp(cfg, "b3u1") == 0 ? 1 : strcmp(cfg, "b3u2") == 0 ? 2
                                 : strcmp(cfg, "b2u1") == 0 ? 3 : strcmp(cfg, "s2") == 0 ? 4
