@@ -41,6 +41,12 @@ __device__ __forceinline__ f2x ffma2(f2x a, f2x b, f2x c) {
     asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(a), "l"(b), "l"(c));
     return r;
 }
+__device__ __forceinline__ f2x fmul2(f2x a, f2x b) {
+    f2x r;
+    asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(a), "l"(b));
+    return r;
+}
+__device__ __forceinline__ f2x bc2(float a) { return pk2(a, a); }
 
 __device__ __forceinline__ uint32_t spread3d(uint32_t v) {
     v &= 0x3ffu;
@@ -565,6 +571,164 @@ __global__ void __launch_bounds__(64) l2p_combine_kernel(
     }
 }
 
+// The same combine with two particles per thread (j, j + 32) in the halves of packed FP32x2
+// registers: one warp per leaf, every D row loaded once for both particles (half the shared-
+// memory loads of l2p_combine_kernel) and the solid-harmonic recurrence run packed.
+template <int SCHEME, int PC>
+__global__ void __launch_bounds__(32) l2p_combine_pair_kernel(
+    const float* __restrict__ s6, const float* __restrict__ near6,
+    const uint32_t* __restrict__ perm, int64_t n, const int* __restrict__ leaf_start,
+    float inv_a, const float* __restrict__ Lleaf, int use_near, int use_far,
+    float* __restrict__ vel, float* __restrict__ dgam, int64_t leaf_lo, int64_t gbase,
+    int64_t nout, const uint4* __restrict__ map_terms) {
+    constexpr int DQ = 12;
+    constexpr int p = PC;
+    constexpr int nc = (p + 1) * (p + 1), ng = p * p;
+    extern __shared__ float4 l2pp_sm4[];
+    float* sm = reinterpret_cast<float*>(l2pp_sm4);
+    const float4* D4 = l2pp_sm4;
+    float* Ls = sm + ng * DQ;
+    const int64_t leaf = leaf_lo + blockIdx.x;
+    const int s = leaf_start[leaf], e = leaf_start[leaf + 1];
+    if (e == s) return;
+    const int lane = threadIdx.x;
+    const float inv4pi = 0.0795774715459476679f;
+    if (use_far) {
+        for (int i = lane; i < 3 * nc; i += 32) Ls[i] = Lleaf[leaf * 3 * nc + i];
+        __syncwarp();
+        auto row = [&](int ei, const float* src_base) {
+            const uint4 q = __ldg(map_terms + ei);
+            auto term = [&](uint32_t u) {
+                return __half2float(__ushort_as_half((unsigned short)(u >> 16))) *
+                       src_base[u & 0xffffu];
+            };
+            sm[ei] = (term(q.x) + term(q.y)) + (term(q.z) + term(q.w));
+        };
+        for (int i = lane; i < ng * 3; i += 32) row((i / 3) * DQ + i % 3, Ls);
+        __syncwarp();
+        for (int i = lane; i < ng * 9; i += 32) row((i / 9) * DQ + 3 + i % 9, sm);
+        __syncwarp();
+    }
+    for (int b = s; b < e; b += 64) {
+        const int ja = b + lane, jb = ja + 32;
+        const bool aa = ja < e, ab = jb < e;
+        float u[2][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}}, sd[2][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
+        float gi[2][3] = {{0.f, 0.f, 0.f}, {0.f, 0.f, 0.f}};
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+            if (aa) gi[0][c] = s6[(3 + c) * n + ja];
+            if (ab) gi[1][c] = s6[(3 + c) * n + jb];
+        }
+        if (use_far) {
+            const float xa = aa ? s6[ja] * inv_a : 0.f, ya = aa ? s6[n + ja] * inv_a : 0.f,
+                        za = aa ? s6[2 * n + ja] * inv_a : 0.f;
+            const float xb = ab ? s6[jb] * inv_a : 0.f, yb = ab ? s6[n + jb] * inv_a : 0.f,
+                        zb = ab ? s6[2 * n + jb] * inv_a : 0.f;
+            const f2x X = pk2(xa, xb), Y = pk2(ya, yb), Z = pk2(za, zb);
+            const f2x R2 = ffma2(X, X, ffma2(Y, Y, fmul2(Z, Z)));
+            const f2x NR2 = fmul2(R2, bc2(-1.f));
+            f2x acc[DQ];
+#pragma unroll
+            for (int q = 0; q < DQ; ++q) acc[q] = pk2(0.f, 0.f);
+            f2x dre = bc2(1.f), dim = bc2(0.f);
+            constexpr int pm = p - 1;
+#pragma unroll
+            for (int m = 0; m <= pm; ++m) {
+                if (m > 0) {
+                    const f2x sc = bc2(c_mhalf[m]);
+                    const f2x nre = fmul2(sc, ffma2(X, dre, fmul2(fmul2(Y, dim), bc2(-1.f))));
+                    const f2x nim = fmul2(sc, ffma2(X, dim, fmul2(Y, dre)));
+                    dre = nre;
+                    dim = nim;
+                }
+                f2x p2re = bc2(0.f), p2im = bc2(0.f), p1re = bc2(0.f), p1im = bc2(0.f);
+#pragma unroll
+                for (int nn = m; nn <= pm; ++nn) {
+                    f2x cre, cim;
+                    if (nn == m) {
+                        cre = dre;
+                        cim = dim;
+                    } else if (nn == m + 1) {
+                        cre = fmul2(Z, dre);
+                        cim = fmul2(Z, dim);
+                    } else {
+                        const f2x inv = bc2(c_rinv[nn * 17 + m]);
+                        const f2x az = fmul2(bc2(2.f * nn - 1.f), Z);
+                        cre = fmul2(ffma2(az, p1re, fmul2(NR2, p2re)), inv);
+                        cim = fmul2(ffma2(az, p1im, fmul2(NR2, p2im)), inv);
+                    }
+                    p2re = p1re;
+                    p2im = p1im;
+                    p1re = cre;
+                    p1im = cim;
+                    const float4* Dr = D4 + pk_re(nn, m) * (DQ / 4);
+                    if (m == 0) {
+#pragma unroll
+                        for (int q4 = 0; q4 < DQ / 4; ++q4) {
+                            const float4 d = Dr[q4];
+                            acc[4 * q4 + 0] = ffma2(bc2(d.x), cre, acc[4 * q4 + 0]);
+                            acc[4 * q4 + 1] = ffma2(bc2(d.y), cre, acc[4 * q4 + 1]);
+                            acc[4 * q4 + 2] = ffma2(bc2(d.z), cre, acc[4 * q4 + 2]);
+                            acc[4 * q4 + 3] = ffma2(bc2(d.w), cre, acc[4 * q4 + 3]);
+                        }
+                    } else {
+                        const float4* Di = D4 + pk_im(nn, m) * (DQ / 4);
+                        const f2x wr = fmul2(bc2(2.f), cre), wi = fmul2(bc2(-2.f), cim);
+#pragma unroll
+                        for (int q4 = 0; q4 < DQ / 4; ++q4) {
+                            const float4 d = Dr[q4], f = Di[q4];
+                            acc[4 * q4 + 0] = ffma2(bc2(d.x), wr, ffma2(bc2(f.x), wi, acc[4 * q4 + 0]));
+                            acc[4 * q4 + 1] = ffma2(bc2(d.y), wr, ffma2(bc2(f.y), wi, acc[4 * q4 + 1]));
+                            acc[4 * q4 + 2] = ffma2(bc2(d.z), wr, ffma2(bc2(f.z), wi, acc[4 * q4 + 2]));
+                            acc[4 * q4 + 3] = ffma2(bc2(d.w), wr, ffma2(bc2(f.w), wi, acc[4 * q4 + 3]));
+                        }
+                    }
+                }
+            }
+            const float sg = inv4pi * inv_a * inv_a;  // gradient scale
+            const float sh = sg * inv_a;              // Hessian scale
+#pragma unroll
+            for (int t = 0; t < 2; ++t) {
+                float A[DQ];
+#pragma unroll
+                for (int q = 0; q < DQ; ++q) {
+                    float lo, hi;
+                    upk2(acc[q], lo, hi);
+                    A[q] = t == 0 ? lo : hi;
+                }
+                u[t][0] = sg * A[0];
+                u[t][1] = sg * A[1];
+                u[t][2] = sg * A[2];
+#pragma unroll
+                for (int a2 = 0; a2 < 3; ++a2) {
+                    if (SCHEME == 0)
+                        sd[t][a2] = sh * (A[3 + 3 * a2] * gi[t][0] + A[4 + 3 * a2] * gi[t][1] +
+                                          A[5 + 3 * a2] * gi[t][2]);
+                    else
+                        sd[t][a2] = sh * (A[3 + a2] * gi[t][0] + A[6 + a2] * gi[t][1] +
+                                          A[9 + a2] * gi[t][2]);
+                }
+            }
+        }
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            const int j = t == 0 ? ja : jb;
+            if (!(t == 0 ? aa : ab)) continue;
+            if (use_near) {
+                for (int a2 = 0; a2 < 3; ++a2) {
+                    u[t][a2] += near6[a2 * n + j];
+                    sd[t][a2] += near6[(3 + a2) * n + j];
+                }
+            }
+            const int64_t i = perm[j - gbase];  // caller's input index (rank-local)
+            for (int a2 = 0; a2 < 3; ++a2) {
+                vel[a2 * nout + i] = u[t][a2];
+                dgam[a2 * nout + i] = sd[t][a2];
+            }
+        }
+    }
+}
+
 // out[i] = sum_{z < nz} part[z * stride + i], in z order (deterministic op-split reduction)
 __global__ void zsum_kernel(const float* __restrict__ part, int64_t stride, int nz,
                             float* __restrict__ out, int64_t count) {
@@ -706,10 +870,34 @@ void launch_l2p_combine(const L2PMap& map, const float* sorted6, const float* ne
                                                    L_leaf, use_near, use_far, vel, dgam, leaf_lo,
                                                    gbase, nout, map.rowptr, map.terms);
     };
+    // two particles per thread (one warp per leaf) for the compile-time orders; VFMM_L2P=single
+    // keeps one particle per thread
+    const char* l2p_env = getenv("VFMM_L2P");
+    const bool pair = !(l2p_env && strcmp(l2p_env, "single") == 0);
+    static PerDeviceOnce once_pair;
+    once_pair([] {
+        const void* ks[] = {(const void*)l2p_combine_pair_kernel<0, 4>,
+                            (const void*)l2p_combine_pair_kernel<1, 4>,
+                            (const void*)l2p_combine_pair_kernel<0, 6>,
+                            (const void*)l2p_combine_pair_kernel<1, 6>,
+                            (const void*)l2p_combine_pair_kernel<0, 8>,
+                            (const void*)l2p_combine_pair_kernel<1, 8>,
+                            (const void*)l2p_combine_pair_kernel<0, 10>,
+                            (const void*)l2p_combine_pair_kernel<1, 10>};
+        for (const void* k : ks)
+            cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    });
+    auto gop = [&](auto kern) {
+        kern<<<(unsigned)leaf_cnt, 32, smem, st>>>(sorted6, near6, perm, n, leaf_start, inv_a,
+                                                   L_leaf, use_near, use_far, vel, dgam, leaf_lo,
+                                                   gbase, nout, map.terms);
+    };
     // compile-time orders for the common p, runtime-p kernel otherwise
 #define L2P_CASE(PV)                                                             \
     case PV:                                                                     \
-        if (scheme == 0) go(l2p_combine_kernel<0, PV>);                         \
+        if (pair && scheme == 0) gop(l2p_combine_pair_kernel<0, PV>);          \
+        else if (pair) gop(l2p_combine_pair_kernel<1, PV>);                    \
+        else if (scheme == 0) go(l2p_combine_kernel<0, PV>);                    \
         else go(l2p_combine_kernel<1, PV>);                                     \
         return;
     switch (p) {
