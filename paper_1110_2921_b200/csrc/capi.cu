@@ -702,6 +702,7 @@ static vfmm_status evaluate_impl(vfmm_ctx* c, int64_t n, const float* pos, const
             return VFMM_OK;
         };
         CK(cudaEventRecord(c->ev[0], st), "event");
+        NvtxRange nv("vfmm/dist/redistribute");
         if ((s = dist_phase0a(R0, D, st, &c->err)) != VFMM_OK) return s;
         if ((s = to_comm(0)) != VFMM_OK) return s;
         if ((s = nccl_x0a(R0, D, c->comm, cs)) != VFMM_OK) return s;
@@ -718,6 +719,7 @@ static vfmm_status evaluate_impl(vfmm_ctx* c, int64_t n, const float* pos, const
         if ((s = nccl_x1(R0, D, c->comm, cs)) != VFMM_OK) return s;
         CK(cudaEventRecord(E[8], cs), "event");
         CK(cudaStreamWaitEvent(st, E[8], 0), "wait");
+        nv.next("vfmm/dist/halo_let");
         if ((s = dist_phase2(R0, D, st, &c->err)) != VFMM_OK) return s;
         if ((s = to_comm(9)) != VFMM_OK) return s;
         if ((s = nccl_x2(R0, D, c->comm, cs)) != VFMM_OK) return s;
@@ -730,10 +732,12 @@ static vfmm_status evaluate_impl(vfmm_ctx* c, int64_t n, const float* pos, const
         CK(cudaEventRecord(E[14], cs), "event");
         CK(cudaEventRecord(E[15], st), "event");  // compute stream ready for the LET
         CK(cudaStreamWaitEvent(st, E[14], 0), "wait");
+        nv.next("vfmm/dist/evaluate");
         if ((s = dist_phase4_far(R0, D, st, &c->err)) != VFMM_OK) return s;
         CK(cudaEventRecord(E[16], st), "event");  // compute stream ready for the halo
         CK(cudaStreamWaitEvent(st, E[11], 0), "wait");
         if ((s = dist_phase4_near(R0, D, st, &c->err)) != VFMM_OK) return s;
+        nv.next("vfmm/dist/return");
         if ((s = dist_phase5a(R0, D, st, &c->err)) != VFMM_OK) return s;
         if ((s = to_comm(17)) != VFMM_OK) return s;
         if ((s = nccl_x5(R0, D, c->comm, cs)) != VFMM_OK) return s;
@@ -840,6 +844,7 @@ static vfmm_status evaluate_impl(vfmm_ctx* c, int64_t n, const float* pos, const
     const float a = (float)((double)P.box_len / (double)(1 << depth));  // exact in float
     int nl = 0;
     // ---- tree ----
+    NvtxRange nv("vfmm/tree");
     launch_keys(pos, n, g, c->keys[0], c->vals[0], c->d_err, st);
     ++nl;
     CK(cudaEventRecord(c->ev[1], st), "event");
@@ -880,6 +885,7 @@ static vfmm_status evaluate_impl(vfmm_ctx* c, int64_t n, const float* pos, const
         CK(cudaGetLastError(), "p2p kernel");
     }
     // ---- upward pass ----
+    nv.next("vfmm/upward");
     if (use_far) {
         launch_p2m(c->sorted6, n, c->leaf_start, p, 1.f / a, Mlev(depth), 0,
                    (int64_t)1 << (3 * depth), fs);
@@ -899,6 +905,7 @@ static vfmm_status evaluate_impl(vfmm_ctx* c, int64_t n, const float* pos, const
     // The levels are independent: levels 1..L-1 (few CTAs each, latency bound) and the
     // periodic-image operator run on a side stream concurrently with level L (fork/join by
     // events), each stream with its own tensor-core staging buffer.
+    nv.next("vfmm/m2l");
     if (use_far) {
         TcOps tco = tc_ops(c);
         tco.lean = cores;
@@ -950,6 +957,7 @@ static vfmm_status evaluate_impl(vfmm_ctx* c, int64_t n, const float* pos, const
         CK(cudaGetLastError(), "m2l kernels");
     }
     CK(cudaEventRecord(c->ev[6], fs), "event");
+    nv.next("vfmm/downward");
     if (use_far) {
         for (int l = 1; l <= depth; ++l) {
             launch_l2l(c->d_l2l, p, H.KP, H.NR, Llev(l - 1), Llev(l), l, 0,
@@ -967,6 +975,7 @@ static vfmm_status evaluate_impl(vfmm_ctx* c, int64_t n, const float* pos, const
     }
     if (getenv("VFMM_DEBUG_SYNC")) CK(cudaStreamSynchronize(st), "debug sync");
     // ---- near field ----
+    nv.next("vfmm/p2p");
     if (use_near && !cores) {
         CK(cudaMemsetAsync(c->d_pairs, 0, sizeof(unsigned long long), st), "memset pairs");
         if (sig) {  // per-particle core radius: sigma into Morton order, the sigma_j P2P
@@ -988,6 +997,7 @@ static vfmm_status evaluate_impl(vfmm_ctx* c, int64_t n, const float* pos, const
         CK(cudaGetLastError(), "p2p kernel");
     }
     CK(cudaEventRecord(c->ev[8], st), "event");
+    nv.next("vfmm/l2p");
     launch_l2p_combine(l2p_map(c), c->sorted6, c->near6, c->perm, n, c->leaf_start, p, a, Llev(depth),
                        P.scheme, use_near, use_far, vel, dgamma, 0, (int64_t)1 << (3 * depth), 0, n,
                        st);

@@ -7,6 +7,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/vfmm.h"
 
 namespace vfmm {
@@ -29,6 +31,20 @@ struct PerDeviceOnce {
         if (d < 0 || d > 63 || ((done >> d) & 1)) return;
         f();
         done |= uint64_t(1) << d;
+    }
+};
+
+// Named NVTX range over the host-side enqueue of one pipeline phase, so that profilers
+// attribute the phase's kernel launches to it (nsys timeline, `ncu --nvtx --nvtx-include
+// "vfmm/p2p/"`).  With no profiler attached, push and pop return at once.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+    void next(const char* name) {
+        nvtxRangePop();
+        nvtxRangePushA(name);
     }
 };
 
