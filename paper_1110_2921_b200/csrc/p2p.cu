@@ -9,7 +9,7 @@
 //              sdot_i = A_i x gamma_i + B_i                          Eq. (8)
 //   transpose: B_i += q (gamma_i . (gamma_j x d)) d; sdot_i = gamma_i x A_i + B_i
 // rho^2 < 1/4: Taylor series in rho^2 (exact r -> 0 limits, no cancellation);
-// otherwise 1 - g = e^{-rho^2} (erfcx(rho) + 2 rho/sqrt(pi)) with erfcx from a degree-5
+// otherwise 1 - g = e^{-rho^2} (erfcx(rho) + 2 rho/sqrt(pi)) with erfcx from a degree-4
 // polynomial in t = 1/(1 + rho/2) (scripts/fit_cutoff_poly.py): 3 MUFU (rsqrt, ex2, rcp).
 #include <cuda_runtime.h>
 
@@ -23,7 +23,6 @@
 namespace vfmm {
 
 // erfcx(rho) / (4 pi) ~= sum_k ERFCX_Ck t^k, t = 1/(1 + rho/2), degree 4
-// (scripts/fit_cutoff_poly.py: relative error of g <= 1.6e-8 over rho in [0.5, 10])
 // (scripts/fit_cutoff_poly.py 4: relative error of g <= 4.8e-7 over rho in [0.5, 10], below
 // the 1.4e-6 FP32 evaluation floor near rho = 0.5; degree 5 reached 1.6e-8 for one more FFMA2)
 constexpr float ERFCX_C0 = -2.582819305e-03f, ERFCX_C1 = 4.079926104e-02f,
