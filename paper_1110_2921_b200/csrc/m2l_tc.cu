@@ -40,6 +40,9 @@
 // both CTAs, halving operator traffic; operator stages are released by both MMA warps.
 #include <cuda.h>
 #include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
 #include <cudaTypedefs.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -206,6 +209,10 @@ struct TcParams {
     const float* rs;   // f16: row scales [128]
     const uint32_t* maxbits;  // f16: the level's max |cs[k] M_k| (float bits)
     const int4* groups;  // [8][72] offset groups per target parity (see m2l_groups)
+    // bit s of full[mt]: K step s (MMA K = 16 halves / 8 tf32) of row tile mt takes the whole
+    // 3-product split; otherwise hi x hi alone (see launch_m2l_tc: low-order terms only)
+    uint32_t full[2];
+    int dbg;  // VFMM_M2L_DBG (measurement only, wrong results): 1 no TMEM drain, 2 no A, 4 no B loads
 };
 
 // f16 staging scale s = 2^(14 - e) for the level max m = f 2^e (f in [0.5, 1)): max |Mhat| < 2^14
@@ -234,6 +241,21 @@ __device__ __forceinline__ void group_rows(const TcParams& P, int g, int* tx, in
     }
     *py0 = P.by0 + gy * P.T;
     *pz = P.bz0 + gz;
+}
+
+// VFMM_M2L_DBG & 8 (measurement only): clock64 timeline of cluster 0 (CTAs 0 and 1) of a
+// launch with >= 1024 CTAs; the next launch prints a summary to stderr.  Events per CTA:
+// 0 producer past a_empty (per operator load), 1 MMA past a_full, 2 MMA past its commits,
+// 3 epilogue warp 2 past acc_full, 4 MMA past acc_empty (per chain); meta: kernel start,
+// MMA loop end, epilogue stores end
+constexpr int TR_N = 1024;
+__device__ long long g_m2l_trace[2][5][TR_N];
+__device__ long long g_m2l_meta[2][4];
+
+__device__ __forceinline__ long long clk() {
+    long long t;
+    asm volatile("mov.u64 %0, %%clock64;" : "=l"(t));
+    return t;
 }
 
 template <bool F16, int MT, bool LEAN = false, int TC_AST = 2>
@@ -293,6 +315,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc_threads<LEAN>(), 
     cluster_sync();  // peer barriers initialised before any multicast lands
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    const bool tr = (P.dbg & 8) && blockIdx.x < 2 && gridDim.x >= 1024;
+    const int tb = blockIdx.x & 1;
+    if (tr && threadIdx.x == 0) g_m2l_meta[tb][0] = clk();
 
     if (warp == 0) {
         // ===================== TMA producer =====================
@@ -300,7 +325,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc_threads<LEAN>(), 
         // gpy0 - 1 .. gpy0 + T) per K chunk serves the group's <= 3 offsets dy = -1, 0, 1;
         // then the operator chunk of each valid offset (shared with the peer CTA)
         if (lane == 0) {
-            int sa = 0, sb = 0;
+            int sa = 0, sb = 0, nload = 0;
             uint32_t pa = 0, pb = 0;
             const uint32_t b_tx = 2u * (uint32_t)((P.T + 2) * P.N) * 128u;
             for (int gi = 0; gi < 72; ++gi) {
@@ -311,12 +336,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc_threads<LEAN>(), 
                 const int c1 = 3 * (2 + P.bx0 + gtx * P.XT + dx);
                 const int c2 = 1 + gpy0, c3 = 2 + gpz + dz;
                 for (int kc = 0; kc < P.nkc; ++kc) {
+                    // the lo halves are loaded only for K chunks with a full-split step
+                    const bool need_lo = (((P.full[0] | (MT == 2 ? P.full[1] : 0u)) >> (4 * kc)) & 15u) != 0;
                     mbar_wait(&b_empty[sb], pb ^ 1);
-                    mbar_expect_tx(&b_full[sb], b_tx);
+                    if (P.dbg & 4) {
+                        mbar_arrive(&b_full[sb]);
+                    } else {
+                    mbar_expect_tx(&b_full[sb], need_lo ? b_tx : b_tx / 2);
                     tma_load_5d(Bbuf + (sb * 2 + 0) * B_BYTES, &tmB_hi, &b_full[sb], kc * tc_ke<F16>(),
                                 c1, c2, c3, pis);
-                    tma_load_5d(Bbuf + (sb * 2 + 1) * B_BYTES, &tmB_lo, &b_full[sb], kc * tc_ke<F16>(),
-                                c1, c2, c3, pis);
+                    if (need_lo)
+                        tma_load_5d(Bbuf + (sb * 2 + 1) * B_BYTES, &tmB_lo, &b_full[sb],
+                                    kc * tc_ke<F16>(), c1, c2, c3, pis);
+                    }
                     if (++sb == TC_BST) {
                         sb = 0;
                         pb ^= 1;
@@ -326,13 +358,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc_threads<LEAN>(), 
                         if (!((mask >> d) & 1)) continue;
                         const int slot = d == 0 ? G.y : (d == 1 ? G.z : G.w);
                         mbar_wait(&a_empty[sa], pa ^ 1);
-                        mbar_expect_tx(&a_full[sa], 2u * A_BYTES);  // hi from rank 0, lo from rank 1
-                        if (crank == 0)
-                            tma_load_3d_mc(Abuf + (sa * 2 + 0) * A_BYTES, &tmA_hi, &a_full[sa],
-                                           kc * tc_ke<F16>(), 0, slot, (uint16_t)3);
-                        else
-                            tma_load_3d_mc(Abuf + (sa * 2 + 1) * A_BYTES, &tmA_lo, &a_full[sa],
-                                           kc * tc_ke<F16>(), 0, slot, (uint16_t)3);
+                        if (tr && nload < TR_N) g_m2l_trace[tb][0][nload] = clk();
+                        ++nload;
+                        if (P.dbg & 2) {
+                            mbar_arrive(&a_full[sa]);
+                        } else if (need_lo) {  // hi from rank 0, lo from rank 1
+                            mbar_expect_tx(&a_full[sa], 2u * A_BYTES);
+                            if (crank == 0)
+                                tma_load_3d_mc(Abuf + (sa * 2 + 0) * A_BYTES, &tmA_hi, &a_full[sa],
+                                               kc * tc_ke<F16>(), 0, slot, (uint16_t)3);
+                            else
+                                tma_load_3d_mc(Abuf + (sa * 2 + 1) * A_BYTES, &tmA_lo, &a_full[sa],
+                                               kc * tc_ke<F16>(), 0, slot, (uint16_t)3);
+                        } else {  // hi only, the ranks take turns
+                            mbar_expect_tx(&a_full[sa], (uint32_t)A_BYTES);
+                            if ((int)crank == ((gi + d) & 1))
+                                tma_load_3d_mc(Abuf + (sa * 2 + 0) * A_BYTES, &tmA_hi, &a_full[sa],
+                                               kc * tc_ke<F16>(), 0, slot, (uint16_t)3);
+                        }
                         if (++sa == TC_AST) {
                             sa = 0;
                             pa ^= 1;
@@ -353,11 +396,51 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc_threads<LEAN>(), 
         const uint64_t slab_step = (uint64_t)((P.N * 128) >> 4);  // descriptor units (16 B)
         int sa = 0, sb = 0;
         uint32_t pa = 0, pb = 0;
-        int chain = 0;  // one TMEM accumulation chain per (offset, K chunk): 4 K-steps x 3 products
+        // One TMEM accumulation chain per (offset, K chunk) -- <= 4 K steps x 3 products -- or,
+        // for a K chunk without full-split steps (hi x hi alone, high orders only), one chain
+        // per (offset group, K chunk): <= 3 offsets x 4 single MMAs.
+        int chain = 0;
+        // issue one chain segment: K steps [0, nks) of every row tile, the first nf[mt] steps
+        // with the whole split; first = this segment opens the TMEM chain
+        auto issue = [&](uint32_t d, uint64_t ahi, uint64_t alo, uint64_t bhi, uint64_t blo,
+                         int nks, int nf0, int nf1, bool first) {
+#pragma unroll
+            for (int mt = 0; mt < MT; ++mt) {  // row tile mt: rows 128 mt ..
+                const uint32_t dm = d + (uint32_t)(mt * P.T * P.N);
+                const uint64_t am = (uint64_t)(mt * (A_TILE >> 4));
+                const int nf = mt == 0 ? nf0 : nf1;
+                for (int ks = 0; ks < nks; ++ks) {  // K = 8 tf32 / 16 f16 = 32 B per MMA
+                    const uint64_t adv = (uint64_t)(ks * 2);
+                    const uint32_t acc = (first && ks == 0) ? 0u : 1u;
+                    if (F16) {
+                        mma_f16(dm, ahi + am + adv, bhi + adv, idesc, acc);
+                        if (ks < nf) {
+                            mma_f16(dm, ahi + am + adv, blo + adv, idesc, 1u);
+                            mma_f16(dm, alo + am + adv, bhi + adv, idesc, 1u);
+                        }
+                    } else {
+                        mma_tf32(dm, ahi + am + adv, bhi + adv, idesc, acc);
+                        if (ks < nf) {
+                            mma_tf32(dm, ahi + am + adv, blo + adv, idesc, 1u);
+                            mma_tf32(dm, alo + am + adv, bhi + adv, idesc, 1u);
+                        }
+                    }
+                }
+            }
+        };
         for (int gi = 0; gi < 72; ++gi) {
             const int mask = P.groups[pi * 72 + gi].x & 7;
             if (!mask) continue;
+            const int last_dd = 31 - __clz(mask);
             for (int kc = 0; kc < P.nkc; ++kc) {
+                // K steps holding real coefficients: the last chunk of a padded K
+                // (e.g. (p+1)^2 = 196 in 4 chunks of 64) skips its all-zero steps
+                const int kleft = P.nc - kc * tc_ke<F16>();
+                const int nks = min(4, (kleft + tc_ke<F16>() / 4 - 1) / (tc_ke<F16>() / 4));
+                // leading full-split steps of this chunk per row tile (a prefix by construction)
+                const int nf0 = __popc((P.full[0] >> (4 * kc)) & 15u);
+                const int nf1 = MT == 2 ? __popc((P.full[1] >> (4 * kc)) & 15u) : 0;
+                const bool merged = nf0 == 0 && nf1 == 0;
                 mbar_wait(&b_full[sb], pb);
                 tc_fence_after();
                 const uint64_t bhi = sw128_desc(Bbuf + (sb * 2 + 0) * B_BYTES);
@@ -366,43 +449,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc_threads<LEAN>(), 
                 for (int dd = 0; dd < 3; ++dd) {
                     if (!((mask >> dd) & 1)) continue;
                     const int buf = chain & 1;
-                    mbar_wait(&acc_empty[buf], ((chain >> 1) & 1) ^ 1);  // epilogue drained it
+                    const bool opens = !merged || dd == __ffs(mask) - 1;
+                    const bool closes = !merged || dd == last_dd;
+                    if (opens) {
+                        mbar_wait(&acc_empty[buf], ((chain >> 1) & 1) ^ 1);  // epilogue drained it
+                        if (tr && lane == 0 && chain < TR_N) g_m2l_trace[tb][4][chain] = clk();
+                    }
                     mbar_wait(&a_full[sa], pa);
+                    if (tr && lane == 0 && chain < TR_N) g_m2l_trace[tb][1][chain] = clk();
                     tc_fence_after();
                     const uint32_t d = tmem + (uint32_t)(buf * 256);
                     const uint64_t ahi = sw128_desc(Abuf + (sa * 2 + 0) * A_BYTES);
                     const uint64_t alo = sw128_desc(Abuf + (sa * 2 + 1) * A_BYTES);
                     const uint64_t bsh = (uint64_t)dd * slab_step;
-                    // K steps holding real coefficients: the last chunk of a padded K
-                    // (e.g. (p+1)^2 = 196 in 4 chunks of 64) skips its all-zero steps
-                    const int kleft = P.nc - kc * tc_ke<F16>();
-                    const int nks = min(4, (kleft + tc_ke<F16>() / 4 - 1) / (tc_ke<F16>() / 4));
                     if (lane == 0) {
-#pragma unroll
-                        for (int ks = 0; ks < 4; ++ks) {  // K = 8 tf32 / 16 f16 = 32 B per MMA
-                            if (ks >= nks) break;
-                            const uint64_t adv = (uint64_t)(ks * 2);
-                            const uint32_t acc = ks == 0 ? 0u : 1u;
-#pragma unroll
-                            for (int mt = 0; mt < MT; ++mt) {  // row tile mt: rows 128 mt ..
-                                const uint32_t dm = d + (uint32_t)(mt * P.T * P.N);
-                                const uint64_t am = (uint64_t)(mt * (A_TILE >> 4));
-                                if (F16) {
-                                    mma_f16(dm, ahi + am + adv, bhi + bsh + adv, idesc, acc);
-                                    mma_f16(dm, ahi + am + adv, blo + bsh + adv, idesc, 1u);
-                                    mma_f16(dm, alo + am + adv, bhi + bsh + adv, idesc, 1u);
-                                } else {
-                                    mma_tf32(dm, ahi + am + adv, bhi + bsh + adv, idesc, acc);
-                                    mma_tf32(dm, ahi + am + adv, blo + bsh + adv, idesc, 1u);
-                                    mma_tf32(dm, alo + am + adv, bhi + bsh + adv, idesc, 1u);
-                                }
-                            }
-                        }
+                        issue(d, ahi, alo, bhi + bsh, blo + bsh, nks, nf0, nf1, opens);
                         mma_commit_mc(&a_empty[sa], (uint16_t)3);  // release in both CTAs
-                        mma_commit(&acc_full[buf]);
+                        if (closes) {
+                            mma_commit(&acc_full[buf]);
+                            if (tr && chain < TR_N) g_m2l_trace[tb][2][chain] = clk();
+                        }
                     }
                     __syncwarp();
-                    ++chain;
+                    if (closes) ++chain;
                     if (++sa == TC_AST) {
                         sa = 0;
                         pa ^= 1;
@@ -430,13 +499,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc_threads<LEAN>(), 
         unsigned long long acc2[48];
 #pragma unroll
         for (int j = 0; j < 48; ++j) acc2[j] = 0ull;
+        // chains: one per (offset, K chunk), or one per (group, K chunk) for a chunk without
+        // full-split steps (see the MMA issuer)
         int nchains = 0;
-        for (int gi = 0; gi < 72; ++gi) nchains += __popc(P.groups[pi * 72 + gi].x & 7);
-        nchains *= P.nkc;
+        for (int gi = 0; gi < 72; ++gi) {
+            const int m = P.groups[pi * 72 + gi].x & 7;
+            if (!m) continue;
+            for (int kc = 0; kc < P.nkc; ++kc) {
+                const bool merged = ((P.full[0] | (MT == 2 ? P.full[1] : 0u)) >> (4 * kc) & 15u) == 0;
+                nchains += merged ? 1 : __popc(m);
+            }
+        }
         for (int ch = 0; ch < nchains; ++ch) {
             const int buf = ch & 1;
             mbar_wait(&acc_full[buf], (ch >> 1) & 1);
+            if (tr && e == 0 && lane == 0 && ch < TR_N) g_m2l_trace[tb][3][ch] = clk();
             tc_fence_after();
+            if (P.dbg & 1) {
+                tc_fence_before();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&acc_empty[buf]);
+                continue;
+            }
             // two halves of 48 accumulator columns (MT = 1: the warp's 96 columns; MT = 2: one
             // row tile each), three 16-column loads in flight, one wait each
 #pragma unroll
@@ -481,6 +565,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc_threads<LEAN>(), 
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[buf]);
         }
+        if (tr && e == 0 && lane == 0) g_m2l_meta[tb][1] = clk();
         float acc[96];
 #pragma unroll
         for (int j = 0; j < 48; ++j)
@@ -511,6 +596,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc_threads<LEAN>(), 
     }
     tc_fence_before();
     __syncthreads();
+    if (tr && threadIdx.x == 0) g_m2l_meta[tb][2] = clk();
     cluster_sync();  // the peer may still multicast into / arrive on this CTA until here
     tc_fence_after();
     if (warp == 1)
@@ -662,6 +748,18 @@ static int pick_T(const int box[6], int MT, bool lean = false) {
     return 0;
 }
 
+// lowest term degree run as hi x hi alone (VFMM_M2L_SPLIT=<degree>; "full" keeps the
+// 3-product split for every term)
+int m2l_split_degree() {
+    const char* e = getenv("VFMM_M2L_SPLIT");
+    if (e && e[0]) {
+        if (!strcmp(e, "full")) return 1 << 20;
+        const int v = atoi(e);
+        if (v > 0) return v;
+    }
+    return 6;
+}
+
 bool m2l_tc_shape_ok(const int box[6], int p) {
     return pick_T(box, (p + 1) * (p + 1) > 128 ? 2 : 1) != 0;
 }
@@ -788,6 +886,61 @@ int launch_m2l_tc(const TcOps& ops, const int* il_slots, int p, const float* M_l
     P.maxbits = maxbits;
     P.T = T;
     P.groups = ops.groups;
+    {
+        const char* d = getenv("VFMM_M2L_DBG");
+        P.dbg = d ? atoi(d) : 0;
+        static bool traced = false;
+        if ((P.dbg & 8) && traced) {  // summary of the previous traced launch
+            static long long T[2][5][TR_N], Mt[2][4];
+            cudaStreamSynchronize(st);
+            cudaMemcpyFromSymbol(T, g_m2l_trace, sizeof(T));
+            cudaMemcpyFromSymbol(Mt, g_m2l_meta, sizeof(Mt));
+            for (int b = 0; b < 2; ++b) {
+                const long long t0 = Mt[b][0];
+                int nch = 0;
+                while (nch < TR_N && T[b][3][nch] > t0) ++nch;
+                double per = 0, ia = 0, ex = 0, pr = 0;
+                int cnt = 0;
+                for (int c = 20; c + 2 < nch - 20; ++c, ++cnt) {
+                    per += (double)(T[b][3][c + 1] - T[b][3][c]);  // chain completion period
+                    ia += (double)(T[b][1][c] - T[b][4][c]);       // acc_empty -> a_full
+                    ex += (double)(T[b][3][c] - T[b][2][c]);       // commit issued -> complete
+                    pr += (double)(T[b][1][c + 2] - T[b][3][c]);   // c done -> c+2 issuable
+                }
+                if (cnt) {
+                    fprintf(stderr,
+                            "[m2l trace] cta %d: kernel %lld cyc, chains %d, MMA loop %lld, "
+                            "stores %lld; per chain: period %.0f, acc_empty->a_full %.0f, "
+                            "issue->complete %.0f, complete(c)->a_full(c+2) %.0f\n",
+                            b, Mt[b][2] - t0, nch, Mt[b][1] - t0, Mt[b][2] - Mt[b][1], per / cnt,
+                            ia / cnt, ex / cnt, pr / cnt);
+                    for (int c = 100; c < 106 && c < nch; ++c)
+                        fprintf(stderr, "  chain %d: acc_empty %lld a_full %lld committed %lld "
+                                "epi %lld (load %lld)\n", c, T[b][4][c] - t0, T[b][1][c] - t0,
+                                T[b][2][c] - t0, T[b][3][c] - t0, T[b][0][c] - t0);
+                }
+            }
+        }
+        if ((P.dbg & 8) && (int)(8 * (bny * bnz * (bnx / XT) / T)) >= 1024) traced = true;
+    }
+    // Split by term order.  Term (r, k) of a translation couples local degree j(r) with
+    // multipole degree n(k); its share of the field falls geometrically with j + n (the p sweep
+    // in DESIGN.md 7: ~0.43 per degree), so the A_hi B_lo + A_lo B_hi correction (2^-11 of a
+    // term) matters only for the low orders.  K step s of row tile mt takes the full split iff
+    // both the tile's lowest row degree and the step's lowest column degree are below
+    // m2l_split_degree(); the others run hi x hi alone (DESIGN.md 6b "order-split M2L").
+    {
+        const int n0 = m2l_split_degree();
+        const int kstep = f16 ? 16 : 8;  // coefficients per MMA K step
+        auto deg = [](int k) { int n = 0; while ((n + 1) * (n + 1) <= k) ++n; return n; };
+        for (int mt = 0; mt < 2; ++mt) {
+            P.full[mt] = 0u;
+            if (mt >= MT) continue;
+            const int jmin = deg(128 * mt);
+            for (int s = 0; s < 4 * nkc && s < 32; ++s)
+                if (jmin < n0 && deg(s * kstep) < n0) P.full[mt] |= 1u << s;
+        }
+    }
     const unsigned grid = (unsigned)(8 * (P.rows / P.T));
     if (f16 && MT == 2)
         m2l_tc_kernel<true, 2><<<grid, tc_threads<false>(), tc_smem<2>(), st>>>(mAh, mAl, mBh, mBl, P);

@@ -165,6 +165,7 @@ struct TcOps {
 std::vector<int> m2l_groups();
 bool m2l_tc_supported(int p, int level);
 bool m2l_tc_shape_ok(const int box[6], int p);
+int m2l_split_degree();  // lowest term degree run as hi x hi alone (m2l_tc.cu)
 size_t m2l_tc_grid_floats(int level);
 // maxbits: one zeroed uint32 per launch (f16: the level's max |cs[k] M_k|, as float bits)
 int launch_m2l_tc(const TcOps& ops, const int* il_slots, int p, const float* M_l, float* L_l,
