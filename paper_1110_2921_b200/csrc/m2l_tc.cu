@@ -259,7 +259,7 @@ __device__ __forceinline__ long long clk() {
 }
 
 template <bool F16, int MT, bool LEAN = false, int TC_AST = 2>
-__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc_threads<LEAN>(), 1)
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc_threads<LEAN>(), LEAN ? 2 : 1)
     m2l_tc_kernel(const __grid_constant__ CUtensorMap tmA_hi, const __grid_constant__ CUtensorMap tmA_lo,
                   const __grid_constant__ CUtensorMap tmB_hi, const __grid_constant__ CUtensorMap tmB_lo,
                   TcParams P) {
@@ -572,25 +572,30 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc_threads<LEAN>(), 
             asm("mov.b64 {%0, %1}, %2;" : "=f"(acc[2 * j]), "=f"(acc[2 * j + 1]) : "l"(acc2[j]));
         const float sinv = F16 ? ldexpf(1.f, -h16_scale_exp(*P.maxbits)) : 1.f;
         const uint32_t cz = spread3t(2 * gpz + piz) << 2;
+        // Stage the scaled sums through shared memory (the operand buffers are idle once the
+        // last chain is drained: every MMA has read them and every load, the peer's multicasts
+        // included, has landed) so the scatter into L is one short loop -- 96 unrolled address
+        // computations made a ~9000-instruction tail that missed the instruction cache
+        float* stg = reinterpret_cast<float*>(sm) + e * (96 * 32);
+        constexpr int CPT = 96 / MT;  // accumulator columns per row tile
 #pragma unroll
         for (int mt = 0; mt < MT; ++mt) {
             const int rr = r + 128 * mt;
-            if (rr < P.nc) {
-                const float fsc = F16 ? P.rs[rr] * sinv : 1.f;  // undo the balancing
+            const float fsc = (F16 && rr < P.nc) ? P.rs[rr] * sinv : 1.f;  // undo the balancing
 #pragma unroll
-                for (int jj = 0; jj < 96 / MT; ++jj) {
-                    if (jj < ncol) {
-                        const int j = mt * (96 / MT) + jj;
-                        const int t = half * tpw + jj / P.N, cj = jj % P.N;
-                        if (cj < P.NV) {
-                            const int py = gpy0 + t;
-                            const int px = P.bx0 + gtx * P.XT + cj / 3, comp = cj % 3;
-                            const uint32_t cell =
-                                spread3t(2 * px + pix) | (spread3t(2 * py + piy) << 1) | cz;
-                            P.L[((int64_t)cell * 3 + comp) * P.nc + rr] = acc[j] * fsc;
-                        }
-                    }
-                }
+            for (int jj = 0; jj < CPT; ++jj) stg[(mt * CPT + jj) * 32 + lane] = acc[mt * CPT + jj] * fsc;
+        }
+        __syncwarp();
+        for (int mt = 0; mt < MT; ++mt) {
+            const int rr = r + 128 * mt;
+            if (rr >= P.nc) continue;
+            for (int jj = 0; jj < ncol; ++jj) {
+                const int t = half * tpw + jj / P.N, cj = jj % P.N;
+                if (cj >= P.NV) continue;
+                const int py = gpy0 + t;
+                const int px = P.bx0 + gtx * P.XT + cj / 3, comp = cj % 3;
+                const uint32_t cell = spread3t(2 * px + pix) | (spread3t(2 * py + piy) << 1) | cz;
+                P.L[((int64_t)cell * 3 + comp) * P.nc + rr] = stg[(mt * CPT + jj) * 32 + lane];
             }
         }
     }
