@@ -70,15 +70,18 @@ template <int MT> __host__ __device__ constexpr int b_bytes() { return b_wrows<M
 // it on the same SM (tensor pipe and FP32 pipe busy at once, capi.cu "co-resident mode")
 template <bool LEAN> __host__ __device__ constexpr int tc_epi() { return LEAN ? 4 : 8; }
 template <bool LEAN> __host__ __device__ constexpr int tc_threads() { return 64 + 32 * tc_epi<LEAN>(); }
-template <int MT, bool LEAN = false> __host__ __device__ constexpr int b_bytes_v() {
-    return LEAN ? 192 * 128 : b_bytes<MT>();
+// window stage bytes: LEAN 192 rows; the 3-stage variant (AST = 3, XT = 8 / T = 8 layout)
+// 240 rows (30 KB), which leaves room for a third operator stage
+template <int MT, bool LEAN = false, int AST = 2> __host__ __device__ constexpr int b_bytes_v() {
+    return LEAN ? 192 * 128 : (AST == 3 ? 240 * 128 : b_bytes<MT>());
 }
 template <int MT, bool LEAN = false, int AST = 2>
 constexpr size_t tc_smem() {
-    return 1024 + (size_t)AST * 2 * a_bytes<MT>() + (size_t)TC_BST * 2 * b_bytes_v<MT, LEAN>() + 512;
+    return 1024 + (size_t)AST * 2 * a_bytes<MT>() + (size_t)TC_BST * 2 * b_bytes_v<MT, LEAN, AST>() + 512;
 }
 static_assert(tc_smem<1, true, 4>() <= 232448, "deep variant exceeds 227 KB");
 static_assert(tc_smem<2>() <= 232448, "MT = 2 stages exceed 227 KB");
+static_assert(tc_smem<1, false, 3>() <= 232448, "3-stage variant exceeds 227 KB");
 static_assert(tc_smem<1, true>() <= 166 * 1024, "LEAN stages exceed 166 KB");
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -132,6 +135,43 @@ __device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
     asm volatile(
         "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
         " [%0], %1;" ::"r"(smem_u32(bar)),
+        "h"(mask)
+        : "memory");
+}
+// Warp-wide issue: the whole (converged) warp executes these, one elected lane issues.  The
+// operands are then warp-uniform values, so no per-instruction elect/broadcast loop is needed
+// to move them into uniform registers (as for an issue under `if (lane == 0)`).
+__device__ __forceinline__ void mma_w(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
+                                      uint32_t accumulate, bool f16) {
+    if (f16)
+        asm volatile(
+            "{\n\t.reg .pred p, e;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+            "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+    else
+        asm volatile(
+            "{\n\t.reg .pred p, e;\n\t"
+            "elect.sync _|e, 0xffffffff;\n\t"
+            "setp.ne.b32 p, %4, 0;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
+            "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
+}
+__device__ __forceinline__ void commit_w(uint32_t bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::
+            "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void commit_mc_w(uint32_t bar, uint16_t mask) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+        " [%0], %1;\n\t}" ::"r"(bar),
         "h"(mask)
         : "memory");
 }
@@ -266,7 +306,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc_threads<LEAN>(), 
     extern __shared__ uint8_t tc_raw[];
     uint8_t* sm = reinterpret_cast<uint8_t*>(((uintptr_t)tc_raw + 1023) & ~(uintptr_t)1023);
     uint8_t* Abuf = sm;                                  // [AST][hi|lo][16 KB]
-    constexpr int A_BYTES = a_bytes<MT>(), B_BYTES = b_bytes_v<MT, LEAN>();
+    constexpr int A_BYTES = a_bytes<MT>(), B_BYTES = b_bytes_v<MT, LEAN, TC_AST>();
     uint8_t* Bbuf = sm + TC_AST * 2 * A_BYTES;           // [BST][hi|lo][B_BYTES]
     uint64_t* bars = reinterpret_cast<uint64_t*>(Bbuf + TC_BST * 2 * B_BYTES);
     uint64_t* a_full = bars;
@@ -412,18 +452,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc_threads<LEAN>(), 
                 for (int ks = 0; ks < nks; ++ks) {  // K = 8 tf32 / 16 f16 = 32 B per MMA
                     const uint64_t adv = (uint64_t)(ks * 2);
                     const uint32_t acc = (first && ks == 0) ? 0u : 1u;
-                    if (F16) {
-                        mma_f16(dm, ahi + am + adv, bhi + adv, idesc, acc);
-                        if (ks < nf) {
-                            mma_f16(dm, ahi + am + adv, blo + adv, idesc, 1u);
-                            mma_f16(dm, alo + am + adv, bhi + adv, idesc, 1u);
-                        }
-                    } else {
-                        mma_tf32(dm, ahi + am + adv, bhi + adv, idesc, acc);
-                        if (ks < nf) {
-                            mma_tf32(dm, ahi + am + adv, blo + adv, idesc, 1u);
-                            mma_tf32(dm, alo + am + adv, bhi + adv, idesc, 1u);
-                        }
+                    mma_w(dm, ahi + am + adv, bhi + adv, idesc, acc, F16);
+                    if (ks < nf) {
+                        mma_w(dm, ahi + am + adv, blo + adv, idesc, 1u, F16);
+                        mma_w(dm, alo + am + adv, bhi + adv, idesc, 1u, F16);
                     }
                 }
             }
@@ -462,13 +494,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc_threads<LEAN>(), 
                     const uint64_t ahi = sw128_desc(Abuf + (sa * 2 + 0) * A_BYTES);
                     const uint64_t alo = sw128_desc(Abuf + (sa * 2 + 1) * A_BYTES);
                     const uint64_t bsh = (uint64_t)dd * slab_step;
-                    if (lane == 0) {
-                        issue(d, ahi, alo, bhi + bsh, blo + bsh, nks, nf0, nf1, opens);
-                        mma_commit_mc(&a_empty[sa], (uint16_t)3);  // release in both CTAs
-                        if (closes) {
-                            mma_commit(&acc_full[buf]);
-                            if (tr && chain < TR_N) g_m2l_trace[tb][2][chain] = clk();
-                        }
+                    __syncwarp();
+                    issue(d, ahi, alo, bhi + bsh, blo + bsh, nks, nf0, nf1, opens);
+                    commit_mc_w(smem_u32(&a_empty[sa]), (uint16_t)3);  // release in both CTAs
+                    if (closes) {
+                        commit_w(smem_u32(&acc_full[buf]));
+                        if (tr && lane == 0 && chain < TR_N) g_m2l_trace[tb][2][chain] = clk();
                     }
                     __syncwarp();
                     if (closes) ++chain;
@@ -477,8 +508,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc_threads<LEAN>(), 
                         pa ^= 1;
                     }
                 }
-                if (lane == 0) mma_commit(&b_empty[sb]);
                 __syncwarp();
+                commit_w(smem_u32(&b_empty[sb]));
                 if (++sb == TC_BST) {
                     sb = 0;
                     pb ^= 1;
@@ -734,19 +765,28 @@ PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
 // rows per CTA for a box: the largest T in {8, 4, 2} with MT T N <= 192 (MT = 2: T N <= 128)
 // and (T + 2) N within the window stage, T | bny and an even number of CTAs (2-CTA clusters);
 // 0 if none
-static int pick_XT(const int box[6]) { return box[3] < 16 ? box[3] : 16; }
+// parents per slab row: 16 (N = 48, T = 4) or VFMM_M2L_XT=8 (N = 24, T = 8: same MMA N', a
+// 240-row window instead of 288)
+static int pick_XT(const int box[6]) {
+    int xt = 16;
+    if (const char* e = getenv("VFMM_M2L_XT")) xt = atoi(e) == 8 ? 8 : 16;
+    return box[3] < xt ? box[3] : xt;
+}
+// slab rows N: 3 XT rounded up to 16, or exactly 24 for XT = 8 (a multiple of the 8-row
+// swizzle atom; the MMA N' = T N stays a multiple of 16 for even T)
+static int slab_N(int XT) { return XT == 8 ? 24 : (3 * XT + 15) / 16 * 16; }
 static int pick_T(const int box[6], int MT, bool lean = false) {
     const int bnx = box[3], bny = box[4], bnz = box[5];
     const int XT = pick_XT(box);
     if (bnx % XT != 0) return 0;
-    const int N = (3 * XT + 15) / 16 * 16;
+    const int N = slab_N(XT);
     const int rows = bny * bnz * (bnx / XT);
     const int wrows = lean ? 192 : (MT == 1 ? b_wrows<1>() : b_wrows<2>());
     for (int T = 8; T >= 2; T /= 2) {
         // accumulator columns per epilogue warp (its tiles x N x row tiles) fit its 96
         // registers; one TMEM buffer (MT T N columns) fits half of the 512 columns
         const int warp_cols = (lean ? T : T / 2) * N * MT;
-        if (warp_cols <= 96 && MT * T * N <= 256 && (T + 2) * N <= wrows &&
+        if (warp_cols <= 96 && MT * T * N <= 256 && (T + 2) * N <= wrows && (T * N) % 16 == 0 &&
             bny % T == 0 && (rows / T) % 2 == 0)
             return T;
     }
@@ -840,7 +880,7 @@ int launch_m2l_tc(const TcOps& ops, const int* il_slots, int p, const float* M_l
     const bool lean = (ops.lean || deep) && MT == 1 && f16 && pick_T(box, 1, true) != 0;
     const int T = pick_T(box, MT, lean);
     if (T == 0) return -4;
-    const int N = (NV + 15) / 16 * 16;  // MMA N (multiple of 16 for M = 128)
+    const int N = slab_N(XT);  // slab rows (T N: the MMA N, a multiple of 16 for M = 128)
     {
         const cuuint64_t row = (cuuint64_t)KPG * esz;
         cuuint64_t dims[5] = {(cuuint64_t)KPG, (cuuint64_t)3 * Xp, (cuuint64_t)Xp, (cuuint64_t)Xp, 8};
@@ -865,6 +905,8 @@ int launch_m2l_tc(const TcOps& ops, const int* il_slots, int p, const float* M_l
                              (int)tc_smem<1>());
         cudaFuncSetAttribute(m2l_tc_kernel<true, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)tc_smem<2>());
+        cudaFuncSetAttribute(m2l_tc_kernel<true, 1, false, 3>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem<1, false, 3>());
         cudaFuncSetAttribute(m2l_tc_kernel<true, 1, true>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tc_smem<1, true>());
         cudaFuncSetAttribute(m2l_tc_kernel<true, 1, true, 4>,
@@ -919,6 +961,11 @@ int launch_m2l_tc(const TcOps& ops, const int* il_slots, int p, const float* M_l
                             "issue->complete %.0f, complete(c)->a_full(c+2) %.0f\n",
                             b, Mt[b][2] - t0, nch, Mt[b][1] - t0, Mt[b][2] - Mt[b][1], per / cnt,
                             ia / cnt, ex / cnt, pr / cnt);
+                    if (P.dbg & 16)  // every chain of this CTA
+                        for (int c = 0; c < nch; ++c)
+                            fprintf(stderr, "T %d %d %lld %lld %lld %lld %lld\n", b, c,
+                                    T[b][4][c] - t0, T[b][1][c] - t0, T[b][2][c] - t0,
+                                    T[b][3][c] - t0, T[b][0][c] - t0);
                     for (int c = 100; c < 106 && c < nch; ++c)
                         fprintf(stderr, "  chain %d: acc_empty %lld a_full %lld committed %lld "
                                 "epi %lld (load %lld)\n", c, T[b][4][c] - t0, T[b][1][c] - t0,
@@ -954,6 +1001,9 @@ int launch_m2l_tc(const TcOps& ops, const int* il_slots, int p, const float* M_l
             mAh, mAl, mBh, mBl, P);
     else if (lean)
         m2l_tc_kernel<true, 1, true><<<grid, tc_threads<true>(), tc_smem<1, true>(), st>>>(
+            mAh, mAl, mBh, mBl, P);
+    else if (f16 && (T + 2) * N <= 240 && getenv("VFMM_M2L_AST3"))  // three operator stages
+        m2l_tc_kernel<true, 1, false, 3><<<grid, tc_threads<false>(), tc_smem<1, false, 3>(), st>>>(
             mAh, mAl, mBh, mBl, P);
     else if (f16)
         m2l_tc_kernel<true, 1><<<grid, tc_threads<false>(), tc_smem<1>(), st>>>(mAh, mAl, mBh, mBl, P);
