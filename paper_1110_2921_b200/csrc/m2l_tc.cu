@@ -131,13 +131,6 @@ __device__ __forceinline__ void tma_load_3d_mc(void* dst, const CUtensorMap* map
         "h"(mask)
         : "memory");
 }
-__device__ __forceinline__ void mma_commit_mc(uint64_t* bar, uint16_t mask) {
-    asm volatile(
-        "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
-        " [%0], %1;" ::"r"(smem_u32(bar)),
-        "h"(mask)
-        : "memory");
-}
 // Warp-wide issue: the whole (converged) warp executes these, one elected lane issues.  The
 // operands are then warp-uniform values, so no per-instruction elect/broadcast loop is needed
 // to move them into uniform registers (as for an issue under `if (lane == 0)`).
@@ -195,27 +188,6 @@ __device__ __forceinline__ uint64_t sw128_desc(const void* p) {
     d |= 2ull << 61;                        // SWIZZLE_128B
     return d;
 }
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
-                                         uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
-}
-__device__ __forceinline__ void mma_f16(uint32_t tmem_d, uint64_t a, uint64_t b, uint32_t idesc,
-                                        uint32_t accumulate) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "setp.ne.b32 p, %4, 0;\n\t"
-        "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_d),
-        "l"(a), "l"(b), "r"(idesc), "r"(accumulate));
-}
-__device__ __forceinline__ void mma_commit(uint64_t* bar) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::
-                     "r"(smem_u32(bar))
-                 : "memory");
-}
 __device__ __forceinline__ void tc_fence_after() {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
@@ -252,6 +224,7 @@ struct TcParams {
     // bit s of full[mt]: K step s (MMA K = 16 halves / 8 tf32) of row tile mt takes the whole
     // 3-product split; otherwise hi x hi alone (see launch_m2l_tc: low-order terms only)
     uint32_t full[2];
+    int chain;  // offsets per TMEM chain of a full-split K chunk (VFMM_M2L_CHAIN, default 1)
     int dbg;  // VFMM_M2L_DBG (measurement only, wrong results): 1 no TMEM drain, 2 no A, 4 no B loads
 };
 
@@ -481,8 +454,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc_threads<LEAN>(), 
                 for (int dd = 0; dd < 3; ++dd) {
                     if (!((mask >> dd) & 1)) continue;
                     const int buf = chain & 1;
-                    const bool opens = !merged || dd == __ffs(mask) - 1;
-                    const bool closes = !merged || dd == last_dd;
+                    // position of this offset among the group's offsets; a full chunk's chain
+                    // spans P.chain consecutive offsets, a hi-only chunk's the whole group
+                    const int pos = __popc(mask & ((1 << dd) - 1));
+                    const bool opens = merged ? pos == 0 : pos % P.chain == 0;
+                    const bool closes = dd == last_dd || (!merged && pos % P.chain == P.chain - 1);
                     if (opens) {
                         mbar_wait(&acc_empty[buf], ((chain >> 1) & 1) ^ 1);  // epilogue drained it
                         if (tr && lane == 0 && chain < TR_N) g_m2l_trace[tb][4][chain] = clk();
@@ -538,7 +514,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc_threads<LEAN>(), 
             if (!m) continue;
             for (int kc = 0; kc < P.nkc; ++kc) {
                 const bool merged = ((P.full[0] | (MT == 2 ? P.full[1] : 0u)) >> (4 * kc) & 15u) == 0;
-                nchains += merged ? 1 : __popc(m);
+                nchains += merged ? 1 : (__popc(m) + P.chain - 1) / P.chain;
             }
         }
         for (int ch = 0; ch < nchains; ++ch) {
@@ -936,6 +912,8 @@ int launch_m2l_tc(const TcOps& ops, const int* il_slots, int p, const float* M_l
     {
         const char* d = getenv("VFMM_M2L_DBG");
         P.dbg = d ? atoi(d) : 0;
+        const char* ch = getenv("VFMM_M2L_CHAIN");
+        P.chain = ch ? std::max(1, std::min(3, atoi(ch))) : 1;
         static bool traced = false;
         if ((P.dbg & 8) && traced) {  // summary of the previous traced launch
             static long long T[2][5][TR_N], Mt[2][4];
