@@ -26,11 +26,12 @@
 //
 // Accuracy: the tensor core accumulates with truncation, so a TMEM chain over all
 // 189 offsets x 16 K-steps x 3 products (~9000 accumulations) drifts by ~1e-4.  The chain is
-// therefore cut after every (offset, K chunk) -- 4 K-steps x 3 products = 12 MMAs: the MMA
-// warp alternates between two TMEM buffers and the epilogue warps add each finished buffer
-// into FP32 registers (round-to-nearest, packed f32x2 adds), so the result keeps ~FP32
-// accuracy (scripts/m2l_precision.py models the truncation: 3x less error than per-group
-// chains of up to 72 MMAs).
+// therefore cut after every (offset group, K chunk) -- at p = 10 with the order split
+// (launch_m2l_tc) <= 3 offsets x 10 MMAs: the MMA warp alternates between two TMEM buffers
+// and the epilogue warps add each finished buffer into FP32 registers (round-to-nearest,
+// packed f32x2 adds), so the result keeps ~FP32 accuracy (scripts/m2l_precision.py models the
+// truncation; VFMM_M2L_CHAIN=1 cuts after every offset: 15 % less rounding in the coarse
+// local expansions, 0.7 ms slower at c4, u and dgamma/dt unchanged).
 //
 // Warp roles (320 threads): warp 0 = TMA producer, warp 1 = TMEM alloc + MMA issuer,
 // warps 2-9 = epilogue (TMEM -> FP32 register sums -> L in Morton order).
@@ -224,7 +225,7 @@ struct TcParams {
     // bit s of full[mt]: K step s (MMA K = 16 halves / 8 tf32) of row tile mt takes the whole
     // 3-product split; otherwise hi x hi alone (see launch_m2l_tc: low-order terms only)
     uint32_t full[2];
-    int chain;  // offsets per TMEM chain of a full-split K chunk (VFMM_M2L_CHAIN, default 1)
+    int chain;  // offsets per TMEM chain of a full-split K chunk (VFMM_M2L_CHAIN, default 3)
     int dbg;  // VFMM_M2L_DBG (measurement only, wrong results): 1 no TMEM drain, 2 no A, 4 no B loads
 };
 
@@ -409,9 +410,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc_threads<LEAN>(), 
         const uint64_t slab_step = (uint64_t)((P.N * 128) >> 4);  // descriptor units (16 B)
         int sa = 0, sb = 0;
         uint32_t pa = 0, pb = 0;
-        // One TMEM accumulation chain per (offset, K chunk) -- <= 4 K steps x 3 products -- or,
-        // for a K chunk without full-split steps (hi x hi alone, high orders only), one chain
-        // per (offset group, K chunk): <= 3 offsets x 4 single MMAs.
+        // One TMEM accumulation chain per P.chain offsets of a group and K chunk (<= 4 K steps
+        // x 3 products each), or, for a K chunk without full-split steps (hi x hi alone, high
+        // orders only), per (offset group, K chunk): <= 3 offsets x 4 single MMAs.
         int chain = 0;
         // issue one chain segment: K steps [0, nks) of every row tile, the first nf[mt] steps
         // with the whole split; first = this segment opens the TMEM chain
@@ -913,7 +914,7 @@ int launch_m2l_tc(const TcOps& ops, const int* il_slots, int p, const float* M_l
         const char* d = getenv("VFMM_M2L_DBG");
         P.dbg = d ? atoi(d) : 0;
         const char* ch = getenv("VFMM_M2L_CHAIN");
-        P.chain = ch ? std::max(1, std::min(3, atoi(ch))) : 1;
+        P.chain = ch ? std::max(1, std::min(3, atoi(ch))) : 3;
         static bool traced = false;
         if ((P.dbg & 8) && traced) {  // summary of the previous traced launch
             static long long T[2][5][TR_N], Mt[2][4];
