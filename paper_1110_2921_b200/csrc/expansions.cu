@@ -159,21 +159,23 @@ __global__ void __launch_bounds__(64) p2m_kernel(const float* __restrict__ s6, i
             }
             __syncthreads();
             const int nq = (cnt + 3) >> 2;
-#pragma unroll
-            for (int w = 0; w < 2; ++w) {
-                const int k = k0 + threadIdx.x + 64 * w;
-                if (k >= nc) continue;
-                const float4* R4 = reinterpret_cast<const float4*>(Rs + k * RST);
-                const float4* G0 = reinterpret_cast<const float4*>(gs);
-                const float4* G1 = reinterpret_cast<const float4*>(gs + CH);
-                const float4* G2 = reinterpret_cast<const float4*>(gs + 2 * CH);
-                // (kept in particle order: the sums cancel in the root multipole)
-                for (int q = 0; q < nq; ++q) {
-                    const float4 r = R4[q], a = G0[q], bb = G1[q], c = G2[q];
-                    acc[w][0] = fmaf(a.x, r.x, fmaf(a.y, r.y, fmaf(a.z, r.z, fmaf(a.w, r.w, acc[w][0]))));
-                    acc[w][1] = fmaf(bb.x, r.x, fmaf(bb.y, r.y, fmaf(bb.z, r.z, fmaf(bb.w, r.w, acc[w][1]))));
-                    acc[w][2] = fmaf(c.x, r.x, fmaf(c.y, r.y, fmaf(c.z, r.z, fmaf(c.w, r.w, acc[w][2]))));
-                }
+            const float4* G0 = reinterpret_cast<const float4*>(gs);
+            const float4* G1 = reinterpret_cast<const float4*>(gs + CH);
+            const float4* G2 = reinterpret_cast<const float4*>(gs + 2 * CH);
+            const int ka = k0 + threadIdx.x, kb = ka + 64;
+            // rows k and k + 64 of this thread (a padded row when out of range: its sums are
+            // never stored); the strengths are loaded once per quad for both rows
+            const float4* Ra = reinterpret_cast<const float4*>(Rs + min(ka, nc - 1) * RST);
+            const float4* Rb = reinterpret_cast<const float4*>(Rs + min(kb, nc - 1) * RST);
+            // (kept in particle order: the sums cancel in the root multipole)
+            for (int q = 0; q < nq; ++q) {
+                const float4 a = G0[q], bb = G1[q], c = G2[q], r = Ra[q], t = Rb[q];
+                acc[0][0] = fmaf(a.x, r.x, fmaf(a.y, r.y, fmaf(a.z, r.z, fmaf(a.w, r.w, acc[0][0]))));
+                acc[0][1] = fmaf(bb.x, r.x, fmaf(bb.y, r.y, fmaf(bb.z, r.z, fmaf(bb.w, r.w, acc[0][1]))));
+                acc[0][2] = fmaf(c.x, r.x, fmaf(c.y, r.y, fmaf(c.z, r.z, fmaf(c.w, r.w, acc[0][2]))));
+                acc[1][0] = fmaf(a.x, t.x, fmaf(a.y, t.y, fmaf(a.z, t.z, fmaf(a.w, t.w, acc[1][0]))));
+                acc[1][1] = fmaf(bb.x, t.x, fmaf(bb.y, t.y, fmaf(bb.z, t.z, fmaf(bb.w, t.w, acc[1][1]))));
+                acc[1][2] = fmaf(c.x, t.x, fmaf(c.y, t.y, fmaf(c.z, t.z, fmaf(c.w, t.w, acc[1][2]))));
             }
         }
         float* out = M + leaf * 3 * nc;

@@ -70,7 +70,11 @@ template <int MT> __host__ __device__ constexpr int b_bytes() { return b_wrows<M
 // y-windows -- 161 KB of shared memory and 192 threads, so one P2P block (62 KB) fits beside
 // it on the same SM (tensor pipe and FP32 pipe busy at once, capi.cu "co-resident mode")
 template <bool LEAN> __host__ __device__ constexpr int tc_epi() { return LEAN ? 4 : 8; }
-template <bool LEAN> __host__ __device__ constexpr int tc_threads() { return 64 + 32 * tc_epi<LEAN>(); }
+// warps: 0 operator producer, 1 MMA issuer, 2 .. 1 + tc_epi epilogue, 2 + tc_epi window producer
+// (LEAN: warp 0 produces both, to stay within its register budget)
+template <bool LEAN> __host__ __device__ constexpr int tc_threads() {
+    return (LEAN ? 64 : 96) + 32 * tc_epi<LEAN>();
+}
 // window stage bytes: LEAN 192 rows; the 3-stage variant (AST = 3, XT = 8 / T = 8 layout)
 // 240 rows (30 KB), which leaves room for a third operator stage
 template <int MT, bool LEAN = false, int AST = 2> __host__ __device__ constexpr int b_bytes_v() {
@@ -333,11 +337,14 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc_threads<LEAN>(), 
     const int tb = blockIdx.x & 1;
     if (tr && threadIdx.x == 0) g_m2l_meta[tb][0] = clk();
 
-    if (warp == 0) {
-        // ===================== TMA producer =====================
+    if (warp == 0 || (!LEAN && warp == 2 + tc_epi<LEAN>())) {
+        // ===================== TMA producers =====================
         // per offset group (dx, dz, source parity): one y-window of T + 2 slabs (rows
-        // gpy0 - 1 .. gpy0 + T) per K chunk serves the group's <= 3 offsets dy = -1, 0, 1;
-        // then the operator chunk of each valid offset (shared with the peer CTA)
+        // gpy0 - 1 .. gpy0 + T) per K chunk serves the group's <= 3 offsets dy = -1, 0, 1
+        // (window producer, the last warp); the operator chunk of each valid offset, shared
+        // with the peer CTA (operator producer, warp 0).  Two threads, so neither stream waits
+        // behind the other's free slots.
+        const bool doA = warp == 0, doB = LEAN || warp != 0;
         if (lane == 0) {
             int sa = 0, sb = 0, nload = 0;
             uint32_t pa = 0, pb = 0;
@@ -352,6 +359,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc_threads<LEAN>(), 
                 for (int kc = 0; kc < P.nkc; ++kc) {
                     // the lo halves are loaded only for K chunks with a full-split step
                     const bool need_lo = (((P.full[0] | (MT == 2 ? P.full[1] : 0u)) >> (4 * kc)) & 15u) != 0;
+                    if (doB) {
                     mbar_wait(&b_empty[sb], pb ^ 1);
                     if (P.dbg & 4) {
                         mbar_arrive(&b_full[sb]);
@@ -367,6 +375,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc_threads<LEAN>(), 
                         sb = 0;
                         pb ^= 1;
                     }
+                    }
+                    if (!doA) continue;
 #pragma unroll
                     for (int d = 0; d < 3; ++d) {
                         if (!((mask >> d) & 1)) continue;
