@@ -135,6 +135,28 @@ vfmm_status vfmm_evaluate(vfmm_ctx* ctx, int64_t n, const float* pos, const floa
 vfmm_status vfmm_evaluate_at(vfmm_ctx* ctx, int64_t n_src, const float* pos, const float* gamma,
                              int64_t n_tgt, const float* tpos, float* tvel, void* cuda_stream);
 
+/* ---- NEXT-4: hybrid treecode, cell-particle traversal (section 3.2) ----
+   Velocity and stretching as vfmm_evaluate computes them (Eqs. 5 and 8), by a stack-based
+   traversal of an adaptive octree instead of the uniform FMM: the leaves are the non-empty
+   cells holding <= n_crit particles (or at the finest level, the context's depth, 0 = auto),
+   "automatically choosing the number of particles per box" (reading R22 in
+   DESIGN.md).  For each leaf B of targets the traversal starts from the near 3^3 root images
+   (free space: the root) and pops cells S: if r_S + r_B < theta |c_B - c_S| (r = half
+   diagonal, the multipole acceptance criterion) S acts on every target of B through its
+   multipole (cell-particle, M2P: Eq. 11's local expansion of order 2 at the target point,
+   then Eqs. 12-15; no cutoff); else a leaf S acts particle-particle (Eq. 5 /
+   Eq. 8 exactly); else its non-empty children are pushed.  Images outside the
+   near block come through the root local expansion as in vfmm_evaluate (image_levels >= 2).
+   The context's p, depth, image_levels, sigma and scheme apply; its mode is ignored.
+   pos, gamma: device 3 x n (SoA), vel, dgamma: device 3 x n outputs (no aliasing), input order.
+   theta in [0, 1) (0: every interaction particle-particle, the direct sum over the near
+   block), n_crit >= 1; else VFMM_EINVAL.  Not for distributed contexts (VFMM_EINVAL).
+   Asynchronous on `cuda_stream`; vfmm_get_stats reports n_p2p_pairs (ordered pairs) and, in
+   n_m2l, the number of cell-particle interactions. */
+vfmm_status vfmm_evaluate_tree(vfmm_ctx* ctx, int64_t n, const float* pos, const float* gamma,
+                               float* vel, float* dgamma, float theta, int32_t n_crit,
+                               void* cuda_stream);
+
 /* One forward-Euler time step of the vortex particle method (section 2; forward
    Euler), the three updates simultaneous:
      x_i     += u_i dt          convection, Eq. (7) PAPER.md:91 (wrapped into the box when

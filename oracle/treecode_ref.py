@@ -14,7 +14,8 @@ particles per box at the deepest levels of the tree".  The cell-cell half is the
   3. the multipole of every cell, Eq. (10) about the cell centre: straight
      from its particles (``fmm_ref.p2m``) -- the definition the FMM's M2M reaches exactly;
   4. per target leaf B, a stack traversal from the near 3^3 root images (reading R5):
-     pop cell S; if r_S + r_B < theta |c_B - c_S| (r = half diagonal, reading R22) the cell
+     pop cell S; if r_S + r_B < theta |c_B - c_S| (r = half diagonal, reading R22; evaluated
+     exactly as 0.75 (w_S + w_B)^2 < theta^2 d^2 in leaf widths) the cell
      interacts with each target of B through its multipole (M2P: Eq. (11)'s local expansion
      at the target point itself, rows n <= 2 of ``fmm_ref.m2l_matrix``'s formula, then Eqs. (12)-(15)'s gradient and
      Hessian at the expansion centre, ``fmm_ref.l2p`` at 0; the cutoff is dropped in the far
@@ -151,7 +152,16 @@ def evaluate(pos, gam, sigma, box_lo, box_len, depth, p, theta, n_crit, image_le
             mcache[(l, c)] = F.p2m(X[s:e] - center(l, c), G[s:e], p)
         return mcache[(l, c)]
 
-    half_diag = lambda l: 0.5 * math.sqrt(3.0) * ln / (1 << l)
+    # MAC r_S + r_B < theta d with r = (sqrt 3 / 2) w, squared and in leaf widths (exact
+    # half-integer centre offsets): 0.75 (w_S + w_B)^2 < theta^2 d^2, theta rounded to float32
+    # as the C ABI receives it (so that ties decide the same way on both sides, reading R22)
+    th = float(np.float32(theta))
+    th2 = th * th
+
+    def cell_lw(l, c):  # centre (leaf widths from the box corner) and width of a cell
+        ix, iy, iz = _decode(c, l)
+        w = float(1 << (L - l))
+        return np.array([(ix + 0.5) * w, (iy + 0.5) * w, (iz + 0.5) * w]), w
     if image_levels > 0:
         images = [(a, b, d) for a in (-1, 0, 1) for b in (-1, 0, 1) for d in (-1, 0, 1)]
     else:
@@ -165,13 +175,17 @@ def evaluate(pos, gam, sigma, box_lo, box_len, depth, p, theta, n_crit, image_le
     for (lb, cb) in leaves:  # step 4
         s, e = rng(lb, cb)
         xi, gi = X[s:e], G[s:e]
-        cB, rB = center(lb, cb), half_diag(lb)
-        stack = [(0, 0, np.array(o, np.float64) * ln) for o in images]
+        cBw, wB = cell_lw(lb, cb)
+        stack = [(0, 0, np.array(o, np.float64)) for o in images]
         xs_list, gs_list, acc = [], [], []
         while stack:
-            l, c, sh = stack.pop()
+            l, c, o = stack.pop()
+            sh = o * ln
             cS = center(l, c) + sh
-            if half_diag(l) + rB < theta * np.linalg.norm(cB - cS):
+            cSw, wS = cell_lw(l, c)
+            dd = cBw - (cSw + o * float(1 << L))
+            d2 = dd[0] * dd[0] + dd[1] * dd[1] + dd[2] * dd[2]
+            if 0.75 * (wS + wB) ** 2 < th2 * d2:
                 acc.append((multipole(l, c), cS))
                 n_m2p += e - s
             elif is_leaf(l, c):
@@ -182,7 +196,7 @@ def evaluate(pos, gam, sigma, box_lo, box_len, depth, p, theta, n_crit, image_le
                 for ch in range(8):
                     a, b = rng(l + 1, 8 * c + ch)
                     if b > a:
-                        stack.append((l + 1, 8 * c + ch, sh))
+                        stack.append((l + 1, 8 * c + ch, o))
         for q0 in range(0, len(acc), 32):  # the accepted cells, in chunks
             ch = acc[q0:q0 + 32]
             Ms = np.stack([a[0] for a in ch])

@@ -63,7 +63,7 @@ EXPORTS = ["vfmm_abi_version", "vfmm_params_default", "vfmm_create", "vfmm_evalu
            "vfmm_last_error_message", "vfmm_destroy", "vfmm_nccl_get_unique_id",
            "vfmm_create_nccl", "vfmm_partition", "vfmm_evaluate_logical", "vfmm_dist_plan",
            "vfmm_route_counts", "vfmm_step", "vfmm_evaluate_at", "vfmm_reinit",
-           "vfmm_evaluate_sigma"]
+           "vfmm_evaluate_sigma", "vfmm_evaluate_tree"]
 
 
 class c_reinit_info(ctypes.Structure):
@@ -111,6 +111,8 @@ def load_library(path: str = LIB_PATH):
     L.vfmm_evaluate_sigma.argtypes = [vp, i64, vp, vp, vp, vp, vp, vp]
     L.vfmm_evaluate_sigma.restype = ctypes.c_int
     L.vfmm_evaluate_at.restype = ctypes.c_int
+    L.vfmm_evaluate_tree.argtypes = [vp, i64, vp, vp, vp, vp, ctypes.c_float, ctypes.c_int32, vp]
+    L.vfmm_evaluate_tree.restype = ctypes.c_int
     L.vfmm_reinit.argtypes = [vp, i64, vp, vp, ctypes.c_float, i64, vp, ctypes.c_float,
                               ctypes.c_float, ctypes.c_int32, ctypes.c_int32, vp, vp,
                               ctypes.POINTER(c_reinit_info), vp]
@@ -266,6 +268,25 @@ class Evaluator:
         vel = torch.empty_like(pos)
         dg = torch.empty_like(pos)
         return self.evaluate_into(pos, gamma, vel, dg, stream)
+
+    def evaluate_tree(self, pos, gamma, theta: float = 0.5, n_crit: int = 64, stream=None):
+        """Hybrid treecode, cell-particle traversal (C ABI vfmm_evaluate_tree):
+        adaptive leaves of <= n_crit particles, multipole acceptance r_S + r_B < theta d."""
+        import torch
+
+        for t in (pos, gamma):
+            if not (t.is_cuda and t.dtype == torch.float32 and t.is_contiguous()
+                    and t.dim() == 2 and t.shape[0] == 3):
+                raise ValueError("expected contiguous float32 CUDA tensors of shape (3, N)")
+        vel = torch.empty_like(pos)
+        dg = torch.empty_like(pos)
+        if stream is None:
+            stream = torch.cuda.current_stream(pos.device)
+        _check(self._L, self._ctx, self._L.vfmm_evaluate_tree(
+            self._ctx, pos.shape[1], pos.data_ptr(), gamma.data_ptr(), vel.data_ptr(),
+            dg.data_ptr(), ctypes.c_float(theta), int(n_crit), ctypes.c_void_p(stream.cuda_stream)))
+        self._n = pos.shape[1]
+        return vel, dg
 
     def evaluate_at(self, pos, gamma, tpos, stream=None):
         """Velocity at target points tpos ((3, T) float32 CUDA tensor) induced by the particles

@@ -79,6 +79,12 @@ struct vfmm_ctx {
     float *Mall = nullptr, *Lall = nullptr;
     int* d_err = nullptr;
     unsigned long long* d_pairs = nullptr;  // P2P pair counter of the last evaluate
+    // vfmm_evaluate_tree: adaptive leaves (level, cell), their count, interaction counters
+    int2* tree_groups = nullptr;
+    size_t tree_groups_cap = 0;
+    int* d_tree_ng = nullptr;
+    unsigned long long* d_tree_cnt = nullptr;
+    bool tree_last = false;  // the last evaluate was a treecode one (stats)
     // host-API staging
     int64_t cap_host_n = 0;
     float* hbuf = nullptr;  // 12 x n
@@ -680,6 +686,7 @@ static vfmm_status evaluate_impl(vfmm_ctx* c, int64_t n, const float* pos, const
     if (c->last_stream != st && c->have_last)
         CK(cudaStreamWaitEvent(st, c->ev[vfmm_ctx::NEV - 1], 0), "order after last evaluate");
     c->have_last = true;
+    c->tree_last = false;
     if (c->dist) {  // distributed evaluation over NCCL (this process = one rank)
         ensure_rank_states(c, c->R, c->rank, 1);
         DistShared D = make_shared(c, c->R);
@@ -1005,6 +1012,124 @@ static vfmm_status evaluate_impl(vfmm_ctx* c, int64_t n, const float* pos, const
     CK(cudaGetLastError(), "l2p kernel");
     CK(cudaEventRecord(c->ev[9], st), "event");
     S.n_kernel_launches = nl;
+    return VFMM_OK;
+}
+
+vfmm_status vfmm_evaluate_tree(vfmm_ctx* c, int64_t n, const float* pos, const float* gamma,
+                               float* vel, float* dgamma, float theta, int32_t n_crit,
+                               void* stream) {
+    if (!c || n < 1 || !pos || !gamma || !vel || !dgamma) return VFMM_EINVAL;
+    if (c->dist || !(theta >= 0.f && theta < 1.f) || n_crit < 1) return VFMM_EINVAL;
+    if (n > ((int64_t)1 << 31) - 1) return VFMM_EINVAL;
+    auto overlap = [n](const void* a, const void* b) {
+        const char* x = (const char*)a;
+        const char* y = (const char*)b;
+        const size_t L = 3 * (size_t)n * sizeof(float);
+        return x < y + L && y < x + L;
+    };
+    if (overlap(vel, dgamma) || overlap(vel, pos) || overlap(vel, gamma) ||
+        overlap(dgamma, pos) || overlap(dgamma, gamma))
+        return VFMM_EINVAL;
+    CK(cudaSetDevice(c->device), "set device");
+    (void)cudaGetLastError();
+    cudaStream_t st = (cudaStream_t)stream;
+    if (c->last_stream != st && c->have_last)
+        CK(cudaStreamWaitEvent(st, c->ev[vfmm_ctx::NEV - 1], 0), "order after last evaluate");
+    c->have_last = true;
+    const vfmm_params& P = c->prm;
+    vfmm_stats& S = c->stats;
+    memset(&S, 0, sizeof(S));
+    c->comm_timed = false;
+    c->last_stream = st;
+    c->last_n = n;
+    c->tree_last = true;
+    const KernelConsts kc = make_kernel_consts(P.sigma);
+    // finest level: the context's depth, else the FMM's automatic one (leaf width >= 4 sigma,
+    // so every cell-particle interaction the MAC accepts is far outside the cores, reading R3)
+    const int depth = P.depth > 0 ? P.depth : auto_depth(P, n);
+    vfmm_status s = ensure_ws(c, n, depth);
+    if (s != VFMM_OK) return s;
+    const size_t gcap = tree_groups_cap(n, depth);
+    if (gcap > c->tree_groups_cap || !c->d_tree_ng) {
+        if (c->last_stream) CK(cudaStreamSynchronize(c->last_stream), "sync");
+        dfree(c->tree_groups);
+        c->tree_groups_cap = 0;
+        CK(cudaMalloc((void**)&c->tree_groups, gcap * sizeof(int2)), "alloc tree groups");
+        c->tree_groups_cap = gcap;
+        if (!c->d_tree_ng) CK(cudaMalloc((void**)&c->d_tree_ng, sizeof(int)), "alloc");
+        if (!c->d_tree_cnt)
+            CK(cudaMalloc((void**)&c->d_tree_cnt, 2 * sizeof(unsigned long long)), "alloc");
+    }
+    c->last_depth = depth;
+    S.depth_used = depth;
+    Geom g{P.box_lo, P.box_len, (double)P.box_lo, (double)P.box_len, depth, P.image_levels > 0};
+    const float a = (float)((double)P.box_len / (double)(1 << depth));
+    const int p = P.p, nc = ncoef(p);
+    const HostOps& H = c->hops;
+    auto Mlev = [&](int l) { return c->Mall + level_offset(l) * 3 * nc; };
+    auto Llev = [&](int l) { return c->Lall + level_offset(l) * 3 * nc; };
+    int nl = 0;
+    NvtxRange nv("vfmm/tree");
+    CK(cudaEventRecord(c->ev[0], st), "event");
+    launch_keys(pos, n, g, c->keys[0], c->vals[0], c->d_err, st);
+    CK(cudaEventRecord(c->ev[1], st), "event");
+    launch_radix_sort(c->keys[0], c->vals[0], c->keys[1], c->vals[1], n, 3 * depth, c->radix_tmp,
+                      st, &c->keys_sorted, &c->perm, &nl);
+    CK(cudaEventRecord(c->ev[2], st), "event");
+    launch_leaf_ranges(c->keys_sorted, n, depth, c->leaf_start, st);
+    launch_gather(pos, gamma, c->perm, c->keys_sorted, n, g, c->sorted6, n, 0, st);
+    nl += 3;
+    CK(cudaGetLastError(), "tree kernels");
+    CK(cudaEventRecord(c->ev[3], st), "event");
+    c->have_tree = true;
+    // multipoles of every cell (Eq. 10 about the cell centres): P2M + M2M, as in the FMM
+    nv.next("vfmm/upward");
+    launch_p2m(c->sorted6, n, c->leaf_start, p, 1.f / a, Mlev(depth), 0, (int64_t)1 << (3 * depth),
+               st);
+    ++nl;
+    CK(cudaEventRecord(c->ev[4], st), "event");
+    for (int l = depth - 1; l >= 0; --l)
+        nl += launch_m2m(c->d_m2m, p, H.KP, H.NR, Mlev(l + 1), Mlev(l), l, 0, (int64_t)1 << (3 * l),
+                         c->m2m_scratch, c->m2m_scratch_floats, st);
+    CK(cudaGetLastError(), "upward kernels");
+    CK(cudaEventRecord(c->ev[5], st), "event");
+    // images outside the near 3^3 block: root local expansion, L2L to the leaves
+    const bool rings = P.image_levels >= 2;
+    nv.next("vfmm/m2l");
+    if (rings) {
+        launch_periodic(c->d_per, p, H.KP, H.NR, Mlev(0), Llev(0), st);
+        CK(cudaMemsetAsync(Llev(1), 0, (level_offset(depth + 1) - 1) * 3 * nc * sizeof(float), st),
+           "memset L");
+        ++nl;
+    }
+    CK(cudaEventRecord(c->ev[6], st), "event");
+    nv.next("vfmm/downward");
+    if (rings) {
+        for (int l = 1; l <= depth; ++l) {
+            launch_l2l(c->d_l2l, p, H.KP, H.NR, Llev(l - 1), Llev(l), l, 0,
+                       (int64_t)1 << (3 * (l - 1)), st);
+            ++nl;
+        }
+        CK(cudaGetLastError(), "downward kernels");
+    }
+    CK(cudaEventRecord(c->ev[7], st), "event");
+    // the traversal: cell-particle and particle-particle interactions into near6
+    nv.next("vfmm/p2p");
+    launch_tree(c->sorted6, n, c->keys_sorted, c->leaf_start, depth, a, P.image_levels > 0,
+                P.scheme, p, n_crit, theta, c->Mall, kc, c->tree_groups, c->d_tree_ng,
+                c->d_tree_cnt, c->near6, st);
+    nl += 2;
+    CK(cudaGetLastError(), "tree traversal");
+    CK(cudaEventRecord(c->ev[8], st), "event");
+    nv.next("vfmm/l2p");
+    launch_l2p_combine(l2p_map(c), c->sorted6, c->near6, c->perm, n, c->leaf_start, p, a,
+                       Llev(depth), P.scheme, true, rings, vel, dgamma, 0,
+                       (int64_t)1 << (3 * depth), 0, n, st);
+    ++nl;
+    CK(cudaGetLastError(), "l2p kernel");
+    CK(cudaEventRecord(c->ev[9], st), "event");
+    S.n_kernel_launches = nl;
+    c->have_exp = false;
     return VFMM_OK;
 }
 
@@ -1447,7 +1572,12 @@ vfmm_status vfmm_get_stats(vfmm_ctx* c, vfmm_stats* out) {
             S.ms_comm = S.ms_comm_exposed = t;
         }
     }
-    if (c->prm.mode == VFMM_MODE_FMM || c->prm.mode == VFMM_MODE_NEAR_ONLY) {
+    if (c->tree_last) {  // treecode: P2P pairs and M2P cell-particle interactions
+        unsigned long long cnt[2] = {0, 0};
+        CK(cudaMemcpy(cnt, c->d_tree_cnt, sizeof(cnt), cudaMemcpyDeviceToHost), "copy counts");
+        S.n_p2p_pairs = (int64_t)cnt[0];
+        S.n_m2l = (int64_t)cnt[1];
+    } else if (c->prm.mode == VFMM_MODE_FMM || c->prm.mode == VFMM_MODE_NEAR_ONLY) {
         unsigned long long pairs = 0;
         CK(cudaMemcpy(&pairs, c->d_pairs, sizeof(pairs), cudaMemcpyDeviceToHost), "copy pairs");
         S.n_p2p_pairs = (int64_t)pairs;
@@ -1491,6 +1621,9 @@ void vfmm_destroy(vfmm_ctx* c) {
     if (!c) return;
     cudaSetDevice(c->device);
     if (c->last_stream) cudaStreamSynchronize(c->last_stream);
+    dfree(c->tree_groups);
+    dfree(c->d_tree_ng);
+    dfree(c->d_tree_cnt);
     dfree(c->d_m2m);
     dfree(c->d_l2l);
     dfree(c->d_m2l);

@@ -1067,4 +1067,414 @@ void launch_direct(const float* pos, const float* gamma, int64_t n, float len, i
         direct_kernel<1><<<grid, 128, 0, st>>>(pos, gamma, n, (double)len, m, kc, vel, dgam);
 }
 
+
+// ---------------------------------------------------------------------------
+// Hybrid treecode, cell-particle half (section 3.2): stack-based traversal
+// of the adaptive octree with cell-particle (M2P) and particle-particle interactions; the
+// adaptive leaves hold <= n_crit particles ("automatically choosing the number of particles
+// per box", reading R22).  The multipoles of every cell are the FMM's P2M / M2M output (Eq. 10
+// about the cell centre, scaled M~ = M / w_l^n); the images outside the near 3^3 block come
+// through the root local expansion (periodic kernel + L2L + L2P, as in the FMM).
+// ---------------------------------------------------------------------------
+namespace {
+
+constexpr int TREE_WARPS = 4;
+constexpr int TREE_STACK = 128;
+
+__host__ __device__ __forceinline__ int64_t lvl_off(int l) { return ((int64_t(1) << (3 * l)) - 1) / 7; }
+
+// adaptive leaves: a non-empty cell of level l >= 1 with count <= n_crit (or l = L) whose parent
+// holds more than n_crit; appended (in no particular order) to groups as (level, cell)
+__global__ void tree_groups_kernel(const int* __restrict__ leaf_start, int L, int ncrit,
+                                   int64_t total, int2* __restrict__ groups,
+                                   int* __restrict__ ngroups) {
+    for (int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; t < total;
+         t += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g = t + 1;  // skip the root
+        int l = 1;
+        while (l < L && g >= lvl_off(l + 1)) ++l;
+        const int64_t c = g - lvl_off(l);
+        const int sh = 3 * (L - l);
+        const int cnt = leaf_start[(c + 1) << sh] - leaf_start[c << sh];
+        if (cnt == 0 || (l < L && cnt > ncrit)) continue;
+        if (l > 1) {
+            const int64_t pc = c >> 3;
+            const int psh = sh + 3;
+            if (leaf_start[(pc + 1) << psh] - leaf_start[pc << psh] <= ncrit) continue;
+        }
+        const int k = atomicAdd(ngroups, 1);
+        groups[k] = make_int2(l, (int)c);
+    }
+}
+
+struct TreeArgs {
+    const float* s6;
+    int64_t n;
+    const uint32_t* keys;
+    const int* leaf_start;
+    const int2* groups;
+    const int* ngroups;
+    const float* Mall;
+    float* near6;
+    unsigned long long* counters;  // [0] P2P pairs, [1] M2P cell-particle interactions
+    int L, p, ncrit, periodic;
+    float aL;      // leaf width at level L (float, exact len / 2^L)
+    float theta;
+    int dbg;       // VFMM_TREE_DBG: bit 0 drops the P2P terms, bit 1 the M2P terms (tests)
+};
+
+// Multipole (scaled, level l, packed real) -> rows n <= 2 of the local expansion at the target
+// point, Eq. (11): L_n^m = sum_{k,l} (-1)^{n+m} I_{n+k}^{l-m}(D) M_k^l, D in cell widths.
+// I_j^q (q >= 0) by I_0^0 = 1/r, I_j^j = -(2j-1)(x+iy)/r^2 I_{j-1}^{j-1},
+// I_j^q = ((2j-1) z I_{j-1}^q - ((j-1)^2 - q^2) I_{j-2}^q) / r^2, rows rolled through 3 slots of
+// the lane's shared-memory column; negative orders by I^{-q} = (-1)^q conj(I^q).
+// out (per component c): [L10, ReL11, ImL11, L20, ReL21, ImL21, ReL22, ImL22]
+__device__ __forceinline__ void m2p_rows(const float* __restrict__ Msh, int p, int nc, float dx,
+                                         float dy, float dz, float* __restrict__ Ish, int lane,
+                                         float out[3][8]) {
+    const int PQ = p + 3;
+    auto IR = [&](int j, int q) -> float& { return Ish[(((j % 3) * PQ + q) * 2) * 32 + lane]; };
+    auto II = [&](int j, int q) -> float& { return Ish[(((j % 3) * PQ + q) * 2 + 1) * 32 + lane]; };
+    const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
+    const float rho = 1.f / r2;
+    auto gen = [&](int j) {
+        if (j == 0) {
+            IR(0, 0) = rsqrtf(r2);
+            II(0, 0) = 0.f;
+            return;
+        }
+        const float f = (float)(2 * j - 1);
+        for (int q = 0; q < j; ++q) {
+            const float a = IR(j - 1, q), b = II(j - 1, q);
+            float vr = f * dz * a, vi = f * dz * b;
+            if (q <= j - 2) {
+                const float w = (float)((j - 1) * (j - 1) - q * q);
+                vr = fmaf(-w, IR(j - 2, q), vr);
+                vi = fmaf(-w, II(j - 2, q), vi);
+            }
+            IR(j, q) = vr * rho;
+            II(j, q) = vi * rho;
+        }
+        const float a = IR(j - 1, j - 1), b = II(j - 1, j - 1);
+        const float s = -f * rho;
+        IR(j, j) = s * (dx * a - dy * b);
+        II(j, j) = s * (dx * b + dy * a);
+    };
+    auto getI = [&](int j, int q, float& re, float& im) {
+        if (q >= 0) {
+            re = IR(j, q);
+            im = II(j, q);
+        } else {
+            const float sg = (q & 1) ? -1.f : 1.f;
+            re = sg * IR(j, -q);
+            im = -sg * II(j, -q);
+        }
+    };
+#pragma unroll
+    for (int c = 0; c < 3; ++c)
+#pragma unroll
+        for (int t = 0; t < 8; ++t) out[c][t] = 0.f;
+    gen(0);
+    gen(1);
+    gen(2);
+    for (int k = 0; k <= p; ++k) {
+        if (k >= 1) gen(k + 2);
+        for (int l = -k; l <= k; ++l) {
+            const int al = l < 0 ? -l : l;
+            float mr[3], mi[3];
+            const float sgm = (l < 0 && (al & 1)) ? -1.f : 1.f;
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                mr[c] = sgm * Msh[c * nc + pk_re(k, al)];
+                const float im = al == 0 ? 0.f : Msh[c * nc + pk_im(k, al)];
+                mi[c] = l < 0 ? -sgm * im : im;
+            }
+            float ar, ai;
+            // (n, m) = (1, 0): sign -1, real part
+            getI(k + 1, l, ar, ai);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) out[c][0] -= ar * mr[c] - ai * mi[c];
+            // (1, 1): sign +1
+            getI(k + 1, l - 1, ar, ai);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                out[c][1] += ar * mr[c] - ai * mi[c];
+                out[c][2] += ar * mi[c] + ai * mr[c];
+            }
+            // (2, 0): sign +1, real part
+            getI(k + 2, l, ar, ai);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) out[c][3] += ar * mr[c] - ai * mi[c];
+            // (2, 1): sign -1
+            getI(k + 2, l - 1, ar, ai);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                out[c][4] -= ar * mr[c] - ai * mi[c];
+                out[c][5] -= ar * mi[c] + ai * mr[c];
+            }
+            // (2, 2): sign +1
+            getI(k + 2, l - 2, ar, ai);
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                out[c][6] += ar * mr[c] - ai * mi[c];
+                out[c][7] += ar * mi[c] + ai * mr[c];
+            }
+        }
+    }
+}
+
+template <int SCHEME>
+__global__ void __launch_bounds__(TREE_WARPS * 32) tree_kernel(TreeArgs A, KernelConsts kc) {
+    extern __shared__ float4 tree_sm4[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int p = A.p, nc = (p + 1) * (p + 1), L = A.L;
+    const int ish_floats = 3 * (p + 3) * 2 * 32;
+    const int msh_floats = (3 * nc + 3) & ~3;
+    float* base = reinterpret_cast<float*>(tree_sm4) + warp * (ish_floats + msh_floats + 9 * 32);
+    float* Ish = base;
+    float* Msh = base + ish_floats;
+    float* Ssh = Msh + msh_floats;  // sources: [dx dy dz gx gy gz ix iy iz][32]
+    __shared__ int2 stack_sm[TREE_WARPS][TREE_STACK];
+    int2* stk = stack_sm[warp];
+    const int ng = *A.ngroups;
+    const int side = 1 << L;
+    const float aL = A.aL;
+    const float inv_aL = 1.f / aL;
+    const int nimg = A.periodic ? 27 : 1;
+    const double th2 = (double)A.theta * (double)A.theta;
+    for (int g = blockIdx.x * TREE_WARPS + warp; g < ng; g += gridDim.x * TREE_WARPS) {
+        const int2 grp = A.groups[g];
+        const int lb = grp.x, cb = grp.y;
+        const int shb = 3 * (L - lb);
+        const int s = A.leaf_start[(int64_t)cb << shb], e = A.leaf_start[((int64_t)cb + 1) << shb];
+        const float wb = (float)(1 << (L - lb));  // group width in leaf widths
+        const float Gx = ((float)compact3p((uint32_t)cb) + 0.5f) * wb;
+        const float Gy = ((float)compact3p((uint32_t)cb >> 1) + 0.5f) * wb;
+        const float Gz = ((float)compact3p((uint32_t)cb >> 2) + 0.5f) * wb;
+        for (int t0 = s; t0 < e; t0 += 32) {
+            const int i = t0 + lane;
+            const bool act = i < e;
+            int tx = 0, ty = 0, tz = 0;
+            float dxi = 0, dyi = 0, dzi = 0, gix = 0, giy = 0, giz = 0;
+            if (act) {
+                const uint32_t key = A.keys[i];
+                tx = (int)compact3p(key);
+                ty = (int)compact3p(key >> 1);
+                tz = (int)compact3p(key >> 2);
+                dxi = A.s6[i];
+                dyi = A.s6[A.n + i];
+                dzi = A.s6[2 * A.n + i];
+                gix = A.s6[3 * A.n + i];
+                giy = A.s6[4 * A.n + i];
+                giz = A.s6[5 * A.n + i];
+            }
+            // target position in leaf widths from the box corner
+            const float Px = (float)tx + 0.5f + dxi * inv_aL;
+            const float Py = (float)ty + 0.5f + dyi * inv_aL;
+            const float Pz = (float)tz + 0.5f + dzi * inv_aL;
+            Acc acc = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+            float Lt[3][8];
+#pragma unroll
+            for (int c = 0; c < 3; ++c)
+#pragma unroll
+                for (int q = 0; q < 8; ++q) Lt[c][q] = 0.f;
+            unsigned long long npairs = 0, nm2p = 0;
+            __syncwarp();
+            if (lane < nimg) stk[lane] = make_int2(lane << 8, 0);  // (image << 8 | level, cell)
+            int sp = nimg;
+            __syncwarp();
+            while (sp > 0) {
+                const int2 ent = stk[--sp];
+                __syncwarp();
+                const int l = ent.x & 0xff, img = ent.x >> 8;
+                const int64_t c = ent.y;
+                const int ox = A.periodic ? img / 9 - 1 : 0, oy = A.periodic ? (img / 3) % 3 - 1 : 0,
+                          oz = A.periodic ? img % 3 - 1 : 0;
+                const int sh = 3 * (L - l);
+                const int rs = A.leaf_start[c << sh], re = A.leaf_start[(c + 1) << sh];
+                if (re == rs) continue;
+                const int wl = 1 << (L - l);
+                const float Cx = ((float)compact3p((uint32_t)c) + 0.5f) * wl + ox * side;
+                const float Cy = ((float)compact3p((uint32_t)c >> 1) + 0.5f) * wl + oy * side;
+                const float Cz = ((float)compact3p((uint32_t)c >> 2) + 0.5f) * wl + oz * side;
+                // MAC r_S + r_B < theta d, r = (sqrt 3 / 2) w: 0.75 (w_S + w_B)^2 < theta^2 d^2 in
+                // leaf widths, in double (every term but the last product exact: the oracle
+                // takes the same decision on ties)
+                const double ddx = (double)Gx - (double)Cx, ddy = (double)Gy - (double)Cy,
+                             ddz = (double)Gz - (double)Cz;
+                const double d2 = ddx * ddx + ddy * ddy + ddz * ddz;
+                const double ws = (double)wl + (double)wb;
+                if (0.75 * ws * ws < th2 * d2) {  // cell-particle: M2P
+                    const float* Mg = A.Mall + (lvl_off(l) + c) * 3 * nc;
+                    for (int k = lane; k < 3 * nc; k += 32) Msh[k] = Mg[k];
+                    __syncwarp();
+                    if (act && !(A.dbg & 2)) {
+                        const float iw = 1.f / (float)wl;
+                        float o[3][8];
+                        m2p_rows(Msh, p, nc, (Px - Cx) * iw, (Py - Cy) * iw, (Pz - Cz) * iw, Ish,
+                                 lane, o);
+                        // L_n (absolute) = sum / w^(n+1), w = wl aL
+                        const float w1 = iw * inv_aL, w2 = w1 * w1, w3 = w2 * w1;
+#pragma unroll
+                        for (int cc = 0; cc < 3; ++cc) {
+                            Lt[cc][0] = fmaf(o[cc][0], w2, Lt[cc][0]);
+                            Lt[cc][1] = fmaf(o[cc][1], w2, Lt[cc][1]);
+                            Lt[cc][2] = fmaf(o[cc][2], w2, Lt[cc][2]);
+#pragma unroll
+                            for (int q = 3; q < 8; ++q) Lt[cc][q] = fmaf(o[cc][q], w3, Lt[cc][q]);
+                        }
+                        ++nm2p;
+                    }
+                    __syncwarp();
+                } else if (l >= 1 && (l == L || re - rs <= A.ncrit)) {  // particle-particle
+                    for (int j0 = rs; j0 < re; j0 += 32) {
+                        const int j = j0 + lane;
+                        if (j < re) {
+                            const uint32_t key = A.keys[j];
+                            Ssh[0 * 32 + lane] = A.s6[j];
+                            Ssh[1 * 32 + lane] = A.s6[A.n + j];
+                            Ssh[2 * 32 + lane] = A.s6[2 * A.n + j];
+                            Ssh[3 * 32 + lane] = A.s6[3 * A.n + j];
+                            Ssh[4 * 32 + lane] = A.s6[4 * A.n + j];
+                            Ssh[5 * 32 + lane] = A.s6[5 * A.n + j];
+                            reinterpret_cast<int*>(Ssh)[6 * 32 + lane] = (int)compact3p(key) + ox * side;
+                            reinterpret_cast<int*>(Ssh)[7 * 32 + lane] = (int)compact3p(key >> 1) + oy * side;
+                            reinterpret_cast<int*>(Ssh)[8 * 32 + lane] = (int)compact3p(key >> 2) + oz * side;
+                        }
+                        __syncwarp();
+                        const int cnt = min(32, re - j0);
+                        if (act) {
+                            for (int q = 0; q < cnt; ++q) {
+                                const int* Si = reinterpret_cast<const int*>(Ssh);
+                                const float dx = fmaf((float)(tx - Si[6 * 32 + q]), aL, dxi - Ssh[q]);
+                                const float dy = fmaf((float)(ty - Si[7 * 32 + q]), aL, dyi - Ssh[32 + q]);
+                                const float dz = fmaf((float)(tz - Si[8 * 32 + q]), aL, dzi - Ssh[64 + q]);
+                                if (!(A.dbg & 1))
+                                    pair<SCHEME>(dx, dy, dz, Ssh[96 + q], Ssh[128 + q],
+                                                 Ssh[160 + q], gix, giy, giz, kc, acc);
+                            }
+                            npairs += cnt;
+                        }
+                        __syncwarp();
+                    }
+                } else {  // open the cell: push its non-empty children
+                    const int csh = sh - 3;
+                    int cnt_c = 0;
+                    if (lane < 8) {
+                        const int64_t ch = 8 * c + lane;
+                        cnt_c = A.leaf_start[(ch + 1) << csh] - A.leaf_start[ch << csh];
+                    }
+                    const unsigned m = __ballot_sync(0xffffffffu, lane < 8 && cnt_c > 0);
+                    if (lane < 8 && cnt_c > 0) {
+                        const int pos = sp + __popc(m & ((1u << lane) - 1u));
+                        if (pos < TREE_STACK)
+                            stk[pos] = make_int2((img << 8) | (l + 1), (int)(8 * c + lane));
+                    }
+                    sp += __popc(m);
+                    if (sp > TREE_STACK) sp = TREE_STACK;  // cannot happen: depth <= 10
+                    __syncwarp();
+                }
+            }
+            if (act) {
+                float o[6];
+                finish<SCHEME>(acc, gix, giy, giz, o);
+                // gradient and Hessian of phi_c from the order-2 local expansion at the target
+                // (derivative rules of the regular harmonics at the expansion centre)
+                float gr[3][3], H[3][6];  // H: xx, xy, xz, yy, yz, zz
+#pragma unroll
+                for (int cc = 0; cc < 3; ++cc) {
+                    gr[cc][0] = -Lt[cc][1];
+                    gr[cc][1] = Lt[cc][2];
+                    gr[cc][2] = Lt[cc][0];
+                    H[cc][0] = 0.5f * Lt[cc][6] - 0.5f * Lt[cc][3];
+                    H[cc][1] = -0.5f * Lt[cc][7];
+                    H[cc][2] = -Lt[cc][4];
+                    H[cc][3] = -0.5f * Lt[cc][6] - 0.5f * Lt[cc][3];
+                    H[cc][4] = Lt[cc][5];
+                    H[cc][5] = Lt[cc][3];
+                }
+                auto Hs = [&](int cc, int a, int b) -> float {
+                    const int lo = a < b ? a : b, hi = a < b ? b : a;
+                    const int idx = lo == 0 ? hi : (lo == 1 ? 2 + hi : 5);
+                    return H[cc][idx];
+                };
+                const float k4 = 0.0795774715459476679f;  // 1 / (4 pi)
+                const float gi[3] = {gix, giy, giz};
+                // u_a = eps_abc d_b phi_c / 4 pi
+                o[0] += k4 * (gr[2][1] - gr[1][2]);
+                o[1] += k4 * (gr[0][2] - gr[2][0]);
+                o[2] += k4 * (gr[1][0] - gr[0][1]);
+                float sv[3];
+                if (SCHEME == 0) {
+                    // s_a = eps_abc (gamma . grad) d_b phi_c / 4 pi
+                    float D[3][3];  // D[c][b] = sum_d g_d d_d d_b phi_c
+#pragma unroll
+                    for (int cc = 0; cc < 3; ++cc)
+#pragma unroll
+                        for (int b = 0; b < 3; ++b)
+                            D[cc][b] = gi[0] * Hs(cc, 0, b) + gi[1] * Hs(cc, 1, b) + gi[2] * Hs(cc, 2, b);
+                    sv[0] = D[2][1] - D[1][2];
+                    sv[1] = D[0][2] - D[2][0];
+                    sv[2] = D[1][0] - D[0][1];
+                } else {
+                    // s_a = eps_dbc g_d d_a d_b phi_c / 4 pi = d_a (gamma . curl phi) / 4 pi
+#pragma unroll
+                    for (int a = 0; a < 3; ++a)
+                        sv[a] = gi[0] * (Hs(2, a, 1) - Hs(1, a, 2)) +
+                                gi[1] * (Hs(0, a, 2) - Hs(2, a, 0)) +
+                                gi[2] * (Hs(1, a, 0) - Hs(0, a, 1));
+                }
+                o[3] += k4 * sv[0];
+                o[4] += k4 * sv[1];
+                o[5] += k4 * sv[2];
+                for (int k = 0; k < 6; ++k) A.near6[k * A.n + i] = o[k];
+            }
+            // interaction counts (one atomic per warp and chunk)
+#pragma unroll
+            for (int off = 16; off > 0; off >>= 1) {
+                npairs += __shfl_xor_sync(0xffffffffu, npairs, off);
+                nm2p += __shfl_xor_sync(0xffffffffu, nm2p, off);
+            }
+            if (lane == 0) {
+                atomicAdd(A.counters, npairs);
+                atomicAdd(A.counters + 1, nm2p);
+            }
+        }
+    }
+}
+
+}  // namespace
+
+size_t tree_groups_cap(int64_t n, int depth) {
+    const int64_t cells = lvl_off(depth + 1) - 1;
+    return (size_t)(n < cells ? n : cells);
+}
+
+void launch_tree(const float* sorted6, int64_t n, const uint32_t* keys_sorted,
+                 const int* leaf_start, int depth, float aL, int periodic, int scheme, int p,
+                 int ncrit, float theta, const float* Mall, KernelConsts kc, int2* groups,
+                 int* ngroups, unsigned long long* counters, float* near6, cudaStream_t st) {
+    cudaMemsetAsync(ngroups, 0, sizeof(int), st);
+    cudaMemsetAsync(counters, 0, 2 * sizeof(unsigned long long), st);
+    const int64_t total = lvl_off(depth + 1) - 1;
+    const int gb = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+    tree_groups_kernel<<<gb, 256, 0, st>>>(leaf_start, depth, ncrit, total, groups, ngroups);
+    TreeArgs A{sorted6, n, keys_sorted, leaf_start, groups, ngroups, Mall, near6, counters,
+               depth, p, ncrit, periodic, aL, theta, 0};
+    if (const char* e = getenv("VFMM_TREE_DBG")) A.dbg = atoi(e);
+    const int nc = (p + 1) * (p + 1);
+    const size_t per_warp = (size_t)(3 * (p + 3) * 2 * 32 + ((3 * nc + 3) & ~3) + 9 * 32);
+    const size_t smem = per_warp * TREE_WARPS * sizeof(float);
+    static PerDeviceOnce once;
+    once([&] {
+        cudaFuncSetAttribute(tree_kernel<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+        cudaFuncSetAttribute(tree_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    });
+    const int grid = 148 * 4;
+    if (scheme == 0)
+        tree_kernel<0><<<grid, TREE_WARPS * 32, smem, st>>>(A, kc);
+    else
+        tree_kernel<1><<<grid, TREE_WARPS * 32, smem, st>>>(A, kc);
+}
+
 }  // namespace vfmm

@@ -194,6 +194,12 @@ void launch_p2p(const float* sorted6, int64_t n, const int* leaf_start, int dept
                 int periodic, int scheme, KernelConsts kc, float* near6,
                 unsigned long long* npairs, int64_t plo, int64_t pcnt, cudaStream_t st,
                 bool lean = false);
+// hybrid treecode, cell-particle half (p2p.cu)
+size_t tree_groups_cap(int64_t n, int depth);
+void launch_tree(const float* sorted6, int64_t n, const uint32_t* keys_sorted,
+                 const int* leaf_start, int depth, float aL, int periodic, int scheme, int p,
+                 int ncrit, float theta, const float* Mall, KernelConsts kc, int2* groups,
+                 int* ngroups, unsigned long long* counters, float* near6, cudaStream_t st);
 // rbf.cu (reinitialization): Gaussian sums over the ws-neighbour leaves, BLAS-1 for GMRES
 void launch_gauss(const float* t6, int64_t nt, const int* tls, const float* s6, int64_t ns,
                   const int* sls, const float* sg, int depth, float a, int periodic, int ws,
