@@ -65,7 +65,11 @@ typedef enum {
     VFMM_MODE_FMM = 0,       /* near (P2P over 27 leaves) + far (expansions)               */
     VFMM_MODE_DIRECT = 1,    /* all-pairs exact sum over the image cube (O(N^2 27^L), tests) */
     VFMM_MODE_NEAR_ONLY = 2, /* only the P2P part of MODE_FMM                               */
-    VFMM_MODE_FAR_ONLY = 3   /* only the expansion part of MODE_FMM                          */
+    VFMM_MODE_FAR_ONLY = 3,  /* only the expansion part of MODE_FMM                          */
+    VFMM_MODE_HYBRID = 4     /* hybrid treecode-FMM auto-tuning: the first
+                                evaluate of a new (n, p, image_levels, depth) times the FMM and
+                                the treecode (vfmm_evaluate_tree, theta = 0.5, n_crit = 64) and
+                                the context keeps the faster; not for distributed contexts     */
 } vfmm_mode;
 
 typedef struct {

@@ -20,7 +20,9 @@ particles per box at the deepest levels of the tree".  The cell-cell half is the
      at the target point itself, rows n <= 2 of ``fmm_ref.m2l_matrix``'s formula, then Eqs. (12)-(15)'s gradient and
      Hessian at the expansion centre, ``fmm_ref.l2p`` at 0; the cutoff is dropped in the far
      field); else if S is a leaf, particle-particle by Eq. (5) / (8) exactly
-     (PAPER.md:144, ``fmm_ref.pair_sum``); else push S's non-empty children;
+     (``fmm_ref.pair_sum``); else push S's non-empty children.  An accepted
+     cell holding fewer than (p+1)^2 particles also acts particle-particle (exact and cheaper
+     than its multipole: the cell-particle / particle-particle choice, reading R22);
   5. images outside the near 3^3 block by multipole expansions: the root's
      local expansion ``fmm_ref.periodic_far`` evaluated at each particle (L2P about the box
      centre).
@@ -157,6 +159,9 @@ def evaluate(pos, gam, sigma, box_lo, box_len, depth, p, theta, n_crit, image_le
     # as the C ABI receives it (so that ties decide the same way on both sides, reading R22)
     th = float(np.float32(theta))
     th2 = th * th
+    # an accepted cell with fewer than (p+1)^2 particles interacts particle-particle: exact,
+    # and cheaper than its multipole (reading R22)
+    n_direct = (p + 1) ** 2
 
     def cell_lw(l, c):  # centre (leaf widths from the box corner) and width of a cell
         ix, iy, iz = _decode(c, l)
@@ -185,10 +190,11 @@ def evaluate(pos, gam, sigma, box_lo, box_len, depth, p, theta, n_crit, image_le
             cSw, wS = cell_lw(l, c)
             dd = cBw - (cSw + o * float(1 << L))
             d2 = dd[0] * dd[0] + dd[1] * dd[1] + dd[2] * dd[2]
-            if 0.75 * (wS + wB) ** 2 < th2 * d2:
+            s2, e2 = rng(l, c)
+            if 0.75 * (wS + wB) ** 2 < th2 * d2 and e2 - s2 >= n_direct:
                 acc.append((multipole(l, c), cS))
                 n_m2p += e - s
-            elif is_leaf(l, c):
+            elif 0.75 * (wS + wB) ** 2 < th2 * d2 or is_leaf(l, c):
                 s2, e2 = rng(l, c)
                 xs_list.append(X[s2:e2] + sh)
                 gs_list.append(G[s2:e2])

@@ -28,7 +28,7 @@ HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "vfmm.h")
 
 VFMM_OK, VFMM_EINVAL, VFMM_EDOMAIN, VFMM_ENOMEM, VFMM_ECUDA, VFMM_ENCCL, VFMM_ESTATE = \
     0, -1, -2, -3, -4, -5, -6
-MODE_FMM, MODE_DIRECT, MODE_NEAR_ONLY, MODE_FAR_ONLY = 0, 1, 2, 3
+MODE_FMM, MODE_DIRECT, MODE_NEAR_ONLY, MODE_FAR_ONLY, MODE_HYBRID = 0, 1, 2, 3, 4
 STRETCH_CLASSICAL, STRETCH_TRANSPOSE = 0, 1
 
 

@@ -85,6 +85,12 @@ struct vfmm_ctx {
     int* d_tree_ng = nullptr;
     unsigned long long* d_tree_cnt = nullptr;
     bool tree_last = false;  // the last evaluate was a treecode one (stats)
+    // VFMM_MODE_HYBRID: the choice between the FMM and the treecode, by timing, cached per
+    // (n, p, image_levels, depth parameter)
+    int64_t hyb_n = -1;
+    int hyb_p = -1, hyb_levels = -1, hyb_depth = -2;
+    bool hyb_tree = false;
+    float hyb_ms[2] = {0, 0};
     // host-API staging
     int64_t cap_host_n = 0;
     float* hbuf = nullptr;  // 12 x n
@@ -180,7 +186,7 @@ vfmm_status validate(const vfmm_params* p) {
     if (p->depth < -1 || p->depth > 10) return VFMM_EINVAL;
     if (p->image_levels < 0 || p->image_levels > 6) return VFMM_EINVAL;
     if (p->scheme != 0 && p->scheme != 1) return VFMM_EINVAL;
-    if (p->mode < 0 || p->mode > 3) return VFMM_EINVAL;
+    if (p->mode < 0 || p->mode > 4) return VFMM_EINVAL;
     if (!finite_pos(p->sigma) || !finite_pos(p->box_len) || !std::isfinite(p->box_lo))
         return VFMM_EINVAL;
     return VFMM_OK;
@@ -445,7 +451,8 @@ vfmm_status vfmm_create_nccl(vfmm_ctx** out, const vfmm_params* prm, int device,
                              const void* nccl_id128, int nranks, int rank) {
     if (!out || !nccl_id128 || !prm || !valid_R(nranks) || rank < 0 || rank >= nranks)
         return VFMM_EINVAL;
-    if (prm->depth < 2 || prm->mode == VFMM_MODE_DIRECT) return VFMM_EINVAL;
+    if (prm->depth < 2 || prm->mode == VFMM_MODE_DIRECT || prm->mode == VFMM_MODE_HYBRID)
+        return VFMM_EINVAL;
     vfmm_status s = vfmm_create(out, prm, device);
     if (s != VFMM_OK) return s;
     vfmm_ctx* c = *out;
@@ -475,7 +482,8 @@ vfmm_status vfmm_evaluate_logical(vfmm_ctx* c, int nranks, const int64_t* n,
                                   const float* const* pos, const float* const* gamma,
                                   float* const* vel, float* const* dgamma, void* stream) {
     if (!c || !valid_R(nranks) || !n || !pos || !gamma || !vel || !dgamma) return VFMM_EINVAL;
-    if (c->prm.depth < 2 || c->prm.mode == VFMM_MODE_DIRECT) return VFMM_EINVAL;
+    if (c->prm.depth < 2 || c->prm.mode == VFMM_MODE_DIRECT || c->prm.mode == VFMM_MODE_HYBRID)
+        return VFMM_EINVAL;
     CK(cudaSetDevice(c->device), "set device");
     (void)cudaGetLastError();
     cudaStream_t st = (cudaStream_t)stream;
@@ -762,6 +770,49 @@ static vfmm_status evaluate_impl(vfmm_ctx* c, int64_t n, const float* pos, const
         c->comm_timed = true;
         c->comm_overlap = true;
         return VFMM_OK;
+    }
+    if (c->prm.mode == VFMM_MODE_HYBRID) {
+        // "a properly implemented FMM [...] always selects the least expensive option"
+        // (PAPER.md:150): the first evaluate of a new (n, p, image_levels, depth) times the
+        // FMM (cell-cell) and the treecode (cell-particle, theta = 0.5, n_crit = 64) and keeps
+        // the faster; per-particle sigma always takes the FMM
+        auto run = [&](bool tree) -> vfmm_status {
+            if (tree) return vfmm_evaluate_tree(c, n, pos, gamma, vel, dgamma, 0.5f, 64, stream);
+            c->prm.mode = VFMM_MODE_FMM;
+            const vfmm_status r = evaluate_impl(c, n, pos, gamma, sig, vel, dgamma, stream);
+            c->prm.mode = VFMM_MODE_HYBRID;
+            return r;
+        };
+        if (sig) return run(false);
+        if (!(c->hyb_n == n && c->hyb_p == c->prm.p && c->hyb_levels == c->prm.image_levels &&
+              c->hyb_depth == c->prm.depth)) {
+            cudaEvent_t t0, t1;
+            CK(cudaEventCreate(&t0), "event");
+            CK(cudaEventCreate(&t1), "event");
+            for (int k = 0; k < 2; ++k) {
+                vfmm_status r = run(k == 1);  // warm-up (and the depth tuning for depth = -1)
+                if (r == VFMM_OK) {
+                    cudaEventRecord(t0, st);
+                    r = run(k == 1);
+                    cudaEventRecord(t1, st);
+                }
+                if (r != VFMM_OK) {
+                    cudaEventDestroy(t0);
+                    cudaEventDestroy(t1);
+                    return r;
+                }
+                CK(cudaEventSynchronize(t1), "sync");
+                cudaEventElapsedTime(&c->hyb_ms[k], t0, t1);
+            }
+            cudaEventDestroy(t0);
+            cudaEventDestroy(t1);
+            c->hyb_tree = c->hyb_ms[1] < c->hyb_ms[0];
+            c->hyb_n = n;
+            c->hyb_p = c->prm.p;
+            c->hyb_levels = c->prm.image_levels;
+            c->hyb_depth = c->prm.depth;
+        }
+        return run(c->hyb_tree);
     }
     const vfmm_params& P = c->prm;
     vfmm_stats& S = c->stats;
@@ -1577,7 +1628,8 @@ vfmm_status vfmm_get_stats(vfmm_ctx* c, vfmm_stats* out) {
         CK(cudaMemcpy(cnt, c->d_tree_cnt, sizeof(cnt), cudaMemcpyDeviceToHost), "copy counts");
         S.n_p2p_pairs = (int64_t)cnt[0];
         S.n_m2l = (int64_t)cnt[1];
-    } else if (c->prm.mode == VFMM_MODE_FMM || c->prm.mode == VFMM_MODE_NEAR_ONLY) {
+    } else if (c->prm.mode == VFMM_MODE_FMM || c->prm.mode == VFMM_MODE_NEAR_ONLY ||
+               c->prm.mode == VFMM_MODE_HYBRID) {
         unsigned long long pairs = 0;
         CK(cudaMemcpy(&pairs, c->d_pairs, sizeof(pairs), cudaMemcpyDeviceToHost), "copy pairs");
         S.n_p2p_pairs = (int64_t)pairs;

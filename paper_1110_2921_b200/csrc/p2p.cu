@@ -1304,7 +1304,10 @@ __global__ void __launch_bounds__(TREE_WARPS * 32) tree_kernel(TreeArgs A, Kerne
                              ddz = (double)Gz - (double)Cz;
                 const double d2 = ddx * ddx + ddy * ddy + ddz * ddz;
                 const double ws = (double)wl + (double)wb;
-                if (0.75 * ws * ws < th2 * d2) {  // cell-particle: M2P
+                // an accepted cell with fewer than (p+1)^2 particles acts particle-particle
+                // (exact, and cheaper than its multipole; reading R22)
+                const bool accept = 0.75 * ws * ws < th2 * d2;
+                if (accept && re - rs >= nc) {  // cell-particle: M2P
                     const float* Mg = A.Mall + (lvl_off(l) + c) * 3 * nc;
                     for (int k = lane; k < 3 * nc; k += 32) Msh[k] = Mg[k];
                     __syncwarp();
@@ -1326,7 +1329,7 @@ __global__ void __launch_bounds__(TREE_WARPS * 32) tree_kernel(TreeArgs A, Kerne
                         ++nm2p;
                     }
                     __syncwarp();
-                } else if (l >= 1 && (l == L || re - rs <= A.ncrit)) {  // particle-particle
+                } else if (accept || (l >= 1 && (l == L || re - rs <= A.ncrit))) {  // P2P
                     for (int j0 = rs; j0 < re; j0 += 32) {
                         const int j = j0 + lane;
                         if (j < re) {
