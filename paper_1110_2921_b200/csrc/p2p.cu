@@ -1179,6 +1179,12 @@ __device__ __forceinline__ void m2p_rows(const float* __restrict__ Msh, int p, i
     gen(2);
     for (int k = 0; k <= p; ++k) {
         if (k >= 1) gen(k + 2);
+        // sliding window over l: each step loads only I_{k+1}^l and I_{k+2}^l (the other three
+        // orders are the previous steps')
+        float a0r, a0i, b0r, b0i, b1r, b1i;
+        getI(k + 1, -k - 1, a0r, a0i);
+        getI(k + 2, -k - 2, b0r, b0i);
+        getI(k + 2, -k - 1, b1r, b1i);
         for (int l = -k; l <= k; ++l) {
             const int al = l < 0 ? -l : l;
             float mr[3], mi[3];
@@ -1189,36 +1195,31 @@ __device__ __forceinline__ void m2p_rows(const float* __restrict__ Msh, int p, i
                 const float im = al == 0 ? 0.f : Msh[c * nc + pk_im(k, al)];
                 mi[c] = l < 0 ? -sgm * im : im;
             }
-            float ar, ai;
-            // (n, m) = (1, 0): sign -1, real part
-            getI(k + 1, l, ar, ai);
-#pragma unroll
-            for (int c = 0; c < 3; ++c) out[c][0] -= ar * mr[c] - ai * mi[c];
-            // (1, 1): sign +1
-            getI(k + 1, l - 1, ar, ai);
+            float a1r, a1i, b2r, b2i;
+            getI(k + 1, l, a1r, a1i);
+            getI(k + 2, l, b2r, b2i);
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
-                out[c][1] += ar * mr[c] - ai * mi[c];
-                out[c][2] += ar * mi[c] + ai * mr[c];
+                // (n, m) = (1, 0): sign -1, real part; I_{k+1}^l
+                out[c][0] -= a1r * mr[c] - a1i * mi[c];
+                // (1, 1): sign +1; I_{k+1}^{l-1}
+                out[c][1] += a0r * mr[c] - a0i * mi[c];
+                out[c][2] += a0r * mi[c] + a0i * mr[c];
+                // (2, 0): sign +1, real part; I_{k+2}^l
+                out[c][3] += b2r * mr[c] - b2i * mi[c];
+                // (2, 1): sign -1; I_{k+2}^{l-1}
+                out[c][4] -= b1r * mr[c] - b1i * mi[c];
+                out[c][5] -= b1r * mi[c] + b1i * mr[c];
+                // (2, 2): sign +1; I_{k+2}^{l-2}
+                out[c][6] += b0r * mr[c] - b0i * mi[c];
+                out[c][7] += b0r * mi[c] + b0i * mr[c];
             }
-            // (2, 0): sign +1, real part
-            getI(k + 2, l, ar, ai);
-#pragma unroll
-            for (int c = 0; c < 3; ++c) out[c][3] += ar * mr[c] - ai * mi[c];
-            // (2, 1): sign -1
-            getI(k + 2, l - 1, ar, ai);
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                out[c][4] -= ar * mr[c] - ai * mi[c];
-                out[c][5] -= ar * mi[c] + ai * mr[c];
-            }
-            // (2, 2): sign +1
-            getI(k + 2, l - 2, ar, ai);
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                out[c][6] += ar * mr[c] - ai * mi[c];
-                out[c][7] += ar * mi[c] + ai * mr[c];
-            }
+            a0r = a1r;
+            a0i = a1i;
+            b0r = b1r;
+            b0i = b1i;
+            b1r = b2r;
+            b1i = b2i;
         }
     }
 }
