@@ -1,0 +1,7 @@
+#!/bin/bash
+# round 2, session 2: treecode work items per 32-target chunk (load balance): tests, timings
+cd "${GRAFT_REPO_ROOT:-/root/repo}"; mkdir -p gpurun_out
+timeout 900 python -m pytest tests/test_gpu_tree.py -q -s > gpurun_out/s2e_tree.log 2>&1; echo "rc=$?" >> gpurun_out/s2e_tree.log
+for a in "--config c2" "--config c3" "--clustered 1000000 --lam 1" "--clustered 1000000 --lam 1 --theta 0.7"; do
+  timeout 300 python scripts/tree_bench.py $a --p 10 >> gpurun_out/s2e_tree_vs_fmm.jsonl 2>> gpurun_out/s2e_tree_vs_fmm.err
+done
