@@ -1084,7 +1084,8 @@ constexpr int TREE_STACK = 128;
 __host__ __device__ __forceinline__ int64_t lvl_off(int l) { return ((int64_t(1) << (3 * l)) - 1) / 7; }
 
 // adaptive leaves: a non-empty cell of level l >= 1 with count <= n_crit (or l = L) whose parent
-// holds more than n_crit; appended (in no particular order) to groups as (level, cell)
+// holds more than n_crit; appended (in no particular order) to groups as one (chunk << 4 |
+// level, cell) item per chunk of 32 targets
 __global__ void tree_groups_kernel(const int* __restrict__ leaf_start, int L, int ncrit,
                                    int64_t total, int2* __restrict__ groups,
                                    int* __restrict__ ngroups) {
@@ -1102,8 +1103,10 @@ __global__ void tree_groups_kernel(const int* __restrict__ leaf_start, int L, in
             const int psh = sh + 3;
             if (leaf_start[(pc + 1) << psh] - leaf_start[pc << psh] <= ncrit) continue;
         }
-        const int k = atomicAdd(ngroups, 1);
-        groups[k] = make_int2(l, (int)c);
+        // one work item per chunk of 32 targets (balances leaves of very different sizes)
+        const int nch = (cnt + 31) >> 5;
+        const int k = atomicAdd(ngroups, nch);
+        for (int q = 0; q < nch; ++q) groups[k + q] = make_int2((q << 4) | l, (int)c);
     }
 }
 
@@ -1160,16 +1163,6 @@ __device__ __forceinline__ void m2p_rows(const float* __restrict__ Msh, int p, i
         IR(j, j) = s * (dx * a - dy * b);
         II(j, j) = s * (dx * b + dy * a);
     };
-    auto getI = [&](int j, int q, float& re, float& im) {
-        if (q >= 0) {
-            re = IR(j, q);
-            im = II(j, q);
-        } else {
-            const float sg = (q & 1) ? -1.f : 1.f;
-            re = sg * IR(j, -q);
-            im = -sg * II(j, -q);
-        }
-    };
 #pragma unroll
     for (int c = 0; c < 3; ++c)
 #pragma unroll
@@ -1180,24 +1173,22 @@ __device__ __forceinline__ void m2p_rows(const float* __restrict__ Msh, int p, i
     for (int k = 0; k <= p; ++k) {
         if (k >= 1) gen(k + 2);
         // sliding window over l: each step loads only I_{k+1}^l and I_{k+2}^l (the other three
-        // orders are the previous steps')
+        // orders are the previous steps'); negative l (conjugate symmetry of M and I) and l >= 0
+        // run as separate loops over linear shared-memory offsets
+        const float* Mk = Msh + k * k;                          // pk_re(k, 0)
+        const float* Ia = Ish + ((k + 1) % 3) * PQ * 64 + lane;  // row k+1: q at [64 q], Im +32
+        const float* Ib = Ish + ((k + 2) % 3) * PQ * 64 + lane;
+        auto ineg = [&](const float* R, int q, float& re, float& im) {  // I^{-q}, q > 0
+            const float sg = (q & 1) ? -1.f : 1.f;
+            re = sg * R[64 * q];
+            im = -sg * R[64 * q + 32];
+        };
         float a0r, a0i, b0r, b0i, b1r, b1i;
-        getI(k + 1, -k - 1, a0r, a0i);
-        getI(k + 2, -k - 2, b0r, b0i);
-        getI(k + 2, -k - 1, b1r, b1i);
-        for (int l = -k; l <= k; ++l) {
-            const int al = l < 0 ? -l : l;
-            float mr[3], mi[3];
-            const float sgm = (l < 0 && (al & 1)) ? -1.f : 1.f;
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                mr[c] = sgm * Msh[c * nc + pk_re(k, al)];
-                const float im = al == 0 ? 0.f : Msh[c * nc + pk_im(k, al)];
-                mi[c] = l < 0 ? -sgm * im : im;
-            }
-            float a1r, a1i, b2r, b2i;
-            getI(k + 1, l, a1r, a1i);
-            getI(k + 2, l, b2r, b2i);
+        ineg(Ia, k + 1, a0r, a0i);
+        ineg(Ib, k + 2, b0r, b0i);
+        ineg(Ib, k + 1, b1r, b1i);
+        auto step = [&](const float (&mr)[3], const float (&mi)[3], float a1r, float a1i, float b2r,
+                        float b2i) {
 #pragma unroll
             for (int c = 0; c < 3; ++c) {
                 // (n, m) = (1, 0): sign -1, real part; I_{k+1}^l
@@ -1220,6 +1211,37 @@ __device__ __forceinline__ void m2p_rows(const float* __restrict__ Msh, int p, i
             b0i = b1i;
             b1r = b2r;
             b1i = b2i;
+        };
+        for (int al = k; al >= 1; --al) {  // l = -al: M^l = (-1)^al conj(M^al)
+            const float sg = (al & 1) ? -1.f : 1.f;
+            float mr[3], mi[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                mr[c] = sg * Mk[c * nc + 2 * al - 1];
+                mi[c] = -sg * Mk[c * nc + 2 * al];
+            }
+            float a1r, a1i, b2r, b2i;
+            ineg(Ia, al, a1r, a1i);
+            ineg(Ib, al, b2r, b2i);
+            step(mr, mi, a1r, a1i, b2r, b2i);
+        }
+        {  // l = 0
+            float mr[3], mi[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                mr[c] = Mk[c * nc];
+                mi[c] = 0.f;
+            }
+            step(mr, mi, Ia[0], Ia[32], Ib[0], Ib[32]);
+        }
+        for (int l = 1; l <= k; ++l) {
+            float mr[3], mi[3];
+#pragma unroll
+            for (int c = 0; c < 3; ++c) {
+                mr[c] = Mk[c * nc + 2 * l - 1];
+                mi[c] = Mk[c * nc + 2 * l];
+            }
+            step(mr, mi, Ia[64 * l], Ia[64 * l + 32], Ib[64 * l], Ib[64 * l + 32]);
         }
     }
 }
@@ -1243,16 +1265,17 @@ __global__ void __launch_bounds__(TREE_WARPS * 32) tree_kernel(TreeArgs A, Kerne
     const float inv_aL = 1.f / aL;
     const int nimg = A.periodic ? 27 : 1;
     const double th2 = (double)A.theta * (double)A.theta;
-    for (int g = blockIdx.x * TREE_WARPS + warp; g < ng; g += gridDim.x * TREE_WARPS) {
+    for (int g = blockIdx.x * TREE_WARPS + warp; g < ng; g += gridDim.x * TREE_WARPS) {  // items
         const int2 grp = A.groups[g];
-        const int lb = grp.x, cb = grp.y;
+        const int lb = grp.x & 15, cb = grp.y, chunk = grp.x >> 4;
         const int shb = 3 * (L - lb);
         const int s = A.leaf_start[(int64_t)cb << shb], e = A.leaf_start[((int64_t)cb + 1) << shb];
         const float wb = (float)(1 << (L - lb));  // group width in leaf widths
         const float Gx = ((float)compact3p((uint32_t)cb) + 0.5f) * wb;
         const float Gy = ((float)compact3p((uint32_t)cb >> 1) + 0.5f) * wb;
         const float Gz = ((float)compact3p((uint32_t)cb >> 2) + 0.5f) * wb;
-        for (int t0 = s; t0 < e; t0 += 32) {
+        {
+            const int t0 = s + 32 * chunk;
             const int i = t0 + lane;
             const bool act = i < e;
             int tx = 0, ty = 0, tz = 0;
@@ -1449,9 +1472,9 @@ __global__ void __launch_bounds__(TREE_WARPS * 32) tree_kernel(TreeArgs A, Kerne
 
 }  // namespace
 
-size_t tree_groups_cap(int64_t n, int depth) {
+size_t tree_groups_cap(int64_t n, int depth) {  // work items: chunks of 32 targets per leaf
     const int64_t cells = lvl_off(depth + 1) - 1;
-    return (size_t)(n < cells ? n : cells);
+    return (size_t)((n < cells ? n : cells) + n / 32 + 1);
 }
 
 void launch_tree(const float* sorted6, int64_t n, const uint32_t* keys_sorted,
