@@ -68,8 +68,9 @@ typedef enum {
     VFMM_MODE_FAR_ONLY = 3,  /* only the expansion part of MODE_FMM                          */
     VFMM_MODE_HYBRID = 4     /* hybrid treecode-FMM auto-tuning: the first
                                 evaluate of a new (n, p, image_levels, depth) times the FMM and
-                                the treecode (vfmm_evaluate_tree, theta = 0.5, n_crit = 64) and
-                                the context keeps the faster; not for distributed contexts     */
+                                the treecode (vfmm_evaluate_tree, theta = 0.5) at n_crit = 32,
+                                64 and 128, and the context keeps the fastest; not for
+                                distributed contexts                                           */
 } vfmm_mode;
 
 typedef struct {

@@ -89,8 +89,8 @@ struct vfmm_ctx {
     // (n, p, image_levels, depth parameter)
     int64_t hyb_n = -1;
     int hyb_p = -1, hyb_levels = -1, hyb_depth = -2;
-    bool hyb_tree = false;
-    float hyb_ms[2] = {0, 0};
+    int hyb_choice = 0;  // 0: FMM; k = 1..3: treecode with n_crit = 16 << k (32, 64, 128)
+    float hyb_ms[4] = {0, 0, 0, 0};
     // host-API staging
     int64_t cap_host_n = 0;
     float* hbuf = nullptr;  // 12 x n
@@ -774,26 +774,29 @@ static vfmm_status evaluate_impl(vfmm_ctx* c, int64_t n, const float* pos, const
     if (c->prm.mode == VFMM_MODE_HYBRID) {
         // "a properly implemented FMM [...] always selects the least expensive option"
         // (PAPER.md:150): the first evaluate of a new (n, p, image_levels, depth) times the
-        // FMM (cell-cell) and the treecode (cell-particle, theta = 0.5, n_crit = 64) and keeps
-        // the faster; per-particle sigma always takes the FMM
-        auto run = [&](bool tree) -> vfmm_status {
-            if (tree) return vfmm_evaluate_tree(c, n, pos, gamma, vel, dgamma, 0.5f, 64, stream);
+        // FMM (cell-cell) and the treecode (cell-particle, theta = 0.5) at n_crit = 32, 64, 128
+        // particles per leaf ("automatically choosing the number of particles per box",
+        // PAPER.md:152) and keeps the fastest; per-particle sigma always takes the FMM
+        auto run = [&](int k) -> vfmm_status {
+            if (k > 0)
+                return vfmm_evaluate_tree(c, n, pos, gamma, vel, dgamma, 0.5f, 16 << k, stream);
             c->prm.mode = VFMM_MODE_FMM;
             const vfmm_status r = evaluate_impl(c, n, pos, gamma, sig, vel, dgamma, stream);
             c->prm.mode = VFMM_MODE_HYBRID;
             return r;
         };
-        if (sig) return run(false);
+        if (sig) return run(0);
         if (!(c->hyb_n == n && c->hyb_p == c->prm.p && c->hyb_levels == c->prm.image_levels &&
               c->hyb_depth == c->prm.depth)) {
             cudaEvent_t t0, t1;
             CK(cudaEventCreate(&t0), "event");
             CK(cudaEventCreate(&t1), "event");
-            for (int k = 0; k < 2; ++k) {
-                vfmm_status r = run(k == 1);  // warm-up (and the depth tuning for depth = -1)
+            int best = 0;
+            for (int k = 0; k < 4; ++k) {
+                vfmm_status r = run(k);  // warm-up (and the depth tuning for depth = -1)
                 if (r == VFMM_OK) {
                     cudaEventRecord(t0, st);
-                    r = run(k == 1);
+                    r = run(k);
                     cudaEventRecord(t1, st);
                 }
                 if (r != VFMM_OK) {
@@ -803,16 +806,17 @@ static vfmm_status evaluate_impl(vfmm_ctx* c, int64_t n, const float* pos, const
                 }
                 CK(cudaEventSynchronize(t1), "sync");
                 cudaEventElapsedTime(&c->hyb_ms[k], t0, t1);
+                if (c->hyb_ms[k] < c->hyb_ms[best]) best = k;
             }
             cudaEventDestroy(t0);
             cudaEventDestroy(t1);
-            c->hyb_tree = c->hyb_ms[1] < c->hyb_ms[0];
+            c->hyb_choice = best;
             c->hyb_n = n;
             c->hyb_p = c->prm.p;
             c->hyb_levels = c->prm.image_levels;
             c->hyb_depth = c->prm.depth;
         }
-        return run(c->hyb_tree);
+        return run(c->hyb_choice);
     }
     const vfmm_params& P = c->prm;
     vfmm_stats& S = c->stats;
