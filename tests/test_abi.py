@@ -43,10 +43,23 @@ def test_create_rejects_bad_params_without_touching_the_gpu():
     ctx = ctypes.c_void_p()
     for bad in (dict(p=0), dict(p=17), dict(sigma=0.0), dict(sigma=float("nan")),
                 dict(depth=11), dict(depth=-2), dict(image_levels=7), dict(scheme=2), dict(mode=9),
+                dict(mode=5), dict(mode=-1),
                 dict(box_len=-1.0)):
         prm = vf.Params(**bad).to_c()
         assert L.vfmm_create(ctypes.byref(ctx), ctypes.byref(prm), 0) == vf.VFMM_EINVAL
         assert not ctx.value
+
+
+def test_tree_entry_rejects_a_null_context_without_touching_the_gpu():
+    """vfmm_evaluate_tree (NEXT-4) validates its arguments before any CUDA call."""
+    L = vf.load_library()
+    L.vfmm_evaluate_tree.argtypes = [ctypes.c_void_p, ctypes.c_int64] + [ctypes.c_void_p] * 4 + [
+        ctypes.c_float, ctypes.c_int32, ctypes.c_void_p]
+    L.vfmm_evaluate_tree.restype = ctypes.c_int
+    buf = (ctypes.c_float * 6)()
+    a = ctypes.cast(buf, ctypes.c_void_p)
+    assert L.vfmm_evaluate_tree(None, 1, a, a, a, a, 0.5, 64, None) == vf.VFMM_EINVAL
+    assert vf.MODE_HYBRID == 4
 
 
 def test_no_oracle_in_product_path():
