@@ -149,8 +149,9 @@ vfmm_status vfmm_evaluate_at(vfmm_ctx* ctx, int64_t n_src, const float* pos, con
    (free space: the root) and pops cells S: if r_S + r_B < theta |c_B - c_S| (r = half
    diagonal, the multipole acceptance criterion) S acts on every target of B through its
    multipole (cell-particle, M2P: Eq. 11's local expansion of order 2 at the target point,
-   then Eqs. 12-15; no cutoff, PAPER.md:138); else a leaf S acts particle-particle (Eq. 5 /
-   Eq. 8 exactly); else its non-empty children are pushed.  Images outside the
+   then Eqs. 12-15; no cutoff), unless S holds fewer than (p+1)^2 particles,
+   when it acts particle-particle (exact and cheaper); else a leaf S acts particle-particle
+   (Eq. 5 / Eq. 8 exactly); else its non-empty children are pushed.  Images outside the
    near block come through the root local expansion as in vfmm_evaluate (image_levels >= 2).
    The context's p, depth, image_levels, sigma and scheme apply; its mode is ignored.
    pos, gamma: device 3 x n (SoA), vel, dgamma: device 3 x n outputs (no aliasing), input order.
