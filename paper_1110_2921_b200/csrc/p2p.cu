@@ -1136,8 +1136,9 @@ __device__ __forceinline__ void m2p_rows(const float* __restrict__ Msh, int p, i
                                          float dy, float dz, float* __restrict__ Ish, int lane,
                                          float out[3][8]) {
     const int PQ = p + 3;
-    auto IR = [&](int j, int q) -> float& { return Ish[(((j % 3) * PQ + q) * 2) * 32 + lane]; };
-    auto II = [&](int j, int q) -> float& { return Ish[(((j % 3) * PQ + q) * 2 + 1) * 32 + lane]; };
+    // I_j^q of this lane at Ish[((j % 3) PQ + q) 64 + 2 lane] (Re, Im adjacent: one 64-bit load)
+    auto IR = [&](int j, int q) -> float& { return Ish[((j % 3) * PQ + q) * 64 + 2 * lane]; };
+    auto II = [&](int j, int q) -> float& { return Ish[((j % 3) * PQ + q) * 64 + 2 * lane + 1]; };
     const float r2 = fmaf(dx, dx, fmaf(dy, dy, dz * dz));
     const float rho = 1.f / r2;
     auto gen = [&](int j) {
@@ -1175,13 +1176,14 @@ __device__ __forceinline__ void m2p_rows(const float* __restrict__ Msh, int p, i
         // sliding window over l: each step loads only I_{k+1}^l and I_{k+2}^l (the other three
         // orders are the previous steps'); negative l (conjugate symmetry of M and I) and l >= 0
         // run as separate loops over linear shared-memory offsets
-        const float* Mk = Msh + k * k;                          // pk_re(k, 0)
-        const float* Ia = Ish + ((k + 1) % 3) * PQ * 64 + lane;  // row k+1: q at [64 q], Im +32
-        const float* Ib = Ish + ((k + 2) % 3) * PQ * 64 + lane;
-        auto ineg = [&](const float* R, int q, float& re, float& im) {  // I^{-q}, q > 0
+        const float4* Mk = reinterpret_cast<const float4*>(Msh) + k * k;  // pk_re(k, 0)
+        const float2* Ia = reinterpret_cast<const float2*>(Ish + ((k + 1) % 3) * PQ * 64) + lane;
+        const float2* Ib = reinterpret_cast<const float2*>(Ish + ((k + 2) % 3) * PQ * 64) + lane;
+        auto ineg = [&](const float2* R, int q, float& re, float& im) {  // I^{-q}, q > 0
             const float sg = (q & 1) ? -1.f : 1.f;
-            re = sg * R[64 * q];
-            im = -sg * R[64 * q + 32];
+            const float2 v = R[32 * q];
+            re = sg * v.x;
+            im = -sg * v.y;
         };
         float a0r, a0i, b0r, b0i, b1r, b1i;
         ineg(Ia, k + 1, a0r, a0i);
@@ -1214,34 +1216,27 @@ __device__ __forceinline__ void m2p_rows(const float* __restrict__ Msh, int p, i
         };
         for (int al = k; al >= 1; --al) {  // l = -al: M^l = (-1)^al conj(M^al)
             const float sg = (al & 1) ? -1.f : 1.f;
-            float mr[3], mi[3];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                mr[c] = sg * Mk[c * nc + 2 * al - 1];
-                mi[c] = -sg * Mk[c * nc + 2 * al];
-            }
+            const float4 re4 = Mk[2 * al - 1], im4 = Mk[2 * al];
+            const float mr[3] = {sg * re4.x, sg * re4.y, sg * re4.z};
+            const float mi[3] = {-sg * im4.x, -sg * im4.y, -sg * im4.z};
             float a1r, a1i, b2r, b2i;
             ineg(Ia, al, a1r, a1i);
             ineg(Ib, al, b2r, b2i);
             step(mr, mi, a1r, a1i, b2r, b2i);
         }
         {  // l = 0
-            float mr[3], mi[3];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                mr[c] = Mk[c * nc];
-                mi[c] = 0.f;
-            }
-            step(mr, mi, Ia[0], Ia[32], Ib[0], Ib[32]);
+            const float4 re4 = Mk[0];
+            const float mr[3] = {re4.x, re4.y, re4.z};
+            const float mi[3] = {0.f, 0.f, 0.f};
+            const float2 ia = Ia[0], ib = Ib[0];
+            step(mr, mi, ia.x, ia.y, ib.x, ib.y);
         }
         for (int l = 1; l <= k; ++l) {
-            float mr[3], mi[3];
-#pragma unroll
-            for (int c = 0; c < 3; ++c) {
-                mr[c] = Mk[c * nc + 2 * l - 1];
-                mi[c] = Mk[c * nc + 2 * l];
-            }
-            step(mr, mi, Ia[64 * l], Ia[64 * l + 32], Ib[64 * l], Ib[64 * l + 32]);
+            const float4 re4 = Mk[2 * l - 1], im4 = Mk[2 * l];
+            const float mr[3] = {re4.x, re4.y, re4.z};
+            const float mi[3] = {im4.x, im4.y, im4.z};
+            const float2 ia = Ia[32 * l], ib = Ib[32 * l];
+            step(mr, mi, ia.x, ia.y, ib.x, ib.y);
         }
     }
 }
@@ -1252,7 +1247,7 @@ __global__ void __launch_bounds__(TREE_WARPS * 32) tree_kernel(TreeArgs A, Kerne
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int p = A.p, nc = (p + 1) * (p + 1), L = A.L;
     const int ish_floats = 3 * (p + 3) * 2 * 32;
-    const int msh_floats = (3 * nc + 3) & ~3;
+    const int msh_floats = 4 * nc;  // [k][component] float4 (one broadcast load per coefficient)
     float* base = reinterpret_cast<float*>(tree_sm4) + warp * (ish_floats + msh_floats + 9 * 32);
     float* Ish = base;
     float* Msh = base + ish_floats;
@@ -1333,7 +1328,7 @@ __global__ void __launch_bounds__(TREE_WARPS * 32) tree_kernel(TreeArgs A, Kerne
                 const bool accept = 0.75 * ws * ws < th2 * d2;
                 if (accept && re - rs >= nc) {  // cell-particle: M2P
                     const float* Mg = A.Mall + (lvl_off(l) + c) * 3 * nc;
-                    for (int k = lane; k < 3 * nc; k += 32) Msh[k] = Mg[k];
+                    for (int k = lane; k < 3 * nc; k += 32) Msh[(k % nc) * 4 + k / nc] = Mg[k];
                     __syncwarp();
                     if (act && !(A.dbg & 2)) {
                         const float iw = 1.f / (float)wl;
@@ -1490,7 +1485,7 @@ void launch_tree(const float* sorted6, int64_t n, const uint32_t* keys_sorted,
                depth, p, ncrit, periodic, aL, theta, 0};
     if (const char* e = getenv("VFMM_TREE_DBG")) A.dbg = atoi(e);
     const int nc = (p + 1) * (p + 1);
-    const size_t per_warp = (size_t)(3 * (p + 3) * 2 * 32 + ((3 * nc + 3) & ~3) + 9 * 32);
+    const size_t per_warp = (size_t)(3 * (p + 3) * 2 * 32 + 4 * nc + 9 * 32);
     const size_t smem = per_warp * TREE_WARPS * sizeof(float);
     static PerDeviceOnce once;
     once([&] {
