@@ -1242,7 +1242,7 @@ __device__ __forceinline__ void m2p_rows(const float* __restrict__ Msh, int p, i
 }
 
 template <int SCHEME>
-__global__ void __launch_bounds__(TREE_WARPS * 32) tree_kernel(TreeArgs A, KernelConsts kc) {
+__global__ void __launch_bounds__(TREE_WARPS * 32, 4) tree_kernel(TreeArgs A, KernelConsts kc) {
     extern __shared__ float4 tree_sm4[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int p = A.p, nc = (p + 1) * (p + 1), L = A.L;
@@ -1251,7 +1251,7 @@ __global__ void __launch_bounds__(TREE_WARPS * 32) tree_kernel(TreeArgs A, Kerne
     float* base = reinterpret_cast<float*>(tree_sm4) + warp * (ish_floats + msh_floats + 9 * 32);
     float* Ish = base;
     float* Msh = base + ish_floats;
-    float* Ssh = Msh + msh_floats;  // sources: [dx dy dz gx gy gz ix iy iz][32]
+    float* Ssh = Msh + msh_floats;  // sources: float4 (dx dy dz ix)[32], (gx gy gz iy)[32], iz[32]
     __shared__ int2 stack_sm[TREE_WARPS][TREE_STACK];
     int2* stk = stack_sm[warp];
     const int ng = *A.ngroups;
@@ -1287,6 +1287,7 @@ __global__ void __launch_bounds__(TREE_WARPS * 32) tree_kernel(TreeArgs A, Kerne
                 giy = A.s6[4 * A.n + i];
                 giz = A.s6[5 * A.n + i];
             }
+            const float txf = (float)tx, tyf = (float)ty, tzf = (float)tz;  // exact leaf indices
             // target position in leaf widths from the box corner
             const float Px = (float)tx + 0.5f + dxi * inv_aL;
             const float Py = (float)ty + 0.5f + dyi * inv_aL;
@@ -1349,31 +1350,33 @@ __global__ void __launch_bounds__(TREE_WARPS * 32) tree_kernel(TreeArgs A, Kerne
                     }
                     __syncwarp();
                 } else if (accept || (l >= 1 && (l == L || re - rs <= A.ncrit))) {  // P2P
+                    // sources staged as (delta, leaf index) float4 pairs: d = (t - s) a + (delta_i -
+                    // delta_j) with exact leaf offsets, three shared loads per pair
+                    float4* SA = reinterpret_cast<float4*>(Ssh);           // dx dy dz ix
+                    float4* SB = reinterpret_cast<float4*>(Ssh + 4 * 32);  // gx gy gz iy
+                    float* SC = Ssh + 8 * 32;                              // iz
                     for (int j0 = rs; j0 < re; j0 += 32) {
                         const int j = j0 + lane;
                         if (j < re) {
                             const uint32_t key = A.keys[j];
-                            Ssh[0 * 32 + lane] = A.s6[j];
-                            Ssh[1 * 32 + lane] = A.s6[A.n + j];
-                            Ssh[2 * 32 + lane] = A.s6[2 * A.n + j];
-                            Ssh[3 * 32 + lane] = A.s6[3 * A.n + j];
-                            Ssh[4 * 32 + lane] = A.s6[4 * A.n + j];
-                            Ssh[5 * 32 + lane] = A.s6[5 * A.n + j];
-                            reinterpret_cast<int*>(Ssh)[6 * 32 + lane] = (int)compact3p(key) + ox * side;
-                            reinterpret_cast<int*>(Ssh)[7 * 32 + lane] = (int)compact3p(key >> 1) + oy * side;
-                            reinterpret_cast<int*>(Ssh)[8 * 32 + lane] = (int)compact3p(key >> 2) + oz * side;
+                            SA[lane] = make_float4(A.s6[j], A.s6[A.n + j], A.s6[2 * A.n + j],
+                                                   (float)((int)compact3p(key) + ox * side));
+                            SB[lane] = make_float4(A.s6[3 * A.n + j], A.s6[4 * A.n + j],
+                                                   A.s6[5 * A.n + j],
+                                                   (float)((int)compact3p(key >> 1) + oy * side));
+                            SC[lane] = (float)((int)compact3p(key >> 2) + oz * side);
                         }
                         __syncwarp();
                         const int cnt = min(32, re - j0);
                         if (act) {
                             for (int q = 0; q < cnt; ++q) {
-                                const int* Si = reinterpret_cast<const int*>(Ssh);
-                                const float dx = fmaf((float)(tx - Si[6 * 32 + q]), aL, dxi - Ssh[q]);
-                                const float dy = fmaf((float)(ty - Si[7 * 32 + q]), aL, dyi - Ssh[32 + q]);
-                                const float dz = fmaf((float)(tz - Si[8 * 32 + q]), aL, dzi - Ssh[64 + q]);
+                                const float4 a4 = SA[q], b4 = SB[q];
+                                const float cz = SC[q];
+                                const float dx = fmaf(txf - a4.w, aL, dxi - a4.x);
+                                const float dy = fmaf(tyf - b4.w, aL, dyi - a4.y);
+                                const float dz = fmaf(tzf - cz, aL, dzi - a4.z);
                                 if (!(A.dbg & 1))
-                                    pair<SCHEME>(dx, dy, dz, Ssh[96 + q], Ssh[128 + q],
-                                                 Ssh[160 + q], gix, giy, giz, kc, acc);
+                                    pair<SCHEME>(dx, dy, dz, b4.x, b4.y, b4.z, gix, giy, giz, kc, acc);
                             }
                             npairs += cnt;
                         }
